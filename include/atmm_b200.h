@@ -1,0 +1,228 @@
+/*
+ * atmm_b200.h -- C ABI of the B200-native ATMM operator (libatmm_b200.so).
+ *
+ * Drop-in boundary for the reference's ATMM hot path (loraserve, header-only
+ * C++ under /root/reference/proj/include/loraserve).  The reference has no C
+ * ABI; each entry point below names the reference function it replaces
+ * (file:line, paths relative to proj/include/loraserve/).  The header-only
+ * C++ shim include/loraserve_b200.hpp restores the reference's C++
+ * signatures and exception types on top of this ABI.
+ *
+ * Conventions
+ *  - Every function returns an int status (ATMM_OK == 0, else an ATMM_ERR_*
+ *    code that maps 1:1 onto the reference's exception classes,
+ *    errors.hpp:10-61); the message is in atmm_last_error() (thread-local).
+ *  - No function throws; all are safe to call from C.
+ *  - Device-pointer entry points are stream-ordered on the caller's
+ *    cudaStream_t (passed as void*; NULL = legacy default stream) and never
+ *    synchronize.  *_host entry points take host buffers and are synchronous.
+ *  - Matrices are row-major, `ld` in elements.  Row-vector convention of the
+ *    reference: y = x . W, down is d_in x r, up is r x d_out (adapter.hpp:15-16).
+ *  - Compute: bf16 operands, fp32 accumulation on tcgen05 tensor cores.
+ *    There is no CPU fallback: without an sm_100 device the compute calls
+ *    return ATMM_ERR_NO_DEVICE.
+ */
+#ifndef ATMM_B200_H_
+#define ATMM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ATMM_ABI_VERSION 1
+
+/* Status codes <-> loraserve exception classes (errors.hpp). */
+enum {
+  ATMM_OK = 0,
+  ATMM_ERR_SHAPE = 1,           /* ShapeError            errors.hpp:16-25 */
+  ATMM_ERR_CONFIG = 2,          /* ConfigError           errors.hpp:27-30 */
+  ATMM_ERR_MODE = 3,            /* ModeError             errors.hpp:32-36 */
+  ATMM_ERR_IO = 4,              /* IoError               errors.hpp:38-41 */
+  ATMM_ERR_PARSE = 5,           /* ParseError            errors.hpp:43-52 */
+  ATMM_ERR_UNKNOWN_ADAPTER = 6, /* UnknownAdapterError   errors.hpp:54-62 */
+  ATMM_ERR_CUDA = 7,            /* CUDA runtime / launch failure          */
+  ATMM_ERR_NO_DEVICE = 8,       /* no sm_100 device: there is no fallback */
+  ATMM_ERR_INTERNAL = 9
+};
+
+/* Element types for activations / outputs / weights. */
+enum { ATMM_BF16 = 0, ATMM_F32 = 1 };
+
+const char* atmm_last_error(void);
+int atmm_abi_version(void);
+/* Number of sm_100 devices visible (0 on a CPU-only host; never fails). */
+int atmm_device_count(void);
+
+/* ===================================================================== */
+/* Planner                                                                */
+/* ===================================================================== */
+
+/* plan_batch (batch.hpp:28-42): stable group-by of rows per adapter id,
+ * segments in ascending id order.  Output is CSR: seg_adapter[S],
+ * seg_offsets[S+1], row_index[n] (caller-allocated, capacity n / n+1 / n).
+ * Empty assignment -> ATMM_ERR_CONFIG. */
+int atmm_plan_batch(const int32_t* assignment, int64_t n, int32_t* seg_adapter,
+                    int64_t* seg_offsets, int64_t* row_index, int64_t* num_segments);
+
+/* ===================================================================== */
+/* Tiling configuration and the shape-keyed table (tiling.hpp)            */
+/* ===================================================================== */
+
+/* cfg = {outer_m, outer_n, outer_k, inner_m, inner_n, inner_k}
+ * (TilingConfig, tiling.hpp:22-65).  On B200 the edges are read as:
+ *   outer_m  rows per cluster tile (segment rows are cut into tiles of this)
+ *   outer_k  K slice per CTA  -> cluster size C = ceil(d_in / outer_k)
+ *   outer_n  expand N chunk per tcgen05.mma (<= 256 columns)
+ *   inner_*  tcgen05 instruction shape (M=128 / N granule / K stage = 64),
+ *            validated like the reference but otherwise informational. */
+int atmm_config_valid(const int32_t cfg[6]); /* structurally_valid tiling.hpp:40-48 -> 1/0 */
+int atmm_m_bucket_of(int64_t m);             /* m_bucket_of tiling.hpp:76-79 */
+
+typedef struct atmm_table atmm_table;
+/* TilingTable() / TilingTable(default) (tiling.hpp:160-162).  NULL default =
+ * the reference default {64,32,32,32,32,32}; a default-constructed table
+ * resolves its default through the B200 heuristic. */
+int atmm_table_create(const int32_t* default_cfg, atmm_table** out);
+void atmm_table_destroy(atmm_table* t);
+/* TilingTable::insert (tiling.hpp:164-167).  sm100 (nullable) = explicit
+ * B200 launch parameters {tile_m, cluster, bn, stages} stored beside the
+ * reference entry (the JSON "sm100" object). */
+int atmm_table_insert(atmm_table* t, int32_t m_bucket, int32_t k, int32_t n,
+                      const int32_t cfg[6], int64_t measured_ns, const int32_t* sm100);
+int atmm_table_set_default(atmm_table* t, const int32_t cfg[6]);
+/* TilingTable::lookup (tiling.hpp:181-199): exact -> nearest same-(k,n)
+ * bucket within 32 (ties to the smaller bucket) -> default. */
+int atmm_table_lookup(const atmm_table* t, int64_t m, int64_t k, int64_t n, int32_t cfg_out[6]);
+int atmm_table_size(const atmm_table* t, int64_t* size);
+/* The B200 launch parameters the table resolves for the fused bypass of a
+ * segment of m rows at (d_in, rank, d_out): {tile_m, cluster, bn, stages}. */
+int atmm_table_resolve_launch(const atmm_table* t, int64_t m, int64_t d_in, int64_t rank,
+                              int64_t d_out, int32_t launch_out[4]);
+/* TilingTable::save / load (tiling.hpp:201-249): same JSON schema,
+ * {"default":[6], "entries":[{m_bucket,k,n,config[6],ns[,sm100]}]}. */
+int atmm_table_save(const atmm_table* t, const char* path);
+int atmm_table_load(const char* path, atmm_table** out);
+/* candidate_configs / default_candidates (tiling.hpp:88-149): writes up to
+ * cap configs (6 ints each) and the total count. */
+int atmm_candidate_configs(size_t cache_budget_bytes, size_t scalar_width, int32_t* out,
+                           size_t cap, size_t* count);
+int atmm_default_candidates(size_t cache_budget_bytes, size_t scalar_width, int32_t* out,
+                            size_t cap, size_t* count);
+
+/* ===================================================================== */
+/* Adapter registry (adapter.hpp:18-110, device resident)                 */
+/* ===================================================================== */
+
+typedef struct atmm_registry atmm_registry;
+/* A registry holds the LoRA factors of every adapter for `num_layers`
+ * layers of one d_in x d_out projection, in HBM, in the tcgen05 operand
+ * layouts.  device = CUDA ordinal. */
+int atmm_registry_create(int device, int64_t num_layers, int64_t d_in, int64_t d_out,
+                         atmm_registry** out);
+void atmm_registry_destroy(atmm_registry* r);
+/* LoraAdapter(...) (adapter.hpp:26-51) + AdapterSet::emplace: host fp32
+ * factors down [L][d_in x r] and up [L][r x d_out]; scale s multiplies the
+ * adapter's contribution (the reference's implicit s = 1).  Requires
+ * 1 <= r <= 128 (the reference additionally requires r < hidden).
+ * Re-putting an id replaces it. */
+int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const float* down,
+                      const float* up, float scale);
+int atmm_registry_remove(atmm_registry* r, int32_t adapter_id);
+/* adapter_at (adapter.hpp:106-110): 1 if present, 0 if not. */
+int atmm_registry_contains(const atmm_registry* r, int32_t adapter_id);
+int atmm_registry_rank(const atmm_registry* r, int32_t adapter_id, int64_t* rank);
+/* Bytes of adapter factors resident in HBM (bf16 operand layouts). */
+int atmm_registry_bytes(const atmm_registry* r, int64_t* bytes);
+
+/* ===================================================================== */
+/* Fused batched-LoRA bypass (batch.hpp:48-81 + model.hpp:239-241)        */
+/* ===================================================================== */
+
+typedef struct atmm_plan atmm_plan;
+/* plan_batch + tile/launch grouping for one batch on one registry.
+ * Unknown ids -> ATMM_ERR_UNKNOWN_ADAPTER (fail fast like
+ * forward_unmerged, model.hpp:226-228).  table may be NULL (heuristic). */
+int atmm_plan_create(atmm_registry* r, const int32_t* assignment, int64_t n,
+                     const atmm_table* table, atmm_plan** out);
+void atmm_plan_destroy(atmm_plan* p);
+/* Routing tables actually uploaded (for bit-exact routing checks):
+ * seg_adapter[S], seg_offsets[S+1], row_index[n]. */
+int atmm_plan_routing(const atmm_plan* p, int32_t* seg_adapter, int64_t* seg_offsets,
+                      int64_t* row_index, int64_t* num_segments);
+/* Number of kernel launches / cluster tiles / CTAs the plan issues. */
+int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64_t* ctas);
+
+/* Y[row, :] += scale * s_a * (X[row, :] . down_a[layer]) . up_a[layer]
+ * for every row, a = assignment[row]: ONE pass, shrink+expand fused, the
+ * rank-r intermediate kept on chip, the residual add fused in the epilogue.
+ * X: n x d_in bf16 (ldx % 8 == 0, 16-byte aligned); Y: n x d_out, y_dtype
+ * ATMM_BF16 or ATMM_F32.  scale = -1 gives the deLoRA cancel branch
+ * (model.hpp:315-321).  Device pointers, stream-ordered. */
+int atmm_bypass_apply(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
+                      int64_t ldy, int y_dtype, float scale, void* stream);
+
+/* run_bypass (batch.hpp:48) with host buffers: out = bypass(x), fp32 in and
+ * out (x rounded to bf16 on the device).  Synchronous. */
+int atmm_run_bypass_host(atmm_registry* r, const float* x, int64_t n,
+                         const int32_t* assignment, int64_t layer, const atmm_table* table,
+                         float* out);
+/* The unmerged-forward residual site (model.hpp:239-241) end to end with
+ * host buffers: H2D x and y, fused bypass into y, D2H y.  bf16 host
+ * buffers (pinned if the caller wants full PCIe bandwidth).  Uses the
+ * plan's device and the given stream; synchronizes on it. */
+int atmm_bypass_residual_host_bf16(const atmm_plan* p, int64_t layer, const uint16_t* x_host,
+                                   uint16_t* y_host, float scale, void* stream);
+
+/* ===================================================================== */
+/* Merge / unmerge  W +-= s . down . up   (model.hpp:120-188)             */
+/* ===================================================================== */
+
+/* W (d_in x d_out, w_dtype ATMM_F32 or ATMM_BF16, in place, address
+ * stable) += sign * s_a * down_a[layer] . up_a[layer].  sign = +1 merges,
+ * -1 unmerges.  Device pointer, stream-ordered. */
+int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* w,
+                     int64_t ldw, int w_dtype, float sign, void* stream);
+/* delta_w (model.hpp:130-140) with a host output: out = s_a * down . up. */
+int atmm_delta_w_host(atmm_registry* r, int32_t adapter_id, int64_t layer, float* out);
+
+/* ===================================================================== */
+/* Plain ATMM GEMM (atmm.hpp:111-154)                                    */
+/* ===================================================================== */
+
+/* atmm_multiply_into with host fp32 buffers: c = a . b, bf16 operands on
+ * tcgen05, fp32 accumulate and output.  cfg is validated like the
+ * reference (ConfigError).  Synchronous. */
+int atmm_multiply_host(const float* a, int64_t m, int64_t k, const float* b, int64_t n,
+                       float* c, const int32_t cfg[6]);
+
+/* ===================================================================== */
+/* Offline tiling search on B200 (atmm.hpp:188-355)                      */
+/* ===================================================================== */
+
+/* Times the fused bypass of one segment shape (m rows, d_in, rank, d_out)
+ * under each candidate launch {tile_m, cluster, bn, stages} with CUDA
+ * events (median of `trials` after a warm-up, L2 flushed between trials)
+ * and writes median ns per candidate (INT64_MAX for a failed candidate). */
+int atmm_bench_launches(int device, int64_t m, int64_t d_in, int64_t rank, int64_t d_out,
+                        const int32_t* launches, int64_t num_launches, int trials,
+                        int64_t* median_ns);
+
+/* ===================================================================== */
+/* Request sharding over GPUs                         */
+/* ===================================================================== */
+
+/* Longest-processing-time partition of the segments of plan_batch(assignment)
+ * over num_shards GPUs, cost = rows * rank * (d_in + d_out) + adapter bytes.
+ * Writes shard_of_row[n]; whole segments stay together.  Deterministic. */
+int atmm_shard_rows(const int32_t* assignment, int64_t n, const int32_t* adapter_ids,
+                    const int64_t* adapter_ranks, int64_t num_adapters, int64_t d_in,
+                    int64_t d_out, int32_t num_shards, int32_t* shard_of_row);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ATMM_B200_H_ */

@@ -1,0 +1,424 @@
+"""Python mirror of the reference's ATMM operator interface over the C ABI.
+
+Names, argument meaning and error behaviour follow loraserve
+(/root/reference/proj/include/loraserve): ``plan_batch`` (batch.hpp:28),
+``run_bypass`` (batch.hpp:48), ``TilingConfig``/``TilingTable``
+(tiling.hpp:22-254), ``delta_w``/``merge``/``unmerge`` (model.hpp:120-188),
+``atmm_multiply`` (atmm.hpp:144).  Exceptions mirror errors.hpp.
+
+Device work goes through libatmm_b200.so (hand-written sm_100a kernels);
+torch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._lib import f32p, i32p, i64p, last_error, lib, u16p
+
+# --------------------------------------------------------------- errors ---
+
+
+class Error(RuntimeError):
+    """loraserve::Error (errors.hpp:10)."""
+
+    code = 9
+
+
+class ShapeError(Error):
+    code = 1
+
+
+class ConfigError(Error):
+    code = 2
+
+
+class ModeError(Error):
+    code = 3
+
+
+class IoError(Error):
+    code = 4
+
+
+class ParseError(Error):
+    code = 5
+
+
+class UnknownAdapterError(Error):
+    code = 6
+
+
+class CudaError(Error):
+    code = 7
+
+
+class NoDeviceError(Error):
+    code = 8
+
+
+_BY_CODE = {c.code: c for c in (ShapeError, ConfigError, ModeError, IoError, ParseError,
+                                 UnknownAdapterError, CudaError, NoDeviceError)}
+
+BF16 = 0
+F32 = 1
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise _BY_CODE.get(status, Error)(last_error())
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def device_count() -> int:
+    """Number of visible sm_100 devices (0 on a CPU host)."""
+    return int(lib.atmm_device_count())
+
+
+# -------------------------------------------------------------- planner ---
+
+
+@dataclass
+class Segment:
+    adapter_id: int
+    rows: List[int]
+
+
+@dataclass
+class BatchPlan:
+    segments: List[Segment] = field(default_factory=list)
+    total_rows: int = 0
+
+
+def plan_batch_csr(assignment: Sequence[int]) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    a = _i32(assignment).reshape(-1)
+    n = a.size
+    seg = np.zeros(max(n, 1), np.int32)
+    off = np.zeros(max(n, 1) + 1, np.int64)
+    rows = np.zeros(max(n, 1), np.int64)
+    S = ctypes.c_int64(0)
+    _check(lib.atmm_plan_batch(_p(a, i32p), n, _p(seg, i32p), _p(off, i64p), _p(rows, i64p), ctypes.byref(S)))
+    s = S.value
+    return seg[:s].copy(), off[: s + 1].copy(), rows[:n].copy()
+
+
+def plan_batch(assignment: Sequence[int]) -> BatchPlan:
+    """batch.hpp:28-42: stable group-by, segments in ascending adapter id."""
+    seg, off, rows = plan_batch_csr(assignment)
+    plan = BatchPlan(total_rows=int(len(rows)))
+    for s in range(len(seg)):
+        plan.segments.append(Segment(int(seg[s]), [int(r) for r in rows[off[s]:off[s + 1]]]))
+    return plan
+
+
+# --------------------------------------------------------------- tiling ---
+
+
+class TilingConfig(tuple):
+    """(outer_m, outer_n, outer_k, inner_m, inner_n, inner_k), tiling.hpp:22."""
+
+    def __new__(cls, *edges):
+        if len(edges) == 1 and not isinstance(edges[0], int):
+            edges = tuple(edges[0])
+        if len(edges) != 6:
+            raise ConfigError("tiling config must have 6 edges")
+        return super().__new__(cls, (int(e) for e in edges))
+
+    def structurally_valid(self) -> bool:
+        return bool(lib.atmm_config_valid(_p(_i32(self), i32p)))
+
+    def validate(self) -> None:
+        if not self.structurally_valid():
+            raise ConfigError(f"invalid tiling config {tuple(self)}")
+
+    def footprint_elems(self) -> int:
+        om, on, ok = self[0], self[1], self[2]
+        return om * ok + ok * on + om * on
+
+
+def m_bucket_of(m: int) -> int:
+    return int(lib.atmm_m_bucket_of(int(m)))
+
+
+def candidate_configs(cache_budget_bytes: int, scalar_width: int) -> List[TilingConfig]:
+    return _configs(lib.atmm_candidate_configs, cache_budget_bytes, scalar_width)
+
+
+def default_candidates(cache_budget_bytes: int, scalar_width: int) -> List[TilingConfig]:
+    return _configs(lib.atmm_default_candidates, cache_budget_bytes, scalar_width)
+
+
+def _configs(fn, budget, width) -> List[TilingConfig]:
+    count = ctypes.c_size_t(0)
+    _check(fn(budget, width, None, 0, ctypes.byref(count)))
+    out = np.zeros(6 * max(count.value, 1), np.int32)
+    _check(fn(budget, width, _p(out, i32p), count.value, ctypes.byref(count)))
+    return [TilingConfig(out[6 * i: 6 * i + 6]) for i in range(count.value)]
+
+
+class TilingTable:
+    """tiling.hpp:153-254 plus the B200 launch resolution."""
+
+    def __init__(self, default: Optional[Sequence[int]] = None, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = ctypes.c_void_p()
+        d = _i32(default) if default is not None else None
+        _check(lib.atmm_table_create(_p(d, i32p) if d is not None else None, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.atmm_table_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def insert(self, m_bucket: int, k: int, n: int, config: Sequence[int], measured_ns: int = 0,
+               sm100: Optional[Sequence[int]] = None) -> None:
+        s = _i32(sm100) if sm100 is not None else None
+        _check(lib.atmm_table_insert(self._h, m_bucket, k, n, _p(_i32(config), i32p), int(measured_ns),
+                                     _p(s, i32p) if s is not None else None))
+
+    def set_default(self, config: Sequence[int]) -> None:
+        _check(lib.atmm_table_set_default(self._h, _p(_i32(config), i32p)))
+
+    def lookup(self, m: int, k: int, n: int) -> TilingConfig:
+        out = np.zeros(6, np.int32)
+        _check(lib.atmm_table_lookup(self._h, m, k, n, _p(out, i32p)))
+        return TilingConfig(out)
+
+    def resolve_launch(self, m: int, d_in: int, rank: int, d_out: int) -> Tuple[int, int, int, int]:
+        out = np.zeros(4, np.int32)
+        _check(lib.atmm_table_resolve_launch(self._h, m, d_in, rank, d_out, _p(out, i32p)))
+        return tuple(int(v) for v in out)
+
+    def __len__(self) -> int:
+        s = ctypes.c_int64(0)
+        _check(lib.atmm_table_size(self._h, ctypes.byref(s)))
+        return s.value
+
+    def save(self, path: str) -> None:
+        _check(lib.atmm_table_save(self._h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path: str) -> "TilingTable":
+        h = ctypes.c_void_p()
+        _check(lib.atmm_table_load(str(path).encode(), ctypes.byref(h)))
+        return cls(_handle=h)
+
+
+def heuristic_launch(m: int, d_in: int, rank: int, d_out: int) -> Tuple[int, int, int, int]:
+    out = np.zeros(4, np.int32)
+    _check(lib.atmm_table_resolve_launch(None, m, d_in, rank, d_out, _p(out, i32p)))
+    return tuple(int(v) for v in out)
+
+
+# ------------------------------------------------------------- registry ---
+
+
+class AdapterRegistry:
+    """Device-resident AdapterSet (adapter.hpp:18-110) for one projection."""
+
+    def __init__(self, num_layers: int, d_in: int, d_out: Optional[int] = None, device: int = 0):
+        d_out = d_in if d_out is None else d_out
+        h = ctypes.c_void_p()
+        _check(lib.atmm_registry_create(device, num_layers, d_in, d_out, ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        self.num_layers, self.d_in, self.d_out = num_layers, d_in, d_out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.atmm_registry_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def put(self, adapter_id: int, down, up, scale: float = 1.0) -> None:
+        """down: [L, d_in, r] (or [d_in, r] for L = 1); up: [L, r, d_out]."""
+        d = _f32(down)
+        u = _f32(up)
+        if d.ndim == 2:
+            d = d[None]
+        if u.ndim == 2:
+            u = u[None]
+        L, di, r = d.shape
+        if L != self.num_layers or di != self.d_in or u.shape != (L, r, self.d_out):
+            raise ShapeError(f"adapter factor shapes {d.shape} / {u.shape} do not match registry "
+                             f"(L={self.num_layers}, d_in={self.d_in}, d_out={self.d_out})")
+        _check(lib.atmm_registry_put(self._h, adapter_id, r, _p(d, f32p), _p(u, f32p), float(scale)))
+
+    def remove(self, adapter_id: int) -> None:
+        _check(lib.atmm_registry_remove(self._h, adapter_id))
+
+    def __contains__(self, adapter_id: int) -> bool:
+        return bool(lib.atmm_registry_contains(self._h, adapter_id))
+
+    def rank(self, adapter_id: int) -> int:
+        r = ctypes.c_int64(0)
+        _check(lib.atmm_registry_rank(self._h, adapter_id, ctypes.byref(r)))
+        return r.value
+
+    def nbytes(self) -> int:
+        b = ctypes.c_int64(0)
+        _check(lib.atmm_registry_bytes(self._h, ctypes.byref(b)))
+        return b.value
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class BypassPlan:
+    """plan_batch + launch grouping for one batch on one registry."""
+
+    def __init__(self, registry: AdapterRegistry, assignment: Sequence[int], table: Optional[TilingTable] = None):
+        a = _i32(assignment).reshape(-1)
+        h = ctypes.c_void_p()
+        _check(lib.atmm_plan_create(registry.handle, _p(a, i32p), a.size, table.handle if table else None,
+                                    ctypes.byref(h)))
+        self._h = h
+        self.registry = registry
+        self.n = int(a.size)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.atmm_plan_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def routing(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        seg = np.zeros(self.n, np.int32)
+        off = np.zeros(self.n + 1, np.int64)
+        rows = np.zeros(self.n, np.int64)
+        S = ctypes.c_int64(0)
+        _check(lib.atmm_plan_routing(self._h, _p(seg, i32p), _p(off, i64p), _p(rows, i64p), ctypes.byref(S)))
+        return seg[: S.value].copy(), off[: S.value + 1].copy(), rows
+
+    def stats(self) -> Tuple[int, int, int]:
+        a, b, c = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(lib.atmm_plan_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def apply(self, x, y, layer: int = 0, scale: float = 1.0, stream=None) -> None:
+        """y[row] += scale * s_a * (x[row] @ down_a[layer]) @ up_a[layer] (torch CUDA tensors)."""
+        import torch
+
+        if x.dtype != torch.bfloat16 or not x.is_cuda:
+            raise ShapeError("x must be a CUDA bfloat16 tensor")
+        if y.dtype not in (torch.bfloat16, torch.float32) or not y.is_cuda:
+            raise ShapeError("y must be a CUDA bfloat16 or float32 tensor")
+        if x.dim() != 2 or y.dim() != 2 or x.shape[0] != self.n or y.shape[0] != self.n:
+            raise ShapeError(f"x/y must be 2-D with {self.n} rows")
+        if x.stride(1) != 1 or y.stride(1) != 1:
+            raise ShapeError("x and y rows must be contiguous")
+        _check(lib.atmm_bypass_apply(self._h, layer, x.data_ptr(), x.stride(0), y.data_ptr(), y.stride(0),
+                                     BF16 if y.dtype == torch.bfloat16 else F32, float(scale), _stream_ptr(stream)))
+
+    def residual_host_bf16(self, x_host: np.ndarray, y_host: np.ndarray, layer: int = 0, scale: float = 1.0,
+                           stream=None) -> None:
+        """End-to-end: host bf16 (uint16) buffers in, y_host updated in place."""
+        if x_host.dtype != np.uint16 or y_host.dtype != np.uint16:
+            raise ShapeError("host buffers must be bf16 bit patterns (uint16)")
+        if not (x_host.flags.c_contiguous and y_host.flags.c_contiguous):
+            raise ShapeError("host buffers must be C-contiguous")
+        _check(lib.atmm_bypass_residual_host_bf16(self._h, layer, _p(x_host, u16p), _p(y_host, u16p),
+                                                  float(scale), _stream_ptr(stream)))
+
+
+def run_bypass(registry: AdapterRegistry, x, assignment: Sequence[int], layer: int = 0,
+               table: Optional[TilingTable] = None) -> np.ndarray:
+    """batch.hpp:48: returns the fresh bypass matrix (host fp32 in/out)."""
+    xa = _f32(x)
+    a = _i32(assignment).reshape(-1)
+    if xa.ndim != 2 or xa.shape[1] != registry.d_in:
+        raise ShapeError(f"run_bypass: x must be n x {registry.d_in}")
+    if xa.shape[0] != a.size:
+        raise ShapeError(f"run_bypass: batch has {xa.shape[0]} rows but plan covers {a.size}")
+    out = np.zeros((a.size, registry.d_out), np.float32)
+    _check(lib.atmm_run_bypass_host(registry.handle, _p(xa, f32p), a.size, _p(a, i32p), layer,
+                                    table.handle if table else None, _p(out, f32p)))
+    return out
+
+
+def delta_w(registry: AdapterRegistry, adapter_id: int, layer: int = 0) -> np.ndarray:
+    """model.hpp:130-140: s * down @ up (host fp32)."""
+    out = np.zeros((registry.d_in, registry.d_out), np.float32)
+    _check(lib.atmm_delta_w_host(registry.handle, adapter_id, layer, _p(out, f32p)))
+    return out
+
+
+def merge_into(registry: AdapterRegistry, adapter_id: int, layer: int, w, sign: float = 1.0, stream=None) -> None:
+    """W (+/-)= s * down @ up in place on a CUDA tensor (fp32 or bf16)."""
+    import torch
+
+    if w.dim() != 2 or w.stride(1) != 1 or not w.is_cuda or w.dtype not in (torch.float32, torch.bfloat16):
+        raise ShapeError("w must be a row-contiguous 2-D CUDA float32/bfloat16 tensor")
+    if tuple(w.shape) != (registry.d_in, registry.d_out):
+        raise ShapeError(f"w shape {tuple(w.shape)} != ({registry.d_in}, {registry.d_out})")
+    _check(lib.atmm_merge_apply(registry.handle, adapter_id, layer, w.data_ptr(), w.stride(0),
+                                F32 if w.dtype == torch.float32 else BF16, float(sign), _stream_ptr(stream)))
+
+
+def atmm_multiply(a, b, config: Sequence[int]) -> np.ndarray:
+    """atmm.hpp:144-154 (host fp32 in/out, bf16 tcgen05 compute)."""
+    aa, bb = _f32(a), _f32(b)
+    if aa.ndim != 2 or bb.ndim != 2 or aa.shape[1] != bb.shape[0]:
+        raise ShapeError(f"atmm_multiply: shape mismatch {aa.shape[0]}x{aa.shape[1]} vs {bb.shape[0]}x{bb.shape[1]}")
+    m, k = aa.shape
+    n = bb.shape[1]
+    out = np.zeros((m, n), np.float32)
+    _check(lib.atmm_multiply_host(_p(aa, f32p), m, k, _p(bb, f32p), n, _p(out, f32p), _p(_i32(config), i32p)))
+    return out
+
+
+def bench_launches(m: int, d_in: int, rank: int, d_out: int, launches: Iterable[Sequence[int]],
+                   trials: int = 5, device: int = 0) -> List[int]:
+    arr = _i32([list(l) for l in launches]).reshape(-1)
+    count = arr.size // 4
+    out = np.zeros(count, np.int64)
+    _check(lib.atmm_bench_launches(device, m, d_in, rank, d_out, _p(arr, i32p), count, trials, _p(out, i64p)))
+    return [int(v) for v in out]
+
+
+def shard_rows(assignment: Sequence[int], adapter_ranks: dict, d_in: int, d_out: int, num_shards: int) -> np.ndarray:
+    """LPT request sharding over GPUs; returns shard index per row."""
+    a = _i32(assignment).reshape(-1)
+    ids = _i32(sorted(adapter_ranks))
+    ranks = np.ascontiguousarray(np.asarray([adapter_ranks[i] for i in sorted(adapter_ranks)], np.int64))
+    out = np.zeros(a.size, np.int32)
+    _check(lib.atmm_shard_rows(_p(a, i32p), a.size, _p(ids, i32p), _p(ranks, i64p), ids.size, d_in, d_out,
+                               num_shards, _p(out, i32p)))
+    return out

@@ -1,0 +1,794 @@
+// device.cu -- the CUDA-runtime side of the C ABI: device registry of
+// adapter factors, batch plans (routing tables in HBM), kernel launch
+// resolution (shared memory carve-up, cluster size, TMEM columns), the
+// host-buffer parity paths, merge/unmerge, the plain GEMM and the tuner's
+// timing primitive.
+//
+// Reference (proj/include/loraserve/): adapter.hpp:18-110 (registry),
+// batch.hpp:28-81 (plan_batch + run_bypass), model.hpp:120-188 (delta_w,
+// merge, unmerge), atmm.hpp:111-154 (atmm_multiply_into), atmm.hpp:188-216
+// (benchmark_config: median of trials after a warm-up).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.hpp"
+#include "device_types.hpp"
+
+namespace atmm {
+
+// kernels.cu
+cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap, const BypassParams& p, int C,
+                          int num_tiles, size_t smem, cudaStream_t stream);
+int bypass_max_active_clusters(int C, size_t smem);
+cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t smem,
+                         cudaStream_t stream);
+cudaError_t launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t rows, int64_t cols,
+                               int64_t lds, int64_t ldd, cudaStream_t stream);
+
+namespace {
+
+constexpr size_t kSmemLimit = 232448;  // 227 KiB opt-in per CTA on sm_100
+constexpr size_t kSmemPerSM = 233472;  // 228 KiB per SM
+constexpr int kMaxStages = 6;
+
+#define CUDA_CHECK(expr)                                                                  \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      fail(ATMM_ERR_CUDA, std::string(#expr) + " failed: " + cudaGetErrorString(e_));      \
+    }                                                                                     \
+  } while (0)
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// No CPU fallback: every compute entry point requires an sm_100 device.
+void require_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(ATMM_ERR_NO_DEVICE, "no CUDA device visible: the ATMM operator has no CPU fallback");
+  }
+  if (device < 0 || device >= count) fail(ATMM_ERR_NO_DEVICE, "device ordinal out of range");
+  cudaDeviceProp prop;
+  CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    fail(ATMM_ERR_NO_DEVICE, std::string("device ") + prop.name +
+                                 " is not sm_100 (Blackwell B200); kernels are built for sm_100a only");
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---- TMA tensor map encode through the driver entry point (no -lcuda) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+  });
+  if (!fn) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// X (n x d_in bf16, row stride ldx): box = one 64-wide row slice, 128-byte
+// swizzle; tile::gather4 loads 4 arbitrary rows per instruction.
+CUtensorMap make_x_map(const void* x, int64_t n, int64_t d_in, int64_t ldx) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d_in), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
+  const cuuint32_t box[2] = {kBK, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(X) failed: " + std::to_string(r));
+  return m;
+}
+
+// ---- host packing into the tcgen05 operand layouts ----
+// down (d_in x r, row-major, ld) -> down^T blocked
+//   [kb = d_in_pad/64][g = r_pad/8][c = 8][row = rank % 8][col = d_in % 8]
+void pack_down_t(const float* down, int64_t d_in, int64_t r, int64_t ld, int64_t d_in_pad,
+                 int64_t r_pad, uint16_t* out) {
+  std::memset(out, 0, static_cast<size_t>(d_in_pad * r_pad) * 2);
+  const int64_t G = r_pad / 8;
+  for (int64_t i = 0; i < d_in; ++i) {
+    const int64_t kb = i / 64, c = (i % 64) / 8, col = i % 8;
+    for (int64_t j = 0; j < r; ++j) {
+      const int64_t g = j / 8, row = j % 8;
+      out[((kb * G + g) * 8 + c) * 64 + row * 8 + col] = f32_to_bf16(down[i * ld + j]);
+    }
+  }
+}
+// up (r x d_out, row-major, ld) -> up^T blocked
+//   [g = d_out_pad/8][c = r_pad/8][row = d_out % 8][col = rank % 8]
+void pack_up_t(const float* up, int64_t r, int64_t d_out, int64_t ld, int64_t d_out_pad,
+               int64_t r_pad, uint16_t* out) {
+  std::memset(out, 0, static_cast<size_t>(d_out_pad * r_pad) * 2);
+  const int64_t Cc = r_pad / 8;
+  for (int64_t j = 0; j < r; ++j) {
+    const int64_t c = j / 8, col = j % 8;
+    for (int64_t nn = 0; nn < d_out; ++nn) {
+      const int64_t g = nn / 8, row = nn % 8;
+      out[(g * Cc + c) * 64 + row * 8 + col] = f32_to_bf16(up[j * ld + nn]);
+    }
+  }
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    release();
+    if (count) CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+}  // namespace
+
+// =========================================================================
+// Registry
+// =========================================================================
+struct Slot {
+  int32_t id = -1;
+  int64_t rank = 0, r_pad = 0;
+  float scale = 1.0f;
+  uint16_t* down_t = nullptr;
+  uint16_t* up_t = nullptr;
+  bool live = false;
+};
+
+}  // namespace atmm
+
+using namespace atmm;
+
+struct atmm_registry {
+  int device = 0;
+  int64_t L = 0, d_in = 0, d_out = 0, d_in_pad = 0, d_out_pad = 0;
+  std::map<int32_t, int> slot_of;
+  std::vector<Slot> slots;
+  DevBuf<SlotDesc> d_slots;
+  uint64_t generation = 0;
+
+  ~atmm_registry() {
+    DeviceGuard g(device);
+    for (auto& s : slots) {
+      if (s.down_t) cudaFree(s.down_t);
+      if (s.up_t) cudaFree(s.up_t);
+    }
+  }
+  void sync_slots() {
+    std::vector<SlotDesc> h(slots.size());
+    for (size_t i = 0; i < slots.size(); ++i) {
+      const Slot& s = slots[i];
+      h[i].down_t = s.down_t;
+      h[i].up_t = s.up_t;
+      h[i].down_layer_stride = d_in_pad * s.r_pad;
+      h[i].up_layer_stride = d_out_pad * s.r_pad;
+      h[i].rank = static_cast<int32_t>(s.rank);
+      h[i].r_pad = static_cast<int32_t>(s.r_pad);
+      h[i].scale = s.scale;
+      h[i].pad = 0;
+    }
+    if (d_slots.n < h.size()) d_slots.alloc(std::max<size_t>(h.size(), 2 * d_slots.n));
+    if (!h.empty()) CUDA_CHECK(cudaMemcpy(d_slots.p, h.data(), h.size() * sizeof(SlotDesc), cudaMemcpyHostToDevice));
+    ++generation;
+  }
+  const Slot& at(int32_t id) const {
+    auto it = slot_of.find(id);
+    if (it == slot_of.end()) fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(id));
+    return slots[static_cast<size_t>(it->second)];
+  }
+};
+
+// =========================================================================
+// Plan: routing tables + launch groups
+// =========================================================================
+namespace atmm {
+struct LaunchGroup {
+  int32_t cluster = 1, bn = 128, stages = 2;
+  int32_t r_pad_max = 16;
+  int64_t tile_offset = 0, num_tiles = 0;
+  int32_t stage_bytes = 0, red_rows = 0;
+  uint32_t off_red = 0, off_mid = 0, off_bar = 0, tmem_cols = 0;
+  size_t smem = 0;
+};
+
+// Shared-memory carve-up and TMEM budget of one fused launch.
+static void resolve_group(LaunchGroup& g, int64_t d_in, int64_t d_out, int32_t tile_rows_max,
+                          int32_t want_stages) {
+  const int64_t nkb = (d_in + kBK - 1) / kBK;
+  const int64_t nun = (d_out + kNUnit - 1) / kNUnit;
+  g.cluster = static_cast<int32_t>(std::clamp<int64_t>(g.cluster, 1, std::min<int64_t>({nkb, nun, kMaxCluster})));
+  const int32_t rp = g.r_pad_max;
+  // A stage holds one gathered 128 x 64 X block + the 64-wide down^T block,
+  // and is reused for expand chunks of bn x r_pad up^T.
+  int64_t stage = round_up(int64_t(kTileM) * kBK * 2 + int64_t(rp) * kBK * 2, 1024);
+  int32_t bn = std::clamp(g.bn / 32 * 32, 32, 256);
+  while (int64_t(bn) * rp * 2 > stage && bn > 32) bn -= 32;
+  g.bn = bn;
+  g.stage_bytes = static_cast<int32_t>(stage);
+  g.red_rows = (tile_rows_max + g.cluster - 1) / g.cluster;
+  const int64_t red = g.cluster > 1 ? round_up(int64_t(g.cluster) * g.red_rows * rp * 4, 1024) : 0;
+  const int64_t mid = round_up(int64_t(kTileM) * rp * 2, 1024);
+  int32_t cols = 32;
+  while (cols < std::max<int32_t>(rp, 2 * bn)) cols <<= 1;
+  g.tmem_cols = static_cast<uint32_t>(cols);
+  auto total = [&](int s) {
+    const int64_t bar = round_up((2 * s + 7) * 8 + 8, 16);
+    return size_t(1024 + int64_t(s) * stage + red + mid + bar);
+  };
+  int s = want_stages > 0 ? want_stages : kMaxStages;
+  while (s > 2 && total(s) > kSmemLimit) --s;
+  if (total(s) > kSmemLimit) fail(ATMM_ERR_CONFIG, "fused bypass does not fit in shared memory (rank too large)");
+  g.stages = s;
+  g.off_red = static_cast<uint32_t>(int64_t(s) * stage);
+  g.off_mid = static_cast<uint32_t>(g.off_red + red);
+  g.off_bar = static_cast<uint32_t>(g.off_mid + mid);
+  g.smem = total(s);
+  // CTAs of one cluster can share an SM; their TMEM allocations must all fit
+  // (512 columns per SM) or the cluster could deadlock.  Pad shared memory
+  // so co-residency never exceeds 512 / cols CTAs per SM.
+  const int max_co = std::max(1, 512 / cols);
+  while (static_cast<int>(kSmemPerSM / (g.smem + 1024)) > max_co) g.smem += 4096;
+}
+}  // namespace atmm
+
+struct atmm_plan {
+  atmm_registry* reg = nullptr;
+  uint64_t generation = 0;
+  int64_t n = 0;
+  BatchPlan bp;
+  std::vector<LaunchGroup> groups;
+  DevBuf<int32_t> d_rows;
+  DevBuf<TileDesc> d_tiles;
+  int64_t total_ctas = 0;
+};
+
+namespace atmm {
+
+// Builds routing tables and launch groups.  `forced` (tuner) overrides the
+// table for every segment.
+static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* assignment,
+                                             int64_t n, const TilingTable* table,
+                                             const LaunchCfg* forced) {
+  auto plan = std::make_unique<atmm_plan>();
+  plan->reg = reg;
+  plan->generation = reg->generation;
+  plan->n = n;
+  plan->bp = plan_batch(assignment, n);
+  if (n > std::numeric_limits<int32_t>::max()) fail(ATMM_ERR_SHAPE, "batch too large");
+  struct Pending {
+    LaunchCfg cfg;
+    std::vector<TileDesc> tiles;
+    int32_t r_pad_max = 16;
+    int32_t rows_max = 1;
+  };
+  std::map<std::pair<int32_t, std::pair<int32_t, int32_t>>, Pending> by_launch;
+  const size_t S = plan->bp.seg_adapter.size();
+  for (size_t s = 0; s < S; ++s) {
+    const int32_t id = plan->bp.seg_adapter[s];
+    auto it = reg->slot_of.find(id);
+    if (it == reg->slot_of.end()) fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(id));
+    const Slot& sl = reg->slots[static_cast<size_t>(it->second)];
+    const int64_t b = plan->bp.seg_offsets[s], e = plan->bp.seg_offsets[s + 1];
+    const int64_t ns = e - b;
+    LaunchCfg lc = forced ? *forced
+                          : (table ? table->resolve_launch(ns, reg->d_in, sl.rank, reg->d_out)
+                                   : heuristic_launch(ns, reg->d_in, sl.rank, reg->d_out));
+    const int64_t tm = std::clamp<int64_t>(lc.tile_m, 1, kTileM);
+    const int64_t ntiles = (ns + tm - 1) / tm;
+    const int64_t per = (ns + ntiles - 1) / ntiles;  // balanced tiles
+    auto& pend = by_launch[{lc.cluster, {lc.bn, lc.stages}}];
+    pend.cfg = lc;
+    pend.r_pad_max = std::max<int32_t>(pend.r_pad_max, static_cast<int32_t>(sl.r_pad));
+    for (int64_t t = 0; t < ntiles; ++t) {
+      const int64_t tb = b + t * per;
+      const int64_t te = std::min(e, tb + per);
+      if (te <= tb) break;
+      TileDesc td{static_cast<int32_t>(tb), static_cast<int32_t>(te - tb), it->second, 0};
+      pend.rows_max = std::max<int32_t>(pend.rows_max, td.rows);
+      pend.tiles.push_back(td);
+    }
+  }
+  std::vector<TileDesc> all_tiles;
+  for (auto& [key, pend] : by_launch) {
+    LaunchGroup g;
+    g.cluster = pend.cfg.cluster;
+    g.bn = pend.cfg.bn;
+    g.r_pad_max = pend.r_pad_max;
+    resolve_group(g, reg->d_in, reg->d_out, pend.rows_max, pend.cfg.stages);
+    g.tile_offset = static_cast<int64_t>(all_tiles.size());
+    g.num_tiles = static_cast<int64_t>(pend.tiles.size());
+    all_tiles.insert(all_tiles.end(), pend.tiles.begin(), pend.tiles.end());
+    plan->total_ctas += g.num_tiles * g.cluster;
+    plan->groups.push_back(g);
+  }
+  std::vector<int32_t> rows32(plan->bp.row_index.begin(), plan->bp.row_index.end());
+  DeviceGuard dg(reg->device);
+  plan->d_rows.alloc(rows32.size());
+  CUDA_CHECK(cudaMemcpy(plan->d_rows.p, rows32.data(), rows32.size() * 4, cudaMemcpyHostToDevice));
+  plan->d_tiles.alloc(all_tiles.size());
+  CUDA_CHECK(cudaMemcpy(plan->d_tiles.p, all_tiles.data(), all_tiles.size() * sizeof(TileDesc),
+                        cudaMemcpyHostToDevice));
+  return plan;
+}
+
+static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
+                       int64_t ldy, int y_dtype, float scale, cudaStream_t stream) {
+  const atmm_registry* reg = p->reg;
+  if (p->generation != reg->generation) fail(ATMM_ERR_CONFIG, "plan is stale: the registry changed after the plan was built");
+  if (layer < 0 || layer >= reg->L) {
+    fail(ATMM_ERR_CONFIG, "layer index " + std::to_string(layer) + " out of range (L=" + std::to_string(reg->L) + ")");
+  }
+  if (y_dtype != ATMM_BF16 && y_dtype != ATMM_F32) fail(ATMM_ERR_CONFIG, "y_dtype must be ATMM_BF16 or ATMM_F32");
+  if (!x || !y) fail(ATMM_ERR_SHAPE, "null X or Y");
+  if (ldx < reg->d_in || ldx % 8 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0) {
+    fail(ATMM_ERR_SHAPE, "X must be 16-byte aligned with ldx >= d_in and ldx % 8 == 0");
+  }
+  const int64_t ysz = y_dtype == ATMM_BF16 ? 2 : 4;
+  if (ldy < reg->d_out || (ldy * ysz) % 16 != 0 || reinterpret_cast<uintptr_t>(y) % 16 != 0) {
+    fail(ATMM_ERR_SHAPE, "Y must be 16-byte aligned with ldy >= d_out and 16-byte row stride");
+  }
+  const CUtensorMap tmap = make_x_map(x, p->n, reg->d_in, ldx);
+  for (const LaunchGroup& g : p->groups) {
+    BypassParams bp{};
+    bp.tiles = p->d_tiles.p + g.tile_offset;
+    bp.row_index = p->d_rows.p;
+    bp.slots = reg->d_slots.p;
+    bp.y = y;
+    bp.ldy = ldy;
+    bp.d_in = static_cast<int32_t>(reg->d_in);
+    bp.d_out = static_cast<int32_t>(reg->d_out);
+    bp.layer = static_cast<int32_t>(layer);
+    bp.scale = scale;
+    bp.stages = g.stages;
+    bp.bn = g.bn;
+    bp.stage_bytes = g.stage_bytes;
+    bp.red_rows = g.red_rows;
+    bp.r_pad_max = g.r_pad_max;
+    bp.off_red = g.off_red;
+    bp.off_mid = g.off_mid;
+    bp.off_bar = g.off_bar;
+    bp.tmem_cols = g.tmem_cols;
+    const cudaError_t e = launch_bypass(y_dtype, tmap, bp, g.cluster, static_cast<int>(g.num_tiles), g.smem, stream);
+    if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
+  }
+}
+
+// W = beta*W + alpha * A . B on the merge kernel; A/B in registry layouts.
+static void run_merge(const uint16_t* a_t, const uint16_t* b_t, int64_t m, int64_t n,
+                      int64_t k_pad, void* w, int64_t ldw, int w_dtype, float alpha, float beta,
+                      cudaStream_t stream) {
+  MergeParams mp{};
+  mp.a_t = a_t;
+  mp.b_t = b_t;
+  mp.w = w;
+  mp.ldw = ldw;
+  mp.m = static_cast<int32_t>(m);
+  mp.n = static_cast<int32_t>(n);
+  mp.k_pad = static_cast<int32_t>(k_pad);
+  mp.bn = k_pad <= 64 ? 256 : 128;
+  mp.num_mtiles = static_cast<int32_t>((m + kTileM - 1) / kTileM);
+  mp.num_nchunks = static_cast<int32_t>((round_up(n, 32) + mp.bn - 1) / mp.bn);
+  mp.alpha = alpha;
+  mp.beta = beta;
+  const int64_t a_bytes = int64_t(kTileM) * k_pad * 2;
+  mp.b_stage_bytes = static_cast<uint32_t>(round_up(int64_t(mp.bn) * k_pad * 2, 1024));
+  int stages = 4;
+  auto total = [&](int s) {
+    return size_t(1024 + a_bytes + int64_t(s) * mp.b_stage_bytes + round_up((2 * s + 6) * 8 + 8, 16));
+  };
+  while (stages > 2 && total(stages) > kSmemLimit) --stages;
+  mp.stages = stages;
+  mp.off_b = static_cast<uint32_t>(a_bytes);
+  mp.off_bar = static_cast<uint32_t>(a_bytes + int64_t(stages) * mp.b_stage_bytes);
+  int32_t cols = 32;
+  while (cols < 2 * mp.bn) cols <<= 1;
+  mp.tmem_cols = static_cast<uint32_t>(cols);
+  size_t smem = total(stages);
+  const int max_co = std::max(1, 512 / cols);
+  while (static_cast<int>(kSmemPerSM / (smem + 1024)) > max_co) smem += 4096;
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = int64_t(mp.num_mtiles) * mp.num_nchunks;
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, sms));
+  const cudaError_t e = launch_merge(w_dtype, mp, grid, smem, stream);
+  if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("merge launch failed: ") + cudaGetErrorString(e));
+}
+
+}  // namespace atmm
+
+extern "C" {
+
+int atmm_device_count(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < count; ++d) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10) ++ok;
+  }
+  return ok;
+}
+
+int atmm_registry_create(int device, int64_t num_layers, int64_t d_in, int64_t d_out,
+                         atmm_registry** out) {
+  return guarded([&] {
+    if (!out) fail(ATMM_ERR_CONFIG, "null output");
+    if (num_layers < 1 || d_in < 1 || d_out < 1) fail(ATMM_ERR_SHAPE, "registry dimensions must be >= 1");
+    require_device(device);
+    auto r = std::make_unique<atmm_registry>();
+    r->device = device;
+    r->L = num_layers;
+    r->d_in = d_in;
+    r->d_out = d_out;
+    r->d_in_pad = round_up(d_in, 128);
+    r->d_out_pad = round_up(d_out, 32);
+    *out = r.release();
+  });
+}
+
+void atmm_registry_destroy(atmm_registry* r) { delete r; }
+
+int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const float* down,
+                      const float* up, float scale) {
+  return guarded([&] {
+    if (!r) fail(ATMM_ERR_CONFIG, "null registry");
+    if (rank < 1 || rank > kMaxRank) fail(ATMM_ERR_CONFIG, "adapter rank must be in [1, 128]");
+    if (!down || !up) fail(ATMM_ERR_SHAPE, "null factors");
+    DeviceGuard g(r->device);
+    const int64_t r_pad = round_up(rank, 16);
+    const size_t dn = static_cast<size_t>(r->d_in_pad * r_pad);
+    const size_t un = static_cast<size_t>(r->d_out_pad * r_pad);
+    std::vector<uint16_t> hd(dn * static_cast<size_t>(r->L)), hu(un * static_cast<size_t>(r->L));
+    for (int64_t l = 0; l < r->L; ++l) {
+      pack_down_t(down + l * r->d_in * rank, r->d_in, rank, rank, r->d_in_pad, r_pad, hd.data() + l * dn);
+      pack_up_t(up + l * rank * r->d_out, rank, r->d_out, r->d_out, r->d_out_pad, r_pad, hu.data() + l * un);
+    }
+    Slot s;
+    s.id = adapter_id;
+    s.rank = rank;
+    s.r_pad = r_pad;
+    s.scale = scale;
+    s.live = true;
+    CUDA_CHECK(cudaMalloc(&s.down_t, hd.size() * 2));
+    CUDA_CHECK(cudaMalloc(&s.up_t, hu.size() * 2));
+    CUDA_CHECK(cudaMemcpy(s.down_t, hd.data(), hd.size() * 2, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(s.up_t, hu.data(), hu.size() * 2, cudaMemcpyHostToDevice));
+    auto it = r->slot_of.find(adapter_id);
+    if (it != r->slot_of.end()) {
+      Slot& old = r->slots[static_cast<size_t>(it->second)];
+      cudaFree(old.down_t);
+      cudaFree(old.up_t);
+      old = s;
+    } else {
+      int idx = -1;
+      for (size_t i = 0; i < r->slots.size(); ++i) {
+        if (!r->slots[i].live) {
+          idx = static_cast<int>(i);
+          break;
+        }
+      }
+      if (idx < 0) {
+        idx = static_cast<int>(r->slots.size());
+        r->slots.push_back(s);
+      } else {
+        r->slots[static_cast<size_t>(idx)] = s;
+      }
+      r->slot_of[adapter_id] = idx;
+    }
+    r->sync_slots();
+  });
+}
+
+int atmm_registry_remove(atmm_registry* r, int32_t adapter_id) {
+  return guarded([&] {
+    if (!r) fail(ATMM_ERR_CONFIG, "null registry");
+    auto it = r->slot_of.find(adapter_id);
+    if (it == r->slot_of.end()) fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(adapter_id));
+    DeviceGuard g(r->device);
+    Slot& s = r->slots[static_cast<size_t>(it->second)];
+    cudaFree(s.down_t);
+    cudaFree(s.up_t);
+    s = Slot{};
+    r->slot_of.erase(it);
+    r->sync_slots();
+  });
+}
+
+int atmm_registry_contains(const atmm_registry* r, int32_t adapter_id) {
+  return r && r->slot_of.count(adapter_id) ? 1 : 0;
+}
+
+int atmm_registry_rank(const atmm_registry* r, int32_t adapter_id, int64_t* rank) {
+  return guarded([&] {
+    if (!r || !rank) fail(ATMM_ERR_CONFIG, "null registry or output");
+    *rank = r->at(adapter_id).rank;
+  });
+}
+
+int atmm_registry_bytes(const atmm_registry* r, int64_t* bytes) {
+  return guarded([&] {
+    if (!r || !bytes) fail(ATMM_ERR_CONFIG, "null registry or output");
+    int64_t b = 0;
+    for (const auto& s : r->slots) {
+      if (s.live) b += r->L * (r->d_in_pad + r->d_out_pad) * s.r_pad * 2;
+    }
+    *bytes = b;
+  });
+}
+
+int atmm_plan_create(atmm_registry* r, const int32_t* assignment, int64_t n, const atmm_table* table,
+                     atmm_plan** out) {
+  return guarded([&] {
+    if (!r || !out) fail(ATMM_ERR_CONFIG, "null registry or output");
+    const TilingTable* t = table ? &table->t : nullptr;
+    *out = build_plan(r, assignment, n, t, nullptr).release();
+  });
+}
+
+void atmm_plan_destroy(atmm_plan* p) {
+  if (!p) return;
+  DeviceGuard g(p->reg->device);
+  delete p;
+}
+
+int atmm_plan_routing(const atmm_plan* p, int32_t* seg_adapter, int64_t* seg_offsets,
+                      int64_t* row_index, int64_t* num_segments) {
+  return guarded([&] {
+    if (!p) fail(ATMM_ERR_CONFIG, "null plan");
+    // Read back what the kernels index with (row_index from HBM).
+    DeviceGuard g(p->reg->device);
+    std::vector<int32_t> rows(static_cast<size_t>(p->n));
+    CUDA_CHECK(cudaMemcpy(rows.data(), p->d_rows.p, rows.size() * 4, cudaMemcpyDeviceToHost));
+    if (seg_adapter) std::copy(p->bp.seg_adapter.begin(), p->bp.seg_adapter.end(), seg_adapter);
+    if (seg_offsets) std::copy(p->bp.seg_offsets.begin(), p->bp.seg_offsets.end(), seg_offsets);
+    if (row_index) std::copy(rows.begin(), rows.end(), row_index);
+    if (num_segments) *num_segments = static_cast<int64_t>(p->bp.seg_adapter.size());
+  });
+}
+
+int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64_t* ctas) {
+  return guarded([&] {
+    if (!p) fail(ATMM_ERR_CONFIG, "null plan");
+    int64_t t = 0;
+    for (const auto& g : p->groups) t += g.num_tiles;
+    if (launches) *launches = static_cast<int64_t>(p->groups.size());
+    if (tiles) *tiles = t;
+    if (ctas) *ctas = p->total_ctas;
+  });
+}
+
+int atmm_bypass_apply(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
+                      int64_t ldy, int y_dtype, float scale, void* stream) {
+  return guarded([&] {
+    if (!p) fail(ATMM_ERR_CONFIG, "null plan");
+    DeviceGuard g(p->reg->device);
+    apply_plan(p, layer, x, ldx, y, ldy, y_dtype, scale, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atmm_run_bypass_host(atmm_registry* r, const float* x, int64_t n, const int32_t* assignment,
+                         int64_t layer, const atmm_table* table, float* out) {
+  return guarded([&] {
+    if (!r || !x || !out) fail(ATMM_ERR_CONFIG, "null registry or buffer");
+    DeviceGuard g(r->device);
+    const TilingTable* t = table ? &table->t : nullptr;
+    auto plan = build_plan(r, assignment, n, t, nullptr);
+    const int64_t ldx = round_up(r->d_in, 8), ldy = round_up(r->d_out, 8);
+    DevBuf<float> xf(static_cast<size_t>(n * r->d_in));
+    DevBuf<uint16_t> xb(static_cast<size_t>(n * ldx));
+    DevBuf<float> y(static_cast<size_t>(n * ldy));
+    CUDA_CHECK(cudaMemcpy(xf.p, x, xf.n * 4, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemset(xb.p, 0, xb.n * 2));
+    CUDA_CHECK(cudaMemset(y.p, 0, y.n * 4));
+    CUDA_CHECK(launch_f32_to_bf16(xf.p, xb.p, n, r->d_in, r->d_in, ldx, nullptr));
+    apply_plan(plan.get(), layer, xb.p, ldx, y.p, ldy, ATMM_F32, 1.0f, nullptr);
+    CUDA_CHECK(cudaMemcpy2D(out, r->d_out * 4, y.p, ldy * 4, r->d_out * 4, n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int atmm_bypass_residual_host_bf16(const atmm_plan* p, int64_t layer, const uint16_t* x_host,
+                                   uint16_t* y_host, float scale, void* stream) {
+  return guarded([&] {
+    if (!p || !x_host || !y_host) fail(ATMM_ERR_CONFIG, "null plan or buffer");
+    const atmm_registry* r = p->reg;
+    DeviceGuard g(r->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // Device staging owned by the plan's registry device; sized per call.
+    thread_local DevBuf<uint16_t> xs, ys;
+    thread_local int dev_of_bufs = -1;
+    const int64_t ldx = round_up(r->d_in, 8), ldy = round_up(r->d_out, 8);
+    const size_t nx = static_cast<size_t>(p->n * ldx), ny = static_cast<size_t>(p->n * ldy);
+    if (dev_of_bufs != r->device || xs.n < nx) xs.alloc(nx);
+    if (dev_of_bufs != r->device || ys.n < ny) ys.alloc(ny);
+    dev_of_bufs = r->device;
+    CUDA_CHECK(cudaMemcpy2DAsync(xs.p, ldx * 2, x_host, r->d_in * 2, r->d_in * 2, p->n, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpy2DAsync(ys.p, ldy * 2, y_host, r->d_out * 2, r->d_out * 2, p->n, cudaMemcpyHostToDevice, s));
+    apply_plan(p, layer, xs.p, ldx, ys.p, ldy, ATMM_BF16, scale, s);
+    CUDA_CHECK(cudaMemcpy2DAsync(y_host, r->d_out * 2, ys.p, ldy * 2, r->d_out * 2, p->n, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* w, int64_t ldw,
+                     int w_dtype, float sign, void* stream) {
+  return guarded([&] {
+    if (!r || !w) fail(ATMM_ERR_CONFIG, "null registry or W");
+    if (layer < 0 || layer >= r->L) {
+      fail(ATMM_ERR_CONFIG, "layer index " + std::to_string(layer) + " out of range (L=" + std::to_string(r->L) + ")");
+    }
+    if (w_dtype != ATMM_BF16 && w_dtype != ATMM_F32) fail(ATMM_ERR_CONFIG, "w_dtype must be ATMM_BF16 or ATMM_F32");
+    const int64_t wsz = w_dtype == ATMM_BF16 ? 2 : 4;
+    if (ldw < r->d_out || (ldw * wsz) % 16 != 0 || reinterpret_cast<uintptr_t>(w) % 16 != 0) {
+      fail(ATMM_ERR_SHAPE, "W must be 16-byte aligned with ldw >= d_out and a 16-byte row stride");
+    }
+    const Slot& s = r->at(adapter_id);
+    DeviceGuard g(r->device);
+    run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
+              r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atmm_delta_w_host(atmm_registry* r, int32_t adapter_id, int64_t layer, float* out) {
+  return guarded([&] {
+    if (!r || !out) fail(ATMM_ERR_CONFIG, "null registry or output");
+    if (layer < 0 || layer >= r->L) {
+      fail(ATMM_ERR_CONFIG, "layer index " + std::to_string(layer) + " out of range (L=" + std::to_string(r->L) + ")");
+    }
+    const Slot& s = r->at(adapter_id);
+    DeviceGuard g(r->device);
+    const int64_t ldw = round_up(r->d_out, 8);
+    DevBuf<float> w(static_cast<size_t>(r->d_in * ldw));
+    run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
+              r->d_out, s.r_pad, w.p, ldw, ATMM_F32, s.scale, 0.0f, nullptr);
+    CUDA_CHECK(cudaMemcpy2D(out, r->d_out * 4, w.p, ldw * 4, r->d_out * 4, r->d_in, cudaMemcpyDeviceToHost));
+  });
+}
+
+int atmm_multiply_host(const float* a, int64_t m, int64_t k, const float* b, int64_t n, float* c,
+                       const int32_t cfg[6]) {
+  return guarded([&] {
+    if (!cfg) fail(ATMM_ERR_CONFIG, "null config");
+    TilingConfig tc;
+    std::copy(cfg, cfg + 6, tc.e.begin());
+    if (m < 1 || k < 1 || n < 1) fail(ATMM_ERR_SHAPE, "atmm_multiply: matrix dimensions must be >= 1");
+    if (!tc.structurally_valid()) fail(ATMM_ERR_CONFIG, "invalid tiling config " + tc.str());
+    if (!a || !b || !c) fail(ATMM_ERR_SHAPE, "null operand");
+    require_device(0);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // K is consumed in chunks of 128 (the merge kernel keeps a whole K chunk
+    // of A on chip); chunks accumulate into the fp32 output.
+    const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 32), ldc = round_up(n, 8);
+    DevBuf<float> cd(static_cast<size_t>(m * ldc));
+    for (int64_t k0 = 0; k0 < k; k0 += 128) {
+      const int64_t kc = std::min<int64_t>(128, k - k0);
+      const int64_t kp = round_up(kc, 16);
+      std::vector<float> at(static_cast<size_t>(m * kc)), bt(static_cast<size_t>(kc * n));
+      for (int64_t i = 0; i < m; ++i) std::memcpy(&at[i * kc], a + i * k + k0, kc * 4);
+      std::memcpy(bt.data(), b + k0 * n, kc * n * 4);
+      std::vector<uint16_t> ha(static_cast<size_t>(m_pad * kp)), hb(static_cast<size_t>(n_pad * kp));
+      pack_down_t(at.data(), m, kc, kc, m_pad, kp, ha.data());
+      pack_up_t(bt.data(), kc, n, n, n_pad, kp, hb.data());
+      DevBuf<uint16_t> da(ha.size()), db(hb.size());
+      CUDA_CHECK(cudaMemcpy(da.p, ha.data(), ha.size() * 2, cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(db.p, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
+      run_merge(da.p, db.p, m, n, kp, cd.p, ldc, ATMM_F32, 1.0f, k0 == 0 ? 0.0f : 1.0f, nullptr);
+      CUDA_CHECK(cudaDeviceSynchronize());
+    }
+    CUDA_CHECK(cudaMemcpy2D(c, n * 4, cd.p, ldc * 4, n * 4, m, cudaMemcpyDeviceToHost));
+  });
+}
+
+int atmm_bench_launches(int device, int64_t m, int64_t d_in, int64_t rank, int64_t d_out,
+                        const int32_t* launches, int64_t num_launches, int trials,
+                        int64_t* median_ns) {
+  return guarded([&] {
+    if (trials < 3) fail(ATMM_ERR_CONFIG, "benchmark needs trials >= 3");
+    if (!launches || !median_ns || num_launches < 1) fail(ATMM_ERR_CONFIG, "null launches or output");
+    require_device(device);
+    DeviceGuard g(device);
+    atmm_registry reg;
+    reg.device = device;
+    reg.L = 1;
+    reg.d_in = d_in;
+    reg.d_out = d_out;
+    reg.d_in_pad = round_up(d_in, 128);
+    reg.d_out_pad = round_up(d_out, 32);
+    {
+      // Synthetic factors (values do not affect timing).
+      std::vector<float> dn(static_cast<size_t>(d_in * rank)), up(static_cast<size_t>(rank * d_out));
+      for (size_t i = 0; i < dn.size(); ++i) dn[i] = 0.001f * static_cast<float>((i * 7919) % 61) - 0.03f;
+      for (size_t i = 0; i < up.size(); ++i) up[i] = 0.001f * static_cast<float>((i * 104729) % 53) - 0.026f;
+      atmm_registry* rp = &reg;
+      const int st = atmm_registry_put(rp, 1, rank, dn.data(), up.data(), 1.0f);
+      if (st != ATMM_OK) fail(st, atmm_last_error());
+    }
+    std::vector<int32_t> assignment(static_cast<size_t>(m), 1);
+    const int64_t ldx = round_up(d_in, 8), ldy = round_up(d_out, 8);
+    DevBuf<uint16_t> x(static_cast<size_t>(m * ldx)), y(static_cast<size_t>(m * ldy));
+    CUDA_CHECK(cudaMemset(x.p, 0, x.n * 2));
+    CUDA_CHECK(cudaMemset(y.p, 0, y.n * 2));
+    DevBuf<uint8_t> flush(size_t(256) << 20);
+    cudaStream_t s;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    CUDA_CHECK(cudaEventCreate(&e0));
+    CUDA_CHECK(cudaEventCreate(&e1));
+    for (int64_t c = 0; c < num_launches; ++c) {
+      median_ns[c] = std::numeric_limits<int64_t>::max();
+      LaunchCfg lc{launches[4 * c], launches[4 * c + 1], launches[4 * c + 2], launches[4 * c + 3]};
+      try {
+        auto plan = build_plan(&reg, assignment.data(), m, nullptr, &lc);
+        std::vector<int64_t> samples;
+        for (int t = 0; t < trials + 1; ++t) {  // first iteration is the warm-up
+          CUDA_CHECK(cudaMemsetAsync(flush.p, t & 0xff, flush.n, s));
+          CUDA_CHECK(cudaEventRecord(e0, s));
+          apply_plan(plan.get(), 0, x.p, ldx, y.p, ldy, ATMM_BF16, 1.0f, s);
+          CUDA_CHECK(cudaEventRecord(e1, s));
+          CUDA_CHECK(cudaEventSynchronize(e1));
+          float ms = 0.f;
+          CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+          if (t > 0) samples.push_back(static_cast<int64_t>(ms * 1e6));
+        }
+        std::sort(samples.begin(), samples.end());
+        median_ns[c] = samples[samples.size() / 2];
+      } catch (const Failure&) {
+        cudaGetLastError();
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+  });
+}
+
+}  // extern "C"
