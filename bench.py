@@ -1,0 +1,482 @@
+#!/usr/bin/env python3
+"""bench.py -- ATMM batched-LoRA benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2|cfg1|cfg3|cfg5|cfg4]
+
+A step is ONE fused bypass pass  Y[rows] += (X[rows] . down_a) . up_a  over
+one batch (default cfg2 = BASELINE.json configs[1]: hidden 4096, rank 16,
+16 adapters, 512 tokens, bf16, 1 x B200).  The workload fits in L2, so steps
+rotate over 32 layer buffer sets (X, Y and adapter factors per layer,
+> 2 x L2 in total).  K steps are captured in one CUDA graph and replayed
+inside the timed region (barrier + synchronize on both sides, CUDA events,
+max over ranks).  Under torchrun each rank runs its own batch of requests
+(request sharding, no collective on the data path): scaling = weak.
+
+One JSON line on rank 0 with value (TFLOP/s, whole job), ms_per_step, the
+dominant kernel's roofline, the CPU baseline (the reference compiled from
+its own headers, oracle/_ref, on a bounded sample), the end-to-end number
+through the C ABI with pinned host buffers, and SM clocks sampled during
+the run.  --impl reference times the reference CPU implementation instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ATMM batched-LoRA TFLOP/s and µs/batch at Qwen-VL-7B shapes vs CPU ref"
+L2_BYTES = 126 * 1024 * 1024
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (GB/s)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0, help="bounded CPU baseline sample (seconds)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--soak-s", type=float, default=1.0, help="load before the timed region while clocks are sampled")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+def committed_traffic(config: str):
+    """dram bytes per launch of the bypass kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_bypass_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config, {}).get("dram_bytes_per_launch")
+    return None
+
+
+# ------------------------------------------------------------ clocks ------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() in ("active", "0x1", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "window": "soak + timed region"}
+
+
+# ------------------------------------------------------ distributed -------
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if n_gpus > 1 and world == 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# -------------------------------------------------- reference (CPU) -------
+def reference_batch_fn(w, seed: int):
+    """Returns (fn, flops): fn() runs the reference's run_bypass + add_inplace
+    (model.hpp:239-241) on one fp32 batch and returns elapsed seconds."""
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    rng = np.random.default_rng(seed)
+    adapters = {}
+    for a, r in w.ranks.items():
+        s = 1.0 / np.sqrt(r)
+        adapters[a] = (rng.uniform(-s, s, (w.d_in, r)).astype(np.float32),
+                       rng.uniform(-s, s, (r, w.d_out)).astype(np.float32))
+    ctx = ref.ctx(w.d_in, adapters)
+    x = rng.uniform(-1, 1, (w.tokens, w.d_in)).astype(np.float32)
+    y = np.zeros((w.tokens, w.d_out), np.float32)
+    a = np.ascontiguousarray(w.assignment, np.int32)
+
+    def fn():
+        return ctx.bypass_residual(x, a, y) * 1e-9
+
+    return fn, w.flops()
+
+
+def run_reference_parallel(w, threads: int, seconds: float = None, steps: int = None):
+    """`threads` independent request batches through the reference on as
+    many host cores (ctypes releases the GIL).  Returns (wall seconds, batches)."""
+    fns = [reference_batch_fn(w, 100 + t)[0] for t in range(threads)]
+    counts = [0] * threads
+    stop = threading.Event()
+
+    def worker(i):
+        if steps is not None:
+            for _ in range(steps):
+                fns[i]()
+                counts[i] += 1
+        else:
+            while not stop.is_set():
+                fns[i]()
+                counts[i] += 1
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    if steps is None:
+        time.sleep(seconds)
+        stop.set()
+    for t in ths:
+        t.join()
+    return time.perf_counter() - t0, sum(counts)
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def impl_reference(args, w):
+    rank, world, _ = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    threads = cpu_threads()
+    for _ in range(max(args.warmup, 1)):
+        run_reference_parallel(w, threads, steps=1)
+    elapsed, batches = run_reference_parallel(w, threads, steps=args.steps)
+    flops = w.flops() * batches
+    value = flops / elapsed / 1e12
+    cfg = {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens, "adapters": len(w.ranks),
+           "ranks": sorted(set(w.ranks.values())), "dtype_ref": "f32"}
+    sample = (f"{args.steps} steps x {threads} concurrent {w.name} batches (one per host thread) through the "
+              f"reference's run_bypass + add_inplace, fp32")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------- ours (GPU) ------
+def impl_ours_bypass(args, w):
+    import torch
+
+    rank, world, local = dist_setup(args.gpus)
+    import paper_2411_00915_b200 as atmm
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    step_bytes = w.bytes(2)
+    layers = max(2, int(np.ceil(2.5 * L2_BYTES / step_bytes)))
+    layers = min(layers, 64)
+    rng = np.random.default_rng(1234 + rank)
+    # Registry: every adapter, every layer (factors differ per layer).
+    reg = atmm.AdapterRegistry(layers, w.d_in, w.d_out, device=local)
+    for a, r in w.ranks.items():
+        s = 1.0 / np.sqrt(r)
+        down = rng.uniform(-s, s, (layers, w.d_in, r)).astype(np.float32)
+        up = rng.uniform(-s, s, (layers, r, w.d_out)).astype(np.float32)
+        reg.put(a, down, up)
+    assignment = w.assignment if rank == 0 else np.random.default_rng(rank).permutation(w.assignment)
+    plan = atmm.BypassPlan(reg, assignment)
+    launches_per_step, tiles, ctas = plan.stats()
+    xs = [torch.empty(w.tokens, w.d_in, dtype=torch.bfloat16, device=dev).uniform_(-1, 1) for _ in range(layers)]
+    ys = [torch.empty(w.tokens, w.d_out, dtype=torch.bfloat16, device=dev).uniform_(-1, 1) for _ in range(layers)]
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(i, s):
+        l = i % layers
+        plan.apply(xs[l], ys[l], layer=l, scale=1.0, stream=s)
+
+    # warm-up (untimed), eager
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i, stream)
+    torch.cuda.synchronize()
+
+    # Capture exactly K steps into one graph.
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+        for i in range(args.steps):
+            step(i, stream)
+    # Soak graph for clock steady state.
+    soak_steps = min(args.steps, 4 * layers)
+    gs = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gs, stream=stream, capture_error_mode="thread_local"):
+        for i in range(soak_steps):
+            step(i, stream)
+    g.replay()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_end = time.perf_counter() + args.soak_s
+    with torch.cuda.stream(stream):
+        while time.perf_counter() < t_end:
+            gs.replay()
+            stream.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+    ms_local = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms_local, world)
+
+    flops_step = w.flops()
+    value = world * flops_step * args.steps / (ms * 1e-3) / 1e12
+    ms_per_step = ms / args.steps
+    # dominant kernel = the fused bypass kernel (the only kernel in the graph)
+    kernel_us = ms_local * 1e3 / (args.steps * launches_per_step)
+    hbm_peak, peak_kind = measured_peaks()
+    achieved_gbs = step_bytes / launches_per_step / (kernel_us * 1e-6) / 1e9
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(w.tokens, w.d_in, dtype=torch.bfloat16).uniform_(-1, 1).pin_memory()
+        yh = torch.zeros(w.tokens, w.d_out, dtype=torch.bfloat16).pin_memory()
+        xh_np = xh.view(torch.int16).numpy().view(np.uint16)
+        yh_np = yh.view(torch.int16).numpy().view(np.uint16)
+        e2e_steps = max(3, min(args.steps, 50))
+        for i in range(2):
+            plan.residual_host_bf16(xh_np, yh_np, layer=i % layers, stream=stream)
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            plan.residual_host_bf16(xh_np, yh_np, layer=i % layers, stream=stream)
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        e2e = {"value": world * flops_step * e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(w.tokens * (w.d_in + w.d_out) * 2),
+               "d2h_bytes_per_step": int(w.tokens * w.d_out * 2),
+               "us_per_batch": e2e_s / e2e_steps * 1e6, "steps": e2e_steps,
+               "path": "atmm_bypass_residual_host_bf16 (pinned host X,Y -> H2D, fused kernel, D2H Y)"}
+
+    # ---- CPU baseline: the reference itself, bounded sample, rank 0, N=1 ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = cpu_threads()
+            run_reference_parallel(w, threads, steps=1)
+            el, batches = run_reference_parallel(w, threads, seconds=args.cpu_sample_s)
+            cpu = {"value": w.flops() * batches / el / 1e12, "unit": "TFLOP/s", "cores": threads,
+                   "kind": "reference",
+                   "sample": f"{batches} {w.name} batches in {el:.1f} s, {threads} concurrent batches "
+                             f"(one per host thread) through the reference run_bypass + add_inplace (fp32), "
+                             f"oracle/_ref built from the reference headers"}
+        except FileNotFoundError as e:
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "us_per_batch": ms_per_step * 1e3,
+            "config": {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens,
+                       "adapters": len(w.ranks), "ranks": sorted(set(w.ranks.values())),
+                       "segment_rows": sorted(set(w.lengths.values()))[:4],
+                       "parallelism": f"request-sharded x{world} (no collective)",
+                       "l2": f"inputs rotate over {layers} layer buffer sets ({layers * step_bytes / 2**20:.0f} MiB "
+                             f"> 2x L2); K steps in one CUDA graph",
+                       "launches_per_step": launches_per_step, "tiles": tiles, "ctas": ctas,
+                       "launch_groups": plan.describe()},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm_peak, "traffic": committed_traffic(w.name),
+                         "peak_kind": peak_kind, "kernel": "atmm_bypass_kernel",
+                         "kernel_us": kernel_us, "algorithmic_bytes_per_launch": step_bytes // launches_per_step},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": int(args.steps * launches_per_step),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def impl_ours_merge(args):
+    """cfg4: merge W(4096 x 11008, bf16) += down.up for all 32 layers per step."""
+    import torch
+
+    rank, world, local = dist_setup(args.gpus)
+    import paper_2411_00915_b200 as atmm
+    from paper_2411_00915_b200.workloads import MergeWorkload
+
+    mw = MergeWorkload()
+    dev = torch.device("cuda", local)
+    reg = atmm.AdapterRegistry(mw.layers, mw.d_in, mw.d_out, device=local)
+    rng = np.random.default_rng(5 + rank)
+    s = 1.0 / np.sqrt(mw.rank)
+    reg.put(1, rng.uniform(-s, s, (mw.layers, mw.d_in, mw.rank)).astype(np.float32),
+            rng.uniform(-s, s, (mw.layers, mw.rank, mw.d_out)).astype(np.float32))
+    W = torch.empty(mw.layers, mw.d_in, mw.d_out, dtype=torch.bfloat16, device=dev).uniform_(-0.02, 0.02)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(i):
+        sign = 1.0 if i % 2 == 0 else -1.0  # merge, unmerge, merge, ...
+        for l in range(mw.layers):
+            atmm.merge_into(reg, 1, l, W[l], sign=sign, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+        for i in range(args.steps):
+            step(i)
+    g.replay()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_end = time.perf_counter() + args.soak_s
+    while time.perf_counter() < t_end:
+        g.replay()
+        torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    per_step_ms = ms / args.steps
+    hbm_peak, peak_kind = measured_peaks()
+    bytes_step = mw.bytes(2)
+    achieved = bytes_step / (per_step_ms * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "ATMM merge/unmerge W +- s.down.up, all 32 layers (mode switch) TFLOP/s", "value":
+                world * mw.flops() / (per_step_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "cfg4", "d_in": mw.d_in, "d_out": mw.d_out, "rank": mw.rank, "layers": mw.layers,
+                       "w_dtype": "bf16", "l2": "W of 32 layers = 2.9 GB >> L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "atmm_merge_kernel"},
+            "clocks": clocks, "gpu_launches": args.steps * mw.layers}), flush=True)
+
+
+def main():
+    args = parse_args()
+    from paper_2411_00915_b200.workloads import bypass_config
+
+    if args.config == "cfg4":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "cfg4 reference arm: use tests/ or profiles/"}))
+            return
+        impl_ours_merge(args)
+        return
+    w = bypass_config(args.config)
+    if args.impl == "reference":
+        impl_reference(args, w)
+    else:
+        impl_ours_bypass(args, w)
+
+
+if __name__ == "__main__":
+    main()

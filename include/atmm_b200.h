@@ -152,6 +152,9 @@ void atmm_plan_destroy(atmm_plan* p);
  * seg_adapter[S], seg_offsets[S+1], row_index[n]. */
 int atmm_plan_routing(const atmm_plan* p, int32_t* seg_adapter, int64_t* seg_offsets,
                       int64_t* row_index, int64_t* num_segments);
+/* JSON description of the resolved launch groups (cluster, bn, stages,
+ * ring depths, shared memory, TMEM columns) into buf (NUL-terminated). */
+int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap);
 /* Number of kernel launches / cluster tiles / CTAs the plan issues. */
 int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64_t* ctas);
 

@@ -55,6 +55,7 @@ _SIGS = {
     "atmm_plan_destroy": (None, [c_void_p]),
     "atmm_plan_routing": (c_int, [c_void_p, i32p, i64p, i64p, i64p]),
     "atmm_plan_stats": (c_int, [c_void_p, i64p, i64p, i64p]),
+    "atmm_plan_describe": (c_int, [c_void_p, ctypes.c_char_p, c_size_t]),
     "atmm_bypass_apply": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int, c_float, c_void_p]),
     "atmm_run_bypass_host": (c_int, [c_void_p, f32p, c_int64, i32p, c_int64, c_void_p, f32p]),
     "atmm_bypass_residual_host_bf16": (c_int, [c_void_p, c_int64, u16p, u16p, c_float, c_void_p]),

@@ -327,6 +327,13 @@ class BypassPlan:
         _check(lib.atmm_plan_routing(self._h, _p(seg, i32p), _p(off, i64p), _p(rows, i64p), ctypes.byref(S)))
         return seg[: S.value].copy(), off[: S.value + 1].copy(), rows
 
+    def describe(self) -> list:
+        import json
+
+        buf = ctypes.create_string_buffer(8192)
+        _check(lib.atmm_plan_describe(self._h, buf, 8192))
+        return json.loads(buf.value.decode())
+
     def stats(self) -> Tuple[int, int, int]:
         a, b, c = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
         _check(lib.atmm_plan_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))

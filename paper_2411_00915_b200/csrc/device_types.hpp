@@ -8,18 +8,23 @@ namespace atmm {
 
 constexpr int kTileM = 128;   // tcgen05 M (TMEM lanes); a tile carries <= 128 valid rows
 constexpr int kBK = 64;       // K block per pipeline stage: one 128-byte swizzle row of bf16
-constexpr int kNUnit = 32;    // expand N granule (one tcgen05.ld 32x32b.x32)
+constexpr int kNUnit = 64;    // expand N granule (one 128-byte Y row slice of bf16)
 constexpr int kMaxRank = 128; // fused kernel limit on the LoRA rank
 constexpr int kMaxCluster = 16;
-constexpr int kBypassThreads = 192;  // w0 TMA producer, w1 MMA + TMEM, w2-5 epilogue
+constexpr int kBypassThreads = 256;  // w0,w7 X/down TMA, w1 MMA + TMEM, w2-5 epilogue, w6 up/Y TMA
 constexpr int kMergeThreads = 192;
 
-// One cluster tile: <= 128 rows of one segment (rows = row_index[row_begin ..]).
+// One cluster tile: <= 128 rows of one segment (rows = row_index[row_begin ..])
+// with its adapter's factor pointers inlined, so a CTA needs one table load.
 struct TileDesc {
+  const uint16_t* down_t;     // layer-0 base (see SlotDesc)
+  const uint16_t* up_t;
+  int64_t down_layer_stride;  // elements
+  int64_t up_layer_stride;
   int32_t row_begin;
   int32_t rows;
-  int32_t slot;
-  int32_t pad;
+  int32_t r_pad;
+  float scale;
 };
 
 // One registry slot (adapter), device resident.  Factors are bf16 in the
@@ -40,23 +45,43 @@ struct SlotDesc {
 struct BypassParams {
   const TileDesc* tiles;
   const int32_t* row_index;
-  const SlotDesc* slots;
+  const uint16_t* x;    // n x d_in bf16, 16-byte aligned rows
+  int64_t ldx;
   void* y;
   int64_t ldy;
+  int32_t n_rows;       // batch rows (an out-of-range row coordinate drops TMA stores)
   int32_t d_in;
   int32_t d_out;
   int32_t layer;
   float scale;
+  // shrink ring: stages x [A: a_bytes gathered X rows (128-byte swizzle) | B: 64 x r_pad down^T]
   int32_t stages;
-  int32_t bn;           // expand chunk (columns per tcgen05.mma), multiple of 32
-  int32_t stage_bytes;  // multiple of 1024
-  int32_t red_rows;     // rows per owner slot (ceil(tile_m / C))
+  int32_t stage_bytes;
+  int32_t a_bytes;
+  // up^T ring: ustages x (bn x r_pad bf16)
+  int32_t bn;           // expand chunk (columns per tcgen05.mma), multiple of 64
+  int32_t ustages;
+  int32_t ustage_bytes;
+  // Y ring: ny x (rows x 128 B), 128-byte swizzle
+  int32_t ny;
+  int32_t ycols;        // columns per Y ring buffer (64 bf16 / 32 fp32)
+  int32_t ybuf_bytes;
+  int32_t red_rows;     // rows per owner slot (ceil(tile rows / C))
   int32_t r_pad_max;
+  uint32_t off_up;
+  uint32_t off_y;
   uint32_t off_red;
   uint32_t off_mid;
   uint32_t off_bar;
   uint32_t tmem_cols;
+  int32_t y_vec;        // 1: Y rows 16-byte aligned -> 128-bit epilogue accesses
+  int32_t y_ring;       // 1: Y staged through the smem ring (cp.async in, coalesced stores out)
+  int32_t rep;          // replicas of the tile rows in the expand accumulator (128 / rows: 1, 2, 4)
+  int32_t nbuf;         // expand accumulator buffers in TMEM (tmem_cols / bn)
+  uint64_t* trace;      // debug: per-CTA phase timestamps (kTraceEvents each), or null
 };
+
+constexpr int kTraceEvents = 32;
 
 struct MergeParams {
   const uint16_t* a_t;  // down^T blocked (MN-major A): [kb][g][c][8x8], K = r_pad
@@ -76,6 +101,8 @@ struct MergeParams {
   uint32_t off_bar;
   uint32_t b_stage_bytes;
   uint32_t tmem_cols;
+  int32_t w_vec;        // 1: W rows 16-byte aligned -> 128-bit epilogue accesses
+  int32_t pad0;
 };
 
 }  // namespace atmm

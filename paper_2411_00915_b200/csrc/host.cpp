@@ -71,7 +71,7 @@ void TilingTable::insert(ShapeKey key, const TilingConfig& cfg, int64_t ns,
   e.measured_ns = ns;
   if (sm100) {
     if (sm100->tile_m < 1 || sm100->tile_m > 128 || sm100->cluster < 1 ||
-        sm100->cluster > 16 || sm100->bn < 32 || sm100->bn > 256 || sm100->bn % 32 != 0 ||
+        sm100->cluster > 16 || sm100->bn < 64 || sm100->bn > 256 || sm100->bn % 64 != 0 ||
         sm100->stages < 0 || sm100->stages > 8) {
       fail(ATMM_ERR_CONFIG, "invalid sm100 launch parameters");
     }
@@ -121,21 +121,22 @@ LaunchCfg launch_from_config(const TilingConfig& cfg, int64_t d_in) {
   l.tile_m = clamp_pow2_rows(cfg.e[0]);
   const int64_t ks = std::max<int64_t>(cfg.e[2], 64);
   l.cluster = static_cast<int32_t>(std::clamp<int64_t>((d_in + ks - 1) / ks, 1, 16));
-  l.bn = std::clamp(cfg.e[1] / 32 * 32, 32, 256);
+  l.bn = std::clamp(cfg.e[1] / 64 * 64, 64, 256);
   l.stages = 0;
   return l;
 }
 
 // Heuristic B200 launch when the table has no profile for the shape:
 // ~512-wide K slices per CTA (cluster of 8 at d = 4096), whole 128-row tiles,
-// expand chunks of 128 (rank >= 64) or 256 columns.
+// expand chunks of 128 (small segments, rank > 32) or 256 columns.
 LaunchCfg heuristic_launch(int64_t m, int64_t d_in, int64_t rank, int64_t d_out) {
-  (void)m;
   (void)d_out;
   LaunchCfg l;
   l.tile_m = 128;
   l.cluster = static_cast<int32_t>(std::clamp<int64_t>((d_in + 511) / 512, 1, 16));
-  l.bn = rank > 32 ? 128 : 256;
+  // Small segments are latency bound: 128-column chunks keep TMEM at 256
+  // columns so two CTAs fit per SM (see resolve_group).
+  l.bn = (m <= 64 || rank > 32) ? 128 : 256;
   l.stages = 0;
   return l;
 }

@@ -42,6 +42,22 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Debug phase trace: event 0 stores %globaltimer (ns, comparable across SMs)
+// in slot 31 and clock64 in slot 0; later events store clock64 (cheap).
+#define TRACE(ev)                                                                 \
+  do {                                                                            \
+    if (p.trace) {                                                                \
+      uint64_t* tr_ = p.trace + static_cast<size_t>(blockIdx.x) * kTraceEvents;    \
+      if ((ev) == 0) tr_[kTraceEvents - 1] = globaltimer();                       \
+      tr_[(ev)] = static_cast<uint64_t>(clock64());                               \
+    }                                                                             \
+  } while (0)
+
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
@@ -53,14 +69,14 @@ __device__ __forceinline__ uint32_t interleave_off(uint32_t i, uint32_t j, uint3
 
 // Y[row, col0 .. col0+32) += s * acc[0..32) ; fp32 math, one rounding.
 template <typename YT>
-__device__ __forceinline__ void epilogue_store32(YT* yrow, int col0, int d_out, float s,
+__device__ __forceinline__ void epilogue_store32(YT* yrow, int col0, int d_out, float s, bool vec,
                                                  const uint32_t (&acc)[32]);
 
 template <>
 __device__ __forceinline__ void epilogue_store32<__nv_bfloat16>(__nv_bfloat16* yrow, int col0,
-                                                                int d_out, float s,
+                                                                int d_out, float s, bool vec,
                                                                 const uint32_t (&acc)[32]) {
-  if (col0 + 32 <= d_out) {
+  if (vec && col0 + 32 <= d_out) {
     uint4* p = reinterpret_cast<uint4*>(yrow + col0);
     uint4 v[4];
 #pragma unroll
@@ -89,8 +105,8 @@ __device__ __forceinline__ void epilogue_store32<__nv_bfloat16>(__nv_bfloat16* y
 
 template <>
 __device__ __forceinline__ void epilogue_store32<float>(float* yrow, int col0, int d_out, float s,
-                                                        const uint32_t (&acc)[32]) {
-  if (col0 + 32 <= d_out) {
+                                                        bool vec, const uint32_t (&acc)[32]) {
+  if (vec && col0 + 32 <= d_out) {
     float4* p = reinterpret_cast<float4*>(yrow + col0);
     float4 v[8];
 #pragma unroll
@@ -114,11 +130,12 @@ __device__ __forceinline__ void epilogue_store32<float>(float* yrow, int col0, i
 // W[row, col0..+32) = beta*W + alpha*acc
 template <typename WT>
 __device__ __forceinline__ void merge_store32(WT* wrow, int col0, int n, float alpha, float beta,
-                                              const uint32_t (&acc)[32]);
+                                              bool vec, const uint32_t (&acc)[32]);
 template <>
 __device__ __forceinline__ void merge_store32<float>(float* wrow, int col0, int n, float alpha,
-                                                     float beta, const uint32_t (&acc)[32]) {
-  if (col0 + 32 <= n) {
+                                                     float beta, bool vec,
+                                                     const uint32_t (&acc)[32]) {
+  if (vec && col0 + 32 <= n) {
     float4* p = reinterpret_cast<float4*>(wrow + col0);
     float4 v[8];
     if (beta != 0.0f) {
@@ -148,9 +165,9 @@ __device__ __forceinline__ void merge_store32<float>(float* wrow, int col0, int 
 }
 template <>
 __device__ __forceinline__ void merge_store32<__nv_bfloat16>(__nv_bfloat16* wrow, int col0, int n,
-                                                             float alpha, float beta,
+                                                             float alpha, float beta, bool vec,
                                                              const uint32_t (&acc)[32]) {
-  if (col0 + 32 <= n) {
+  if (vec && col0 + 32 <= n) {
     uint4* p = reinterpret_cast<uint4*>(wrow + col0);
     uint4 v[4];
     if (beta != 0.0f) {
@@ -187,145 +204,257 @@ __device__ __forceinline__ void merge_store32<__nv_bfloat16>(__nv_bfloat16* wrow
 // =========================================================================
 // Fused bypass kernel
 // =========================================================================
+// Scattered rows (X rows of the tile, Y rows of the tile) move through the
+// LSU with cp.async, eight lanes per 128-byte row slice, into 128-byte
+// swizzled smem rows (chunk q of row i at i*128 + ((q ^ (i & 7)) * 16)):
+// measured on B200, TMA tile::gather4 sustains ~7 B/cycle/SM (one 512-byte
+// request per ~70 cycles) against ~18+ for cp.async, so TMA is kept for the
+// large contiguous factor copies only.
+
+// y_new = y + s * acc for one 128-byte row slice, in place in the smem ring.
 template <typename YT>
-__global__ void __launch_bounds__(kBypassThreads, 1)
-    atmm_bypass_kernel(const __grid_constant__ CUtensorMap tmap_x, const BypassParams p) {
+__device__ __forceinline__ void ring_update(uint32_t row_saddr, uint32_t i, float s,
+                                            const uint32_t (&acc)[64]);
+
+template <>
+__device__ __forceinline__ void ring_update<__nv_bfloat16>(uint32_t row_saddr, uint32_t i, float s,
+                                                           const uint32_t (&acc)[64]) {
+  uint4 y[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) y[q] = ld_shared_v4(row_saddr + ((static_cast<uint32_t>(q) ^ (i & 7u)) << 4));
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t w[4] = {y[q].x, y[q].y, y[q].z, y[q].w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float lo = fmaf(s, __uint_as_float(acc[q * 8 + 2 * e]), bf16lo(w[e]));
+      const float hi = fmaf(s, __uint_as_float(acc[q * 8 + 2 * e + 1]), bf16hi(w[e]));
+      o[e] = pack_bf16x2(lo, hi);
+    }
+    st_shared_v4(row_saddr + ((static_cast<uint32_t>(q) ^ (i & 7u)) << 4), o[0], o[1], o[2], o[3]);
+  }
+}
+
+template <>
+__device__ __forceinline__ void ring_update<float>(uint32_t row_saddr, uint32_t i, float s,
+                                                   const uint32_t (&acc)[64]) {
+  uint4 y[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) y[q] = ld_shared_v4(row_saddr + ((static_cast<uint32_t>(q) ^ (i & 7u)) << 4));
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    st_shared_v4(row_saddr + ((static_cast<uint32_t>(q) ^ (i & 7u)) << 4),
+                 __float_as_uint(fmaf(s, __uint_as_float(acc[4 * q + 0]), __uint_as_float(y[q].x))),
+                 __float_as_uint(fmaf(s, __uint_as_float(acc[4 * q + 1]), __uint_as_float(y[q].y))),
+                 __float_as_uint(fmaf(s, __uint_as_float(acc[4 * q + 2]), __uint_as_float(y[q].z))),
+                 __float_as_uint(fmaf(s, __uint_as_float(acc[4 * q + 3]), __uint_as_float(y[q].w))));
+  }
+}
+
+// Issue cp.async for `rows` rows x 8 16-byte chunks of one 128-byte column
+// slice: lane handles chunk (lane & 7) of rows (lane >> 3) + 4j.
+__device__ __forceinline__ void cp_async_rows(uint32_t dst_base, const uint8_t* src, int64_t ld_bytes,
+                                              const int32_t* rows_s, int rows, int64_t col_byte,
+                                              int64_t row_bytes, uint32_t lane) {
+  const uint32_t c = lane & 7u;
+  const int64_t cb = col_byte + c * 16;
+  const uint32_t nbytes = cb >= row_bytes ? 0u : static_cast<uint32_t>(row_bytes - cb >= 16 ? 16 : row_bytes - cb);
+  for (int i = static_cast<int>(lane >> 3); i < rows; i += 4) {
+    const uint8_t* g = nbytes ? src + static_cast<int64_t>(rows_s[i]) * ld_bytes + cb : src;
+    cp_async16(dst_base + static_cast<uint32_t>(i) * 128u + ((c ^ (static_cast<uint32_t>(i) & 7u)) << 4), g, nbytes);
+  }
+}
+
+template <typename YT>
+__global__ void __launch_bounds__(kBypassThreads, 2)
+    atmm_bypass_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
+                       const BypassParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  __shared__ int32_t rows_s[kTileM];  // batch row of each tile row
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TRACE(0);
 
   const uint32_t C = cluster_nctarank();
   const uint32_t crank = cluster_ctarank();
   const TileDesc tile = p.tiles[cluster_id_x()];
-  const SlotDesc slot = p.slots[tile.slot];
   const int rows = tile.rows;
-  const int r_pad = slot.r_pad;
-  const uint16_t* down_t = slot.down_t + static_cast<int64_t>(p.layer) * slot.down_layer_stride;
-  const uint16_t* up_t = slot.up_t + static_cast<int64_t>(p.layer) * slot.up_layer_stride;
+  const int r_pad = tile.r_pad;
+  const uint16_t* down_t = tile.down_t + static_cast<int64_t>(p.layer) * tile.down_layer_stride;
+  const uint16_t* up_t = tile.up_t + static_cast<int64_t>(p.layer) * tile.up_layer_stride;
 
-  // K blocks (64 wide) and N units (32 wide) owned by this CTA.
+  // K blocks (64 wide) and N units (64 wide) owned by this CTA.
   const int nkb = (p.d_in + kBK - 1) / kBK;
   const int kb_lo = (nkb * static_cast<int>(crank)) / static_cast<int>(C);
   const int kb_hi = (nkb * static_cast<int>(crank + 1)) / static_cast<int>(C);
   const int nun = (p.d_out + kNUnit - 1) / kNUnit;
-  const int nu_lo = (nun * static_cast<int>(crank)) / static_cast<int>(C);
-  const int nu_hi = (nun * static_cast<int>(crank + 1)) / static_cast<int>(C);
-  const int n_lo = nu_lo * kNUnit;
-  const int n_hi = nu_hi * kNUnit;
+  const int n_lo = (nun * static_cast<int>(crank)) / static_cast<int>(C) * kNUnit;
+  const int n_hi = (nun * static_cast<int>(crank + 1)) / static_cast<int>(C) * kNUnit;
   const int num_chunks = (n_hi - n_lo + p.bn - 1) / p.bn;
+  const int ycols = p.ycols;
 
   // Owner partition of the tile rows for the DSMEM reduction.
   const int R = (rows + static_cast<int>(C) - 1) / static_cast<int>(C);
   const int own_lo = min(rows, static_cast<int>(crank) * R);
   const int own_hi = min(rows, static_cast<int>(crank + 1) * R);
   const int owned = own_hi - own_lo;
+  // The expand accumulator holds p.rep replicas of the tile rows (rows_q
+  // TMEM lanes apart) so that every epilogue warp has data to work on.
+  const int rows_q = kTileM / p.rep;
 
   uint8_t* ring = smem;
+  uint8_t* upr = smem + p.off_up;
+  uint8_t* ybuf = smem + p.off_y;
   float* red = reinterpret_cast<float*>(smem + p.off_red);
   uint8_t* mid = smem + p.off_mid;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   const int S = p.stages;
-  uint64_t* full = bars;
-  uint64_t* empty = bars + S;
-  uint64_t* shrink_full = bars + 2 * S;
-  uint64_t* acc_full = bars + 2 * S + 1;   // [2]
-  uint64_t* acc_empty = bars + 2 * S + 3;  // [2]
-  uint64_t* red_full = bars + 2 * S + 5;
-  uint64_t* mid_full = bars + 2 * S + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 7);
+  const int U = p.ustages;
+  const int NY = p.ny;
+  const int NB = p.nbuf;
+  uint64_t* full = bars;                   // [S]
+  uint64_t* empty = full + S;              // [S]
+  uint64_t* up_full = empty + S;           // [U]
+  uint64_t* up_empty = up_full + U;        // [U]
+  uint64_t* y_full = up_empty + U;         // [NY]
+  uint64_t* y_empty = y_full + NY;         // [NY]
+  uint64_t* shrink_full = y_empty + NY;
+  uint64_t* acc_full = shrink_full + 1;    // [NB]
+  uint64_t* acc_empty = acc_full + NB;     // [NB]
+  uint64_t* red_full = acc_empty + NB;
+  uint64_t* mid_full = red_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mid_full + 1);
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+  // Barrier init spread over warp 0; the DSMEM exchange barriers count bytes
+  // (st.async complete_tx) with one local arrival carrying the total.
+  if (warp == 0) {
+    const int nb = 2 * S + 2 * U + 2 * NY + 2 * NB + 3;
+    const uint32_t qpr = static_cast<uint32_t>(4 / p.rep);
+    for (int b = static_cast<int>(lane); b < nb; b += 32) {
+      uint32_t count = 1;
+      if (b >= 2 * S + 2 * U + NY && b < 2 * S + 2 * U + 2 * NY) count = qpr;   // y_empty
+      if (b >= 2 * S + 2 * U + 2 * NY + 1 + NB && b < 2 * S + 2 * U + 2 * NY + 1 + 2 * NB) count = qpr;  // acc_empty
+      mbar_init(bars + b, count);
     }
-    mbar_init(shrink_full, 1);
-    mbar_init(&acc_full[0], 1);
-    mbar_init(&acc_full[1], 1);
-    mbar_init(&acc_empty[0], 4);
-    mbar_init(&acc_empty[1], 4);
-    mbar_init(red_full, owned > 0 ? static_cast<uint32_t>(owned) * C : 1u);
-    mbar_init(mid_full, static_cast<uint32_t>(rows * (r_pad / 8)));
+    for (int i = static_cast<int>(lane); i < kTileM; i += 32) {
+      rows_s[i] = p.row_index[tile.row_begin + min(i, rows - 1)];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (owned > 0) mbar_arrive_expect_tx(red_full, static_cast<uint32_t>(owned) * C * r_pad * 4u);
+      mbar_arrive_expect_tx(mid_full, static_cast<uint32_t>(p.rep * rows * r_pad * 2));
+    }
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap_x);
   if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
   tc_fence_before();
-  cluster_sync();  // barrier inits + TMEM address visible cluster-wide
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Cluster barrier phase 1 (barrier inits visible to peers): arrive now,
+  // wait only right before the first remote access, so loads start at once.
+  cluster_arrive();
+  if (threadIdx.x == 0) TRACE(1);
 
-  const uint32_t a_bytes_per_group = 4u * kBK * 2u;  // one gather4 = 4 rows x 128 B
-  const int ngroups = (rows + 3) / 4;
-
-  if (warp == 0) {
-    // ===================== TMA producer =====================
-    YT* y = reinterpret_cast<YT*>(p.y);
-    // Warm L2 with this CTA's Y slice and up^T slice: independent of the
-    // shrink, so their HBM reads overlap it.
-    const int n_hi_c = min(n_hi, p.d_out);
-    if (n_hi_c > n_lo) {
-      const uint32_t ybytes = static_cast<uint32_t>((n_hi_c - n_lo) * sizeof(YT)) & ~15u;
-      for (int i = static_cast<int>(lane); i < rows; i += 32) {
-        const int64_t row = p.row_index[tile.row_begin + i];
-        if (ybytes) prefetch_l2(y + row * p.ldy + n_lo, ybytes);
+  const int ngroups = (rows + 3) / 4;       // gather4 groups of tile rows
+  const int ngroups0 = (ngroups + 1) / 2;    // groups issued by warp 0 (warp 7 takes the rest)
+  if (warp == 0 || warp == 7) {
+    // ===================== X / down^T producers (shrink ring) =====================
+    // Two issuing warps: TMA gather4 throughput scales with issuers.
+    const int g_lo = warp == 0 ? 0 : ngroups0;
+    const int g_hi = warp == 0 ? ngroups0 : ngroups;
+    if (warp == 0 && lane == 0) {
+      tma_prefetch_desc(&tmap_x);
+      // Weights do not depend on the previous kernel: warm L2 with this
+      // CTA's up^T slice now so the expand chunks stream from L2.
+      if (n_hi > n_lo) {
+        prefetch_l2(up_t + static_cast<int64_t>(n_lo) * r_pad, static_cast<uint32_t>((n_hi - n_lo) * r_pad * 2));
       }
     }
-    if (lane == 0 && n_hi > n_lo) {
-      prefetch_l2(up_t + static_cast<int64_t>(n_lo) * r_pad,
-                  static_cast<uint32_t>((n_hi - n_lo) * r_pad * 2));
-    }
-    // Row coordinates of this lane's gather4 group (constant over K).
+    const int g = g_lo + static_cast<int>(lane);
     int32_t gr[4] = {0, 0, 0, 0};
-    if (static_cast<int>(lane) < ngroups) {
+    if (g < g_hi) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = min(static_cast<int>(lane) * 4 + q, rows - 1);
-        gr[q] = p.row_index[tile.row_begin + i];
-      }
+      for (int q = 0; q < 4; ++q) gr[q] = rows_s[min(g * 4 + q, rows - 1)];
     }
     const uint32_t b_bytes = static_cast<uint32_t>(r_pad) * kBK * 2u;
-    const uint32_t a_bytes = static_cast<uint32_t>(ngroups) * a_bytes_per_group;
+    const uint32_t a_bytes = static_cast<uint32_t>(ngroups) * 512u;
+    // X may be produced by the previous kernel (programmatic dependent launch).
+    griddep_wait();
     int stage = 0;
     uint32_t phase = 0;
     for (int kb = kb_lo; kb < kb_hi; ++kb) {
       uint8_t* st = ring + static_cast<size_t>(stage) * p.stage_bytes;
       if (lane == 0) {
         mbar_wait(&empty[stage], phase ^ 1u);
-        mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+        if (warp == 0) {
+          mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+          bulk_g2s(st + p.a_bytes, down_t + static_cast<int64_t>(kb) * r_pad * kBK, b_bytes, &full[stage]);
+        }
       }
       __syncwarp();
-      if (static_cast<int>(lane) < ngroups) {
-        tma_gather4(st + lane * a_bytes_per_group, &tmap_x, &full[stage], kb * kBK, gr[0], gr[1],
-                    gr[2], gr[3]);
-      }
-      if (lane == 0) {
-        bulk_g2s(st + kTileM * kBK * 2, down_t + static_cast<int64_t>(kb) * r_pad * kBK, b_bytes,
-                 &full[stage]);
-      }
+      if (g < g_hi) tma_gather4(st + g * 512u, &tmap_x, &full[stage], kb * kBK, gr[0], gr[1], gr[2], gr[3]);
       if (++stage == S) {
         stage = 0;
         phase ^= 1u;
       }
     }
-    // Expand operand: up^T rows [n0, n0 + bn_c) of the CTA's N slice.
-    for (int c = 0; c < num_chunks; ++c) {
-      const int n0 = n_lo + c * p.bn;
-      const int bn_c = min(p.bn, n_hi - n0);
+    if (warp == 0 && lane == 0) TRACE(2);
+    __syncwarp();
+    cluster_wait();
+  } else if (warp == 6) {
+    // ===================== up^T + Y producer =====================
+    // Order: up^T chunks 0..U-1 (weights: no dependency on the previous
+    // kernel), then per chunk c its Y sub-chunks and up^T chunk c+U.
+    auto issue_up = [&](int c) {
       if (lane == 0) {
-        uint8_t* st = ring + static_cast<size_t>(stage) * p.stage_bytes;
+        const int u = c % U;
+        const uint32_t ph = static_cast<uint32_t>((c / U) & 1);
+        const int n0 = n_lo + c * p.bn;
+        const int bn_c = min(p.bn, n_hi - n0);
         const uint32_t bytes = static_cast<uint32_t>(bn_c * r_pad * 2);
-        mbar_wait(&empty[stage], phase ^ 1u);
-        mbar_arrive_expect_tx(&full[stage], bytes);
-        bulk_g2s(st, up_t + static_cast<int64_t>(n0) * r_pad, bytes, &full[stage]);
+        mbar_wait(&up_empty[u], ph ^ 1u);
+        mbar_arrive_expect_tx(&up_full[u], bytes);
+        bulk_g2s(upr + static_cast<size_t>(u) * p.ustage_bytes, up_t + static_cast<int64_t>(n0) * r_pad, bytes,
+                 &up_full[u]);
       }
-      if (++stage == S) {
-        stage = 0;
-        phase ^= 1u;
+    };
+    for (int c = 0; c < min(U, num_chunks); ++c) issue_up(c);
+    int32_t gr[4] = {0, 0, 0, 0};
+    if (p.y_ring) {
+      if (lane == 0) tma_prefetch_desc(&tmap_y);
+      if (static_cast<int>(lane) < ngroups) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gr[q] = rows_s[min(static_cast<int>(lane) * 4 + q, rows - 1)];
       }
     }
+    griddep_wait();  // Y may be produced by the previous kernel
+    int j = 0;       // Y sub-chunk sequence number
+    for (int c = 0; c < num_chunks; ++c) {
+      if (p.y_ring) {
+        const int n0 = n_lo + c * p.bn;
+        const int bn_c = min(p.bn, n_hi - n0);
+        for (int sub = 0; sub < bn_c; sub += ycols, ++j) {
+          const int b = j % NY;
+          const uint32_t ph = static_cast<uint32_t>((j / NY) & 1);
+          if (lane == 0) {
+            mbar_wait(&y_empty[b], ph ^ 1u);
+            mbar_arrive_expect_tx(&y_full[b], static_cast<uint32_t>(ngroups) * 512u);
+          }
+          __syncwarp();
+          if (static_cast<int>(lane) < ngroups) {
+            tma_gather4(ybuf + static_cast<size_t>(b) * p.ybuf_bytes + lane * 512u, &tmap_y, &y_full[b], n0 + sub,
+                        gr[0], gr[1], gr[2], gr[3]);
+          }
+        }
+      }
+      if (c + U < num_chunks) issue_up(c + U);
+    }
+    __syncwarp();
+    cluster_wait();
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
@@ -336,10 +465,13 @@ __global__ void __launch_bounds__(kBypassThreads, 1)
         uint8_t* st = ring + static_cast<size_t>(stage) * p.stage_bytes;
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (kb == kb_lo) TRACE(3);
         const uint32_t a0 = smem_u32(st);
-        const uint32_t b0 = smem_u32(st + kTileM * kBK * 2);
+        const uint32_t b0 = smem_u32(st + p.a_bytes);
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk) {
+          // A rows beyond the tile read neighbouring smem: those TMEM lanes are
+          // never consumed (each MMA row depends only on its own A row).
           const uint64_t ad = smem_desc(a0 + kk * 32u, 16u, 1024u, kLayoutSW128);
           const uint64_t bd = smem_desc(b0 + kk * 256u, 128u, 1024u, kLayoutNone);
           mma_bf16(tmem_base, ad, bd, idesc_s, (kb > kb_lo || kk > 0) ? 1u : 0u);
@@ -351,36 +483,36 @@ __global__ void __launch_bounds__(kBypassThreads, 1)
         }
       }
       mma_commit(shrink_full);
-      // Wait for the reduced bf16 mid (written through DSMEM by the owners).
+      TRACE(4);
+      // The reduced bf16 mid lands through st.async (DSMEM) from the owners.
       mbar_wait_cluster(mid_full, 0);
-      tc_fence_after();
       fence_proxy_async_smem();
+      tc_fence_after();
+      TRACE(9);
       const uint32_t mid0 = smem_u32(mid);
       const uint32_t sbo = static_cast<uint32_t>(r_pad) * 16u;
       for (int c = 0; c < num_chunks; ++c) {
         const int n0 = n_lo + c * p.bn;
         const int bn_c = min(p.bn, n_hi - n0);
-        const int buf = c & 1;
-        mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1u);
-        mbar_wait(&full[stage], phase);
+        const int buf = c % NB;
+        const int u = c % U;
+        mbar_wait(&acc_empty[buf], static_cast<uint32_t>((c / NB) & 1) ^ 1u);
+        mbar_wait(&up_full[u], static_cast<uint32_t>((c / U) & 1));
         tc_fence_after();
-        const uint32_t b0 = smem_u32(ring + static_cast<size_t>(stage) * p.stage_bytes);
+        const uint32_t b0 = smem_u32(upr + static_cast<size_t>(u) * p.ustage_bytes);
         const uint32_t idesc_e = idesc_bf16(kTileM, static_cast<uint32_t>(bn_c));
         for (int kk = 0; kk < r_pad / 16; ++kk) {
           const uint64_t ad = smem_desc(mid0 + kk * 256u, 128u, sbo, kLayoutNone);
           const uint64_t bd = smem_desc(b0 + kk * 256u, 128u, sbo, kLayoutNone);
-          mma_bf16(tmem_base + static_cast<uint32_t>(buf * p.bn), ad, bd, idesc_e,
-                   kk > 0 ? 1u : 0u);
+          mma_bf16(tmem_base + static_cast<uint32_t>(buf * p.bn), ad, bd, idesc_e, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&empty[stage]);
+        mma_commit(&up_empty[u]);
         mma_commit(&acc_full[buf]);
-        if (++stage == S) {
-          stage = 0;
-          phase ^= 1u;
-        }
       }
+      TRACE(10);
     }
     __syncwarp();
+    cluster_wait();
   } else {
     // ===================== epilogue (warps 2..5) =====================
     const uint32_t quad = warp & 3u;
@@ -389,156 +521,194 @@ __global__ void __launch_bounds__(kBypassThreads, 1)
     const uint32_t lane_addr = (quad * 32u) << 16;
     const int ew = static_cast<int>(warp) - 2;
     const bool warp_active = static_cast<int>(quad * 32) < rows;
+    const bool tracer = (warp == 4) && lane == 0;
 
-    // ---- shrink partial: TMEM -> registers ----
+    // ---- shrink partial: TMEM -> registers -> DSMEM, 32 columns at a time ----
     mbar_wait(shrink_full, 0);
     tc_fence_after();
-    uint32_t part[kMaxRank];
+    if (tracer) TRACE(5);
+    cluster_wait();  // peers' barriers are initialized before any st.async
+    const uint32_t mid_s = smem_u32(mid);
     if (warp_active) {
+      // Destination of this row: the whole bf16 mid row in this CTA (C == 1)
+      // or the fp32 partial slot of the row's owner CTA.
+      const int owner = valid ? row_local / R : 0;
+      uint32_t dst = 0, bar = 0;
+      if (C == 1) {
+        bar = map_cta(smem_u32(mid_full), crank);
+      } else {
+        float* slot_row =
+            red + (static_cast<size_t>(crank) * p.red_rows + (row_local - owner * R)) * r_pad;
+        dst = map_cta(smem_u32(slot_row), static_cast<uint32_t>(owner));
+        bar = map_cta(smem_u32(red_full), static_cast<uint32_t>(owner));
+      }
+      for (int g = 0; g < r_pad; g += 32) {
+        uint32_t v[32];
+        if (g + 32 <= r_pad) {
+          tmem_ld32(tmem_base + lane_addr + g, v);
+        } else {
+          tmem_ld16(tmem_base + lane_addr + g, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+        }
+        tmem_wait_ld();
+        if (valid) {
+          const int ncols = min(32, r_pad - g);
+          if (C == 1) {
 #pragma unroll
-      for (int g = 0; g < kMaxRank / 32; ++g) {
-        if (g * 32 < r_pad) {
-          if (r_pad - g * 32 >= 32) {
-            uint32_t v[32];
-            tmem_ld32(tmem_base + lane_addr + g * 32, v);
-            tmem_wait_ld();
+            for (int ch = 0; ch < 4; ++ch) {
+              if (ch * 8 < ncols) {
+                uint32_t w[4];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) part[g * 32 + j] = v[j];
+                for (int e = 0; e < 4; ++e) {
+                  w[e] = pack_bf16x2(__uint_as_float(v[ch * 8 + 2 * e]), __uint_as_float(v[ch * 8 + 2 * e + 1]));
+                }
+                for (int f = 0; f < p.rep; ++f) {
+                  st_async_v4(map_cta(mid_s + interleave_off(row_local + f * rows_q, g + ch * 8, r_pad), crank),
+                              w[0], w[1], w[2], w[3], bar);
+                }
+              }
+            }
           } else {
-            uint32_t v[16];
-            tmem_ld16(tmem_base + lane_addr + g * 32, v);
-            tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) part[g * 32 + j] = v[j];
+            for (int jj = 0; jj < 32; jj += 4) {
+              if (jj < ncols) st_async_v4(dst + (g + jj) * 4, v[jj], v[jj + 1], v[jj + 2], v[jj + 3], bar);
+            }
           }
         }
       }
     }
     tc_fence_before();
-    const uint32_t mid_s = smem_u32(mid);
-
-    if (C == 1) {
-      // Single CTA: the partial is the whole mid; write it as bf16.
-      if (valid) {
-#pragma unroll
-        for (int ch = 0; ch < kMaxRank / 8; ++ch) {
-          if (ch < r_pad / 8) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              w[e] = pack_bf16x2(__uint_as_float(part[ch * 8 + 2 * e]),
-                                 __uint_as_float(part[ch * 8 + 2 * e + 1]));
-            }
-            st_cluster_v4(mid_s + interleave_off(row_local, ch * 8, r_pad), w[0], w[1], w[2],
-                          w[3]);
-          }
-        }
-      }
-      fence_proxy_async_cluster();
-      __syncwarp();
-      const uint32_t nvalid = __popc(__ballot_sync(0xffffffffu, valid));
-      if (lane == 0 && nvalid) {
-        fence_acq_rel_cluster();
-        mbar_arrive_remote(mid_full, crank, nvalid * static_cast<uint32_t>(r_pad / 8));
-      }
-    } else {
-      // ---- 1. scatter fp32 partial rows to their owners' slots ----
-      const int owner = valid ? row_local / R : -1;
-      if (valid) {
-        float* slot_row =
-            red + (static_cast<size_t>(crank) * p.red_rows + (row_local - owner * R)) * r_pad;
-        const uint32_t dst = map_cta(smem_u32(slot_row), static_cast<uint32_t>(owner));
-#pragma unroll
-        for (int j = 0; j < kMaxRank; j += 4) {
-          if (j < r_pad) st_cluster_v4(dst + j * 4, part[j], part[j + 1], part[j + 2], part[j + 3]);
-        }
-      }
-      __syncwarp();
-      if (warp_active) {
-        const int first_owner = (quad * 32) / R;
-        const int last_row = min(rows - 1, static_cast<int>(quad * 32 + 31));
-        const int last_owner = last_row / R;
-        if (lane == 0) fence_acq_rel_cluster();
-        for (int o = first_owner; o <= last_owner; ++o) {
-          const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, owner == o));
-          if (lane == 0 && cnt) mbar_arrive_remote(red_full, static_cast<uint32_t>(o), cnt);
-        }
-      }
-      // ---- 2. owner: fixed-order reduction of C partials, bf16 broadcast ----
+    if (C > 1) {
+      if (tracer) TRACE(6);
+      // ---- owner: fixed-order reduction of C partials, bf16 broadcast ----
       if (owned > 0) {
         mbar_wait_cluster(red_full, 0);
+        if (warp == 2 && lane == 0) TRACE(7);
         const int cpr = r_pad / 8;  // 8-column chunks per row
         const int items = owned * cpr;
-        for (int t = ew * 32 + static_cast<int>(lane); t < items; t += 128) {
-          const int rl = t / cpr;
-          const int ch = t - rl * cpr;
+        const uint32_t red_s = smem_u32(red);
+        const uint32_t bar_l = smem_u32(mid_full);
+        // work unit = (item, destination CTA): every unit re-sums its item
+        // (C x 32 B of local smem) so the C x rep st.async spread over threads
+        const int units = items * static_cast<int>(C);
+        for (int t = ew * 32 + static_cast<int>(lane); t < units; t += 128) {
+          const int it = t / static_cast<int>(C);
+          const uint32_t q = static_cast<uint32_t>(t - it * static_cast<int>(C));
+          const int rl = it / cpr;
+          const int ch = it - rl * cpr;
           float acc[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
           for (uint32_t c = 0; c < C; ++c) {
-            const float4* src = reinterpret_cast<const float4*>(
-                red + (static_cast<size_t>(c) * p.red_rows + rl) * r_pad + ch * 8);
-            const float4 u = src[0];
-            const float4 v = src[1];
-            acc[0] += u.x;
-            acc[1] += u.y;
-            acc[2] += u.z;
-            acc[3] += u.w;
-            acc[4] += v.x;
-            acc[5] += v.y;
-            acc[6] += v.z;
-            acc[7] += v.w;
+            const uint32_t src = red_s + static_cast<uint32_t>(((c * p.red_rows + rl) * r_pad + ch * 8) * 4);
+            const uint4 u = ld_shared_v4(src);
+            const uint4 v = ld_shared_v4(src + 16);
+            acc[0] += __uint_as_float(u.x);
+            acc[1] += __uint_as_float(u.y);
+            acc[2] += __uint_as_float(u.z);
+            acc[3] += __uint_as_float(u.w);
+            acc[4] += __uint_as_float(v.x);
+            acc[5] += __uint_as_float(v.y);
+            acc[6] += __uint_as_float(v.z);
+            acc[7] += __uint_as_float(v.w);
           }
           const uint32_t w0 = pack_bf16x2(acc[0], acc[1]);
           const uint32_t w1 = pack_bf16x2(acc[2], acc[3]);
           const uint32_t w2 = pack_bf16x2(acc[4], acc[5]);
           const uint32_t w3 = pack_bf16x2(acc[6], acc[7]);
-          const uint32_t off = mid_s + interleave_off(own_lo + rl, ch * 8, r_pad);
-          for (uint32_t q = 0; q < C; ++q) st_cluster_v4(map_cta(off, q), w0, w1, w2, w3);
+          const uint32_t rbar = map_cta(bar_l, q);
+          for (int f = 0; f < p.rep; ++f) {
+            const uint32_t off = mid_s + interleave_off(own_lo + rl + f * rows_q, ch * 8, r_pad);
+            st_async_v4(map_cta(off, q), w0, w1, w2, w3, rbar);
+          }
         }
-        fence_proxy_async_cluster();
-        __syncwarp();
-        const int full_rounds = items / 128;
-        const int rem = items - full_rounds * 128;
-        const uint32_t cnt =
-            static_cast<uint32_t>(full_rounds * 32 + max(0, min(32, rem - ew * 32)));
-        if (lane == 0 && cnt) {
-          fence_acq_rel_cluster();
-          for (uint32_t q = 0; q < C; ++q) mbar_arrive_remote(mid_full, q, cnt);
-        }
+        if (warp == 2 && lane == 0) TRACE(8);
       }
     }
 
-    // ---- 3. expand epilogue: Y += s * acc ----
-    const float s = p.scale * slot.scale;
-    YT* yrow = nullptr;
-    if (valid) {
-      yrow = reinterpret_cast<YT*>(p.y) +
-             static_cast<int64_t>(p.row_index[tile.row_begin + row_local]) * p.ldy;
-    }
+    // ---- expand epilogue: Y += s * acc ----
+    // Quad q reads TMEM lanes 32q..32q+31 = replica q / (4 / rep), tile rows
+    // (q % (4 / rep)) * 32 + lane; replicas take whole chunks round robin.
+    griddep_launch_dependents();
+    const float s = p.scale * tile.scale;
+    const int qpr = 4 / p.rep;  // quads per replica
+    const int my_rep = static_cast<int>(quad) / qpr;
+    const int erow0 = (static_cast<int>(quad) % qpr) * 32;
+    const int erow = erow0 + static_cast<int>(lane);
+    const bool evalid = erow < rows;
+    const bool ewarp = erow0 < rows;
+    const int32_t my_yrow = rows_s[min(erow, kTileM - 1)];
+    YT* yrow = evalid ? reinterpret_cast<YT*>(p.y) + static_cast<int64_t>(my_yrow) * p.ldy : nullptr;
+    constexpr int kEpc = 16 / static_cast<int>(sizeof(YT));  // elements per 16-byte chunk
+    int ysub = 0;  // Y sub-chunk sequence number (same order the producer fills)
+    const uint32_t ybuf_s = smem_u32(ybuf);
     for (int c = 0; c < num_chunks; ++c) {
       const int n0 = n_lo + c * p.bn;
       const int bn_c = min(p.bn, n_hi - n0);
-      const int buf = c & 1;
-      mbar_wait(&acc_full[buf], (c >> 1) & 1);
+      const int nsub = p.y_ring ? (bn_c + ycols - 1) / ycols : 0;
+      if ((c % p.rep) != my_rep) {  // another replica's chunk
+        ysub += nsub;
+        continue;
+      }
+      const int buf = c % NB;
+      mbar_wait(&acc_full[buf], static_cast<uint32_t>((c / NB) & 1));
       tc_fence_after();
-      if (warp_active) {
+      if (tracer && c == 0) TRACE(11);
+      if (p.y_ring) {
+        for (int sub = 0; sub < bn_c; sub += ycols, ++ysub) {
+          const int yb = ysub % NY;
+          mbar_wait(&y_full[yb], static_cast<uint32_t>((ysub / NY) & 1));
+          const uint32_t bufs = ybuf_s + static_cast<uint32_t>(yb) * p.ybuf_bytes;
+          if (ewarp) {
+            uint32_t v[64];
+            const uint32_t ta = tmem_base + lane_addr + static_cast<uint32_t>(buf * p.bn + sub);
+            tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+            if (ycols == 64) tmem_ld32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+            tmem_wait_ld();
+            if (evalid) ring_update<YT>(bufs + static_cast<uint32_t>(erow) * 128u, static_cast<uint32_t>(erow), s, v);
+            __syncwarp();
+            // Coalesced write-out: 8 lanes per 128-byte row slice, 4 rows per instruction.
+            const int col0 = n0 + sub;
+            const uint32_t ch = lane & 7u;
+            const int cc = col0 + static_cast<int>(ch) * kEpc;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = erow0 + it * 4 + static_cast<int>(lane >> 3);
+              const int32_t yr = __shfl_sync(0xffffffffu, my_yrow, it * 4 + static_cast<int>(lane >> 3));
+              if (r < rows && cc < p.d_out) {
+                const uint4 val = ld_shared_v4(bufs + static_cast<uint32_t>(r) * 128u +
+                                               ((ch ^ (static_cast<uint32_t>(r) & 7u)) << 4));
+                YT* dstp = reinterpret_cast<YT*>(p.y) + static_cast<int64_t>(yr) * p.ldy + cc;
+                if (cc + kEpc <= p.d_out) {
+                  *reinterpret_cast<uint4*>(dstp) = val;
+                } else {
+                  const YT* pv = reinterpret_cast<const YT*>(&val);
+                  for (int e = 0; e < kEpc && cc + e < p.d_out; ++e) dstp[e] = pv[e];
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&y_empty[yb]);
+        }
+      } else if (ewarp) {
         for (int sub = 0; sub < bn_c; sub += 32) {
           uint32_t v[32];
           tmem_ld32(tmem_base + lane_addr + static_cast<uint32_t>(buf * p.bn + sub), v);
           tmem_wait_ld();
-          if (valid && n0 + sub < p.d_out) epilogue_store32<YT>(yrow, n0 + sub, p.d_out, s, v);
+          if (evalid && n0 + sub < p.d_out) epilogue_store32<YT>(yrow, n0 + sub, p.d_out, s, p.y_vec != 0, v);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
+    if (tracer) TRACE(12);
   }
 
   __syncwarp();
   tc_fence_before();
-  cluster_sync();  // no CTA leaves while a peer may still touch its smem
+  __syncthreads();
+  if (threadIdx.x == 0) TRACE(13);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
@@ -693,7 +863,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1) atmm_merge_kernel(const Merg
         uint32_t v[32];
         tmem_ld32(tmem_base + lane_addr + static_cast<uint32_t>(buf * p.bn + sub), v);
         tmem_wait_ld();
-        if (row < p.m && n0 + sub < p.n) merge_store32<WT>(wrow, n0 + sub, p.n, p.alpha, p.beta, v);
+        if (row < p.m && n0 + sub < p.n) merge_store32<WT>(wrow, n0 + sub, p.n, p.alpha, p.beta, p.w_vec != 0, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -724,8 +894,10 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ src, uint16_t* __re
 
 // Explicit instantiations reachable from the host launcher.
 template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant__ CUtensorMap,
+                                                           const __grid_constant__ CUtensorMap,
                                                            const BypassParams);
 template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUtensorMap,
+                                                   const __grid_constant__ CUtensorMap,
                                                    const BypassParams);
 template __global__ void atmm_merge_kernel<float>(const MergeParams);
 template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
@@ -737,41 +909,78 @@ template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
 // =========================================================================
 namespace atmm {
 
+// Function attributes are raised once per (kernel, device) and only when a
+// launch needs more, so steady-state launches (and CUDA-graph capture) issue
+// no attribute calls.
 template <typename K>
 static cudaError_t prepare(K kernel, size_t smem, bool nonportable) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  if (nonportable) {
-    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  struct State {
+    const void* fn;
+    int dev;
+    size_t smem;
+    bool nonportable;
+  };
+  static thread_local State cache[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  State* st = nullptr;
+  for (auto& c : cache) {
+    if (c.fn == reinterpret_cast<const void*>(kernel) && c.dev == dev) {
+      st = &c;
+      break;
+    }
   }
-  return e;
+  if (!st) {
+    for (auto& c : cache) {
+      if (!c.fn) {
+        c = State{reinterpret_cast<const void*>(kernel), dev, 0, false};
+        st = &c;
+        break;
+      }
+    }
+  }
+  if (!st || smem > st->smem) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    if (st) st->smem = smem;
+  }
+  if (nonportable && (!st || !st->nonportable)) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    if (st) st->nonportable = true;
+  }
+  return cudaSuccess;
 }
 
-cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap, const BypassParams& p, int C,
-                          int num_tiles, size_t smem, cudaStream_t stream) {
+cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensorMap& tmap_y,
+                          const BypassParams& p, int C, int num_tiles, size_t smem, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(C * num_tiles), 1, 1);
   cfg.blockDim = dim3(kBypassThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(C);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // Programmatic dependent launch: the prologue overlaps the previous
+  // kernel on the stream; the kernel waits (griddepcontrol.wait) before X/Y.
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (y_dtype == 0) {
     auto k = atmm_bypass_kernel<__nv_bfloat16>;
     cudaError_t e = prepare(k, smem, C > 8);
     if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, k, tmap, p);
+    return cudaLaunchKernelEx(&cfg, k, tmap_x, tmap_y, p);
   }
   auto k = atmm_bypass_kernel<float>;
   cudaError_t e = prepare(k, smem, C > 8);
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, k, tmap, p);
+  return cudaLaunchKernelEx(&cfg, k, tmap_x, tmap_y, p);
 }
 
 int bypass_max_active_clusters(int C, size_t smem) {

@@ -148,8 +148,8 @@ def test_cluster_sizes_agree(gpu, atmm, oracle):
     x = _x(oracle, n, d)
     assignment = np.asarray([(1, 2, 3)[i % 3] for i in range(n)], np.int32)
     want = oracle.bypass_rows_f64(x, assignment, {a: (f[0][0], f[1][0]) for a, f in facs.items()})
-    for sm100 in [(128, 1, 256, 0), (128, 2, 128, 2), (64, 3, 64, 3), (128, 5, 96, 0),
-                  (32, 8, 256, 4), (128, 16, 32, 0), (128, 12, 160, 0)]:
+    for sm100 in [(128, 1, 256, 0), (128, 2, 128, 2), (64, 3, 64, 3), (128, 5, 192, 0),
+                  (32, 8, 256, 4), (128, 16, 64, 0), (128, 12, 128, 0)]:
         t = atmm.TilingTable()
         for m_bucket in range(32, 129, 32):
             for r in ranks.values():
@@ -181,3 +181,21 @@ def test_adapter_scale(gpu, atmm, oracle):
     want[assignment == 1] *= 2.0
     want[assignment == 2] *= -0.5
     assert np.max(np.abs(got - want)) <= tol_for(want)
+
+
+def test_unaligned_y_rows(gpu, atmm, oracle):
+    """Y rows that are not 16-byte aligned take the non-TMA epilogue path."""
+    import torch
+
+    d_in, d_out, n = 256, 777, 70
+    reg, facs = _setup(atmm, oracle, d_in, d_out, {1: 16, 2: 32})
+    assignment = np.asarray([1, 2] * 35, np.int32)
+    x = _x(oracle, n, d_in)
+    want = oracle.bypass_rows_f64(x, assignment, {a: (f[0][0], f[1][0]) for a, f in facs.items()})
+    plan = atmm.BypassPlan(reg, assignment)
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    for dtype in (torch.float32, torch.bfloat16):
+        yt = torch.zeros(n, d_out, dtype=dtype, device="cuda")
+        plan.apply(xt, yt)
+        torch.cuda.synchronize()
+        assert np.max(np.abs(yt.float().cpu().numpy() - want)) <= tol_for(want), dtype
