@@ -1,0 +1,216 @@
+// loraserve_b200.hpp -- header-only C++ shim restoring the reference's
+// operator interface (namespace loraserve, /root/reference/proj/include/
+// loraserve/) on top of the B200 C ABI (atmm_b200.h).
+//
+// A reference caller switches by including this header instead of
+// batch.hpp / tiling.hpp / model.hpp for the ATMM path and linking
+// libatmm_b200.so.  Names, argument meaning and exception types follow the
+// reference:
+//   plan_batch            batch.hpp:28     -> loraserve_b200::plan_batch
+//   run_bypass            batch.hpp:48     -> loraserve_b200::run_bypass
+//   TilingConfig/ShapeKey tiling.hpp:22-83 -> same names
+//   TilingTable           tiling.hpp:153   -> loraserve_b200::TilingTable
+//   delta_w / merge       model.hpp:120-188-> delta_w / merge_into / unmerge_into
+//   atmm_multiply         atmm.hpp:144     -> loraserve_b200::atmm_multiply
+//   errors.hpp classes    -> same class names, rethrown from ATMM status codes
+// The adapter set lives on the device (AdapterRegistry, adapter.hpp:18-110).
+#pragma once
+
+#include <array>
+#include <compare>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "atmm_b200.h"
+
+namespace loraserve_b200 {
+
+// ------------------------------------------------------------- errors ----
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ShapeError : public Error { using Error::Error; };
+class ConfigError : public Error { using Error::Error; };
+class ModeError : public Error { using Error::Error; };
+class IoError : public Error { using Error::Error; };
+class ParseError : public Error { using Error::Error; };
+class UnknownAdapterError : public Error { using Error::Error; };
+class DeviceError : public Error { using Error::Error; };
+
+inline void check(int status) {
+  if (status == ATMM_OK) return;
+  const std::string msg = atmm_last_error();
+  switch (status) {
+    case ATMM_ERR_SHAPE: throw ShapeError(msg);
+    case ATMM_ERR_CONFIG: throw ConfigError(msg);
+    case ATMM_ERR_MODE: throw ModeError(msg);
+    case ATMM_ERR_IO: throw IoError(msg);
+    case ATMM_ERR_PARSE: throw ParseError(msg);
+    case ATMM_ERR_UNKNOWN_ADAPTER: throw UnknownAdapterError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+// ------------------------------------------------------------- tiling ----
+struct TilingConfig {
+  int outer_m = 0, outer_n = 0, outer_k = 0;
+  int inner_m = 0, inner_n = 0, inner_k = 0;
+  auto operator<=>(const TilingConfig&) const = default;
+  std::array<int32_t, 6> edges() const { return {outer_m, outer_n, outer_k, inner_m, inner_n, inner_k}; }
+  static TilingConfig from(const int32_t* e) { return {e[0], e[1], e[2], e[3], e[4], e[5]}; }
+  bool structurally_valid() const { return atmm_config_valid(edges().data()) == 1; }
+  void validate() const {
+    if (!structurally_valid()) throw ConfigError("invalid tiling config");
+  }
+};
+
+struct ShapeKey {
+  int m_bucket = 32, k = 0, n = 0;
+  auto operator<=>(const ShapeKey&) const = default;
+};
+inline int m_bucket_of(std::size_t m) { return atmm_m_bucket_of(static_cast<int64_t>(m)); }
+inline ShapeKey shape_key(std::size_t m, std::size_t k, std::size_t n) {
+  return ShapeKey{m_bucket_of(m), static_cast<int>(k), static_cast<int>(n)};
+}
+
+class TilingTable {
+ public:
+  TilingTable() { check(atmm_table_create(nullptr, &h_)); }
+  explicit TilingTable(TilingConfig d) {
+    auto e = d.edges();
+    check(atmm_table_create(e.data(), &h_));
+  }
+  ~TilingTable() { atmm_table_destroy(h_); }
+  TilingTable(const TilingTable&) = delete;
+  TilingTable& operator=(const TilingTable&) = delete;
+  TilingTable(TilingTable&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+
+  void insert(ShapeKey key, TilingConfig config, std::int64_t measured_ns) {
+    auto e = config.edges();
+    check(atmm_table_insert(h_, key.m_bucket, key.k, key.n, e.data(), measured_ns, nullptr));
+  }
+  TilingConfig lookup(std::size_t m, std::size_t k, std::size_t n) const {
+    int32_t out[6];
+    check(atmm_table_lookup(h_, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(n), out));
+    return TilingConfig::from(out);
+  }
+  std::size_t size() const {
+    int64_t s = 0;
+    check(atmm_table_size(h_, &s));
+    return static_cast<std::size_t>(s);
+  }
+  void save(const std::string& path) const { check(atmm_table_save(h_, path.c_str())); }
+  static TilingTable load(const std::string& path) {
+    TilingTable t(nullptr);
+    check(atmm_table_load(path.c_str(), &t.h_));
+    return t;
+  }
+  const atmm_table* handle() const { return h_; }
+
+ private:
+  explicit TilingTable(std::nullptr_t) {}
+  atmm_table* h_ = nullptr;
+};
+
+// ------------------------------------------------------------ planner ----
+struct Segment {
+  int adapter_id = 0;
+  std::vector<std::size_t> rows;
+};
+struct BatchPlan {
+  std::vector<Segment> segments;
+  std::size_t total_rows = 0;
+};
+
+inline BatchPlan plan_batch(const std::vector<int>& assignment) {
+  const int64_t n = static_cast<int64_t>(assignment.size());
+  std::vector<int32_t> a(assignment.begin(), assignment.end());
+  std::vector<int32_t> seg(std::max<int64_t>(n, 1));
+  std::vector<int64_t> off(std::max<int64_t>(n, 1) + 1), rows(std::max<int64_t>(n, 1));
+  int64_t S = 0;
+  check(atmm_plan_batch(a.data(), n, seg.data(), off.data(), rows.data(), &S));
+  BatchPlan p;
+  p.total_rows = static_cast<std::size_t>(n);
+  for (int64_t s = 0; s < S; ++s) {
+    Segment g;
+    g.adapter_id = seg[s];
+    for (int64_t i = off[s]; i < off[s + 1]; ++i) g.rows.push_back(static_cast<std::size_t>(rows[i]));
+    p.segments.push_back(std::move(g));
+  }
+  return p;
+}
+
+// ----------------------------------------------------- adapter registry --
+class AdapterRegistry {
+ public:
+  AdapterRegistry(int device, std::size_t num_layers, std::size_t d_in, std::size_t d_out)
+      : d_in_(d_in), d_out_(d_out) {
+    check(atmm_registry_create(device, static_cast<int64_t>(num_layers), static_cast<int64_t>(d_in),
+                               static_cast<int64_t>(d_out), &h_));
+  }
+  ~AdapterRegistry() { atmm_registry_destroy(h_); }
+  AdapterRegistry(const AdapterRegistry&) = delete;
+  AdapterRegistry& operator=(const AdapterRegistry&) = delete;
+
+  // down: [L][d_in x r], up: [L][r x d_out], host fp32 (LoraAdapter layout).
+  void put(int adapter_id, std::size_t rank, const float* down, const float* up, float scale = 1.0f) {
+    check(atmm_registry_put(h_, adapter_id, static_cast<int64_t>(rank), down, up, scale));
+  }
+  bool contains(int adapter_id) const { return atmm_registry_contains(h_, adapter_id) == 1; }
+  atmm_registry* handle() const { return h_; }
+  std::size_t d_in() const { return d_in_; }
+  std::size_t d_out() const { return d_out_; }
+
+ private:
+  atmm_registry* h_ = nullptr;
+  std::size_t d_in_, d_out_;
+};
+
+// run_bypass (batch.hpp:48): fresh n x d_out bypass from host fp32 x.
+inline std::vector<float> run_bypass(const AdapterRegistry& reg, const std::vector<float>& x,
+                                     const std::vector<int>& assignment, std::size_t layer,
+                                     const TilingTable* table = nullptr) {
+  const std::size_t n = assignment.size();
+  if (x.size() != n * reg.d_in()) throw ShapeError("run_bypass: x must be n x d_in");
+  std::vector<int32_t> a(assignment.begin(), assignment.end());
+  std::vector<float> out(n * reg.d_out());
+  check(atmm_run_bypass_host(reg.handle(), x.data(), static_cast<int64_t>(n), a.data(),
+                             static_cast<int64_t>(layer), table ? table->handle() : nullptr, out.data()));
+  return out;
+}
+
+// delta_w (model.hpp:130-140) for one layer, host fp32 d_in x d_out.
+inline std::vector<float> delta_w(const AdapterRegistry& reg, int adapter_id, std::size_t layer) {
+  std::vector<float> out(reg.d_in() * reg.d_out());
+  check(atmm_delta_w_host(reg.handle(), adapter_id, static_cast<int64_t>(layer), out.data()));
+  return out;
+}
+
+// merge / unmerge one layer in place on a device weight (W +-= s.down.up).
+inline void merge_into(const AdapterRegistry& reg, int adapter_id, std::size_t layer, void* w_device,
+                       std::size_t ldw, int w_dtype, void* stream = nullptr) {
+  check(atmm_merge_apply(reg.handle(), adapter_id, static_cast<int64_t>(layer), w_device,
+                         static_cast<int64_t>(ldw), w_dtype, +1.0f, stream));
+}
+inline void unmerge_into(const AdapterRegistry& reg, int adapter_id, std::size_t layer, void* w_device,
+                         std::size_t ldw, int w_dtype, void* stream = nullptr) {
+  check(atmm_merge_apply(reg.handle(), adapter_id, static_cast<int64_t>(layer), w_device,
+                         static_cast<int64_t>(ldw), w_dtype, -1.0f, stream));
+}
+
+// atmm_multiply (atmm.hpp:144-154): host fp32 a (m x k) . b (k x n).
+inline std::vector<float> atmm_multiply(const std::vector<float>& a, std::size_t m, std::size_t k,
+                                        const std::vector<float>& b, std::size_t n, const TilingConfig& cfg) {
+  if (a.size() != m * k || b.size() != k * n) throw ShapeError("atmm_multiply: shape mismatch");
+  std::vector<float> c(m * n);
+  auto e = cfg.edges();
+  check(atmm_multiply_host(a.data(), static_cast<int64_t>(m), static_cast<int64_t>(k), b.data(),
+                           static_cast<int64_t>(n), c.data(), e.data()));
+  return c;
+}
+
+}  // namespace loraserve_b200

@@ -1,0 +1,241 @@
+"""CPU: host logic of the product library (no kernels run here).
+
+* the C-ABI library loads on a GPU-less host and exports every symbol
+  include/atmm_b200.h declares;
+* plan_batch routing is bit-exact with the oracle (and the reference KATs);
+* the tiling table follows tiling.hpp (bucketing, lookup, JSON) and its JSON
+  is loadable by the reference's own TilingTable::load;
+* request sharding (LPT) partitions whole segments deterministically;
+* without a device every compute entry point fails loudly (no CPU fallback);
+* the header-only C++ shim compiles against the ABI and passes the
+  reference's host-side cases.
+"""
+import json
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "atmm_b200.h")
+LIB = os.path.join(ROOT, "paper_2411_00915_b200", "libatmm_b200.so")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(atmm_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (atmm_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+
+
+def test_python_binding_covers_the_abi(atmm):
+    from paper_2411_00915_b200._lib import EXPORTED, lib
+
+    assert lib.atmm_abi_version() == 1
+    for s in declared_symbols():
+        assert s in EXPORTED, s
+
+
+def test_library_has_no_driver_or_torch_dependency():
+    out = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
+    assert "libcuda.so" not in out and "torch" not in out and "libcudart.so" not in out
+
+
+# --------------------------------------------------------------- planner --
+
+
+def test_plan_batch_kats(atmm):
+    """test_batch.cpp:40-61."""
+    p = atmm.plan_batch([3, 3, 3])
+    assert [(s.adapter_id, s.rows) for s in p.segments] == [(3, [0, 1, 2])]
+    p = atmm.plan_batch([7, 2, 7, 2])
+    assert [(s.adapter_id, s.rows) for s in p.segments] == [(2, [1, 3]), (7, [0, 2])]
+    p = atmm.plan_batch([5, 1, 9])
+    assert [len(s.rows) for s in p.segments] == [1, 1, 1]
+    with pytest.raises(atmm.ConfigError):
+        atmm.plan_batch([])
+
+
+def test_plan_batch_bit_exact_with_oracle(atmm, oracle):
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 64, 512, 2048, 8192):
+        a = rng.integers(-3, 70, n).astype(np.int32)
+        for x, y in zip(atmm.plan_batch_csr(a), oracle.plan_batch(a)):
+            assert np.array_equal(x, y)
+
+
+def test_plan_batch_matches_reference_golden(atmm):
+    g = np.load(os.path.join(ROOT, "tests", "golden", "reference_vectors.npz"))
+    for name in ("same", "interleaved", "distinct", "random64"):
+        seg, off, rows = atmm.plan_batch_csr(g[f"plan_{name}_assignment"])
+        assert np.array_equal(seg, g[f"plan_{name}_seg"])
+        assert np.array_equal(off, g[f"plan_{name}_off"])
+        assert np.array_equal(rows, g[f"plan_{name}_rows"])
+
+
+# ---------------------------------------------------------------- tiling --
+
+
+def test_tiling_kats(atmm):
+    """test_tiling.cpp:55-87."""
+    assert [atmm.m_bucket_of(m) for m in (1, 32, 33, 4096)] == [32, 32, 64, 4096]
+    assert atmm.TilingConfig(64, 32, 32, 32, 32, 32).structurally_valid()
+    for bad in [(48, 32, 32, 16, 16, 16), (8, 32, 32, 8, 16, 16), (32, 32, 32, 64, 16, 16)]:
+        assert not atmm.TilingConfig(bad).structurally_valid()
+    t = atmm.TilingTable((32, 32, 32, 32, 32, 32))
+    stored = (64, 32, 32, 32, 32, 32)
+    t.insert(64, 256, 16, stored, 1000)
+    assert t.lookup(33, 256, 16) == stored
+    assert t.lookup(90, 256, 16) == stored
+    assert t.lookup(200, 256, 16) == (32,) * 6
+    assert t.lookup(64, 128, 16) == (32,) * 6
+    t.insert(128, 256, 16, (128, 64, 64, 32, 32, 32), 900)
+    assert t.lookup(96, 256, 16) == stored
+    with pytest.raises(atmm.ConfigError):
+        t.insert(32, 1, 1, (24, 16, 16, 8, 16, 16), 1)
+
+
+def test_tiling_lookup_matches_reference_golden(atmm):
+    with open(os.path.join(ROOT, "tests", "golden", "tiling_vectors.json")) as f:
+        g = json.load(f)
+    t = atmm.TilingTable(g["default"])
+    for e in g["entries"]:
+        t.insert(*e["key"], e["config"], 1)
+    for q in g["lookups"]:
+        assert list(t.lookup(q["m"], q["k"], q["n"])) == q["config"]
+    for m, b in g["m_bucket_of"].items():
+        assert atmm.m_bucket_of(int(m)) == b
+
+
+def test_candidate_enumeration(atmm):
+    """test_tiling.cpp:11-52: count by brute force, sortedness, budget edges."""
+    budget, width = 1 << 20, 4
+    cfgs = atmm.candidate_configs(budget, width)
+    expected = 0
+    for om in (16, 32, 64, 128, 256):
+        for on in (16, 32, 64, 128, 256):
+            for ok in (16, 32, 64, 128, 256):
+                if (om * ok + ok * on + om * on) * width > budget:
+                    continue
+                expected += sum(1 for im in (16, 32, 64, 128, 256) if im <= om for inn in (16, 32, 64, 128, 256)
+                                if inn <= on for ik in (16, 32, 64, 128, 256) if ik <= ok)
+    assert len(cfgs) == expected == 3375
+    assert cfgs == sorted(cfgs)
+    assert (64, 32, 32, 32, 32, 32) in cfgs and (64, 64, 64, 32, 64, 64) in cfgs
+    assert atmm.candidate_configs(3 * 16 * 16 * 4, 4) == [(16,) * 6]
+    with pytest.raises(atmm.ConfigError):
+        atmm.candidate_configs(3 * 16 * 16 * 4 - 1, 4)
+    dc = atmm.default_candidates(1 << 20, 4)
+    assert len(dc) >= 8 and all(c.structurally_valid() and c.footprint_elems() * 4 <= (1 << 20) for c in dc)
+
+
+def test_table_json_round_trip_and_reference_loadable(atmm, tmp_path, reference):
+    """test_tiling.cpp:89-104; the product's JSON (with the sm100 extension)
+    loads in the reference's TilingTable::load and resolves identically."""
+    import ctypes
+
+    t = atmm.TilingTable((64, 32, 32, 32, 32, 32))
+    t.insert(256, 4096, 32, (64, 32, 32, 32, 32, 32), 70000)
+    t.insert(8192, 4096, 128, (64, 64, 64, 32, 64, 64), 100000, sm100=(128, 8, 128, 3))
+    path = str(tmp_path / "table.json")
+    t.save(path)
+    back = atmm.TilingTable.load(path)
+    assert len(back) == 2
+    assert back.lookup(256, 4096, 32) == (64, 32, 32, 32, 32, 32)
+    assert back.lookup(8192, 4096, 128) == (64, 64, 64, 32, 64, 64)
+    assert back.resolve_launch(8192, 4096, 128, 4096) == (128, 8, 128, 3)
+    for (m, k, n) in [(256, 4096, 32), (8192, 4096, 128), (5, 5, 5), (8000, 4096, 128)]:
+        out = np.zeros(6, np.int32)
+        st = reference.L.ref_table_load_lookup(path.encode(), m, k, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+        assert st == 0
+        assert tuple(out) == back.lookup(m, k, n)
+
+
+def test_table_load_errors(atmm, tmp_path):
+    p = tmp_path / "bad.json"
+    p.write_text("{not json")
+    with pytest.raises(atmm.IoError):
+        atmm.TilingTable.load(str(p))
+    p.write_text('{"default": [1, 2, 3], "entries": []}')
+    with pytest.raises(atmm.IoError):
+        atmm.TilingTable.load(str(p))
+    p.write_text('{"default": [24, 16, 16, 8, 16, 16], "entries": []}')
+    with pytest.raises(atmm.ConfigError):
+        atmm.TilingTable.load(str(p))
+    with pytest.raises(atmm.IoError):
+        atmm.TilingTable.load(str(tmp_path / "missing.json"))
+
+
+def test_launch_resolution(atmm):
+    """B200 reading of the six edges and the heuristic default."""
+    t = atmm.TilingTable()
+    tm, c, bn, st = t.resolve_launch(32, 4096, 16, 4096)
+    assert (tm, c) == (128, 8) and bn in (64, 128, 256)
+    t2 = atmm.TilingTable((64, 256, 1024, 64, 16, 64))
+    assert t2.resolve_launch(32, 4096, 16, 4096) == (64, 4, 256, 0)
+    t2.insert(32, 4096, 16, (128, 128, 512, 128, 16, 64), 5)
+    assert t2.resolve_launch(20, 4096, 16, 4096) == (128, 8, 128, 0)
+    with pytest.raises(atmm.ConfigError):
+        t2.insert(32, 4096, 16, (128, 128, 512, 128, 16, 64), 5, sm100=(128, 17, 128, 0))
+
+
+# -------------------------------------------------------------- sharding --
+
+
+def test_shard_rows_lpt(atmm):
+    from paper_2411_00915_b200.sharding import shard_batch, shard_cost
+    from paper_2411_00915_b200.workloads import bypass_config
+
+    w = bypass_config("cfg3")
+    for world in (1, 2, 4, 8):
+        shards = shard_batch(w.assignment, w.ranks, w.d_in, w.d_out, world)
+        allrows = np.sort(np.concatenate([s.rows for s in shards]))
+        assert np.array_equal(allrows, np.arange(w.tokens))
+        for s in shards:  # whole segments stay together
+            for a in s.adapters:
+                assert np.count_nonzero(w.assignment[s.rows] == a) == w.lengths[a]
+        costs = [shard_cost(s, w.ranks, w.d_in, w.d_out) for s in shards]
+        biggest = max(w.lengths[a] * (6.0 * w.d_in) + 2.0 * w.ranks[a] * 2 * w.d_in for a in w.ranks)
+        assert max(costs) - min(costs) <= biggest + 1e-6  # LPT bound
+        again = shard_batch(w.assignment, w.ranks, w.d_in, w.d_out, world)
+        assert all(np.array_equal(x.rows, y.rows) for x, y in zip(shards, again))
+    with pytest.raises(atmm.UnknownAdapterError):
+        atmm.shard_rows([1, 2], {1: 16}, 64, 64, 2)
+
+
+# ------------------------------------------------------------- no device --
+
+
+def test_compute_fails_loudly_without_device(atmm):
+    if atmm.device_count() > 0:
+        pytest.skip("a device is present")
+    with pytest.raises(atmm.NoDeviceError):
+        atmm.AdapterRegistry(1, 64, 64)
+    with pytest.raises(atmm.NoDeviceError):
+        atmm.atmm_multiply(np.ones((2, 2)), np.ones((2, 2)), (16,) * 6)
+
+
+# -------------------------------------------------------------- C++ shim --
+
+
+def _build_shim(tmp_path):
+    exe = tmp_path / "shim_test"
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp", "shim_test.cpp"),
+           "-L", os.path.dirname(LIB), "-l:libatmm_b200.so", f"-Wl,-rpath,{os.path.dirname(LIB)}", "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return exe
+
+
+def test_cpp_shim_host_cases(tmp_path):
+    exe = _build_shim(tmp_path)
+    out = subprocess.run([str(exe), "host"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
