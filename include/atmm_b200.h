@@ -179,6 +179,15 @@ int atmm_run_bypass_host(atmm_registry* r, const float* x, int64_t n,
 int atmm_bypass_residual_host_bf16(const atmm_plan* p, int64_t layer, const uint16_t* x_host,
                                    uint16_t* y_host, float scale, void* stream);
 
+/* Serving form of the above: `count` micro-batches on the same plan, each with
+ * its own host buffers (pinned for overlap), pipelined over two streams and
+ * two device staging slots so the H2D of batch i+1 overlaps the kernel and
+ * the D2H of batch i.  Returns when every y_hosts[i] holds its result. */
+int atmm_bypass_residual_host_bf16_pipelined(const atmm_plan* p, const int64_t* layers,
+                                             const uint16_t* const* x_hosts,
+                                             uint16_t* const* y_hosts, int64_t count,
+                                             float scale);
+
 /* ===================================================================== */
 /* Merge / unmerge  W +-= s . down . up   (model.hpp:120-188)             */
 /* ===================================================================== */

@@ -32,6 +32,7 @@ from .atmm import (  # noqa: F401
     merge_into,
     plan_batch,
     plan_batch_csr,
+    residual_host_bf16_pipelined,
     run_bypass,
     shard_rows,
 )

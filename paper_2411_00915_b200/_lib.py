@@ -59,6 +59,7 @@ _SIGS = {
     "atmm_bypass_apply": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int, c_float, c_void_p]),
     "atmm_run_bypass_host": (c_int, [c_void_p, f32p, c_int64, i32p, c_int64, c_void_p, f32p]),
     "atmm_bypass_residual_host_bf16": (c_int, [c_void_p, c_int64, u16p, u16p, c_float, c_void_p]),
+    "atmm_bypass_residual_host_bf16_pipelined": (c_int, [c_void_p, i64p, POINTER(c_void_p), POINTER(c_void_p), c_int64, c_float]),
     "atmm_merge_apply": (c_int, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int, c_float, c_void_p]),
     "atmm_delta_w_host": (c_int, [c_void_p, c_int32, c_int64, f32p]),
     "atmm_multiply_host": (c_int, [f32p, c_int64, c_int64, f32p, c_int64, f32p, i32p]),

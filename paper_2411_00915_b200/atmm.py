@@ -365,6 +365,21 @@ class BypassPlan:
                                                   float(scale), _stream_ptr(stream)))
 
 
+def residual_host_bf16_pipelined(plan: "BypassPlan", xs, ys, layers, scale: float = 1.0) -> None:
+    """Serving form: one micro-batch per (x, y) host pair (uint16 bf16 bit
+    patterns, pinned for overlap), pipelined H2D / kernel / D2H."""
+    count = len(xs)
+    if len(ys) != count or len(layers) != count:
+        raise ShapeError("xs, ys and layers must have the same length")
+    for x, y in zip(xs, ys):
+        if x.dtype != np.uint16 or y.dtype != np.uint16 or not (x.flags.c_contiguous and y.flags.c_contiguous):
+            raise ShapeError("host buffers must be C-contiguous uint16 (bf16 bit patterns)")
+    xp = (ctypes.c_void_p * count)(*[x.ctypes.data for x in xs])
+    yp = (ctypes.c_void_p * count)(*[y.ctypes.data for y in ys])
+    la = np.ascontiguousarray(np.asarray(layers, np.int64))
+    _check(lib.atmm_bypass_residual_host_bf16_pipelined(plan.handle, _p(la, i64p), xp, yp, count, float(scale)))
+
+
 def run_bypass(registry: AdapterRegistry, x, assignment: Sequence[int], layer: int = 0,
                table: Optional[TilingTable] = None) -> np.ndarray:
     """batch.hpp:48: returns the fresh bypass matrix (host fp32 in/out)."""

@@ -781,6 +781,43 @@ int atmm_bypass_residual_host_bf16(const atmm_plan* p, int64_t layer, const uint
   });
 }
 
+int atmm_bypass_residual_host_bf16_pipelined(const atmm_plan* p, const int64_t* layers,
+                                             const uint16_t* const* x_hosts, uint16_t* const* y_hosts,
+                                             int64_t count, float scale) {
+  return guarded([&] {
+    if (!p || !layers || !x_hosts || !y_hosts || count < 0) fail(ATMM_ERR_CONFIG, "null plan or buffers");
+    const atmm_registry* r = p->reg;
+    DeviceGuard g(r->device);
+    const int64_t ldx = round_up(r->d_in, 8), ldy = round_up(r->d_out, 8);
+    const size_t nx = static_cast<size_t>(p->n * ldx), ny = static_cast<size_t>(p->n * ldy);
+    struct Slot {
+      DevBuf<uint16_t> x, y;
+      cudaStream_t s = nullptr;
+    };
+    thread_local std::vector<std::unique_ptr<Slot>> slots;
+    thread_local int slots_dev = -1;
+    if (slots_dev != r->device) slots.clear();
+    slots_dev = r->device;
+    while (slots.size() < 2) {
+      auto s = std::make_unique<Slot>();
+      CUDA_CHECK(cudaStreamCreateWithFlags(&s->s, cudaStreamNonBlocking));
+      slots.push_back(std::move(s));
+    }
+    for (auto& s : slots) {
+      if (s->x.n < nx) s->x.alloc(nx);
+      if (s->y.n < ny) s->y.alloc(ny);
+    }
+    for (int64_t i = 0; i < count; ++i) {
+      Slot& s = *slots[static_cast<size_t>(i & 1)];
+      CUDA_CHECK(cudaMemcpy2DAsync(s.x.p, ldx * 2, x_hosts[i], r->d_in * 2, r->d_in * 2, p->n, cudaMemcpyHostToDevice, s.s));
+      CUDA_CHECK(cudaMemcpy2DAsync(s.y.p, ldy * 2, y_hosts[i], r->d_out * 2, r->d_out * 2, p->n, cudaMemcpyHostToDevice, s.s));
+      apply_plan(p, layers[i], s.x.p, ldx, s.y.p, ldy, ATMM_BF16, scale, s.s);
+      CUDA_CHECK(cudaMemcpy2DAsync(y_hosts[i], r->d_out * 2, s.y.p, ldy * 2, r->d_out * 2, p->n, cudaMemcpyDeviceToHost, s.s));
+    }
+    for (auto& s : slots) CUDA_CHECK(cudaStreamSynchronize(s->s));
+  });
+}
+
 int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* w, int64_t ldw,
                      int w_dtype, float sign, void* stream) {
   return guarded([&] {

@@ -199,3 +199,30 @@ def test_unaligned_y_rows(gpu, atmm, oracle):
         plan.apply(xt, yt)
         torch.cuda.synchronize()
         assert np.max(np.abs(yt.float().cpu().numpy() - want)) <= tol_for(want), dtype
+
+
+def test_pipelined_host_residual(gpu, atmm, oracle):
+    """Serving path: micro-batches through pinned host buffers, H2D/kernel/D2H pipelined."""
+    import torch
+
+    d, n = 256, 64
+    reg, facs = _setup(atmm, oracle, d, d, {1: 16, 2: 32}, L=2)
+    assignment = np.asarray([1, 2] * (n // 2), np.int32)
+    plan = atmm.BypassPlan(reg, assignment)
+    xs, ys, wants, layers = [], [], [], []
+    for i in range(5):
+        x = oracle.round_bf16(oracle.random_matrix(oracle.rng(100 + i), n, d))
+        y0 = oracle.round_bf16(oracle.random_matrix(oracle.rng(200 + i), n, d))
+        layer = i % 2
+        want = y0.astype(np.float64) + oracle.bypass_rows_f64(
+            x, assignment, {a: (f[0][layer], f[1][layer]) for a, f in facs.items()})
+        xt = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
+        yt = torch.from_numpy(y0).to(torch.bfloat16).pin_memory()
+        xs.append(xt.view(torch.int16).numpy().view(np.uint16))
+        ys.append(yt.view(torch.int16).numpy().view(np.uint16))
+        wants.append((want, yt))
+        layers.append(layer)
+    atmm.residual_host_bf16_pipelined(plan, xs, ys, layers)
+    for want, yt in wants:
+        got = yt.float().numpy()
+        assert np.max(np.abs(got - want)) <= tol_for(want)
