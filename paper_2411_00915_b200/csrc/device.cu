@@ -29,6 +29,8 @@ cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensor
 int bypass_max_active_clusters(int C, size_t smem);
 cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t smem,
                          cudaStream_t stream);
+cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const MergeParams& p, int grid,
+                             size_t smem, cudaStream_t stream);
 cudaError_t launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t rows, int64_t cols,
                                int64_t lds, int64_t ldd, cudaStream_t stream);
 
@@ -129,6 +131,23 @@ CUtensorMap make_y_map(const void* y, int64_t n, int64_t d_out, int64_t ldy, int
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(Y) failed: " + std::to_string(r));
   return m;
+}
+
+// W (m x n, bf16 or fp32, row stride ldw) for the TMA-staged merge: box =
+// 128 rows x one 128-byte column slab, 128-byte swizzle (loads and stores).
+CUtensorMap make_w_map(void* w, int64_t m, int64_t n, int64_t ldw, int w_dtype) {
+  CUtensorMap map;
+  const int64_t esz = w_dtype == ATMM_BF16 ? 2 : 4;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldw * esz)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(kTileM)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&map, w_dtype == ATMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 2, w, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(W) failed: " + std::to_string(r));
+  return map;
 }
 
 // ---- host packing into the tcgen05 operand layouts ----
@@ -514,6 +533,36 @@ static void run_merge(const uint16_t* a_t, const uint16_t* b_t, int64_t m, int64
   const int64_t wsz = w_dtype == ATMM_BF16 ? 2 : 4;
   mp.w_vec = ((ldw * wsz) % 16 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0) ? 1 : 0;
   const int64_t a_bytes = int64_t(kTileM) * k_pad * 2;
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (mp.w_vec) {
+    // TMA-staged W: 128-column chunks (two TMEM accumulators of 128 columns),
+    // two B stages, and every remaining byte of shared memory as W slabs.
+    mp.bn = 128;
+    mp.num_nchunks = static_cast<int32_t>((round_up(n, 32) + mp.bn - 1) / mp.bn);
+    mp.slab_cols = static_cast<int32_t>(128 / wsz);
+    mp.b_stage_bytes = static_cast<uint32_t>(round_up(int64_t(mp.bn) * k_pad * 2, 1024));
+    mp.stages = 2;
+    mp.off_b = static_cast<uint32_t>(round_up(a_bytes, 1024));
+    mp.off_w = static_cast<uint32_t>(mp.off_b + int64_t(mp.stages) * mp.b_stage_bytes);
+    const int64_t slab = int64_t(kTileM) * 128;
+    auto total_w = [&](int sw) {
+      return size_t(1024 + mp.off_w + int64_t(sw) * slab + round_up((2 * mp.stages + 6 + 2 * sw) * 8 + 8, 16));
+    };
+    int sw = 12;
+    while (sw > 2 && total_w(sw) > kSmemLimit) --sw;
+    mp.w_stages = sw;
+    mp.off_bar = static_cast<uint32_t>(mp.off_w + int64_t(sw) * slab);
+    mp.tmem_cols = 256;
+    const int64_t tiles = int64_t(mp.num_mtiles) * mp.num_nchunks;
+    const int grid = static_cast<int>(std::min<int64_t>(tiles, sms));
+    const CUtensorMap tmap_w = make_w_map(w, m, n, ldw, w_dtype);
+    const cudaError_t e = launch_merge_tma(w_dtype, tmap_w, mp, grid, total_w(sw), stream);
+    if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("merge launch failed: ") + cudaGetErrorString(e));
+    return;
+  }
   mp.b_stage_bytes = static_cast<uint32_t>(round_up(int64_t(mp.bn) * k_pad * 2, 1024));
   int stages = 4;
   auto total = [&](int s) {
@@ -529,10 +578,6 @@ static void run_merge(const uint16_t* a_t, const uint16_t* b_t, int64_t m, int64
   size_t smem = total(stages);
   const int max_co = std::max(1, 512 / cols);
   while (static_cast<int>(kSmemPerSM / (smem + 1024)) > max_co) smem += 4096;
-  int sms = 148;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = int64_t(mp.num_mtiles) * mp.num_nchunks;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, sms));
   const cudaError_t e = launch_merge(w_dtype, mp, grid, smem, stream);

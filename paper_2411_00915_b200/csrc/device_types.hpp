@@ -102,6 +102,11 @@ struct MergeParams {
   uint32_t b_stage_bytes;
   uint32_t tmem_cols;
   int32_t w_vec;        // 1: W rows 16-byte aligned -> 128-bit epilogue accesses
+  // TMA-staged W (atmm_merge_tma_kernel): W moves through an smem ring of
+  // 128-row x 128-byte slabs (128-byte swizzle), loaded and stored by TMA.
+  int32_t w_stages;
+  uint32_t off_w;
+  int32_t slab_cols;    // W columns per slab (64 bf16 / 32 fp32)
   int32_t pad0;
 };
 

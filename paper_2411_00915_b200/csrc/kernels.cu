@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
       }
       if (c + U < num_chunks) issue_up(c + U);
     }
+    if (lane == 0) TRACE(29);
     __syncwarp();
     cluster_wait();
   } else if (warp == kWarpMMA) {
@@ -666,13 +667,16 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
         continue;
       }
       const int buf = c % NB;
+      const int kown = c / p.rep;  // this warp's k-th chunk (trace slots 14 + 3k)
       mbar_wait(&acc_full[buf], static_cast<uint32_t>((c / NB) & 1));
       tc_fence_after();
       if (tracer && c == 0) TRACE(11);
+      if (tracer && kown < 5) TRACE(14 + 3 * kown);
       if (p.y_ring) {
         for (int sub = 0; sub < bn_c; sub += ycols, ++ysub) {
           const int yb = ysub % NY;
           mbar_wait(&y_full[yb], static_cast<uint32_t>((ysub / NY) & 1));
+          if (tracer && kown < 5 && sub == 0) TRACE(15 + 3 * kown);
           const uint32_t bufs = ybuf_s + static_cast<uint32_t>(yb) * p.ybuf_bytes;
           if (ewarp) {
             uint32_t v[64];
@@ -706,6 +710,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
           __syncwarp();
           if (lane == 0) mbar_arrive(&y_empty[yb]);
         }
+        if (tracer && kown < 5) TRACE(16 + 3 * kown);
       } else if (ewarp) {
         for (int sub = 0; sub < bn_c; sub += 32) {
           uint32_t v[32];
@@ -895,6 +900,248 @@ __global__ void __launch_bounds__(kMergeThreads, 1) atmm_merge_kernel(const Merg
   }
 }
 
+// =========================================================================
+// TMA-staged merge / GEMM kernel:  W = beta*W + alpha * A . B
+// Same tiles and MMA pipeline as atmm_merge_kernel, but W streams through
+// shared memory: warp 0 TMA-loads 128-row x 128-byte W slabs (128-byte
+// swizzle) into a ring as far ahead as the ring allows (W does not depend on
+// the MMA), the epilogue updates its row of the slab in place from TMEM and
+// one elected thread TMA-stores the slab back.  HBM sees one streaming read
+// and one streaming write of W with ~w_stages x 16 KiB in flight per SM.
+// Warps: 0 = TMA producer, 1 = TMEM owner + MMA issuer, 2..5 = epilogue
+// (warp w reads TMEM lanes 32*(w%4)..+31).
+// =========================================================================
+template <typename WT>
+__device__ __forceinline__ void slab_update(uint32_t row_saddr, uint32_t i, float alpha, bool load,
+                                            const uint32_t (&acc)[64]);
+template <>
+__device__ __forceinline__ void slab_update<__nv_bfloat16>(uint32_t row_saddr, uint32_t i, float alpha,
+                                                           bool load, const uint32_t (&acc)[64]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t a = row_saddr + ((static_cast<uint32_t>(q) ^ (i & 7u)) << 4);
+    const uint4 y = load ? ld_shared_v4(a) : make_uint4(0, 0, 0, 0);
+    const uint32_t w[4] = {y.x, y.y, y.z, y.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float lo = fmaf(alpha, __uint_as_float(acc[q * 8 + 2 * e]), bf16lo(w[e]));
+      const float hi = fmaf(alpha, __uint_as_float(acc[q * 8 + 2 * e + 1]), bf16hi(w[e]));
+      o[e] = pack_bf16x2(lo, hi);
+    }
+    st_shared_v4(a, o[0], o[1], o[2], o[3]);
+  }
+}
+template <>
+__device__ __forceinline__ void slab_update<float>(uint32_t row_saddr, uint32_t i, float alpha, bool load,
+                                                   const uint32_t (&acc)[64]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t a = row_saddr + ((static_cast<uint32_t>(q) ^ (i & 7u)) << 4);
+    const uint4 y = load ? ld_shared_v4(a) : make_uint4(0, 0, 0, 0);
+    st_shared_v4(a, __float_as_uint(fmaf(alpha, __uint_as_float(acc[4 * q + 0]), __uint_as_float(y.x))),
+                 __float_as_uint(fmaf(alpha, __uint_as_float(acc[4 * q + 1]), __uint_as_float(y.y))),
+                 __float_as_uint(fmaf(alpha, __uint_as_float(acc[4 * q + 2]), __uint_as_float(y.z))),
+                 __float_as_uint(fmaf(alpha, __uint_as_float(acc[4 * q + 3]), __uint_as_float(y.w))));
+  }
+}
+
+template <typename WT>
+__global__ void __launch_bounds__(kMergeThreads, 1)
+    atmm_merge_tma_kernel(const __grid_constant__ CUtensorMap tmap_w, const MergeParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const int S = p.stages;
+  const int SW = p.w_stages;
+  const int kp = p.k_pad;
+  const int kg = kp / 8;
+  const int sc = p.slab_cols;
+  constexpr uint32_t kSlabBytes = kTileM * 128u;
+  const bool load_w = p.beta != 0.0f;
+
+  uint8_t* a_buf = smem;
+  uint8_t* b_ring = smem + p.off_b;
+  uint8_t* w_ring = smem + p.off_w;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* full = bars;                  // [S]
+  uint64_t* empty = full + S;             // [S]
+  uint64_t* a_full = empty + S;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* acc_full = a_empty + 1;       // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint64_t* w_full = acc_empty + 2;       // [SW]
+  uint64_t* w_empty = w_full + SW;        // [SW]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_empty + SW);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);
+    }
+    for (int s = 0; s < SW; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.num_mtiles * p.num_nchunks;
+  const int n32 = ((p.n + 31) / 32) * 32;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmap_w);
+      int stage = 0;
+      uint32_t phase = 0;
+      int cur_mt = -1;
+      uint32_t a_phase = 0;
+      int j = 0;  // W slab sequence number
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int mt = t / p.num_nchunks;
+        const int nc = t - mt * p.num_nchunks;
+        const int n0 = nc * p.bn;
+        const int bn_c = min(p.bn, n32 - n0);
+        if (mt != cur_mt) {
+          mbar_wait(a_empty, a_phase ^ 1u);
+          mbar_arrive_expect_tx(a_full, static_cast<uint32_t>(128 * kp * 2));
+          for (int h = 0; h < 2; ++h) {
+            const int64_t kb = static_cast<int64_t>(mt) * 2 + h;
+            for (int g = 0; g < kg; ++g) {
+              bulk_g2s(a_buf + g * 2048 + h * 1024, p.a_t + (kb * kg + g) * 512, 1024u, a_full);
+            }
+          }
+          a_phase ^= 1u;
+          cur_mt = mt;
+        }
+        mbar_wait(&empty[stage], phase ^ 1u);
+        mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(bn_c * kp * 2));
+        bulk_g2s(b_ring + static_cast<size_t>(stage) * p.b_stage_bytes, p.b_t + static_cast<int64_t>(n0) * kp,
+                 static_cast<uint32_t>(bn_c * kp * 2), &full[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+        const int nslab = (min(bn_c, p.n - n0) + sc - 1) / sc;
+        for (int sl = 0; sl < nslab; ++sl, ++j) {
+          const int b = j % SW;
+          mbar_wait(&w_empty[b], static_cast<uint32_t>((j / SW) & 1) ^ 1u);
+          if (load_w) {
+            mbar_arrive_expect_tx(&w_full[b], kSlabBytes);
+            tma_load_2d(w_ring + static_cast<size_t>(b) * kSlabBytes, &tmap_w, &w_full[b], n0 + sl * sc,
+                        mt * kTileM);
+          } else {
+            mbar_arrive(&w_full[b]);  // overwrite mode: the slab buffer is merely free
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int cur_mt = -1;
+      uint32_t a_phase = 0;
+      int local = 0;
+      const uint32_t a0 = smem_u32(a_buf);
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        const int mt = t / p.num_nchunks;
+        const int nc = t - mt * p.num_nchunks;
+        const int n0 = nc * p.bn;
+        const int bn_c = min(p.bn, n32 - n0);
+        const int next_t = t + static_cast<int>(gridDim.x);
+        const bool last_of_a = next_t >= num_tiles || (next_t / p.num_nchunks) != mt;
+        if (mt != cur_mt) {
+          mbar_wait(a_full, a_phase);
+          a_phase ^= 1u;
+          cur_mt = mt;
+        }
+        const int buf = local & 1;
+        mbar_wait(&acc_empty[buf], ((local >> 1) & 1) ^ 1u);
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t b0 = smem_u32(b_ring + static_cast<size_t>(stage) * p.b_stage_bytes);
+        const uint32_t idesc = idesc_bf16(kTileM, static_cast<uint32_t>(bn_c), 1u, 0u);
+        for (int kk = 0; kk < kp / 16; ++kk) {
+          const uint64_t ad = smem_desc(a0 + kk * 4096u, 2048u, 128u, kLayoutNone);
+          const uint64_t bd = smem_desc(b0 + kk * 256u, 128u, static_cast<uint32_t>(kp) * 16u, kLayoutNone);
+          mma_bf16(tmem_base + static_cast<uint32_t>(buf * p.bn), ad, bd, idesc, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&empty[stage]);
+        mma_commit(&acc_full[buf]);
+        if (last_of_a) mma_commit(a_empty);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const uint32_t quad = warp & 3u;
+    const uint32_t lane_addr = (quad * 32u) << 16;
+    const uint32_t row = quad * 32u + lane;  // row within the 128-row tile
+    const bool leader = warp == 2 && lane == 0;
+    const uint32_t w0 = smem_u32(w_ring);
+    int local = 0;
+    int j = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+      const int mt = t / p.num_nchunks;
+      const int nc = t - mt * p.num_nchunks;
+      const int n0 = nc * p.bn;
+      const int bn_c = min(p.bn, n32 - n0);
+      const int nslab = (min(bn_c, p.n - n0) + sc - 1) / sc;
+      const int buf = local & 1;
+      mbar_wait(&acc_full[buf], (local >> 1) & 1);
+      tc_fence_after();
+      for (int sl = 0; sl < nslab; ++sl, ++j) {
+        const int b = j % SW;
+        uint32_t v[64];
+        const uint32_t ta = tmem_base + lane_addr + static_cast<uint32_t>(buf * p.bn + sl * sc);
+        tmem_ld32(ta, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        if (sc == 64) tmem_ld32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        mbar_wait(&w_full[b], static_cast<uint32_t>((j / SW) & 1));
+        tmem_wait_ld();
+        const uint32_t slab = w0 + static_cast<uint32_t>(b) * kSlabBytes;
+        slab_update<WT>(slab + row * 128u, row, p.alpha, load_w, v);
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA store
+        named_bar_sync(1, 128);
+        if (leader) {
+          tma_store_2d(&tmap_w, w_ring + static_cast<size_t>(b) * kSlabBytes, n0 + sl * sc, mt * kTileM);
+          bulk_commit();
+          // The previous slab's store has finished reading smem: release it.
+          bulk_wait_read<1>();
+          if (j > 0) mbar_arrive(&w_empty[(j - 1) % SW]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+    if (leader) bulk_wait0();
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
 // ---------------------------------------------------------------- utils --
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, uint16_t* __restrict__ dst,
                                    int64_t rows, int64_t cols, int64_t lds, int64_t ldd) {
@@ -917,6 +1164,9 @@ template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUten
                                                    const BypassParams);
 template __global__ void atmm_merge_kernel<float>(const MergeParams);
 template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
+template __global__ void atmm_merge_tma_kernel<float>(const __grid_constant__ CUtensorMap, const MergeParams);
+template __global__ void atmm_merge_tma_kernel<__nv_bfloat16>(const __grid_constant__ CUtensorMap,
+                                                              const MergeParams);
 
 }  // namespace atmm
 
@@ -1031,6 +1281,22 @@ cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t sme
   cudaError_t e = prepare(k, smem, false);
   if (e != cudaSuccess) return e;
   k<<<grid, kMergeThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const MergeParams& p, int grid,
+                             size_t smem, cudaStream_t stream) {
+  if (w_dtype == 0) {
+    auto k = atmm_merge_tma_kernel<__nv_bfloat16>;
+    cudaError_t e = prepare(k, smem, false);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kMergeThreads, smem, stream>>>(tmap_w, p);
+    return cudaGetLastError();
+  }
+  auto k = atmm_merge_tma_kernel<float>;
+  cudaError_t e = prepare(k, smem, false);
+  if (e != cudaSuccess) return e;
+  k<<<grid, kMergeThreads, smem, stream>>>(tmap_w, p);
   return cudaGetLastError();
 }
 

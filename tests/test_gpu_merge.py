@@ -147,3 +147,32 @@ def test_atmm_multiply_kat_and_errors(gpu, atmm):
         atmm.atmm_multiply(np.zeros((4, 5)), np.zeros((4, 5)), (16, 16, 16, 16, 16, 16))
     with pytest.raises(atmm.ConfigError):
         atmm.atmm_multiply(np.zeros((4, 5)), np.zeros((5, 4)), (24, 16, 16, 8, 16, 16))
+
+
+@pytest.mark.parametrize("w_dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("d_in,d_out,pad", [(200, 136, 8), (300, 520, 0), (128, 4104, 24)])
+def test_merge_tma_staged_strided(gpu, atmm, oracle, w_dtype, d_in, d_out, pad):
+    """TMA-staged W path: partial 128-row tiles, partial slabs, a row stride
+    wider than d_out; the padding columns must stay untouched."""
+    import torch
+
+    r = 32
+    rng = oracle.rng(d_in * 7 + d_out)
+    s = 1.0 / np.sqrt(np.float32(r))
+    down = oracle.round_bf16(oracle.random_matrix(rng, d_in, r, -s, s))
+    up = oracle.round_bf16(oracle.random_matrix(rng, r, d_out, -s, s))
+    base = oracle.random_matrix(rng, d_in, d_out + pad, -0.05, 0.05)
+    if w_dtype == "bf16":
+        base = oracle.round_bf16(base)
+    reg = atmm.AdapterRegistry(1, d_in, d_out)
+    reg.put(1, down, up, scale=2.0)
+    dt = torch.float32 if w_dtype == "f32" else torch.bfloat16
+    full = torch.from_numpy(base).to("cuda", dt)
+    view = full[:, :d_out]
+    atmm.merge_into(reg, 1, 0, view, sign=+1.0)
+    torch.cuda.synchronize()
+    got = full.float().cpu().numpy()
+    want = base[:, :d_out].astype(np.float64) + 2.0 * oracle.gemm_reference_f64(down, up)
+    tol = 1e-4 * max(1.0, np.max(np.abs(want))) if w_dtype == "f32" else tol_for(want)
+    assert np.max(np.abs(got[:, :d_out] - want)) <= tol
+    assert np.array_equal(got[:, d_out:], base[:, d_out:].astype(np.float32))

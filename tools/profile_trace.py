@@ -17,7 +17,8 @@ EVENTS = ["start", "cluster_synced", "prod_shrink_issued", "mma_first_full", "mm
           "epi_shrink_full", "epi_partials_sent", "owner_red_full", "owner_bcast_done", "mma_mid_full",
           "mma_expand_issued", "epi_first_acc", "epi_done", "end"]
 for _c in range(5):
-    EVENTS += [f"c{_c}_begin", f"c{_c}_acc_empty_ok", f"c{_c}_up_full_ok"]
+    EVENTS += [f"w0_chunk{_c}_acc_full", f"w0_chunk{_c}_y_full", f"w0_chunk{_c}_stored"]
+EVENTS += ["y_producer_done"]
 NEV = 32
 
 
