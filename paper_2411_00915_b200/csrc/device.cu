@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -29,6 +30,8 @@ cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensor
 int bypass_max_active_clusters(int C, size_t smem);
 cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t smem,
                          cudaStream_t stream);
+cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const BypassParams& p, int C, int num_tiles,
+                              size_t smem, cudaStream_t stream);
 cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const MergeParams& p, int grid,
                              size_t smem, cudaStream_t stream);
 cudaError_t launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t rows, int64_t cols,
@@ -262,7 +265,16 @@ struct atmm_registry {
 // Plan: routing tables + launch groups
 // =========================================================================
 namespace atmm {
+// Shared-memory / TMEM layout of one atmm_bypass_a2a_kernel launch.
+struct A2aLayout {
+  bool ok = false;
+  int32_t stages = 0, stage_bytes = 0, a_bytes = 0, ypitch = 0, gcols = 1;
+  uint32_t off_up = 0, off_y = 0, off_red = 0, off_mid = 0, off_bar = 0, tmem_cols = 0;
+  size_t smem = 0;
+};
+
 struct LaunchGroup {
+  A2aLayout a2a[2];  // per Y dtype (ATMM_BF16, ATMM_F32)
   int32_t cluster = 1, bn = 128, stages = 2, ustages = 1, ny = 2;
   int32_t a_bytes = 0, ustage_bytes = 0, ybuf_bytes = 0, rep = 1, nbuf = 2;
   uint32_t off_up = 0, off_y = 0;
@@ -368,6 +380,75 @@ static void resolve_group(LaunchGroup& g, int64_t d_in, int64_t d_out, int32_t t
 }
 }  // namespace atmm
 
+// All-to-all variant eligibility and layout (kernels.cu atmm_bypass_a2a_kernel):
+//   [ring: S x (rows8 x 128 B X | 64 x r_pad down^T)][up^T slice][Y slice: rows x slice x esz]
+//   [red: C x rows x r_pad fp32][mid: rows16 x r_pad bf16][mbarriers]
+// The shrink (M = 128) over-reads 16 KiB from each stage base and the expand
+// (M = 128) 128 up^T rows from each group base; both land inside the
+// allocation (guard) and feed TMEM lanes that are never read.
+static A2aLayout resolve_a2a(int64_t d_in, int64_t d_out, int32_t cluster, int32_t rows_max, int32_t r_pad,
+                             int64_t esz) {
+  A2aLayout l;
+  if (std::getenv("ATMM_DISABLE_A2A")) return l;
+  if (rows_max > kTileM || d_out % 8 != 0) return l;
+  const int64_t nkb = (d_in + kBK - 1) / kBK;
+  const int64_t nun = (d_out + kNUnit - 1) / kNUnit;
+  const int64_t slice = (nun + cluster - 1) / cluster * kNUnit;
+  const int64_t kb_per_cta = (nkb + cluster - 1) / cluster;
+  const int64_t rows8 = round_up(std::max<int32_t>(rows_max, 1), 8);
+  const int64_t rows16 = round_up(std::max<int32_t>(rows_max, 1), 16);
+  // G expand MMAs of 128 output columns; epilogue threads own G adjacent columns.
+  int32_t G = 1;
+  while (int64_t(G) * kTileM < slice) G <<= 1;
+  if (G > 8) return l;
+  int32_t cols = 32;
+  while (cols < std::max<int64_t>({int64_t(r_pad), int64_t(G) * rows16})) cols <<= 1;
+  if (cols > 512) return l;
+  l.gcols = G;
+  l.a_bytes = static_cast<int32_t>(rows8 * 128);
+  const int64_t stage = round_up(rows8 * 128 + int64_t(r_pad) * kBK * 2, 1024);
+  l.stage_bytes = static_cast<int32_t>(stage);
+  l.ypitch = static_cast<int32_t>(round_up(slice * esz, 16));
+  const int64_t up = round_up(int64_t(G) * kTileM * r_pad * 2, 1024);
+  const int64_t ybuf = round_up(int64_t(rows_max) * l.ypitch, 1024);
+  const int64_t red = round_up(int64_t(cluster) * rows_max * r_pad * 4, 1024);
+  // mid (rows16 x r_pad bf16) aliases ring stage 0 (dead once the shrink is done)
+  if (rows16 * r_pad * 2 > stage) return l;
+  auto total = [&](int64_t S) {
+    const int64_t bar = round_up((2 * S + 6) * 8 + 8, 16);
+    const int64_t body = S * stage + up + ybuf + red + bar;
+    const int64_t guard_a = (S - 1) * stage + kTileM * 128;  // shrink A over-read (M = 128)
+    return size_t(1024 + std::max(body, guard_a));
+  };
+  // Prefer a layout that fits two CTAs per SM (the next launch's prologue
+  // overlaps this one under programmatic dependent launch), then depth.
+  int64_t s_first = std::min<int64_t>(kb_per_cta, 8);
+  if (cols <= 256) {
+    for (int64_t S = s_first; S >= std::min<int64_t>(4, kb_per_cta); --S) {
+      if (total(S) <= kSmemPerSM / 2 - 1024) {
+        s_first = S;
+        break;
+      }
+    }
+  }
+  for (int64_t S = s_first; S >= std::min<int64_t>(2, kb_per_cta); --S) {
+    if (total(S) > kSmemLimit) continue;
+    l.stages = static_cast<int32_t>(S);
+    l.off_up = static_cast<uint32_t>(S * stage);
+    l.off_y = static_cast<uint32_t>(l.off_up + up);
+    l.off_red = static_cast<uint32_t>(l.off_y + ybuf);
+    l.off_mid = 0;
+    l.off_bar = static_cast<uint32_t>(l.off_red + red);
+    l.tmem_cols = static_cast<uint32_t>(cols);
+    l.smem = total(S);
+    const int max_co = std::max(1, 512 / cols);
+    while (static_cast<int>(kSmemPerSM / (l.smem + 1024)) > max_co) l.smem += 4096;
+    l.ok = true;
+    return l;
+  }
+  return l;
+}
+
 struct atmm_plan {
   atmm_registry* reg = nullptr;
   uint64_t generation = 0;
@@ -434,6 +515,8 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     g.bn = pend.cfg.bn;
     g.r_pad_max = pend.r_pad_max;
     resolve_group(g, reg->d_in, reg->d_out, pend.rows_max, pend.cfg.stages);
+    g.a2a[0] = resolve_a2a(reg->d_in, reg->d_out, g.cluster, pend.rows_max, pend.r_pad_max, 2);
+    g.a2a[1] = resolve_a2a(reg->d_in, reg->d_out, g.cluster, pend.rows_max, pend.r_pad_max, 4);
     g.tile_offset = static_cast<int64_t>(all_tiles.size());
     g.num_tiles = static_cast<int64_t>(pend.tiles.size());
     all_tiles.insert(all_tiles.end(), pend.tiles.begin(), pend.tiles.end());
@@ -508,6 +591,23 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
     bp.rep = g.rep;
     bp.nbuf = g.nbuf;
     bp.trace = g_trace;
+    const A2aLayout& al = g.a2a[y_dtype == ATMM_BF16 ? 0 : 1];
+    if (al.ok && y_vec) {
+      bp.stages = al.stages;
+      bp.stage_bytes = al.stage_bytes;
+      bp.a_bytes = al.a_bytes;
+      bp.ypitch = al.ypitch;
+      bp.gcols = al.gcols;
+      bp.off_up = al.off_up;
+      bp.off_y = al.off_y;
+      bp.off_red = al.off_red;
+      bp.off_mid = al.off_mid;
+      bp.off_bar = al.off_bar;
+      bp.tmem_cols = al.tmem_cols;
+      const cudaError_t e = launch_bypass_a2a(y_dtype, tmap_x, bp, g.cluster, static_cast<int>(g.num_tiles), al.smem, stream);
+      if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
+      continue;
+    }
     const cudaError_t e = launch_bypass(y_dtype, tmap_x, tmap_y, bp, g.cluster, static_cast<int>(g.num_tiles), g.smem, stream);
     if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
   }
@@ -755,7 +855,12 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
            ", \"stages\": " + std::to_string(g.stages) + ", \"ustages\": " + std::to_string(g.ustages) +
            ", \"ny\": " + std::to_string(g.ny) + ", \"rep\": " + std::to_string(g.rep) +
            ", \"nbuf\": " + std::to_string(g.nbuf) + ", \"r_pad\": " + std::to_string(g.r_pad_max) +
-           ", \"tmem_cols\": " + std::to_string(g.tmem_cols) + ", \"smem\": " + std::to_string(g.smem) + "}";
+           ", \"tmem_cols\": " + std::to_string(g.tmem_cols) + ", \"smem\": " + std::to_string(g.smem) +
+           ", \"a2a_bf16\": " + (g.a2a[0].ok ? std::string("{\"stages\": ") + std::to_string(g.a2a[0].stages) +
+                                                  ", \"tmem_cols\": " + std::to_string(g.a2a[0].tmem_cols) +
+                                                  ", \"smem\": " + std::to_string(g.a2a[0].smem) + "}"
+                                            : std::string("null")) +
+           "}";
     }
     s += "]";
     std::strncpy(buf, s.c_str(), cap - 1);

@@ -79,6 +79,10 @@ struct BypassParams {
   int32_t rep;          // replicas of the tile rows in the expand accumulator (128 / rows: 1, 2, 4)
   int32_t nbuf;         // expand accumulator buffers in TMEM (tmem_cols / bn)
   uint64_t* trace;      // debug: per-CTA phase timestamps (kTraceEvents each), or null
+  // atmm_bypass_a2a_kernel only: Y slice buffer row pitch (bytes); off_y is
+  // the buffer, off_up the whole up^T slice of the CTA.
+  int32_t ypitch;
+  int32_t gcols;        // output columns owned per epilogue thread (= expand MMAs per CTA: 1, 2, 4, 8)
 };
 
 constexpr int kTraceEvents = 32;

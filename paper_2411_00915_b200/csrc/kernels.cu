@@ -513,7 +513,10 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
       const int buf = c % NB;
       const int u = c % U;
       mbar_wait(&acc_empty[buf], static_cast<uint32_t>((c / NB) & 1) ^ 1u);
+      if (c == 1 && lane == 0) TRACE(24);
       mbar_wait(&up_full[u], static_cast<uint32_t>((c / U) & 1));
+      if (c == 1 && lane == 0) TRACE(25);
+      if (c == 0 && lane == 0) TRACE(27);
       tc_fence_after();
       const uint32_t b0 = smem_u32(upr + static_cast<size_t>(u) * p.ustage_bytes);
       const uint32_t idesc_e = idesc_bf16(kTileM, static_cast<uint32_t>(bn_c));
@@ -523,8 +526,10 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
           const uint64_t bd = smem_desc(b0 + kk * 256u, 128u, sbo, kLayoutNone);
           mma_bf16(tmem_base + static_cast<uint32_t>(buf * p.bn), ad, bd, idesc_e, kk > 0 ? 1u : 0u);
         }
+        if (c == 1) TRACE(26);
         mma_commit(&up_empty[u]);
         mma_commit(&acc_full[buf]);
+        if (c < 4) TRACE(20 + c);
       }
       __syncwarp();
     }
@@ -671,12 +676,12 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
       mbar_wait(&acc_full[buf], static_cast<uint32_t>((c / NB) & 1));
       tc_fence_after();
       if (tracer && c == 0) TRACE(11);
-      if (tracer && kown < 5) TRACE(14 + 3 * kown);
+      if (tracer && kown < 2) TRACE(14 + 3 * kown);
       if (p.y_ring) {
         for (int sub = 0; sub < bn_c; sub += ycols, ++ysub) {
           const int yb = ysub % NY;
           mbar_wait(&y_full[yb], static_cast<uint32_t>((ysub / NY) & 1));
-          if (tracer && kown < 5 && sub == 0) TRACE(15 + 3 * kown);
+          if (tracer && kown < 2 && sub == 0) TRACE(15 + 3 * kown);
           const uint32_t bufs = ybuf_s + static_cast<uint32_t>(yb) * p.ybuf_bytes;
           if (ewarp) {
             uint32_t v[64];
@@ -710,7 +715,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
           __syncwarp();
           if (lane == 0) mbar_arrive(&y_empty[yb]);
         }
-        if (tracer && kown < 5) TRACE(16 + 3 * kown);
+        if (tracer && kown < 2) TRACE(16 + 3 * kown);
       } else if (ewarp) {
         for (int sub = 0; sub < bn_c; sub += 32) {
           uint32_t v[32];
@@ -734,6 +739,468 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
   }
+}
+
+// =========================================================================
+// Fused bypass, all-to-all variant (atmm_bypass_a2a_kernel)
+// =========================================================================
+// For tiles whose per-CTA Y slice, fp32 partials of every cluster peer and
+// expand accumulator fit on chip (the latency-bound small-segment batches,
+// e.g. cfg2: 32-row segments).  Differences from atmm_bypass_kernel, each
+// removing work from the CTA's serial chain:
+//   * exchange: the CTA's fp32 partial mid rows are staged once in shared
+//     memory and pushed to each peer with ONE bulk DSMEM copy
+//     (cp.async.bulk.shared::cluster, byte-counted on the peer's barrier);
+//     every CTA sums the C partials locally in the same fixed order
+//     (deterministic, identical in all CTAs): one hop, C - 1 instructions;
+//   * expand: swap-AB, D[out column][row] = up^T . mid^T, M = 128 output
+//     columns, N = the tile rows (no row replication), K = r.  The CTA's
+//     G * 128-column slice is G MMAs behind one commit; up^T rows are staged
+//     PERMUTED (MMA j, lane m <-> column m * G + j), so epilogue thread m
+//     owns G adjacent output columns: vector Y loads (shared) and stores
+//     (global, coalesced across the warp), no write-back pass;
+//   * up^T (by warps 0..3, before griddepcontrol.wait) and Y (by warp 4,
+//     right after it) are staged with cp.async (LSU), in parallel with the
+//     TMA X gathers;
+//   * the producer and MMA warps join the Y update (warp w reads TMEM lane
+//     quadrant w % 4; warps w and w + 4 split the row blocks).
+// Warps: 0..3 up^T staging, partials, reduction; 4 Y staging; 5/6 X
+// gathers (6 also down^T); 7 TMEM owner + MMA issuer; all 8: Y update.
+template <typename YT, int G>
+__device__ __forceinline__ void a2a_update_rows(const uint32_t (&acc)[64], int rb, int nrows, uint32_t ysrc,
+                                                uint32_t pitch, uint8_t* ydst_col, uint32_t rows_s,
+                                                int64_t ldy_b, float s) {
+  constexpr int RB = 64 / G > 32 ? 32 : 64 / G;  // rows per block (acc[j * RB + i])
+  constexpr int kBytes = G * static_cast<int>(sizeof(YT));
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    if (i < nrows) {
+      const uint32_t ya = ysrc + static_cast<uint32_t>(rb + i) * pitch;
+      uint8_t* gp = ydst_col + static_cast<int64_t>(static_cast<int32_t>(ld_shared_u32(rows_s + (rb + i) * 4))) * ldy_b;
+      if constexpr (sizeof(YT) == 2) {
+        uint32_t in[(G + 1) / 2];
+        if constexpr (kBytes == 2) {
+          in[0] = ld_shared_u16(ya);
+        } else if constexpr (kBytes == 4) {
+          in[0] = ld_shared_u32(ya);
+        } else if constexpr (kBytes == 8) {
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(in[0]), "=r"(in[1]) : "r"(ya));
+        } else {
+          const uint4 v = ld_shared_v4(ya);
+          in[0] = v.x; in[1] = v.y; in[2] = v.z; in[3] = v.w;
+        }
+        uint32_t out[(G + 1) / 2];
+#pragma unroll
+        for (int j = 0; j < G; j += 2) {
+          const float lo = fmaf(s, __uint_as_float(acc[j * RB + i]), bf16lo(in[j / 2]));
+          if (G == 1) {
+            out[0] = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+          } else {
+            const float hi = fmaf(s, __uint_as_float(acc[(j + 1) * RB + i]), bf16hi(in[j / 2]));
+            out[j / 2] = pack_bf16x2(lo, hi);
+          }
+        }
+        if constexpr (kBytes == 2) {
+          *reinterpret_cast<uint16_t*>(gp) = static_cast<uint16_t>(out[0]);
+        } else if constexpr (kBytes == 4) {
+          *reinterpret_cast<uint32_t*>(gp) = out[0];
+        } else if constexpr (kBytes == 8) {
+          *reinterpret_cast<uint2*>(gp) = make_uint2(out[0], out[1]);
+        } else {
+          *reinterpret_cast<uint4*>(gp) = make_uint4(out[0], out[1], out[2], out[3]);
+        }
+      } else {
+        uint32_t in[G];
+        if constexpr (kBytes == 4) {
+          in[0] = ld_shared_u32(ya);
+        } else if constexpr (kBytes == 8) {
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(in[0]), "=r"(in[1]) : "r"(ya));
+        } else {
+#pragma unroll
+          for (int q = 0; q < G; q += 4) {
+            const uint4 v = ld_shared_v4(ya + q * 4);
+            in[q] = v.x; in[q + 1] = v.y; in[q + 2] = v.z; in[q + 3] = v.w;
+          }
+        }
+        float out[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) out[j] = fmaf(s, __uint_as_float(acc[j * RB + i]), __uint_as_float(in[j]));
+        if constexpr (kBytes == 4) {
+          *reinterpret_cast<float*>(gp) = out[0];
+        } else if constexpr (kBytes == 8) {
+          *reinterpret_cast<float2*>(gp) = make_float2(out[0], out[1]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < G; q += 4) {
+            *reinterpret_cast<float4*>(gp + q * 4) = make_float4(out[q], out[q + 1], out[q + 2], out[q + 3]);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int RB>
+__device__ __forceinline__ void tmem_ld_rows(uint32_t taddr, uint32_t* v) {
+  if constexpr (RB == 32) {
+    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
+  } else if constexpr (RB == 16) {
+    tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(v));
+  } else {
+    tmem_ld8(taddr, *reinterpret_cast<uint32_t(*)[8]>(v));
+  }
+}
+
+template <typename YT, int G>
+__device__ __forceinline__ void a2a_epilogue(uint32_t tmem_base, uint32_t lane_addr, int half, int rows, int rows16,
+                                             int m, int ncols, uint32_t ybuf_s, uint32_t pitch, uint8_t* ycols_g,
+                                             uint32_t rows_s, int64_t ldy_b, float s) {
+  constexpr int RB = 64 / G > 32 ? 32 : 64 / G;
+  const int c0 = m * G;  // first owned local column
+  const bool col_ok = c0 < ncols;
+  const uint32_t ysrc = ybuf_s + static_cast<uint32_t>(c0 * static_cast<int>(sizeof(YT)));
+  uint8_t* ydst = ycols_g + static_cast<int64_t>(c0) * static_cast<int>(sizeof(YT));
+  const int nrb = (rows16 + RB - 1) / RB;
+  for (int b = half; b < nrb; b += 2) {
+    const int rb = b * RB;
+    uint32_t acc[64];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      tmem_ld_rows<RB>(tmem_base + lane_addr + static_cast<uint32_t>(j * rows16 + rb), &acc[j * RB]);
+    }
+    tmem_wait_ld();
+    if (col_ok) a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), ysrc, pitch, ydst, rows_s, ldy_b, s);
+  }
+}
+
+template <typename YT>
+__global__ void __launch_bounds__(kBypassThreads, 2)
+    atmm_bypass_a2a_kernel(const __grid_constant__ CUtensorMap tmap_x, const BypassParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  __shared__ int32_t rows_s[kTileM];
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TRACE(0);
+
+  const uint32_t C = cluster_nctarank();
+  const uint32_t crank = cluster_ctarank();
+  const TileDesc tile = p.tiles[cluster_id_x()];
+  const int rows = tile.rows;
+  const int r_pad = tile.r_pad;
+  const int rows16 = (rows + 15) & ~15;
+  const int G = p.gcols;
+  const uint16_t* down_t = tile.down_t + static_cast<int64_t>(p.layer) * tile.down_layer_stride;
+  const uint16_t* up_t = tile.up_t + static_cast<int64_t>(p.layer) * tile.up_layer_stride;
+  const int nkb = (p.d_in + kBK - 1) / kBK;
+  const int kb_lo = (nkb * static_cast<int>(crank)) / static_cast<int>(C);
+  const int kb_hi = (nkb * static_cast<int>(crank + 1)) / static_cast<int>(C);
+  const int nun = (p.d_out + kNUnit - 1) / kNUnit;
+  const int n_lo = (nun * static_cast<int>(crank)) / static_cast<int>(C) * kNUnit;
+  const int n_hi = (nun * static_cast<int>(crank + 1)) / static_cast<int>(C) * kNUnit;
+  const int ncols = max(0, min(n_hi, p.d_out) - n_lo);  // valid output columns of this CTA
+  constexpr int kEsz = static_cast<int>(sizeof(YT));
+  const uint32_t block_bytes = static_cast<uint32_t>(rows * r_pad * 4);  // one peer's partial
+
+  uint8_t* ring = smem;
+  uint8_t* upr = smem + p.off_up;
+  uint8_t* ybuf = smem + p.off_y;
+  float* red = reinterpret_cast<float*>(smem + p.off_red);
+  uint8_t* mid = smem;  // aliases ring stage 0: written only after shrink_full
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  const int S = p.stages;
+  uint64_t* full = bars;              // [S]
+  uint64_t* empty = full + S;         // [S]
+  uint64_t* up_full = empty + S;      // 128 cp.async arrivals (warps 0..3)
+  uint64_t* y_full = up_full + 1;     // 32 cp.async arrivals (warp 4)
+  uint64_t* shrink_full = y_full + 1;
+  uint64_t* red_full = shrink_full + 1;
+  uint64_t* mid_ready = red_full + 1; // 128 arrivals
+  uint64_t* acc_full = mid_ready + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  if (warp == 0) {
+    for (int b = static_cast<int>(lane); b < 2 * S + 6; b += 32) {
+      // up_full, mid_ready: 128 arrivals (warps 0..3); y_full: 32 (warp 4)
+      const uint32_t cnt = (b == 2 * S || b == 2 * S + 4) ? 128u : (b == 2 * S + 1 ? 32u : 1u);
+      mbar_init(bars + b, cnt);
+    }
+    for (int i = static_cast<int>(lane); i < kTileM; i += 32) rows_s[i] = p.row_index[tile.row_begin + min(i, rows - 1)];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(red_full, (C - 1) * block_bytes);
+    fence_mbar_init();
+  }
+  if (warp == kWarpMMA) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  cluster_arrive();  // phase 1: barrier inits visible to peers
+  if (threadIdx.x == 0) TRACE(1);
+
+  const uint32_t ybuf_s = smem_u32(ybuf);
+  const int ngroups = (rows + 3) / 4;
+  const int ngroups0 = (ngroups + 1) / 2;
+  if (warp == kWarpXA || warp == kWarpXB) {
+    // ===================== X / down^T producers (shrink ring) =====================
+    const bool xa = warp == kWarpXA;
+    const int g_lo = xa ? 0 : ngroups0;
+    const int g_hi = xa ? ngroups0 : ngroups;
+    const uint32_t b_bytes = static_cast<uint32_t>(r_pad) * kBK * 2u;
+    const uint32_t a_bytes = static_cast<uint32_t>(ngroups) * 512u;
+    if (xa && lane == 0) {
+      tma_prefetch_desc(&tmap_x);
+      // Weights do not depend on the previous kernel: the first ring round of
+      // down^T blocks goes out before griddepcontrol.wait.
+      for (int kb = kb_lo; kb < min(kb_hi, kb_lo + S); ++kb) {
+        const int st = kb - kb_lo;
+        mbar_arrive_expect_tx(&full[st], a_bytes + b_bytes);
+        bulk_g2s(ring + static_cast<size_t>(st) * p.stage_bytes + p.a_bytes,
+                 down_t + static_cast<int64_t>(kb) * r_pad * kBK, b_bytes, &full[st]);
+      }
+    }
+    const int g = g_lo + static_cast<int>(lane);
+    int32_t gr[4] = {0, 0, 0, 0};
+    if (g < g_hi) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) gr[q] = rows_s[min(g * 4 + q, rows - 1)];
+    }
+    griddep_wait();  // X may be produced by the previous kernel
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = kb_lo; kb < kb_hi; ++kb) {
+      uint8_t* st = ring + static_cast<size_t>(stage) * p.stage_bytes;
+      if (kb - kb_lo >= S) {  // ring reuse: wait for the MMA to drain the stage
+        if (lane == 0) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (xa) {
+            mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+            bulk_g2s(st + p.a_bytes, down_t + static_cast<int64_t>(kb) * r_pad * kBK, b_bytes, &full[stage]);
+          }
+        }
+        __syncwarp();
+      }
+      if (g < g_hi) tma_gather4(st + g * 512u, &tmap_x, &full[stage], kb * kBK, gr[0], gr[1], gr[2], gr[3]);
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    if (xa && lane == 0) TRACE(2);
+    __syncwarp();
+    cluster_wait();
+  } else if (warp == kWarpMMA) {
+    // ===================== MMA issuer =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t idesc_s = idesc_bf16(kTileM, static_cast<uint32_t>(r_pad));
+    for (int kb = kb_lo; kb < kb_hi; ++kb) {
+      uint8_t* st = ring + static_cast<size_t>(stage) * p.stage_bytes;
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (kb == kb_lo && lane == 0) TRACE(3);
+      const uint32_t a0 = smem_u32(st);
+      const uint32_t b0 = smem_u32(st + p.a_bytes);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk) {
+          const uint64_t ad = smem_desc(a0 + kk * 32u, 16u, 1024u, kLayoutSW128);
+          const uint64_t bd = smem_desc(b0 + kk * 256u, 128u, 1024u, kLayoutNone);
+          mma_bf16(tmem_base, ad, bd, idesc_s, (kb > kb_lo || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[stage]);
+      }
+      __syncwarp();
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    if (elect_one()) mma_commit(shrink_full);
+    __syncwarp();
+    if (lane == 0) TRACE(4);
+    cluster_wait();
+    // ---- expand (swap-AB): MMA j -> TMEM columns [j * rows16, +rows16); it
+    // aliases the shrink accumulator (mid_ready implies the partials were read) ----
+    mbar_wait(mid_ready, 0);
+    mbar_wait(up_full, 0);
+    tc_fence_after();
+    if (lane == 0) TRACE(9);
+    const uint32_t up0 = smem_u32(upr);
+    const uint32_t mid0 = smem_u32(mid);
+    const uint32_t sbo = static_cast<uint32_t>(r_pad) * 16u;
+    const uint32_t idesc_e = idesc_bf16(kTileM, static_cast<uint32_t>(rows16));
+    if (elect_one()) {
+      for (int j = 0; j < G; ++j) {
+        for (int kk = 0; kk < r_pad / 16; ++kk) {
+          const uint64_t ad = smem_desc(up0 + static_cast<uint32_t>(j) * 16u * sbo + kk * 256u, 128u, sbo, kLayoutNone);
+          const uint64_t bd = smem_desc(mid0 + kk * 256u, 128u, sbo, kLayoutNone);
+          mma_bf16(tmem_base + static_cast<uint32_t>(j * rows16), ad, bd, idesc_e, kk > 0 ? 1u : 0u);
+        }
+      }
+      mma_commit(acc_full);
+    }
+    __syncwarp();
+    if (lane == 0) TRACE(10);
+  } else if (warp == kWarpY) {
+    // ===================== Y slice -> shared memory (cp.async) =====================
+    // Issued by this otherwise idle warp so that the proxy fences of warps
+    // 0..3 never wait behind these HBM reads.
+    griddep_wait();
+    const int cpr = ncols * kEsz / 16;  // 16-byte chunks per row
+    const uint8_t* ybase = reinterpret_cast<const uint8_t*>(p.y) + static_cast<int64_t>(n_lo) * kEsz;
+    const int64_t ldy_b = p.ldy * kEsz;
+    for (int q = static_cast<int>(lane); q < rows * cpr; q += 32) {
+      const int r = q / cpr;
+      const int c = q - r * cpr;
+      cp_async16(ybuf_s + static_cast<uint32_t>(r * p.ypitch + c * 16), ybase + rows_s[r] * ldy_b + c * 16, 16u);
+    }
+    cp_async_arrive_noinc(y_full);
+    __syncwarp();
+    cluster_wait();
+  } else {
+    // ===================== warps 0..3 =====================
+    // (a) up^T slice, permuted (MMA j, lane m <- column m * G + j), then
+    //     (after griddepcontrol.wait) the Y slice, both by cp.async.
+    {
+      const int kc = r_pad / 8;  // 16-byte units per up^T row
+      const uint32_t up_s = smem_u32(upr);
+      const int units = (n_hi - n_lo) * kc;
+      for (int q = static_cast<int>(threadIdx.x); q < units; q += 128) {
+        const int nl = q / kc;
+        const int c = q - nl * kc;
+        const int n = n_lo + nl;
+        const int a_row = (nl % G) * kTileM + nl / G;
+        cp_async16(up_s + interleave_off(static_cast<uint32_t>(a_row), static_cast<uint32_t>(c * 8), static_cast<uint32_t>(r_pad)),
+                   up_t + ((static_cast<int64_t>(n >> 3) * kc + c) * 64 + (n & 7) * 8), 16u);
+      }
+      cp_async_arrive_noinc(up_full);
+    }
+    // (b) shrink partial (thread = row) -> red[crank] locally, then one bulk
+    //     DSMEM copy of the whole block to each peer.
+    const uint32_t quad = warp;
+    const int row = static_cast<int>(quad * 32 + lane);
+    const bool tracer = warp == 0 && lane == 0;
+    mbar_wait(shrink_full, 0);
+    tc_fence_after();
+    if (tracer) TRACE(5);
+    const uint32_t red_s = smem_u32(red);
+    const uint32_t my_block = red_s + crank * block_bytes;
+    if (static_cast<int>(quad * 32) < rows) {
+      for (int g = 0; g < r_pad; g += 32) {
+        uint32_t v[32];
+        if (g + 32 <= r_pad) {
+          tmem_ld32(tmem_base + ((quad * 32u) << 16) + g, v);
+        } else {
+          tmem_ld16(tmem_base + ((quad * 32u) << 16) + g, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+        }
+        tmem_wait_ld();
+        if (row < rows) {
+          const int nc = min(32, r_pad - g);
+          const uint32_t dst = my_block + static_cast<uint32_t>((row * r_pad + g) * 4);
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += 4) {
+            if (jj < nc) st_shared_v4(dst + jj * 4, v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();  // the block is read by the bulk-copy engine
+    cluster_wait();            // peers' barriers are initialized
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 0) {
+      for (uint32_t cc = 1; cc < C; ++cc) {
+        const uint32_t peer = (crank + cc) % C;
+        bulk_s2cluster(map_cta(my_block, peer), my_block, block_bytes, map_cta(smem_u32(red_full), peer));
+      }
+    }
+    if (tracer) TRACE(6);
+    // (c) fixed-order sum of the C partials -> bf16 mid (local)
+    mbar_wait_cluster(red_full, 0);
+    if (tracer) TRACE(7);
+    const uint32_t mid_s = smem_u32(mid);
+    const int cpr8 = r_pad / 8;
+    for (int it = static_cast<int>(threadIdx.x); it < rows * cpr8; it += 128) {
+      const int rr = it / cpr8;
+      const int ch = it - rr * cpr8;
+      const uint32_t src0 = red_s + static_cast<uint32_t>((rr * r_pad + ch * 8) * 4);
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+      for (int c0 = 0; c0 < static_cast<int>(C); c0 += 4) {  // batches of 4 peers: loads, then adds
+        uint4 u[4], w[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c0 + c < static_cast<int>(C)) {
+            u[c] = ld_shared_v4(src0 + (c0 + c) * block_bytes);
+            w[c] = ld_shared_v4(src0 + (c0 + c) * block_bytes + 16);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c0 + c < static_cast<int>(C)) {
+            acc[0] += __uint_as_float(u[c].x);
+            acc[1] += __uint_as_float(u[c].y);
+            acc[2] += __uint_as_float(u[c].z);
+            acc[3] += __uint_as_float(u[c].w);
+            acc[4] += __uint_as_float(w[c].x);
+            acc[5] += __uint_as_float(w[c].y);
+            acc[6] += __uint_as_float(w[c].z);
+            acc[7] += __uint_as_float(w[c].w);
+          }
+        }
+      }
+      st_shared_v4(mid_s + interleave_off(static_cast<uint32_t>(rr), static_cast<uint32_t>(ch * 8), static_cast<uint32_t>(r_pad)),
+                   pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                   pack_bf16x2(acc[6], acc[7]));
+    }
+    fence_proxy_async_smem();  // mid (generic writes) -> the tensor core (async proxy)
+    mbar_arrive(mid_ready);
+    if (tracer) TRACE(8);
+    griddep_launch_dependents();
+  }
+
+  // Every peer has received all its partials once its red_full completed:
+  // phase 2 of the cluster barrier (arrive here, wait at exit) keeps every
+  // CTA's shared memory alive until all bulk DSMEM copies have landed.
+  mbar_wait_cluster(red_full, 0);
+  cluster_arrive();
+
+  // ===================== all warps: Y[rows, cols] += s * acc =====================
+  {
+    const bool tracer = warp == 0 && lane == 0;
+    const float s = p.scale * tile.scale;
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    if (tracer) TRACE(11);
+    mbar_wait(y_full, 0);
+    if (tracer) TRACE(14);
+    const uint32_t quad = warp & 3u;
+    const uint32_t lane_addr = (quad * 32u) << 16;
+    const int m = static_cast<int>(quad * 32 + lane);
+    const int half = static_cast<int>(warp >> 2);
+    uint8_t* ycols = reinterpret_cast<uint8_t*>(p.y) + static_cast<int64_t>(n_lo) * kEsz;
+    const int64_t ldy_b = p.ldy * kEsz;
+    const uint32_t pitch = static_cast<uint32_t>(p.ypitch);
+    const uint32_t rows_sa = smem_u32(rows_s);
+    switch (G) {
+      case 1: a2a_epilogue<YT, 1>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
+      case 2: a2a_epilogue<YT, 2>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
+      case 4: a2a_epilogue<YT, 4>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
+      default: a2a_epilogue<YT, 8>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
+    }
+    if (tracer) TRACE(12);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) TRACE(13);
+  if (warp == kWarpMMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+  cluster_wait();
 }
 
 // =========================================================================
@@ -1162,6 +1629,9 @@ template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant
 template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap,
                                                    const BypassParams);
+template __global__ void atmm_bypass_a2a_kernel<__nv_bfloat16>(const __grid_constant__ CUtensorMap,
+                                                               const BypassParams);
+template __global__ void atmm_bypass_a2a_kernel<float>(const __grid_constant__ CUtensorMap, const BypassParams);
 template __global__ void atmm_merge_kernel<float>(const MergeParams);
 template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
 template __global__ void atmm_merge_tma_kernel<float>(const __grid_constant__ CUtensorMap, const MergeParams);
@@ -1247,6 +1717,34 @@ cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensor
   cudaError_t e = prepare(k, smem, C > 8);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k, tmap_x, tmap_y, p);
+}
+
+cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const BypassParams& p, int C, int num_tiles,
+                              size_t smem, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(C * num_tiles), 1, 1);
+  cfg.blockDim = dim3(kBypassThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(C);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  if (y_dtype == 0) {
+    auto k = atmm_bypass_a2a_kernel<__nv_bfloat16>;
+    cudaError_t e = prepare(k, smem, C > 8);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, k, tmap_x, p);
+  }
+  auto k = atmm_bypass_a2a_kernel<float>;
+  cudaError_t e = prepare(k, smem, C > 8);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, k, tmap_x, p);
 }
 
 int bypass_max_active_clusters(int C, size_t smem) {

@@ -16,9 +16,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 EVENTS = ["start", "cluster_synced", "prod_shrink_issued", "mma_first_full", "mma_shrink_done",
           "epi_shrink_full", "epi_partials_sent", "owner_red_full", "owner_bcast_done", "mma_mid_full",
           "mma_expand_issued", "epi_first_acc", "epi_done", "end"]
-for _c in range(5):
-    EVENTS += [f"w0_chunk{_c}_acc_full", f"w0_chunk{_c}_y_full", f"w0_chunk{_c}_stored"]
-EVENTS += ["y_producer_done"]
+# slots 14..30 are kernel specific (see the TRACE calls in kernels.cu)
+EVENTS += [f"slot{_c}" for _c in range(14, 31)]
 NEV = 32
 
 
@@ -78,14 +77,17 @@ def main():
         t0 = t[:, 0][t[:, 0] > 0].min()
         print(f"rep {rep}: event-timed kernel {e0.elapsed_time(e1) * 1e3:.1f} us; "
               f"CTA start spread {(t[:, 0].max() - t0) / 1e3:.2f} us")
+        own = np.where(raw > 0, (raw - raw[:, :1]) / ghz, np.nan)  # cycle-exact, per CTA
         for ev in range(min(NEV - 1, len(EVENTS))):
             col = t[:, ev]
-            col = col[col > 0]
+            sel = col > 0
+            col = col[sel]
             if col.size == 0:
                 continue
+            o = own[sel, ev] / 1e3
             rel = (col - t0) / 1e3
             print(f"   {ev:2d} {EVENTS[ev]:<20} n={col.size:4d}  min {rel.min():7.2f}  med {np.median(rel):7.2f}  "
-                  f"max {rel.max():7.2f} us")
+                  f"max {rel.max():7.2f} us | own-clock med {np.nanmedian(o):7.3f}")
 
 
 if __name__ == "__main__":
