@@ -1165,13 +1165,19 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
   // Every peer has received all its partials once its red_full completed:
   // phase 2 of the cluster barrier (arrive here, wait at exit) keeps every
   // CTA's shared memory alive until all bulk DSMEM copies have landed.
-  mbar_wait_cluster(red_full, 0);
+  if (warp >= 4) {
+    mbar_wait_sleep(red_full, 0);
+    fence_acq_rel_cluster();
+  } else {
+    mbar_wait_cluster(red_full, 0);
+  }
   cluster_arrive();
 
   // ===================== all warps: Y[rows, cols] += s * acc =====================
   {
     const bool tracer = warp == 0 && lane == 0;
     const float s = p.scale * tile.scale;
+    if (warp >= 4) mbar_wait_sleep(acc_full, 0, 64);
     mbar_wait(acc_full, 0);
     tc_fence_after();
     if (tracer) TRACE(11);

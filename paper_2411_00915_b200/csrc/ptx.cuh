@@ -76,6 +76,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// Polite wait for warps with nothing else to do: back off between probes so
+// the spinning warp does not steal shared-memory pipe slots from the warps
+// doing the work it waits for.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns = 128) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (done) break;
+    __nanosleep(ns);
+  }
+}
 // Acquire at cluster scope: pairs with mbar_arrive_remote's release.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
   asm volatile(
