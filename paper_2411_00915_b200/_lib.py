@@ -12,6 +12,10 @@ from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libatmm_b200.so")
+# Development A/B runs only: load another in-tree build of the same library
+# (e.g. tools/ab/libatmm_b200_<tag>.so).  Must live inside the repository.
+if os.environ.get("ATMM_LIB_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(_HERE), "tools", "ab", f"libatmm_b200_{os.environ['ATMM_LIB_VARIANT']}.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

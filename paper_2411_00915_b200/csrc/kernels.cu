@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "device_types.hpp"
@@ -1651,6 +1652,13 @@ template __global__ void atmm_merge_tma_kernel<__nv_bfloat16>(const __grid_const
 // =========================================================================
 namespace atmm {
 
+// Programmatic dependent launch on by default; ATMM_NO_PDL=1 turns it off
+// (A/B measurements).
+static bool pdl_enabled() {
+  static const bool on = std::getenv("ATMM_NO_PDL") == nullptr;
+  return on;
+}
+
 // Function attributes are raised once per (kernel, device) and only when a
 // launch needs more, so steady-state launches (and CUDA-graph capture) issue
 // no attribute calls.
@@ -1712,7 +1720,7 @@ cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensor
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   if (y_dtype == 0) {
     auto k = atmm_bypass_kernel<__nv_bfloat16>;
     cudaError_t e = prepare(k, smem, C > 8);
@@ -1740,7 +1748,7 @@ cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const Bypa
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   if (y_dtype == 0) {
     auto k = atmm_bypass_a2a_kernel<__nv_bfloat16>;
     cudaError_t e = prepare(k, smem, C > 8);
