@@ -5,7 +5,7 @@
 OUT=gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout 400 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-   -c 200 --csv --log-file $OUT/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --soak-s 0 \
+   -k regex:atmm -c 200 --csv --log-file $OUT/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --soak-s 0 \
    > $OUT/launches_bench.log 2>&1
 for cfg in cfg2 cfg3 cfg5; do
   timeout 400 $NCU --set full --clock-control none --import-source on -k regex:atmm_bypass -s 4 -c 1 \

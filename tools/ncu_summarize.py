@@ -92,9 +92,11 @@ def main():
         lines = [l for l in text.splitlines() if not l.startswith("==")]
         rows = list(csv.DictReader(io.StringIO("\n".join(lines))))
         per = {}
+        dur_unit = "nsecond"
         for r in rows:
             if r.get("Metric Name") != "gpu__time_duration.sum":
                 continue
+            dur_unit = r.get("Metric Unit", dur_unit)
             name = r["Kernel Name"].split("(")[0][:60]
             v = float(r["Metric Value"].replace(",", ""))
             per.setdefault(name, []).append(v)
@@ -103,7 +105,7 @@ def main():
                "| kernel | launches | mean us | share of GPU time |", "|---|---|---|---|"]
         shares = {}
         for name, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
-            u = to_us(1.0, rows[0].get("Metric Unit", "nsecond"))
+            u = to_us(1.0, dur_unit)
             shares[name] = {"launches": len(v), "mean_us": sum(v) / len(v) * u, "share": sum(v) / tot}
             md.append(f"| {name} | {len(v)} | {sum(v) / len(v) * u:.2f} | {100 * sum(v) / tot:.1f}% |")
         summary["bench_launch_list"] = shares
