@@ -17,6 +17,7 @@
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.hpp"
@@ -32,6 +33,8 @@ cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t sme
                          cudaStream_t stream);
 cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const BypassParams& p, int C, int num_tiles,
                               size_t smem, cudaStream_t stream);
+cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,
+                         cudaStream_t stream);
 cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const MergeParams& p, int grid,
                              size_t smem, cudaStream_t stream);
 cudaError_t launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t rows, int64_t cols,
@@ -273,8 +276,17 @@ struct A2aLayout {
   size_t smem = 0;
 };
 
+// Split-path (shrink + expand launches) geometry of one launch group.
+struct SplitLayout {
+  bool ok = false;
+  int32_t stages = 0, estages[2] = {0, 0};
+  size_t smem_s = 0, smem_e[2] = {0, 0};
+};
+
 struct LaunchGroup {
   A2aLayout a2a[2];  // per Y dtype (ATMM_BF16, ATMM_F32)
+  SplitLayout split;
+  int32_t rows_max = 0;
   int32_t cluster = 1, bn = 128, stages = 2, ustages = 1, ny = 2;
   int32_t a_bytes = 0, ustage_bytes = 0, ybuf_bytes = 0, rep = 1, nbuf = 2;
   uint32_t off_up = 0, off_y = 0;
@@ -449,16 +461,93 @@ static A2aLayout resolve_a2a(int64_t d_in, int64_t d_out, int32_t cluster, int32
   return l;
 }
 
+// Split path: mid partials (fp32, per tile x K slice), bf16 mid per tile and
+// per-tile arrival counters of one launch group, allocated with the plan.
+struct SplitBufs {
+  DevBuf<float> part;
+  DevBuf<uint16_t> mid;
+  DevBuf<int32_t> counter;
+  DevBuf<int32_t> tables;  // [s_begin | e_begin bf16 | e_begin fp32 (P+1 each) | seg_slot0 (P) | nseg (T) | part_off (T)]
+  int32_t grid = 0;
+};
+
 struct atmm_plan {
   atmm_registry* reg = nullptr;
   uint64_t generation = 0;
   int64_t n = 0;
   BatchPlan bp;
   std::vector<LaunchGroup> groups;
+  // groups[merged_first ..] all take the split path for bf16 Y: one launch
+  // pair over their contiguous tile range (merged.tile_offset, num_tiles).
+  int merged_first = -1;
+  LaunchGroup merged;
+  std::unique_ptr<SplitBufs> merged_bufs;
   DevBuf<int32_t> d_rows;
   DevBuf<TileDesc> d_tiles;
   int64_t total_ctas = 0;
 };
+
+namespace atmm {
+// Which kernel a launch group runs: the fused all-to-all kernel for small
+// (latency-bound) tiles, the split shrink + expand pair for large ones, the
+// general fused kernel otherwise.  ATMM_PATH=a2a|split|fused forces one
+// where it is applicable (A/B runs).
+enum class BypassPath { kA2a, kSplit, kFused };
+static BypassPath choose_path(const LaunchGroup& g, int y_dtype, bool y_vec) {
+  const int di = y_dtype == ATMM_BF16 ? 0 : 1;
+  const bool a2a = g.a2a[di].ok && y_vec;
+  const bool split = g.split.ok && y_vec;
+  if (const char* e = std::getenv("ATMM_PATH")) {
+    const std::string f(e);
+    if (f == "a2a" && a2a) return BypassPath::kA2a;
+    if (f == "split" && split) return BypassPath::kSplit;
+    if (f == "fused") return BypassPath::kFused;
+  }
+  if (a2a && g.rows_max <= 32) return BypassPath::kA2a;
+  if (split) return BypassPath::kSplit;  // taken through the plan's merged split range
+  if (a2a) return BypassPath::kA2a;
+  return BypassPath::kFused;
+}
+
+static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, int32_t r_pad) {
+  SplitLayout l;
+  (void)d_in;
+  if (d_out % 8 != 0 || r_pad > 128 || rows_max > kTileM) return l;
+  const int64_t avail = int64_t(kSmemLimit) - 1024 - 512;  // alignment slack + the kernels' static smem
+  const int64_t stage = int64_t(kTileM) * 128 + int64_t(r_pad) * kBK * 2;
+  l.stages = static_cast<int32_t>(std::min<int64_t>(8, avail / stage));
+  l.smem_s = size_t(1024 + l.stages * stage);
+  const int64_t rows16 = round_up(rows_max, 16);
+  bool ok = l.stages >= 2;
+  for (int di = 0; di < 2; ++di) {
+    const int64_t esz = di == 0 ? 2 : 4;
+    const int64_t cols = int64_t(kTileM) * (di == 0 ? 2 : 1);  // expand item width (G = 2 bf16, 1 fp32)
+    const int64_t est = round_up(cols * r_pad * 2 + round_up(rows16 * r_pad * 2, 128) + int64_t(rows_max) * cols * esz + kTileM * 4, 128);
+    l.estages[di] = static_cast<int32_t>(std::min<int64_t>(4, (avail + 1024 - 128) / est));  // 128-byte aligned kernel
+    l.smem_e[di] = size_t(128 + l.estages[di] * est);
+    ok = ok && l.estages[di] >= 2;
+  }
+  l.ok = ok;
+  return l;
+}
+
+// Balanced split of a flattened, weighted work list over `parts` CTAs:
+// begin[b] = first item whose cost prefix reaches b * total / parts.
+static std::vector<int32_t> balance(const std::vector<int64_t>& cost, int parts) {
+  std::vector<int32_t> begin(static_cast<size_t>(parts) + 1, static_cast<int32_t>(cost.size()));
+  int64_t total = 0;
+  for (int64_t c : cost) total += c;
+  int64_t acc = 0;
+  int b = 0;
+  for (size_t i = 0; i < cost.size() && b < parts; ++i) {
+    while (b < parts && acc >= (total * b + parts - 1) / parts) begin[static_cast<size_t>(b++)] = static_cast<int32_t>(i);
+    acc += cost[i];
+  }
+  begin[0] = 0;
+  return begin;
+}
+
+}  // namespace atmm
 
 namespace atmm {
 
@@ -509,6 +598,9 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     }
   }
   std::vector<TileDesc> all_tiles;
+  // Groups that run the split path (bf16 Y) go last, so their tiles form one
+  // contiguous range launched as a single shrink + expand pair.
+  std::vector<std::pair<LaunchGroup, std::vector<TileDesc>>> built;
   for (auto& [key, pend] : by_launch) {
     LaunchGroup g;
     g.cluster = pend.cfg.cluster;
@@ -517,14 +609,86 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     resolve_group(g, reg->d_in, reg->d_out, pend.rows_max, pend.cfg.stages);
     g.a2a[0] = resolve_a2a(reg->d_in, reg->d_out, g.cluster, pend.rows_max, pend.r_pad_max, 2);
     g.a2a[1] = resolve_a2a(reg->d_in, reg->d_out, g.cluster, pend.rows_max, pend.r_pad_max, 4);
-    g.tile_offset = static_cast<int64_t>(all_tiles.size());
+    g.split = resolve_split(reg->d_in, reg->d_out, pend.rows_max, pend.r_pad_max);
+    g.rows_max = pend.rows_max;
     g.num_tiles = static_cast<int64_t>(pend.tiles.size());
-    all_tiles.insert(all_tiles.end(), pend.tiles.begin(), pend.tiles.end());
+    built.emplace_back(g, std::move(pend.tiles));
+  }
+  std::stable_partition(built.begin(), built.end(), [](const auto& b) {
+    return choose_path(b.first, ATMM_BF16, true) != BypassPath::kSplit;
+  });
+  for (auto& [g, tiles] : built) {
+    g.tile_offset = static_cast<int64_t>(all_tiles.size());
+    all_tiles.insert(all_tiles.end(), tiles.begin(), tiles.end());
     plan->total_ctas += g.num_tiles * g.cluster;
+    if (choose_path(g, ATMM_BF16, true) == BypassPath::kSplit) {
+      if (plan->merged_first < 0) {
+        plan->merged_first = static_cast<int>(plan->groups.size());
+        plan->merged.tile_offset = g.tile_offset;
+      }
+      plan->merged.num_tiles += g.num_tiles;
+      plan->merged.r_pad_max = std::max(plan->merged.r_pad_max, g.r_pad_max);
+      plan->merged.rows_max = std::max(plan->merged.rows_max, g.rows_max);
+    }
     plan->groups.push_back(g);
+  }
+  if (plan->merged_first >= 0) {
+    plan->merged.split = resolve_split(reg->d_in, reg->d_out, plan->merged.rows_max, plan->merged.r_pad_max);
+    if (!plan->merged.split.ok) plan->merged_first = -1;
   }
   std::vector<int32_t> rows32(plan->bp.row_index.begin(), plan->bp.row_index.end());
   DeviceGuard dg(reg->device);
+  if (plan->merged_first >= 0) {
+    // Persistent split kernels: balanced work ranges over the SMs.
+    const LaunchGroup& g = plan->merged;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, reg->device);
+    const int T = static_cast<int>(g.num_tiles);
+    const int nkb = static_cast<int>((reg->d_in + kBK - 1) / kBK);
+    std::vector<int64_t> scost, ecost[2];
+    for (int t = 0; t < T; ++t) {
+      const TileDesc& td = all_tiles[static_cast<size_t>(g.tile_offset + t)];
+      for (int k = 0; k < nkb; ++k) scost.push_back(int64_t(td.rows) * 128 + int64_t(td.r_pad) * 128 + 512);
+      for (int di = 0; di < 2; ++di) {
+        const int64_t cols = int64_t(kTileM) * (di == 0 ? 2 : 1), esz = di == 0 ? 2 : 4;
+        const int nsl = static_cast<int>((reg->d_out + cols - 1) / cols);
+        for (int k = 0; k < nsl; ++k) ecost[di].push_back(int64_t(td.rows) * cols * esz * 2 + cols * td.r_pad * 2 + 1024);
+      }
+    }
+    const int P = std::max(1, std::min<int>(sms, static_cast<int>(scost.size())));
+    std::vector<int32_t> sb = balance(scost, P), eb0 = balance(ecost[0], P), eb1 = balance(ecost[1], P);
+    // Segments: the run of one tile inside one non-empty CTA range; slots are
+    // numbered per tile in CTA order (fixed reduction order).
+    std::vector<int32_t> slot0(static_cast<size_t>(P), 0), nseg(T, 0), off(T);
+    for (int b = 0; b < P; ++b) {
+      if (sb[b] >= sb[b + 1]) continue;
+      const int t0 = sb[b] / nkb, t1 = (sb[b + 1] - 1) / nkb;
+      slot0[static_cast<size_t>(b)] = nseg[t0];
+      for (int t = t0; t <= t1; ++t) ++nseg[t];
+    }
+    int32_t total_seg = 0;
+    for (int t = 0; t < T; ++t) {
+      off[t] = total_seg;
+      total_seg += nseg[t];
+    }
+    std::vector<int32_t> tables;
+    tables.insert(tables.end(), sb.begin(), sb.end());
+    tables.insert(tables.end(), eb0.begin(), eb0.end());
+    tables.insert(tables.end(), eb1.begin(), eb1.end());
+    tables.insert(tables.end(), slot0.begin(), slot0.end());
+    tables.insert(tables.end(), nseg.begin(), nseg.end());
+    tables.insert(tables.end(), off.begin(), off.end());
+    auto& mb = plan->merged_bufs;
+    mb = std::make_unique<SplitBufs>();
+    mb->grid = P;
+    mb->part.alloc(static_cast<size_t>(total_seg) * kTileM * g.r_pad_max);
+    mb->mid.alloc(static_cast<size_t>(T) * kTileM * g.r_pad_max);
+    mb->counter.alloc(static_cast<size_t>(T));
+    mb->tables.alloc(tables.size());
+    CUDA_CHECK(cudaMemset(mb->mid.p, 0, mb->mid.n * sizeof(uint16_t)));
+    CUDA_CHECK(cudaMemset(mb->counter.p, 0, mb->counter.n * sizeof(int32_t)));
+    CUDA_CHECK(cudaMemcpy(mb->tables.p, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice));
+  }
   plan->d_rows.alloc(rows32.size());
   CUDA_CHECK(cudaMemcpy(plan->d_rows.p, rows32.data(), rows32.size() * 4, cudaMemcpyHostToDevice));
   plan->d_tiles.alloc(all_tiles.size());
@@ -556,7 +720,51 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
   const CUtensorMap tmap_x = make_x_map(x, p->n, reg->d_in, ldx);
   const CUtensorMap tmap_y = y_vec ? make_y_map(y, p->n, reg->d_out, ldy, y_dtype) : tmap_x;
 
-  for (const LaunchGroup& g : p->groups) {
+  bool merged_ok = p->merged_first >= 0;
+  for (size_t gi = merged_ok ? static_cast<size_t>(p->merged_first) : 0; merged_ok && gi < p->groups.size(); ++gi) {
+    merged_ok = choose_path(p->groups[gi], y_dtype, y_vec != 0) == BypassPath::kSplit;
+  }
+  const size_t ng = merged_ok ? static_cast<size_t>(p->merged_first) + 1 : p->groups.size();
+  for (size_t gi = 0; gi < ng; ++gi) {
+    const bool as_merged = merged_ok && gi == static_cast<size_t>(p->merged_first);
+    const LaunchGroup& g = as_merged ? p->merged : p->groups[gi];
+    BypassPath path = as_merged ? BypassPath::kSplit : choose_path(g, y_dtype, y_vec != 0);
+    if (path == BypassPath::kSplit && !as_merged) path = BypassPath::kFused;  // split runs only as the merged range
+    if (path == BypassPath::kSplit) {
+      const SplitBufs& sb = *p->merged_bufs;
+      const int P = sb.grid;
+      const int T = static_cast<int>(g.num_tiles);
+      SplitParams sp{};
+      sp.tiles = p->d_tiles.p + g.tile_offset;
+      sp.row_index = p->d_rows.p;
+      sp.x = static_cast<const uint16_t*>(x);
+      sp.ldx = ldx;
+      sp.y = y;
+      sp.ldy = ldy;
+      sp.d_in = static_cast<int32_t>(reg->d_in);
+      sp.d_out = static_cast<int32_t>(reg->d_out);
+      sp.layer = static_cast<int32_t>(layer);
+      sp.scale = scale;
+      sp.num_tiles = T;
+      sp.nkb = static_cast<int32_t>((reg->d_in + kBK - 1) / kBK);
+      sp.r_pad_max = g.r_pad_max;
+      sp.stages = g.split.stages;
+      sp.y_dtype = y_dtype == ATMM_BF16 ? 0 : 1;
+      sp.estages = g.split.estages[sp.y_dtype];
+      sp.rows_max = g.rows_max;
+      sp.s_begin = sb.tables.p;
+      sp.e_begin = sb.tables.p + (P + 1) * (sp.y_dtype == 0 ? 1 : 2);
+      sp.seg_slot0 = sb.tables.p + 3 * (P + 1);
+      sp.nseg = sp.seg_slot0 + P;
+      sp.part_off = sp.nseg + T;
+      sp.part = sb.part.p;
+      sp.mid = sb.mid.p;
+      sp.counter = sb.counter.p;
+      sp.trace = g_trace;
+      const cudaError_t e = launch_split(sp.y_dtype, sp, P, g.split.smem_s, g.split.smem_e[sp.y_dtype], stream);
+      if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
+      continue;
+    }
     BypassParams bp{};
     bp.tiles = p->d_tiles.p + g.tile_offset;
     bp.row_index = p->d_rows.p;
@@ -592,7 +800,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
     bp.nbuf = g.nbuf;
     bp.trace = g_trace;
     const A2aLayout& al = g.a2a[y_dtype == ATMM_BF16 ? 0 : 1];
-    if (al.ok && y_vec) {
+    if (path == BypassPath::kA2a) {
       bp.stages = al.stages;
       bp.stage_bytes = al.stage_bytes;
       bp.a_bytes = al.a_bytes;
@@ -719,7 +927,7 @@ int atmm_registry_create(int device, int64_t num_layers, int64_t d_in, int64_t d
     r->d_in = d_in;
     r->d_out = d_out;
     r->d_in_pad = round_up(d_in, 128);
-    r->d_out_pad = round_up(d_out, 32);
+    r->d_out_pad = round_up(d_out, 128);  // every kernel may read up^T rows up to a 128-row boundary
     *out = r.release();
   });
 }
@@ -856,6 +1064,11 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
            ", \"ny\": " + std::to_string(g.ny) + ", \"rep\": " + std::to_string(g.rep) +
            ", \"nbuf\": " + std::to_string(g.nbuf) + ", \"r_pad\": " + std::to_string(g.r_pad_max) +
            ", \"tmem_cols\": " + std::to_string(g.tmem_cols) + ", \"smem\": " + std::to_string(g.smem) +
+           ", \"path_bf16\": \"" +
+           std::string(choose_path(g, ATMM_BF16, true) == BypassPath::kA2a ? "a2a" : (choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? "split" : "fused")) +
+           "\", \"split\": " + (g.split.ok ? std::string("{\"stages\": ") + std::to_string(g.split.stages) +
+                                                   ", \"estages_bf16\": " + std::to_string(g.split.estages[0]) + "}"
+                                             : std::string("null")) +
            ", \"a2a_bf16\": " + (g.a2a[0].ok ? std::string("{\"stages\": ") + std::to_string(g.a2a[0].stages) +
                                                   ", \"tmem_cols\": " + std::to_string(g.a2a[0].tmem_cols) +
                                                   ", \"smem\": " + std::to_string(g.a2a[0].smem) + "}"
@@ -871,9 +1084,13 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
 int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64_t* ctas) {
   return guarded([&] {
     if (!p) fail(ATMM_ERR_CONFIG, "null plan");
-    int64_t t = 0;
-    for (const auto& g : p->groups) t += g.num_tiles;
-    if (launches) *launches = static_cast<int64_t>(p->groups.size());
+    int64_t t = 0, nl = 0;
+    for (const auto& g : p->groups) {
+      t += g.num_tiles;
+      nl += choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? 0 : 1;  // bf16 Y, aligned
+    }
+    if (p->merged_first >= 0) nl += 2;  // one shrink + expand pair for all split groups
+    if (launches) *launches = nl;
     if (tiles) *tiles = t;
     if (ctas) *ctas = p->total_ctas;
   });
@@ -1051,7 +1268,7 @@ int atmm_bench_launches(int device, int64_t m, int64_t d_in, int64_t rank, int64
     reg.d_in = d_in;
     reg.d_out = d_out;
     reg.d_in_pad = round_up(d_in, 128);
-    reg.d_out_pad = round_up(d_out, 32);
+    reg.d_out_pad = round_up(d_out, 128);
     {
       // Synthetic factors (values do not affect timing).
       std::vector<float> dn(static_cast<size_t>(d_in * rank)), up(static_cast<size_t>(rank * d_out));

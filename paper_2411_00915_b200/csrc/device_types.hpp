@@ -87,6 +87,48 @@ struct BypassParams {
 
 constexpr int kTraceEvents = 32;
 
+// Split path (atmm_shrink_kernel + atmm_expand_kernel) for large batches.
+// Both kernels are persistent (one CTA per SM) over host-balanced ranges of a
+// flattened work list:
+//   shrink items = (tile, 64-wide K block), tile-major.  CTA b runs items
+//     [s_begin[b], s_begin[b+1]); the run of one tile inside one CTA is a
+//     "segment" whose fp32 partial mid rows go to part[part_off[t] + slot]
+//     (slots numbered in CTA order).  The segment that completes a tile (per-tile
+//     arrival counter) sums its nseg[t] partials in FIXED order and writes
+//     bf16 mid[t] in the expand's B-operand (interleave) layout.
+//   expand items = (tile, 128 output columns), tile-major; CTA b runs items
+//     [e_begin[b], e_begin[b+1]): Y[rows, cols] += s * mid . up.
+// part / mid stay in L2 between the two launches.
+struct SplitParams {
+  const TileDesc* tiles;
+  const int32_t* row_index;
+  const uint16_t* x;   // n x d_in bf16
+  int64_t ldx;
+  void* y;             // n x d_out (bf16 or fp32)
+  int64_t ldy;
+  int32_t d_in;
+  int32_t d_out;
+  int32_t layer;
+  float scale;
+  int32_t num_tiles;
+  int32_t nkb;           // 64-wide K blocks per tile
+  int32_t nslices_unused;
+  int32_t r_pad_max;
+  int32_t stages;        // shrink ring depth
+  int32_t estages;       // expand ring depth
+  int32_t y_dtype;       // 0 bf16, 1 fp32
+  int32_t rows_max;
+  const int32_t* s_begin;    // [grid + 1]
+  const int32_t* e_begin;    // [grid + 1]
+  const int32_t* seg_slot0;  // [grid] slot (within its tile) of the CTA's first segment
+  const int32_t* nseg;       // [tile]
+  const int32_t* part_off;   // [tile]
+  float* part;               // [sum nseg][128][r_pad_max]
+  uint16_t* mid;             // [tile][128 x r_pad_max] bf16, interleave layout
+  int32_t* counter;          // [tile] segment arrivals; the completing one resets it to 0
+  uint64_t* trace;
+};
+
 struct MergeParams {
   const uint16_t* a_t;  // down^T blocked (MN-major A): [kb][g][c][8x8], K = r_pad
   const uint16_t* b_t;  // up^T blocked (K-major B):    [g][c][8x8]

@@ -1211,6 +1211,416 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
 }
 
 // =========================================================================
+// Split path for large batches: atmm_shrink_kernel + atmm_expand_kernel
+// =========================================================================
+// Large batches are bandwidth bound and their scattered X / Y rows are
+// gathered at the LSU: 16-byte cp.async from four loader warps (a TMA
+// gather4 request moves 512 B per ~85 cycles per SM, a third of the SM's
+// share of HBM bandwidth).  Both kernels are persistent, one CTA per SM, over
+// host-balanced work ranges (device_types.hpp SplitParams), warp-specialised:
+//   warps 0..7  loaders: cp.async into a ring of stages; each loader thread
+//               keeps D = stages - 1 stages in flight, then (wait_group,
+//               fence.proxy.async) its warp arrives on the stage's full barrier;
+//   warp 8      TMEM owner + tcgen05.mma issuer (one elected lane);
+//   warps 9..   epilogue (warp w reads TMEM lane quadrant w % 4): 4 in the
+//               shrink, 8 in the expand (two per quadrant, splitting rows).
+constexpr int kSplitLoaderWarps = 8;  // LSU gather throughput scales with issuing warps
+constexpr int kSplitLoaders = kSplitLoaderWarps * 32;
+constexpr uint32_t kSplitWarpMMA = kSplitLoaderWarps;
+constexpr uint32_t kSplitWarpEpi = kSplitWarpMMA + 1;
+constexpr int kShrinkThreads = (kSplitLoaderWarps + 1 + 4) * 32;  // 4 epilogue warps
+constexpr int kExpandThreads = (kSplitLoaderWarps + 1 + 8) * 32;  // 8 epilogue warps
+
+// Loader-side completion: after issuing item j (committed as one cp.async
+// group), the item D groups back has landed for every lane of the warp;
+// lane 0 publishes it (full barriers count one arrival per loader warp).
+__device__ __forceinline__ void loader_publish(int j, int D, int S, uint64_t* full, uint32_t lane) {
+  if (j - D + 1 >= 0) {
+    cp_async_wait<7>(D - 1);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&full[(j - D + 1) % S]);
+  }
+}
+__device__ __forceinline__ void loader_drain(int n, int D, int S, uint64_t* full, uint32_t lane) {
+  cp_async_wait<0>(0);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    for (int j = max(0, n - D + 1); j < n; ++j) mbar_arrive(&full[j % S]);
+  }
+}
+
+// ---- shrink: partial mid rows per (tile, CTA) segment, stream-K over K ----
+//   stage = [A: 128 rows x 128 B, 128-byte swizzle | B: r_pad_max x 64 down^T]
+__global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const SplitParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t bars[2 * 8 + 4];
+  __shared__ uint32_t tmem_slot;
+  __shared__ int32_t last_flag;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t warp = tid >> 5;
+  const uint32_t lane = tid & 31;
+  const int S = p.stages;
+  const int D = S - 1;
+  uint64_t* full = bars;            // [S], one arrival per loader warp
+  uint64_t* empty = bars + 8;       // [S], MMA commit
+  uint64_t* acc_full = bars + 16;   // [2], MMA commit
+  uint64_t* acc_empty = bars + 18;  // [2], 128 epilogue arrivals
+  const uint32_t a_bytes = kTileM * 128u;
+  const uint32_t stage_bytes = a_bytes + static_cast<uint32_t>(p.r_pad_max * kBK * 2);
+  const uint32_t tcols = p.r_pad_max <= 32 ? 64u : (p.r_pad_max <= 64 ? 128u : 256u);  // 2 accumulators
+  const int i_beg = p.s_begin[blockIdx.x];
+  const int i_end = p.s_begin[blockIdx.x + 1];
+
+  if (warp == 0) {
+    if (lane < 2 * 8 + 4) mbar_init(&bars[lane], lane < 8 ? kSplitLoaderWarps : (lane >= 18 ? 128u : 1u));
+    fence_mbar_init();
+  }
+  if (warp == kSplitWarpMMA) tmem_alloc(&tmem_slot, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+  const uint32_t smem0 = smem_u32(smem);
+
+  if (warp < kSplitLoaderWarps) {
+    // ===================== loaders =====================
+    // X chunk (row, ch) of an item: ch = tid & 7 fixed, rows (tid >> 3) + 48 i.
+    constexpr int kRowStep = kSplitLoaders / 8;
+    constexpr int kRowsPer = (kTileM + kRowStep - 1) / kRowStep;
+    const int ch = static_cast<int>(tid & 7);
+    const int r0 = static_cast<int>(tid >> 3);
+    int64_t xoff[kRowsPer];
+    int cur_t = -1, rows = 0, r_pad = 0;
+    const uint16_t* down_t = nullptr;
+    griddep_wait();  // X may be produced by the previous kernel
+    int j = 0;
+    for (int item = i_beg; item < i_end; ++item, ++j) {
+      const int t = item / p.nkb;
+      const int kb = item - t * p.nkb;
+      if (t != cur_t) {
+        const TileDesc tile = p.tiles[t];
+        cur_t = t;
+        rows = tile.rows;
+        r_pad = tile.r_pad;
+        down_t = tile.down_t + static_cast<int64_t>(p.layer) * tile.down_layer_stride;
+#pragma unroll
+        for (int i = 0; i < kRowsPer; ++i) {
+          const int r = r0 + kRowStep * i;
+          xoff[i] = r < rows ? static_cast<int64_t>(p.row_index[tile.row_begin + r]) * p.ldx : 0;
+        }
+      }
+      const int st = j % S;
+      mbar_wait(&empty[st], static_cast<uint32_t>(((j / S) & 1) ^ 1));
+      const uint32_t A = smem0 + static_cast<uint32_t>(st) * stage_bytes;
+      const uint16_t* xk = p.x + static_cast<int64_t>(kb) * kBK + ch * 8;
+#pragma unroll
+      for (int i = 0; i < kRowsPer; ++i) {
+        const int r = r0 + kRowStep * i;
+        if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], 16u);
+      }
+      const uint16_t* dk = down_t + static_cast<int64_t>(kb) * r_pad * kBK;
+      for (int q = static_cast<int>(tid); q < r_pad * 8; q += kSplitLoaders) cp_async16(A + a_bytes + q * 16, dk + q * 8, 16u);
+      cp_async_commit();
+      loader_publish(j, D, S, full, lane);
+    }
+    loader_drain(j, D, S, full, lane);
+  } else if (warp == kSplitWarpMMA) {
+    // ===================== MMA issuer =====================
+    int j = 0, seg = 0;
+    for (int item = i_beg; item < i_end; ++item, ++j) {
+      const int t = item / p.nkb;
+      const int kb = item - t * p.nkb;
+      const bool first = item == i_beg || kb == 0;
+      const bool last = item == i_end - 1 || kb == p.nkb - 1;
+      const int r_pad = p.tiles[t].r_pad;
+      const int buf = seg & 1;
+      if (first) mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((seg >> 1) & 1) ^ 1));
+      const int st = j % S;
+      mbar_wait(&full[st], static_cast<uint32_t>((j / S) & 1));
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t A = smem0 + static_cast<uint32_t>(st) * stage_bytes;
+        const uint64_t ad0 = smem_desc(A, 16u, 1024u, kLayoutSW128);
+        const uint64_t bd0 = smem_desc(A + a_bytes, 128u, 1024u, kLayoutNone);
+        const uint32_t idesc = idesc_bf16(kTileM, static_cast<uint32_t>(r_pad));
+        const uint32_t d = tmem_base + static_cast<uint32_t>(buf * (tcols / 2));
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk) {
+          mma_bf16(d, ad0 + static_cast<uint64_t>(kk * 2), bd0 + static_cast<uint64_t>(kk * 16), idesc,
+                   (first && kk == 0) ? 0u : 1u);
+        }
+        mma_commit(&empty[st]);
+        if (last) mma_commit(&acc_full[buf]);
+      }
+      __syncwarp();
+      if (last) ++seg;
+    }
+  } else {
+    // ===================== epilogue: segment partials, tile reductions =====================
+    const uint32_t quad = warp & 3u;
+    const int row = static_cast<int>(quad * 32 + lane);
+    const uint32_t et = tid - kSplitWarpEpi * 32;  // 0..127
+    int seg = 0;
+    for (int item = i_beg; item < i_end; ++item) {
+      const int t = item / p.nkb;
+      const int kb = item - t * p.nkb;
+      if (!(item == i_end - 1 || kb == p.nkb - 1)) continue;  // act at segment ends
+      const TileDesc tile = p.tiles[t];
+      const int rows = tile.rows;
+      const int r_pad = tile.r_pad;
+      const int buf = seg & 1;
+      mbar_wait_sleep(&acc_full[buf], static_cast<uint32_t>((seg >> 1) & 1), 64);
+      tc_fence_after();
+      // slot of this segment among the tile's segments: the CTA's first
+      // segment may continue a tile begun by earlier CTAs; later ones start it.
+      const int sidx = seg == 0 ? p.seg_slot0[blockIdx.x] : 0;
+      float* slot = p.part + (static_cast<int64_t>(p.part_off[t] + sidx) * kTileM) * p.r_pad_max;
+      if (static_cast<int>(quad * 32) < rows) {
+        for (int g = 0; g < r_pad; g += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(buf * (tcols / 2) + g), v);
+          tmem_wait_ld();
+          if (row < rows) {
+            float4* dst = reinterpret_cast<float4*>(slot + static_cast<int64_t>(row) * p.r_pad_max + g);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              __stcg(dst + q, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                          __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      ++seg;
+      // publish the partial; the segment completing the tile reduces it
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (et == 0) last_flag = atomicAdd(&p.counter[t], 1) == p.nseg[t] - 1;
+      named_bar_sync(1, 128);
+      if (last_flag) {
+        __threadfence();
+        const int ns = p.nseg[t];
+        const float* part_t = p.part + static_cast<int64_t>(p.part_off[t]) * kTileM * p.r_pad_max;
+        uint16_t* mid_t = p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max;
+        const int cpr4 = r_pad / 4;
+        for (int it = static_cast<int>(et); it < rows * cpr4; it += 128) {
+          const int rr = it / cpr4;
+          const int c4 = it - rr * cpr4;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int sg = 0; sg < ns; ++sg) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(part_t + (static_cast<int64_t>(sg) * kTileM + rr) * p.r_pad_max + c4 * 4));
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+          }
+          const uint32_t off = interleave_off(static_cast<uint32_t>(rr), static_cast<uint32_t>(c4 * 4), static_cast<uint32_t>(r_pad));
+          *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(mid_t) + off) = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
+        }
+        if (et == 0) p.counter[t] = 0;  // ready for the next launch (stream order)
+      }
+    }
+  }
+  __syncthreads();
+  griddep_launch_dependents();
+  if (warp == kSplitWarpMMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, tcols);
+  }
+}
+
+// ---- expand: Y[rows, n0 .. n0 + 128 G) += s * (mid . up), swap-AB ----
+//   D_j[out column][row] = up^T[128 cols, r] . mid^T: G MMAs of M = 128,
+//   N = rows16.  up^T rows are staged PERMUTED (MMA j, lane m <- column
+//   m G + j), so epilogue thread (quadrant q, lane l) owns the G adjacent
+//   output columns (32 q + l) G .. + G - 1 (one 2 G-byte access per row).
+//   stage = [up^T 128 G x r_pad_max | mid rows16_max x r_pad_max | Y rows_max x 128 G | rows]
+template <typename YT, int G>
+__global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const SplitParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  // interleave (no-swizzle) operands only need 16-byte alignment: align to 128
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~static_cast<uintptr_t>(127));
+  __shared__ uint64_t bars[2 * 4 + 4];
+  __shared__ uint32_t tmem_slot;
+  constexpr int kEsz = static_cast<int>(sizeof(YT));
+  constexpr int kCols = kTileM * G;  // output columns per item
+  const uint32_t tid = threadIdx.x;
+  const uint32_t warp = tid >> 5;
+  const uint32_t lane = tid & 31;
+  const int S = p.estages;
+  const int D = S - 1;
+  uint64_t* full = bars;           // [S], one arrival per loader warp
+  uint64_t* empty = bars + 4;      // [S], 256 epilogue arrivals
+  uint64_t* acc_full = bars + 8;   // [2], MMA commit
+  uint64_t* acc_empty = bars + 10; // [2], 256 epilogue arrivals
+  const int rows16_max = (p.rows_max + 15) & ~15;
+  const uint32_t up_bytes = static_cast<uint32_t>(kCols * p.r_pad_max * 2);
+  const uint32_t mid_bytes = static_cast<uint32_t>((rows16_max * p.r_pad_max * 2 + 127) & ~127);
+  const uint32_t ypitch = kCols * kEsz;
+  const uint32_t y_bytes = static_cast<uint32_t>(p.rows_max) * ypitch;
+  // + the global row index of each Y row (kTileM int32) at the end of the stage
+  const uint32_t stage_bytes = (up_bytes + mid_bytes + y_bytes + kTileM * 4 + 127) & ~127u;
+  const uint32_t acc_cols = static_cast<uint32_t>(G * rows16_max);
+  const uint32_t tcols = acc_cols <= 16 ? 32u : (acc_cols <= 32 ? 64u : (acc_cols <= 64 ? 128u : 256u));  // 2 accumulators
+  const int i_beg = p.e_begin[blockIdx.x];
+  const int i_end = p.e_begin[blockIdx.x + 1];
+  const int64_t ldy_b = p.ldy * kEsz;
+  const int nsl = (p.d_out + kCols - 1) / kCols;
+
+  if (warp == 0) {
+    if (lane < 12) mbar_init(&bars[lane], lane < 4 ? kSplitLoaderWarps : ((lane < 8 || lane >= 10) ? 256u : 1u));
+    fence_mbar_init();
+  }
+  if (warp == kSplitWarpMMA) tmem_alloc(&tmem_slot, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+  const uint32_t smem0 = smem_u32(smem);
+
+  if (warp < kSplitLoaderWarps) {
+    // ===================== loaders =====================
+    bool waited = false;
+    int j = 0;
+    for (int item = i_beg; item < i_end; ++item, ++j) {
+      const int t = item / nsl;
+      const int n0 = (item - t * nsl) * kCols;
+      const int ncols = min(kCols, p.d_out - n0);
+      const TileDesc tile = p.tiles[t];
+      const int rows = tile.rows;
+      const int r_pad = tile.r_pad;
+      const int st = j % S;
+      mbar_wait(&empty[st], static_cast<uint32_t>(((j / S) & 1) ^ 1));
+      const uint32_t U = smem0 + static_cast<uint32_t>(st) * stage_bytes;
+      const uint32_t M = U + up_bytes;
+      const uint32_t Yb = M + mid_bytes;
+      const uint32_t Rb = Yb + y_bytes;  // rows of this stage
+      if (tid < static_cast<uint32_t>(kTileM)) st_shared_u32(Rb + tid * 4, static_cast<uint32_t>(p.row_index[tile.row_begin + min(static_cast<int>(tid), rows - 1)]));
+      named_bar_sync(2, kSplitLoaders);  // the stage's row indices are written
+      // up^T rows n0 .. n0 + kCols - 1, 16-byte units permuted: column n0 + nl
+      // -> MMA j = nl % G, A row nl / G.
+      const uint16_t* us = tile.up_t + static_cast<int64_t>(p.layer) * tile.up_layer_stride;
+      const int kc = r_pad / 8;
+      for (int q = static_cast<int>(tid); q < kCols * kc; q += kSplitLoaders) {
+        const int nl = q / kc;
+        const int c = q - nl * kc;
+        const int n = n0 + nl;
+        const int a_row = (nl % G) * kTileM + nl / G;
+        cp_async16(U + interleave_off(static_cast<uint32_t>(a_row), static_cast<uint32_t>(c * 8), static_cast<uint32_t>(r_pad)),
+                   us + ((static_cast<int64_t>(n >> 3) * kc + c) * 64 + (n & 7) * 8), 16u);
+      }
+      // Y rows: the shrink launch (our predecessor) does not write Y and fires
+      // its dependents only after its own griddepcontrol.wait, so every earlier
+      // writer of Y has completed: Y may be read before our own wait.
+      const int cpr = ncols * kEsz / 16;
+      const uint8_t* yb = reinterpret_cast<const uint8_t*>(p.y) + static_cast<int64_t>(n0) * kEsz;
+      for (int q = static_cast<int>(tid); q < rows * cpr; q += kSplitLoaders) {
+        const int r = q / cpr;
+        const int c = q - r * cpr;
+        cp_async16(Yb + static_cast<uint32_t>(r) * ypitch + c * 16, yb + static_cast<int64_t>(static_cast<int32_t>(ld_shared_u32(Rb + r * 4))) * ldy_b + c * 16, 16u);
+      }
+      if (!waited) {
+        griddep_wait();  // mid is produced by the shrink launch
+        waited = true;
+      }
+      const uint16_t* ms = p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max;
+      const int rows16 = (rows + 15) & ~15;
+      for (int q = static_cast<int>(tid); q < rows16 * r_pad / 8; q += kSplitLoaders) cp_async16(M + q * 16, ms + q * 8, 16u);
+      cp_async_commit();
+      loader_publish(j, D, S, full, lane);
+    }
+    if (!waited) griddep_wait();
+    loader_drain(j, D, S, full, lane);
+  } else if (warp == kSplitWarpMMA) {
+    // ===================== MMA issuer =====================
+    int j = 0;
+    for (int item = i_beg; item < i_end; ++item, ++j) {
+      const int t = item / nsl;
+      const TileDesc tile = p.tiles[t];
+      const int rows16 = (tile.rows + 15) & ~15;
+      const int r_pad = tile.r_pad;
+      const int st = j % S;
+      const int buf = j & 1;
+      mbar_wait(&acc_empty[buf], static_cast<uint32_t>(((j >> 1) & 1) ^ 1));
+      mbar_wait(&full[st], static_cast<uint32_t>((j / S) & 1));
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t U = smem0 + static_cast<uint32_t>(st) * stage_bytes;
+        const uint32_t sbo = static_cast<uint32_t>(r_pad) * 16u;
+        const uint64_t bd0 = smem_desc(U + up_bytes, 128u, sbo, kLayoutNone);
+        const uint32_t idesc = idesc_bf16(kTileM, static_cast<uint32_t>(rows16));
+#pragma unroll
+        for (int jj = 0; jj < G; ++jj) {
+          const uint64_t ad0 = smem_desc(U + static_cast<uint32_t>(jj) * 16u * sbo, 128u, sbo, kLayoutNone);
+          const uint32_t d = tmem_base + static_cast<uint32_t>(buf * (tcols / 2) + jj * rows16);
+          for (int kk = 0; kk < r_pad / 16; ++kk) {
+            mma_bf16(d, ad0 + static_cast<uint64_t>(kk * 16), bd0 + static_cast<uint64_t>(kk * 16), idesc, kk > 0 ? 1u : 0u);
+          }
+        }
+        mma_commit(&acc_full[buf]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ===================== epilogue (8 warps) =====================
+    // Warp w: TMEM lane quadrant w % 4, row blocks of RB rows alternating
+    // between the two warps of a quadrant.
+    constexpr int RB = 64 / G > 32 ? 32 : 64 / G;
+    const uint32_t quad = warp & 3u;
+    const int half = static_cast<int>(warp - kSplitWarpEpi) >> 2;
+    const int m = static_cast<int>(quad * 32 + lane);
+    int j = 0;
+    for (int item = i_beg; item < i_end; ++item, ++j) {
+      const int t = item / nsl;
+      const int n0 = (item - t * nsl) * kCols;
+      const int ncols = min(kCols, p.d_out - n0);
+      const TileDesc tile = p.tiles[t];
+      const int rows = tile.rows;
+      const int rows16 = (rows + 15) & ~15;
+      const float s = p.scale * tile.scale;
+      const int st = j % S;
+      const int buf = j & 1;
+      mbar_wait(&full[st], static_cast<uint32_t>((j / S) & 1));  // acquire the loaders' Y / row data
+      mbar_wait(&acc_full[buf], static_cast<uint32_t>((j >> 1) & 1));
+      tc_fence_after();
+      const int c0 = m * G;
+      const bool col_ok = c0 < ncols;
+      const uint32_t Yb = smem0 + static_cast<uint32_t>(st) * stage_bytes + up_bytes + mid_bytes;
+      const uint32_t rring = Yb + y_bytes;
+      uint8_t* ydst = reinterpret_cast<uint8_t*>(p.y) + static_cast<int64_t>(n0 + c0) * kEsz;
+      for (int rb = half * RB; rb < rows16; rb += 2 * RB) {
+        uint32_t acc[64];
+#pragma unroll
+        for (int jj = 0; jj < G; ++jj) {
+          tmem_ld_rows<RB>(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(buf * (tcols / 2) + jj * rows16 + rb),
+                           &acc[jj * RB]);
+        }
+        tmem_wait_ld();
+        if (col_ok) {
+          a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), Yb + static_cast<uint32_t>(c0 * kEsz), ypitch, ydst, rring,
+                                 ldy_b, s);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      mbar_arrive(&empty[st]);
+    }
+  }
+  __syncthreads();
+  griddep_launch_dependents();
+  if (warp == kSplitWarpMMA) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, tcols);
+  }
+}
+
+// =========================================================================
 // Merge / GEMM kernel:  W = beta*W + alpha * A . B
 //   A (M x K): MN-major operand assembled from the down^T blocked layout.
 //   B (N x K): up^T blocked, K-major.
@@ -1639,6 +2049,8 @@ template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUten
 template __global__ void atmm_bypass_a2a_kernel<__nv_bfloat16>(const __grid_constant__ CUtensorMap,
                                                                const BypassParams);
 template __global__ void atmm_bypass_a2a_kernel<float>(const __grid_constant__ CUtensorMap, const BypassParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 2>(const SplitParams);
+template __global__ void atmm_expand_kernel<float, 1>(const SplitParams);
 template __global__ void atmm_merge_kernel<float>(const MergeParams);
 template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
 template __global__ void atmm_merge_tma_kernel<float>(const __grid_constant__ CUtensorMap, const MergeParams);
@@ -1759,6 +2171,36 @@ cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const Bypa
   cudaError_t e = prepare(k, smem, C > 8);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k, tmap_x, p);
+}
+
+cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,
+                         cudaStream_t stream) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kShrinkThreads, 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.dynamicSmemBytes = smem_s;
+  cudaError_t e = prepare(atmm_shrink_kernel, smem_s, false);
+  if (e != cudaSuccess) return e;
+  e = cudaLaunchKernelEx(&cfg, atmm_shrink_kernel, p);
+  if (e != cudaSuccess) return e;
+  cfg.blockDim = dim3(kExpandThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem_e;
+  if (y_dtype == 0) {
+    auto k = atmm_expand_kernel<__nv_bfloat16, 2>;
+    e = prepare(k, smem_e, false);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, k, p);
+  }
+  auto k = atmm_expand_kernel<float, 1>;
+  e = prepare(k, smem_e, false);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, k, p);
 }
 
 int bypass_max_active_clusters(int C, size_t smem) {

@@ -367,6 +367,21 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
                : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Wait until at most `n` of this thread's committed cp.async groups are pending
+// (n is runtime, 0 <= n <= N; the instruction takes an immediate).
+template <int N>
+__device__ __forceinline__ void cp_async_wait(int n) {
+  if constexpr (N <= 0) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else {
+    if (n >= N) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+    } else {
+      cp_async_wait<N - 1>(n);
+    }
+  }
+}
 // Arrive on `bar` once all prior cp.async of this thread have landed (the
 // arrival counts against the barrier's expected count).
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
