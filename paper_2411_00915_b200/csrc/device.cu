@@ -467,7 +467,7 @@ struct SplitBufs {
   DevBuf<float> part;
   DevBuf<uint16_t> mid;
   DevBuf<int32_t> counter;
-  DevBuf<int32_t> tables;  // [s_begin | e_begin bf16 | e_begin fp32 (P+1 each) | seg_slot0 (P) | nseg (T) | part_off (T)]
+  DevBuf<int32_t> tables;  // [s_begin | e_begin bf16 | e_begin fp32 (P+1 each) | seg_slot0 (P) | nseg | part_off (T) | red_off (T+1)]
   int32_t grid = 0;
 };
 
@@ -509,6 +509,27 @@ static BypassPath choose_path(const LaunchGroup& g, int y_dtype, bool y_vec) {
   return BypassPath::kFused;
 }
 
+// Expand item width for bf16 Y: 128 G columns, G adjacent columns per
+// epilogue thread (ATMM_EXPAND_G=1|2 for A/B runs).
+static int expand_g_bf16() {
+  static const int g = [] {
+    const char* e = std::getenv("ATMM_EXPAND_G");
+    return e && std::atoi(e) == 1 ? 1 : 2;
+  }();
+  return g;
+}
+
+// Fixed per-item costs (bytes-equivalent) of the split kernels' balancing
+// (ATMM_SCOST / ATMM_ECOST for A/B runs).
+static int64_t shrink_fixed_cost() {
+  static const int64_t v = std::getenv("ATMM_SCOST") ? std::atoll(std::getenv("ATMM_SCOST")) : 16384;
+  return v;
+}
+static int64_t expand_fixed_cost() {
+  static const int64_t v = std::getenv("ATMM_ECOST") ? std::atoll(std::getenv("ATMM_ECOST")) : 32768;
+  return v;
+}
+
 static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, int32_t r_pad) {
   SplitLayout l;
   (void)d_in;
@@ -521,7 +542,7 @@ static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, 
   bool ok = l.stages >= 2;
   for (int di = 0; di < 2; ++di) {
     const int64_t esz = di == 0 ? 2 : 4;
-    const int64_t cols = int64_t(kTileM) * (di == 0 ? 2 : 1);  // expand item width (G = 2 bf16, 1 fp32)
+    const int64_t cols = int64_t(kTileM) * (di == 0 ? expand_g_bf16() : 1);  // expand item width (128 G columns)
     const int64_t est = round_up(cols * r_pad * 2 + round_up(rows16 * r_pad * 2, 128) + int64_t(rows_max) * cols * esz + kTileM * 4, 128);
     l.estages[di] = static_cast<int32_t>(std::min<int64_t>(4, (avail + 1024 - 128) / est));  // 128-byte aligned kernel
     l.smem_e[di] = size_t(128 + l.estages[di] * est);
@@ -648,11 +669,12 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     std::vector<int64_t> scost, ecost[2];
     for (int t = 0; t < T; ++t) {
       const TileDesc& td = all_tiles[static_cast<size_t>(g.tile_offset + t)];
-      for (int k = 0; k < nkb; ++k) scost.push_back(int64_t(td.rows) * 128 + int64_t(td.r_pad) * 128 + 512);
+      // bytes moved + a fixed per-item cost (pipeline step: barriers, 4 MMAs)
+      for (int k = 0; k < nkb; ++k) scost.push_back(int64_t(td.rows) * 128 + int64_t(td.r_pad) * 128 + shrink_fixed_cost());
       for (int di = 0; di < 2; ++di) {
-        const int64_t cols = int64_t(kTileM) * (di == 0 ? 2 : 1), esz = di == 0 ? 2 : 4;
+        const int64_t cols = int64_t(kTileM) * (di == 0 ? expand_g_bf16() : 1), esz = di == 0 ? 2 : 4;
         const int nsl = static_cast<int>((reg->d_out + cols - 1) / cols);
-        for (int k = 0; k < nsl; ++k) ecost[di].push_back(int64_t(td.rows) * cols * esz * 2 + cols * td.r_pad * 2 + 1024);
+        for (int k = 0; k < nsl; ++k) ecost[di].push_back(int64_t(td.rows) * cols * esz * 2 + cols * td.r_pad * 2 + expand_fixed_cost());
       }
     }
     const int P = std::max(1, std::min<int>(sms, static_cast<int>(scost.size())));
@@ -671,6 +693,11 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
       off[t] = total_seg;
       total_seg += nseg[t];
     }
+    std::vector<int32_t> red_off(static_cast<size_t>(T) + 1, 0);
+    for (int t = 0; t < T; ++t) {
+      const TileDesc& td = all_tiles[static_cast<size_t>(g.tile_offset + t)];
+      red_off[static_cast<size_t>(t) + 1] = red_off[static_cast<size_t>(t)] + td.rows * (td.r_pad / 4);
+    }
     std::vector<int32_t> tables;
     tables.insert(tables.end(), sb.begin(), sb.end());
     tables.insert(tables.end(), eb0.begin(), eb0.end());
@@ -678,12 +705,13 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     tables.insert(tables.end(), slot0.begin(), slot0.end());
     tables.insert(tables.end(), nseg.begin(), nseg.end());
     tables.insert(tables.end(), off.begin(), off.end());
+    tables.insert(tables.end(), red_off.begin(), red_off.end());
     auto& mb = plan->merged_bufs;
     mb = std::make_unique<SplitBufs>();
     mb->grid = P;
     mb->part.alloc(static_cast<size_t>(total_seg) * kTileM * g.r_pad_max);
     mb->mid.alloc(static_cast<size_t>(T) * kTileM * g.r_pad_max);
-    mb->counter.alloc(static_cast<size_t>(T));
+    mb->counter.alloc(2);
     mb->tables.alloc(tables.size());
     CUDA_CHECK(cudaMemset(mb->mid.p, 0, mb->mid.n * sizeof(uint16_t)));
     CUDA_CHECK(cudaMemset(mb->counter.p, 0, mb->counter.n * sizeof(int32_t)));
@@ -751,12 +779,14 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.stages = g.split.stages;
       sp.y_dtype = y_dtype == ATMM_BF16 ? 0 : 1;
       sp.estages = g.split.estages[sp.y_dtype];
+      sp.expand_g = sp.y_dtype == 0 ? expand_g_bf16() : 1;
       sp.rows_max = g.rows_max;
       sp.s_begin = sb.tables.p;
       sp.e_begin = sb.tables.p + (P + 1) * (sp.y_dtype == 0 ? 1 : 2);
       sp.seg_slot0 = sb.tables.p + 3 * (P + 1);
       sp.nseg = sp.seg_slot0 + P;
       sp.part_off = sp.nseg + T;
+      sp.red_off = sp.part_off + T;
       sp.part = sb.part.p;
       sp.mid = sb.mid.p;
       sp.counter = sb.counter.p;

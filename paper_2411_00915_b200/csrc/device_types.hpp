@@ -93,9 +93,10 @@ constexpr int kTraceEvents = 32;
 //   shrink items = (tile, 64-wide K block), tile-major.  CTA b runs items
 //     [s_begin[b], s_begin[b+1]); the run of one tile inside one CTA is a
 //     "segment" whose fp32 partial mid rows go to part[part_off[t] + slot]
-//     (slots numbered in CTA order).  The segment that completes a tile (per-tile
-//     arrival counter) sums its nseg[t] partials in FIXED order and writes
-//     bf16 mid[t] in the expand's B-operand (interleave) layout.
+//     (slots numbered in CTA order).  After a grid-wide barrier every CTA
+//     sums a share of the (tile, row, 4 columns) items over the tile's nseg[t]
+//     partials in FIXED slot order and writes bf16 mid[t] in the expand's
+//     B-operand (interleave) layout.
 //   expand items = (tile, 128 output columns), tile-major; CTA b runs items
 //     [e_begin[b], e_begin[b+1]): Y[rows, cols] += s * mid . up.
 // part / mid stay in L2 between the two launches.
@@ -112,7 +113,7 @@ struct SplitParams {
   float scale;
   int32_t num_tiles;
   int32_t nkb;           // 64-wide K blocks per tile
-  int32_t nslices_unused;
+  int32_t expand_g;      // output columns per expand epilogue thread (items of 128 G columns)
   int32_t r_pad_max;
   int32_t stages;        // shrink ring depth
   int32_t estages;       // expand ring depth
@@ -125,7 +126,8 @@ struct SplitParams {
   const int32_t* part_off;   // [tile]
   float* part;               // [sum nseg][128][r_pad_max]
   uint16_t* mid;             // [tile][128 x r_pad_max] bf16, interleave layout
-  int32_t* counter;          // [tile] segment arrivals; the completing one resets it to 0
+  int32_t* counter;          // [2] grid barrier (arrivals, sense flag)
+  const int32_t* red_off;    // [tile + 1] prefix of rows x r_pad / 4 reduction items
   uint64_t* trace;
 };
 

@@ -1231,6 +1231,32 @@ constexpr uint32_t kSplitWarpEpi = kSplitWarpMMA + 1;
 constexpr int kShrinkThreads = (kSplitLoaderWarps + 1 + 4) * 32;  // 4 epilogue warps
 constexpr int kExpandThreads = (kSplitLoaderWarps + 1 + 8) * 32;  // 8 epilogue warps
 
+// Debug trace (tools/profile_trace.py --split): %globaltimer per CTA event.
+#define STRACE(ev)                                                                          \
+  do {                                                                                      \
+    if (p.trace) p.trace[static_cast<size_t>(blockIdx.x) * kTraceEvents + (ev)] = globaltimer(); \
+  } while (0)
+
+// Grid-wide barrier for a persistent grid whose CTAs are all co-resident:
+// ctr[0] counts arrivals, ctr[1] is a sense flag flipped by the last arrival
+// (which also resets ctr[0] for the next launch).
+__device__ __forceinline__ void grid_barrier(int32_t* ctr, uint32_t nblocks) {
+  if (threadIdx.x == 0) {
+    volatile int32_t* flag = ctr + 1;
+    const int32_t sense = *flag;
+    __threadfence();
+    if (atomicAdd(ctr, 1) == static_cast<int32_t>(nblocks) - 1) {
+      ctr[0] = 0;
+      __threadfence();
+      atomicExch(ctr + 1, sense ^ 1);
+    } else {
+      while (*flag == sense) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // Loader-side completion: after issuing item j (committed as one cp.async
 // group), the item D groups back has landed for every lane of the warp;
 // lane 0 publishes it (full barriers count one arrival per loader warp).
@@ -1259,7 +1285,6 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
                                              ~static_cast<uintptr_t>(1023));
   __shared__ uint64_t bars[2 * 8 + 4];
   __shared__ uint32_t tmem_slot;
-  __shared__ int32_t last_flag;
   const uint32_t tid = threadIdx.x;
   const uint32_t warp = tid >> 5;
   const uint32_t lane = tid & 31;
@@ -1274,6 +1299,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
   const uint32_t tcols = p.r_pad_max <= 32 ? 64u : (p.r_pad_max <= 64 ? 128u : 256u);  // 2 accumulators
   const int i_beg = p.s_begin[blockIdx.x];
   const int i_end = p.s_begin[blockIdx.x + 1];
+  if (tid == 0) STRACE(0);
 
   if (warp == 0) {
     if (lane < 2 * 8 + 4) mbar_init(&bars[lane], lane < 8 ? kSplitLoaderWarps : (lane >= 18 ? 128u : 1u));
@@ -1328,6 +1354,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
       loader_publish(j, D, S, full, lane);
     }
     loader_drain(j, D, S, full, lane);
+    if (tid == 0) STRACE(1);
   } else if (warp == kSplitWarpMMA) {
     // ===================== MMA issuer =====================
     int j = 0, seg = 0;
@@ -1397,36 +1424,85 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
       ++seg;
-      // publish the partial; the segment completing the tile reduces it
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (et == 0) last_flag = atomicAdd(&p.counter[t], 1) == p.nseg[t] - 1;
-      named_bar_sync(1, 128);
-      if (last_flag) {
-        __threadfence();
-        const int ns = p.nseg[t];
-        const float* part_t = p.part + static_cast<int64_t>(p.part_off[t]) * kTileM * p.r_pad_max;
-        uint16_t* mid_t = p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max;
-        const int cpr4 = r_pad / 4;
-        for (int it = static_cast<int>(et); it < rows * cpr4; it += 128) {
-          const int rr = it / cpr4;
-          const int c4 = it - rr * cpr4;
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int sg = 0; sg < ns; ++sg) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(part_t + (static_cast<int64_t>(sg) * kTileM + rr) * p.r_pad_max + c4 * 4));
-            acc.x += v.x;
-            acc.y += v.y;
-            acc.z += v.z;
-            acc.w += v.w;
+    }
+  }
+  if (tid == kSplitWarpEpi * 32) STRACE(2);
+  // ---- all partials written: grid-wide barrier, then every thread of every
+  // CTA sums a share of the (tile, row, 4 columns) items over the tile's
+  // segments in FIXED slot order -> bf16 mid.  (The grid is one CTA per SM,
+  // all co-resident, so the barrier cannot deadlock.) ----
+  __threadfence();
+  __syncthreads();
+  grid_barrier(p.counter, gridDim.x);
+  {
+    const int T = p.num_tiles;
+    // tile lookup table in shared memory (the ring is dead now)
+    int32_t* red_off_s = reinterpret_cast<int32_t*>(smem);
+    for (int i = static_cast<int>(tid); i <= T; i += static_cast<int>(blockDim.x)) red_off_s[i] = p.red_off[i];
+    __syncthreads();
+    const int total = red_off_s[T];
+    const int64_t seg_stride = static_cast<int64_t>(kTileM) * p.r_pad_max;
+    const int gstride = static_cast<int>(gridDim.x * blockDim.x);
+    constexpr int kB = 2;
+    for (int i0 = static_cast<int>(blockIdx.x * blockDim.x + tid); i0 < total; i0 += gstride * kB) {
+      float4 acc[kB];
+      const float* src[kB];
+      uint8_t* dst[kB];
+      int ns[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int i = i0 + b * gstride;
+        ns[b] = 0;
+        src[b] = p.part;
+        dst[b] = nullptr;
+        if (i < total) {
+          int lo = 0, hi = T;  // tile t: red_off[t] <= i < red_off[t + 1]
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (red_off_s[mid] <= i) lo = mid; else hi = mid;
           }
-          const uint32_t off = interleave_off(static_cast<uint32_t>(rr), static_cast<uint32_t>(c4 * 4), static_cast<uint32_t>(r_pad));
-          *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(mid_t) + off) = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
+          const int t = lo;
+          const int r_pad = p.tiles[t].r_pad;
+          const int local = i - red_off_s[t];
+          const int rr = local / (r_pad / 4);
+          const int c4 = local - rr * (r_pad / 4);
+          ns[b] = p.nseg[t];
+          src[b] = p.part + static_cast<int64_t>(p.part_off[t]) * seg_stride + static_cast<int64_t>(rr) * p.r_pad_max + c4 * 4;
+          dst[b] = reinterpret_cast<uint8_t*>(p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max) +
+                   interleave_off(static_cast<uint32_t>(rr), static_cast<uint32_t>(c4 * 4), static_cast<uint32_t>(r_pad));
         }
-        if (et == 0) p.counter[t] = 0;  // ready for the next launch (stream order)
+      }
+      const int nmax = max(ns[0], ns[kB - 1]);
+      for (int sg0 = 0; sg0 < nmax; sg0 += 4) {
+        float4 v[kB][4];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            v[b][q] = sg0 + q < ns[b] ? __ldcg(reinterpret_cast<const float4*>(src[b] + (sg0 + q) * seg_stride))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc[b].x += v[b][q].x;
+            acc[b].y += v[b][q].y;
+            acc[b].z += v[b][q].z;
+            acc[b].w += v[b][q].w;
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        if (dst[b]) *reinterpret_cast<uint2*>(dst[b]) = make_uint2(pack_bf16x2(acc[b].x, acc[b].y), pack_bf16x2(acc[b].z, acc[b].w));
       }
     }
   }
   __syncthreads();
+  if (tid == 0) STRACE(3);
   griddep_launch_dependents();
   if (warp == kSplitWarpMMA) {
     tc_fence_after();
@@ -1470,6 +1546,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   const uint32_t tcols = acc_cols <= 16 ? 32u : (acc_cols <= 32 ? 64u : (acc_cols <= 64 ? 128u : 256u));  // 2 accumulators
   const int i_beg = p.e_begin[blockIdx.x];
   const int i_end = p.e_begin[blockIdx.x + 1];
+  if (tid == 0) STRACE(8);
   const int64_t ldy_b = p.ldy * kEsz;
   const int nsl = (p.d_out + kCols - 1) / kCols;
 
@@ -1528,6 +1605,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       if (!waited) {
         griddep_wait();  // mid is produced by the shrink launch
         waited = true;
+        if (tid == 0) STRACE(12);
       }
       const uint16_t* ms = p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max;
       const int rows16 = (rows + 15) & ~15;
@@ -1537,6 +1615,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
     }
     if (!waited) griddep_wait();
     loader_drain(j, D, S, full, lane);
+    if (tid == 0) STRACE(9);
   } else if (warp == kSplitWarpMMA) {
     // ===================== MMA issuer =====================
     int j = 0;
@@ -1612,7 +1691,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       mbar_arrive(&empty[st]);
     }
   }
+  if (tid == kSplitWarpEpi * 32) STRACE(10);
   __syncthreads();
+  if (tid == 0) STRACE(11);
   griddep_launch_dependents();
   if (warp == kSplitWarpMMA) {
     tc_fence_after();
@@ -2050,6 +2131,7 @@ template __global__ void atmm_bypass_a2a_kernel<__nv_bfloat16>(const __grid_cons
                                                                const BypassParams);
 template __global__ void atmm_bypass_a2a_kernel<float>(const __grid_constant__ CUtensorMap, const BypassParams);
 template __global__ void atmm_expand_kernel<__nv_bfloat16, 2>(const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 1>(const SplitParams);
 template __global__ void atmm_expand_kernel<float, 1>(const SplitParams);
 template __global__ void atmm_merge_kernel<float>(const MergeParams);
 template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
@@ -2191,6 +2273,12 @@ cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t sme
   if (e != cudaSuccess) return e;
   cfg.blockDim = dim3(kExpandThreads, 1, 1);
   cfg.dynamicSmemBytes = smem_e;
+  if (y_dtype == 0 && p.expand_g == 1) {
+    auto k = atmm_expand_kernel<__nv_bfloat16, 1>;
+    e = prepare(k, smem_e, false);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, k, p);
+  }
   if (y_dtype == 0) {
     auto k = atmm_expand_kernel<__nv_bfloat16, 2>;
     e = prepare(k, smem_e, false);
