@@ -131,6 +131,15 @@ void atmm_registry_destroy(atmm_registry* r);
 int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const float* down,
                       const float* up, float scale);
 int atmm_registry_remove(atmm_registry* r, int32_t adapter_id);
+/* Mixture / deLoRA branch (model.hpp:252-328): a slot whose
+ * factors are the rank-concatenation of existing adapters,
+ *   down = [down_1 | down_2 | ...],  up = [s_1 sign_1 up_1 ; s_2 sign_2 up_2 ; ...],
+ * so ONE fused bypass adds sum_i sign_i s_i (x.down_i).up_i with a single
+ * rounding into Y (e.g. parts {a, merged} signs {+1, -1}: own adapter minus
+ * the cancel branch of the merged adapter).  Sum of padded ranks <= 128.
+ * Signs / scales of +-1 (and powers of two) are folded exactly. */
+int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts, const int32_t* part_ids,
+                               const float* part_signs);
 /* adapter_at (adapter.hpp:106-110): 1 if present, 0 if not. */
 int atmm_registry_contains(const atmm_registry* r, int32_t adapter_id);
 int atmm_registry_rank(const atmm_registry* r, int32_t adapter_id, int64_t* rank);
@@ -147,6 +156,12 @@ typedef struct atmm_plan atmm_plan;
  * forward_unmerged, model.hpp:226-228).  table may be NULL (heuristic). */
 int atmm_plan_create(atmm_registry* r, const int32_t* assignment, int64_t n,
                      const atmm_table* table, atmm_plan** out);
+/* plan_batch over a subset of the rows: routed entry i (adapter
+ * assignment[i]) is row rows[i] of X / Y, which have n_rows rows (rows
+ * distinct).  Used for mixture mode, where only the guest rows (those not
+ * served by the merged weights, model.hpp:273-280) take a bypass. */
+int atmm_plan_create_mapped(atmm_registry* r, const int32_t* assignment, const int32_t* rows, int64_t n,
+                            int64_t n_rows, const atmm_table* table, atmm_plan** out);
 void atmm_plan_destroy(atmm_plan* p);
 /* Routing tables actually uploaded (for bit-exact routing checks):
  * seg_adapter[S], seg_offsets[S+1], row_index[n]. */

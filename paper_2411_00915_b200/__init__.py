@@ -13,6 +13,7 @@ from .atmm import (  # noqa: F401
     CudaError,
     Error,
     IoError,
+    MixturePlan,
     ModeError,
     NoDeviceError,
     ParseError,

@@ -269,9 +269,25 @@ class AdapterRegistry:
             raise ShapeError(f"adapter factor shapes {d.shape} / {u.shape} do not match registry "
                              f"(L={self.num_layers}, d_in={self.d_in}, d_out={self.d_out})")
         _check(lib.atmm_registry_put(self._h, adapter_id, r, _p(d, f32p), _p(u, f32p), float(scale)))
+        self._drop_combined(adapter_id)
+
+    def _drop_combined(self, adapter_id: int) -> None:
+        """Combined (mixture) slots built from adapter_id are stale now."""
+        combos = self.__dict__.get("_combined", {})
+        for key in [k for k in combos if adapter_id in k]:
+            lib.atmm_registry_remove(self._h, combos.pop(key))
+
+    def put_combined(self, new_id: int, parts: Sequence[Tuple[int, float]]) -> None:
+        """A slot = rank-concatenation of existing adapters with signs folded
+        into up (include/atmm_b200.h atmm_registry_put_combined): one fused
+        bypass then adds sum_i sign_i s_i (x.down_i).up_i."""
+        ids = _i32([p[0] for p in parts])
+        signs = _f32([p[1] for p in parts])
+        _check(lib.atmm_registry_put_combined(self._h, int(new_id), ids.size, _p(ids, i32p), _p(signs, f32p)))
 
     def remove(self, adapter_id: int) -> None:
         _check(lib.atmm_registry_remove(self._h, adapter_id))
+        self._drop_combined(adapter_id)
 
     def __contains__(self, adapter_id: int) -> bool:
         return bool(lib.atmm_registry_contains(self._h, adapter_id))
@@ -300,14 +316,26 @@ def _stream_ptr(stream) -> Optional[int]:
 class BypassPlan:
     """plan_batch + launch grouping for one batch on one registry."""
 
-    def __init__(self, registry: AdapterRegistry, assignment: Sequence[int], table: Optional[TilingTable] = None):
+    def __init__(self, registry: AdapterRegistry, assignment: Sequence[int], table: Optional[TilingTable] = None,
+                 rows: Optional[Sequence[int]] = None, n_rows: Optional[int] = None):
+        """rows (optional): routed entry i is row rows[i] of X / Y, which
+        have n_rows rows (atmm_plan_create_mapped); default: entry i = row i."""
         a = _i32(assignment).reshape(-1)
         h = ctypes.c_void_p()
-        _check(lib.atmm_plan_create(registry.handle, _p(a, i32p), a.size, table.handle if table else None,
-                                    ctypes.byref(h)))
+        if rows is None:
+            _check(lib.atmm_plan_create(registry.handle, _p(a, i32p), a.size, table.handle if table else None,
+                                        ctypes.byref(h)))
+            self.n = int(a.size)
+        else:
+            rw = _i32(rows).reshape(-1)
+            if rw.size != a.size or n_rows is None:
+                raise ShapeError("rows must match the assignment length and n_rows must be given")
+            _check(lib.atmm_plan_create_mapped(registry.handle, _p(a, i32p), _p(rw, i32p), a.size, int(n_rows),
+                                               table.handle if table else None, ctypes.byref(h)))
+            self.n = int(n_rows)
         self._h = h
         self.registry = registry
-        self.n = int(a.size)
+        self.n_routed = int(a.size)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -320,9 +348,9 @@ class BypassPlan:
         return self._h
 
     def routing(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
-        seg = np.zeros(self.n, np.int32)
-        off = np.zeros(self.n + 1, np.int64)
-        rows = np.zeros(self.n, np.int64)
+        seg = np.zeros(self.n_routed, np.int32)
+        off = np.zeros(self.n_routed + 1, np.int64)
+        rows = np.zeros(self.n_routed, np.int64)
         S = ctypes.c_int64(0)
         _check(lib.atmm_plan_routing(self._h, _p(seg, i32p), _p(off, i64p), _p(rows, i64p), ctypes.byref(S)))
         return seg[: S.value].copy(), off[: S.value + 1].copy(), rows
@@ -363,6 +391,41 @@ class BypassPlan:
             raise ShapeError("host buffers must be C-contiguous")
         _check(lib.atmm_bypass_residual_host_bf16(self._h, layer, _p(x_host, u16p), _p(y_host, u16p),
                                                   float(scale), _stream_ptr(stream)))
+
+
+class MixturePlan:
+    """forward_mixture's bypass (model.hpp:252-328) for one layer as ONE fused
+    launch: rows assigned to the merged adapter ride the merged weights (no
+    bypass); every guest row a gets (x.down_a).up_a - (x.down_m).up_m through
+    a combined slot [down_a | down_m], [up_a ; -up_m] (K concatenation), so
+    the own branch and the cancel branch are summed in fp32 in TMEM and
+    rounded into Y once.  Combined slots are created once per (a, merged)
+    pair and cached on the registry (negative ids, never user-visible)."""
+
+    def __init__(self, registry: AdapterRegistry, assignment: Sequence[int], merged_id: int,
+                 table: Optional[TilingTable] = None):
+        a = _i32(assignment).reshape(-1)
+        if merged_id not in registry:
+            raise ModeError("mixture integrity: subtraction branch missing (merged adapter not in the registry)")
+        combos = registry.__dict__.setdefault("_combined", {})
+        guest = np.nonzero(a != merged_id)[0].astype(np.int32)
+        virt = np.empty(guest.size, np.int32)
+        for i, row in enumerate(guest):
+            key = (int(a[row]), int(merged_id))
+            if key not in combos:
+                if key[0] not in registry:
+                    raise UnknownAdapterError(f"unknown adapter id {key[0]}")
+                vid = -(1 << 20) - len(combos)
+                registry.put_combined(vid, [(key[0], 1.0), (key[1], -1.0)])
+                combos[key] = vid
+            virt[i] = combos[key]
+        self.n = int(a.size)
+        self.guest_rows = guest
+        self.plan = BypassPlan(registry, virt, table, rows=guest, n_rows=self.n) if guest.size else None
+
+    def apply(self, x, y, layer: int = 0, scale: float = 1.0, stream=None) -> None:
+        if self.plan is not None:
+            self.plan.apply(x, y, layer, scale, stream)
 
 
 def residual_host_bf16_pipelined(plan: "BypassPlan", xs, ys, layers, scale: float = 1.0) -> None:

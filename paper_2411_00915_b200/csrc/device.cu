@@ -39,6 +39,8 @@ cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const Merge
                              size_t smem, cudaStream_t stream);
 cudaError_t launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t rows, int64_t cols,
                                int64_t lds, int64_t ldd, cudaStream_t stream);
+cudaError_t launch_scale_bf16_2d(uint16_t* base, int64_t rows, int64_t cols, int64_t ld, float f,
+                                 cudaStream_t stream);
 
 namespace {
 
@@ -474,7 +476,8 @@ struct SplitBufs {
 struct atmm_plan {
   atmm_registry* reg = nullptr;
   uint64_t generation = 0;
-  int64_t n = 0;
+  int64_t n = 0;         // rows of X / Y
+  int64_t n_assign = 0;  // routed rows (== n unless the plan maps rows)
   BatchPlan bp;
   std::vector<LaunchGroup> groups;
   // groups[merged_first ..] all take the split path for bf16 Y: one launch
@@ -576,11 +579,13 @@ namespace atmm {
 // table for every segment.
 static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* assignment,
                                              int64_t n, const TilingTable* table,
-                                             const LaunchCfg* forced) {
+                                             const LaunchCfg* forced, const int32_t* row_map = nullptr,
+                                             int64_t n_rows = -1) {
   auto plan = std::make_unique<atmm_plan>();
   plan->reg = reg;
   plan->generation = reg->generation;
-  plan->n = n;
+  plan->n = row_map ? n_rows : n;
+  plan->n_assign = n;
   plan->bp = plan_batch(assignment, n);
   if (n > std::numeric_limits<int32_t>::max()) fail(ATMM_ERR_SHAPE, "batch too large");
   struct Pending {
@@ -658,6 +663,17 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     if (!plan->merged.split.ok) plan->merged_first = -1;
   }
   std::vector<int32_t> rows32(plan->bp.row_index.begin(), plan->bp.row_index.end());
+  if (row_map) {
+    // routed entry i lives in X / Y row row_map[i] (mixture guest rows)
+    std::vector<char> seen(static_cast<size_t>(n_rows), 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (row_map[i] < 0 || row_map[i] >= n_rows || seen[static_cast<size_t>(row_map[i])]) {
+        fail(ATMM_ERR_SHAPE, "row map entries must be distinct rows in [0, n_rows)");
+      }
+      seen[static_cast<size_t>(row_map[i])] = 1;
+    }
+    for (auto& v : rows32) v = row_map[v];
+  }
   DeviceGuard dg(reg->device);
   if (plan->merged_first >= 0) {
     // Persistent split kernels: balanced work ranges over the SMs.
@@ -1015,6 +1031,75 @@ int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const 
   });
 }
 
+int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts, const int32_t* part_ids,
+                               const float* part_signs) {
+  return guarded([&] {
+    if (!r || !part_ids || !part_signs || n_parts < 1) fail(ATMM_ERR_CONFIG, "null registry or empty part list");
+    std::vector<Slot> parts;
+    int64_t r_c = 0;
+    for (int64_t i = 0; i < n_parts; ++i) {
+      parts.push_back(r->at(part_ids[i]));
+      r_c += parts.back().r_pad;
+    }
+    if (r_c > kMaxRank) fail(ATMM_ERR_CONFIG, "combined rank " + std::to_string(r_c) + " exceeds 128");
+    DeviceGuard g(r->device);
+    Slot s;
+    s.id = new_id;
+    s.rank = r_c;
+    s.r_pad = r_c;
+    s.scale = 1.0f;
+    s.live = true;
+    const size_t dn = static_cast<size_t>(r->d_in_pad * r_c), un = static_cast<size_t>(r->d_out_pad * r_c);
+    CUDA_CHECK(cudaMalloc(&s.down_t, dn * static_cast<size_t>(r->L) * 2));
+    CUDA_CHECK(cudaMalloc(&s.up_t, un * static_cast<size_t>(r->L) * 2));
+    int64_t off = 0;
+    for (size_t i = 0; i < parts.size(); ++i) {
+      const Slot& ps = parts[i];
+      const float f = part_signs[i] * ps.scale;
+      for (int64_t l = 0; l < r->L; ++l) {
+        // down^T: per 64-wide K block r_pad x 64 contiguous -> rank rows off ..
+        CUDA_CHECK(cudaMemcpy2D(s.down_t + l * dn + off * kBK, static_cast<size_t>(r_c * kBK * 2),
+                                ps.down_t + l * r->d_in_pad * ps.r_pad, static_cast<size_t>(ps.r_pad * kBK * 2),
+                                static_cast<size_t>(ps.r_pad * kBK * 2), static_cast<size_t>(r->d_in_pad / kBK),
+                                cudaMemcpyDeviceToDevice));
+        // up^T: per 8 output columns r_pad x 8 contiguous -> rank columns off ..
+        uint16_t* ud = s.up_t + l * un + off * 8;
+        CUDA_CHECK(cudaMemcpy2D(ud, static_cast<size_t>(r_c * 16), ps.up_t + l * r->d_out_pad * ps.r_pad,
+                                static_cast<size_t>(ps.r_pad * 16), static_cast<size_t>(ps.r_pad * 16),
+                                static_cast<size_t>(r->d_out_pad / 8), cudaMemcpyDeviceToDevice));
+        if (f != 1.0f) {
+          CUDA_CHECK(launch_scale_bf16_2d(ud, r->d_out_pad / 8, ps.r_pad * 8, r_c * 8, f, nullptr));
+        }
+      }
+      off += ps.r_pad;
+    }
+    CUDA_CHECK(cudaDeviceSynchronize());
+    auto it = r->slot_of.find(new_id);
+    if (it != r->slot_of.end()) {
+      Slot& old = r->slots[static_cast<size_t>(it->second)];
+      cudaFree(old.down_t);
+      cudaFree(old.up_t);
+      old = s;
+    } else {
+      int idx = -1;
+      for (size_t i = 0; i < r->slots.size(); ++i) {
+        if (!r->slots[i].live) {
+          idx = static_cast<int>(i);
+          break;
+        }
+      }
+      if (idx < 0) {
+        idx = static_cast<int>(r->slots.size());
+        r->slots.push_back(s);
+      } else {
+        r->slots[static_cast<size_t>(idx)] = s;
+      }
+      r->slot_of[new_id] = idx;
+    }
+    r->sync_slots();
+  });
+}
+
 int atmm_registry_remove(atmm_registry* r, int32_t adapter_id) {
   return guarded([&] {
     if (!r) fail(ATMM_ERR_CONFIG, "null registry");
@@ -1061,6 +1146,17 @@ int atmm_plan_create(atmm_registry* r, const int32_t* assignment, int64_t n, con
   });
 }
 
+int atmm_plan_create_mapped(atmm_registry* r, const int32_t* assignment, const int32_t* rows, int64_t n,
+                            int64_t n_rows, const atmm_table* table, atmm_plan** out) {
+  return guarded([&] {
+    if (!r || !out) fail(ATMM_ERR_CONFIG, "null registry or output");
+    if (!rows) fail(ATMM_ERR_SHAPE, "null row map");
+    if (n_rows < n) fail(ATMM_ERR_SHAPE, "n_rows must be >= the number of routed rows");
+    const TilingTable* t = table ? &table->t : nullptr;
+    *out = build_plan(r, assignment, n, t, nullptr, rows, n_rows).release();
+  });
+}
+
 void atmm_plan_destroy(atmm_plan* p) {
   if (!p) return;
   DeviceGuard g(p->reg->device);
@@ -1073,7 +1169,7 @@ int atmm_plan_routing(const atmm_plan* p, int32_t* seg_adapter, int64_t* seg_off
     if (!p) fail(ATMM_ERR_CONFIG, "null plan");
     // Read back what the kernels index with (row_index from HBM).
     DeviceGuard g(p->reg->device);
-    std::vector<int32_t> rows(static_cast<size_t>(p->n));
+    std::vector<int32_t> rows(static_cast<size_t>(p->n_assign));
     CUDA_CHECK(cudaMemcpy(rows.data(), p->d_rows.p, rows.size() * 4, cudaMemcpyDeviceToHost));
     if (seg_adapter) std::copy(p->bp.seg_adapter.begin(), p->bp.seg_adapter.end(), seg_adapter);
     if (seg_offsets) std::copy(p->bp.seg_offsets.begin(), p->bp.seg_offsets.end(), seg_offsets);

@@ -2120,6 +2120,17 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ src, uint16_t* __re
   }
 }
 
+// base[r * ld + c] *= f (bf16, round to nearest even), r < rows, c < cols.
+__global__ void scale_bf16_2d_kernel(uint16_t* __restrict__ base, int64_t rows, int64_t cols, int64_t ld, float f) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols;
+    uint16_t* p = base + r * ld + (i - r * cols);
+    *p = __bfloat16_as_ushort(__float2bfloat16_rn(__bfloat162float(__ushort_as_bfloat16(*p)) * f));
+  }
+}
+
 // Explicit instantiations reachable from the host launcher.
 template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant__ CUtensorMap,
                                                            const __grid_constant__ CUtensorMap,
@@ -2339,6 +2350,14 @@ cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const Merge
   cudaError_t e = prepare(k, smem, false);
   if (e != cudaSuccess) return e;
   k<<<grid, kMergeThreads, smem, stream>>>(tmap_w, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_bf16_2d(uint16_t* base, int64_t rows, int64_t cols, int64_t ld, float f,
+                                 cudaStream_t stream) {
+  const int64_t total = rows * cols;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  scale_bf16_2d_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(base, rows, cols, ld, f);
   return cudaGetLastError();
 }
 

@@ -27,20 +27,31 @@ METRICS = {
 
 
 def raw(rep):
+    """Metrics of the captured launches; a split-path step (shrink + expand)
+    is captured as two kernels whose durations and DRAM bytes are summed."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return {}
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
     d = {}
-    for h, u, v in zip(hdr, units, vals):
-        if h in METRICS:
-            try:
-                d[METRICS.get(h, h)] = (float(v.replace(",", "")), u)
-            except ValueError:
-                d[METRICS.get(h, h)] = (v, u)
-        if h == "Kernel Name":
-            d["kernel"] = (v, "")
+    names = []
+    for vals in rows[2:]:
+        for h, u, v in zip(hdr, units, vals):
+            if h in METRICS:
+                key = METRICS[h]
+                try:
+                    fv = float(v.replace(",", ""))
+                except ValueError:
+                    d.setdefault(key, (v, u))
+                    continue
+                if key in ("duration", "dram_read", "dram_write", "l2_bytes") and key in d:
+                    d[key] = (d[key][0] + fv, u)
+                else:
+                    d.setdefault(key, (fv, u))
+            if h == "Kernel Name":
+                names.append(v.split("(")[0].replace("void ", "")[:40])
+    d["kernel"] = (" + ".join(names), "")
     return d
 
 
