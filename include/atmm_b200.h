@@ -213,6 +213,12 @@ int atmm_bypass_residual_host_bf16_pipelined(const atmm_plan* p, const int64_t* 
 int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* w,
                      int64_t ldw, int w_dtype, float sign, void* stream);
 /* delta_w (model.hpp:130-140) with a host output: out = s_a * down . up. */
+/* merge / unmerge of ALL layers [layer0, layer0 + num_layers) in ONE launch
+ * (model.hpp:144-188, the mode switch's one-shot merge): layer l's W is at
+ * w + (l - layer0) * w_layer_stride elements.  One persistent grid streams
+ * every layer's W through shared memory (TMA, 3-D tensor map). */
+int atmm_merge_apply_layers(atmm_registry* r, int32_t adapter_id, int64_t layer0, int64_t num_layers, void* w,
+                            int64_t ldw, int64_t w_layer_stride, int w_dtype, float sign, void* stream);
 int atmm_delta_w_host(atmm_registry* r, int32_t adapter_id, int64_t layer, float* out);
 
 /* ===================================================================== */

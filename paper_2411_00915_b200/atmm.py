@@ -477,6 +477,22 @@ def merge_into(registry: AdapterRegistry, adapter_id: int, layer: int, w, sign: 
                                 F32 if w.dtype == torch.float32 else BF16, float(sign), _stream_ptr(stream)))
 
 
+def merge_layers_into(registry: AdapterRegistry, adapter_id: int, w, sign: float = 1.0, layer0: int = 0,
+                      stream=None) -> None:
+    """W[l] (+/-)= s * down[layer0 + l] @ up[layer0 + l] for every layer of a
+    [L, d_in, d_out] CUDA tensor in ONE launch (the mode switch's merge of
+    all layers, model.hpp:144-188)."""
+    import torch
+
+    if w.dim() != 3 or w.stride(2) != 1 or not w.is_cuda or w.dtype not in (torch.float32, torch.bfloat16):
+        raise ShapeError("w must be a [L, d_in, d_out] CUDA float32/bfloat16 tensor with contiguous rows")
+    if tuple(w.shape[1:]) != (registry.d_in, registry.d_out):
+        raise ShapeError(f"w shape {tuple(w.shape)} != (L, {registry.d_in}, {registry.d_out})")
+    _check(lib.atmm_merge_apply_layers(registry.handle, adapter_id, layer0, w.shape[0], w.data_ptr(), w.stride(1),
+                                       w.stride(0), F32 if w.dtype == torch.float32 else BF16, float(sign),
+                                       _stream_ptr(stream)))
+
+
 def atmm_multiply(a, b, config: Sequence[int]) -> np.ndarray:
     """atmm.hpp:144-154 (host fp32 in/out, bf16 tcgen05 compute)."""
     aa, bb = _f32(a), _f32(b)

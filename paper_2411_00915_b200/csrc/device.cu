@@ -143,15 +143,17 @@ CUtensorMap make_y_map(const void* y, int64_t n, int64_t d_out, int64_t ldy, int
 
 // W (m x n, bf16 or fp32, row stride ldw) for the TMA-staged merge: box =
 // 128 rows x one 128-byte column slab, 128-byte swizzle (loads and stores).
-CUtensorMap make_w_map(void* w, int64_t m, int64_t n, int64_t ldw, int w_dtype) {
+// 3-D over layers: (n, m, L) with layer stride w_ls elements (L = 1: one matrix).
+CUtensorMap make_w_map(void* w, int64_t m, int64_t n, int64_t ldw, int w_dtype, int64_t L = 1, int64_t w_ls = 0) {
   CUtensorMap map;
   const int64_t esz = w_dtype == ATMM_BF16 ? 2 : 4;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldw * esz)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(kTileM)};
-  const cuuint32_t estr[2] = {1, 1};
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(L)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldw * esz),
+                                 static_cast<cuuint64_t>((L > 1 ? w_ls : ldw * m) * esz)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(kTileM), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&map, w_dtype == ATMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                 2, w, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 3, w, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(W) failed: " + std::to_string(r));
@@ -870,8 +872,9 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
 // W = beta*W + alpha * A . B on the merge kernel; A/B in registry layouts.
 static void run_merge(const uint16_t* a_t, const uint16_t* b_t, int64_t m, int64_t n,
                       int64_t k_pad, void* w, int64_t ldw, int w_dtype, float alpha, float beta,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, int64_t L = 1, int64_t a_ls = 0, int64_t b_ls = 0, int64_t w_ls = 0) {
   MergeParams mp{};
+  mp.num_layers = 1;
   mp.a_t = a_t;
   mp.b_t = b_t;
   mp.w = w;
@@ -885,7 +888,14 @@ static void run_merge(const uint16_t* a_t, const uint16_t* b_t, int64_t m, int64
   mp.alpha = alpha;
   mp.beta = beta;
   const int64_t wsz = w_dtype == ATMM_BF16 ? 2 : 4;
-  mp.w_vec = ((ldw * wsz) % 16 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0) ? 1 : 0;
+  mp.w_vec = ((ldw * wsz) % 16 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0 && (w_ls * wsz) % 16 == 0) ? 1 : 0;
+  if (L > 1 && !mp.w_vec) {  // one launch per layer on the direct-epilogue kernel
+    for (int64_t l = 0; l < L; ++l) {
+      run_merge(a_t + l * a_ls, b_t + l * b_ls, m, n, k_pad, static_cast<uint8_t*>(w) + l * w_ls * wsz, ldw, w_dtype,
+                alpha, beta, stream);
+    }
+    return;
+  }
   const int64_t a_bytes = int64_t(kTileM) * k_pad * 2;
   int sms = 148;
   int dev = 0;
@@ -910,9 +920,12 @@ static void run_merge(const uint16_t* a_t, const uint16_t* b_t, int64_t m, int64
     mp.w_stages = sw;
     mp.off_bar = static_cast<uint32_t>(mp.off_w + int64_t(sw) * slab);
     mp.tmem_cols = 256;
-    const int64_t tiles = int64_t(mp.num_mtiles) * mp.num_nchunks;
+    mp.num_layers = static_cast<int32_t>(L);
+    mp.a_layer_stride = a_ls;
+    mp.b_layer_stride = b_ls;
+    const int64_t tiles = L * int64_t(mp.num_mtiles) * mp.num_nchunks;
     const int grid = static_cast<int>(std::min<int64_t>(tiles, sms));
-    const CUtensorMap tmap_w = make_w_map(w, m, n, ldw, w_dtype);
+    const CUtensorMap tmap_w = make_w_map(w, m, n, ldw, w_dtype, L, w_ls);
     const cudaError_t e = launch_merge_tma(w_dtype, tmap_w, mp, grid, total_w(sw), stream);
     if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("merge launch failed: ") + cudaGetErrorString(e));
     return;
@@ -1326,6 +1339,27 @@ int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* 
     DeviceGuard g(r->device);
     run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
               r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atmm_merge_apply_layers(atmm_registry* r, int32_t adapter_id, int64_t layer0, int64_t num_layers, void* w,
+                            int64_t ldw, int64_t w_layer_stride, int w_dtype, float sign, void* stream) {
+  return guarded([&] {
+    if (!r || !w) fail(ATMM_ERR_CONFIG, "null registry or W");
+    if (num_layers < 1 || layer0 < 0 || layer0 + num_layers > r->L) {
+      fail(ATMM_ERR_CONFIG, "layer range [" + std::to_string(layer0) + ", " + std::to_string(layer0 + num_layers) +
+                                ") out of range (L=" + std::to_string(r->L) + ")");
+    }
+    if (w_dtype != ATMM_BF16 && w_dtype != ATMM_F32) fail(ATMM_ERR_CONFIG, "w_dtype must be ATMM_BF16 or ATMM_F32");
+    const int64_t wsz = w_dtype == ATMM_BF16 ? 2 : 4;
+    if (ldw < r->d_out) fail(ATMM_ERR_SHAPE, "W row stride ldw must be >= d_out");
+    if (num_layers > 1 && w_layer_stride < ldw * r->d_in) fail(ATMM_ERR_SHAPE, "W layer stride must be >= ldw * d_in");
+    if (reinterpret_cast<uintptr_t>(w) % wsz != 0) fail(ATMM_ERR_SHAPE, "W is not element aligned");
+    const Slot& s = r->at(adapter_id);
+    DeviceGuard g(r->device);
+    run_merge(s.down_t + layer0 * r->d_in_pad * s.r_pad, s.up_t + layer0 * r->d_out_pad * s.r_pad, r->d_in,
+              r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream), num_layers,
+              r->d_in_pad * s.r_pad, r->d_out_pad * s.r_pad, w_layer_stride);
   });
 }
 

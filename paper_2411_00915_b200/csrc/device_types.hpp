@@ -155,7 +155,9 @@ struct MergeParams {
   int32_t w_stages;
   uint32_t off_w;
   int32_t slab_cols;    // W columns per slab (64 bf16 / 32 fp32)
-  int32_t pad0;
+  int32_t num_layers;   // TMA-staged path: layers merged by one launch (W is a 3-D tensor map)
+  int64_t a_layer_stride;  // elements between consecutive layers' down^T / up^T
+  int64_t b_layer_stride;
 };
 
 }  // namespace atmm

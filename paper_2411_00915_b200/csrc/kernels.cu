@@ -1963,7 +1963,8 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int num_tiles = p.num_mtiles * p.num_nchunks;
+  // tiles: (layer, m-tile, n-chunk), layer-major; gm = layer * num_mtiles + mt
+  const int num_tiles = p.num_layers * p.num_mtiles * p.num_nchunks;
   const int n32 = ((p.n + 31) / 32) * 32;
 
   if (warp == 0) {
@@ -1975,25 +1976,29 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
       uint32_t a_phase = 0;
       int j = 0;  // W slab sequence number
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int mt = t / p.num_nchunks;
-        const int nc = t - mt * p.num_nchunks;
+        const int gm = t / p.num_nchunks;
+        const int nc = t - gm * p.num_nchunks;
+        const int layer = gm / p.num_mtiles;
+        const int mt = gm - layer * p.num_mtiles;
         const int n0 = nc * p.bn;
         const int bn_c = min(p.bn, n32 - n0);
-        if (mt != cur_mt) {
+        if (gm != cur_mt) {
           mbar_wait(a_empty, a_phase ^ 1u);
           mbar_arrive_expect_tx(a_full, static_cast<uint32_t>(128 * kp * 2));
+          const uint16_t* a_l = p.a_t + static_cast<int64_t>(layer) * p.a_layer_stride;
           for (int h = 0; h < 2; ++h) {
             const int64_t kb = static_cast<int64_t>(mt) * 2 + h;
             for (int g = 0; g < kg; ++g) {
-              bulk_g2s(a_buf + g * 2048 + h * 1024, p.a_t + (kb * kg + g) * 512, 1024u, a_full);
+              bulk_g2s(a_buf + g * 2048 + h * 1024, a_l + (kb * kg + g) * 512, 1024u, a_full);
             }
           }
           a_phase ^= 1u;
-          cur_mt = mt;
+          cur_mt = gm;
         }
         mbar_wait(&empty[stage], phase ^ 1u);
         mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(bn_c * kp * 2));
-        bulk_g2s(b_ring + static_cast<size_t>(stage) * p.b_stage_bytes, p.b_t + static_cast<int64_t>(n0) * kp,
+        bulk_g2s(b_ring + static_cast<size_t>(stage) * p.b_stage_bytes,
+                 p.b_t + static_cast<int64_t>(layer) * p.b_layer_stride + static_cast<int64_t>(n0) * kp,
                  static_cast<uint32_t>(bn_c * kp * 2), &full[stage]);
         if (++stage == S) {
           stage = 0;
@@ -2005,8 +2010,8 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
           mbar_wait(&w_empty[b], static_cast<uint32_t>((j / SW) & 1) ^ 1u);
           if (load_w) {
             mbar_arrive_expect_tx(&w_full[b], kSlabBytes);
-            tma_load_2d(w_ring + static_cast<size_t>(b) * kSlabBytes, &tmap_w, &w_full[b], n0 + sl * sc,
-                        mt * kTileM);
+            tma_load_3d(w_ring + static_cast<size_t>(b) * kSlabBytes, &tmap_w, &w_full[b], n0 + sl * sc,
+                        mt * kTileM, layer);
           } else {
             mbar_arrive(&w_full[b]);  // overwrite mode: the slab buffer is merely free
           }
@@ -2023,16 +2028,16 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
       int local = 0;
       const uint32_t a0 = smem_u32(a_buf);
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-        const int mt = t / p.num_nchunks;
-        const int nc = t - mt * p.num_nchunks;
+        const int gm = t / p.num_nchunks;
+        const int nc = t - gm * p.num_nchunks;
         const int n0 = nc * p.bn;
         const int bn_c = min(p.bn, n32 - n0);
         const int next_t = t + static_cast<int>(gridDim.x);
-        const bool last_of_a = next_t >= num_tiles || (next_t / p.num_nchunks) != mt;
-        if (mt != cur_mt) {
+        const bool last_of_a = next_t >= num_tiles || (next_t / p.num_nchunks) != gm;
+        if (gm != cur_mt) {
           mbar_wait(a_full, a_phase);
           a_phase ^= 1u;
-          cur_mt = mt;
+          cur_mt = gm;
         }
         const int buf = local & 1;
         mbar_wait(&acc_empty[buf], ((local >> 1) & 1) ^ 1u);
@@ -2064,8 +2069,10 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
     int local = 0;
     int j = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
-      const int mt = t / p.num_nchunks;
-      const int nc = t - mt * p.num_nchunks;
+      const int gm = t / p.num_nchunks;
+      const int nc = t - gm * p.num_nchunks;
+      const int layer = gm / p.num_mtiles;
+      const int mt = gm - layer * p.num_mtiles;
       const int n0 = nc * p.bn;
       const int bn_c = min(p.bn, n32 - n0);
       const int nslab = (min(bn_c, p.n - n0) + sc - 1) / sc;
@@ -2085,7 +2092,7 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
         fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA store
         named_bar_sync(1, 128);
         if (leader) {
-          tma_store_2d(&tmap_w, w_ring + static_cast<size_t>(b) * kSlabBytes, n0 + sl * sc, mt * kTileM);
+          tma_store_3d(&tmap_w, w_ring + static_cast<size_t>(b) * kSlabBytes, n0 + sl * sc, mt * kTileM, layer);
           bulk_commit();
           // The previous slab's store has finished reading smem: release it.
           bulk_wait_read<1>();

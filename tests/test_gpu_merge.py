@@ -176,3 +176,43 @@ def test_merge_tma_staged_strided(gpu, atmm, oracle, w_dtype, d_in, d_out, pad):
     tol = 1e-4 * max(1.0, np.max(np.abs(want))) if w_dtype == "f32" else tol_for(want)
     assert np.max(np.abs(got[:, :d_out] - want)) <= tol
     assert np.array_equal(got[:, d_out:], base[:, d_out:].astype(np.float32))
+
+
+@pytest.mark.parametrize("w_dtype", ["f32", "bf16"])
+def test_merge_all_layers_one_launch(gpu, atmm, oracle, w_dtype):
+    """The mode switch's one-shot merge of every layer (model.hpp:144-188) in
+    one launch equals the per-layer merges; unmerge restores W (fp32)."""
+    import torch
+
+    L, d_in, d_out, r = 5, 384, 520, 48
+    rng = oracle.rng(77)
+    s = 1.0 / np.sqrt(np.float32(r))
+    down = oracle.round_bf16(oracle.random_matrix(rng, L * d_in, r, -s, s).reshape(L, d_in, r))
+    up = oracle.round_bf16(oracle.random_matrix(rng, L * r, d_out, -s, s).reshape(L, r, d_out))
+    w0 = oracle.random_matrix(rng, L * d_in, d_out, -0.05, 0.05).reshape(L, d_in, d_out)
+    if w_dtype == "bf16":
+        w0 = oracle.round_bf16(w0)
+    reg = atmm.AdapterRegistry(L, d_in, d_out)
+    reg.put(1, down, up)
+    dt = torch.float32 if w_dtype == "f32" else torch.bfloat16
+    wa = torch.from_numpy(w0).to("cuda", dt)
+    wb = wa.clone()
+    atmm.merge_layers_into(reg, 1, wa, sign=+1.0)
+    for l in range(L):
+        atmm.merge_into(reg, 1, l, wb[l], sign=+1.0)
+    torch.cuda.synchronize()
+    assert torch.equal(wa, wb)
+    got = wa.float().cpu().numpy()
+    for l in range(L):
+        want = w0[l].astype(np.float64) + oracle.gemm_reference_f64(down[l], up[l])
+        tol = 1e-4 * max(1.0, np.max(np.abs(want))) if w_dtype == "f32" else tol_for(want)
+        assert np.max(np.abs(got[l] - want)) <= tol
+    # a sub-range of layers on a strided view, then unmerge everything
+    if w_dtype == "f32":
+        atmm.merge_layers_into(reg, 1, wa[1:4], sign=-1.0, layer0=1)
+        atmm.merge_layers_into(reg, 1, wa[0:1], sign=-1.0, layer0=0)
+        atmm.merge_layers_into(reg, 1, wa[4:5], sign=-1.0, layer0=4)
+        torch.cuda.synchronize()
+        assert np.max(np.abs(wa.cpu().numpy() - w0)) <= 1e-5
+    with pytest.raises(atmm.ConfigError):
+        atmm.merge_layers_into(reg, 1, wa[0:2], layer0=4)
