@@ -182,6 +182,15 @@ int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64
 int atmm_bypass_apply(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
                       int64_t ldy, int y_dtype, float scale, void* stream);
 
+/* `count` (1..8) independent applications of one plan -- call c computes
+ * ys[c][row] += scale * s_a * (xs[c][row] . down_a[layers[c]]) . up_a[layers[c]]
+ * -- as ONE launch when every launch group runs the all-to-all kernel (e.g.
+ * the q / k / v projections of a decoder layer: same tokens and adapters,
+ * per-projection factors stored as separate layers of the registry), else one
+ * launch per call.  The calls must not write each other's inputs. */
+int atmm_bypass_apply_group(const atmm_plan* p, int64_t count, const int64_t* layers, const void* const* xs,
+                            int64_t ldx, void* const* ys, int64_t ldy, int y_dtype, float scale, void* stream);
+
 /* run_bypass (batch.hpp:48) with host buffers: out = bypass(x), fp32 in and
  * out (x rounded to bf16 on the device).  Synchronous. */
 int atmm_run_bypass_host(atmm_registry* r, const float* x, int64_t n,

@@ -58,6 +58,8 @@ _SIGS = {
     "atmm_plan_create": (c_int, [c_void_p, i32p, c_int64, c_void_p, POINTER(c_void_p)]),
     "atmm_plan_create_mapped": (c_int, [c_void_p, i32p, i32p, c_int64, c_int64, c_void_p, POINTER(c_void_p)]),
     "atmm_registry_put_combined": (c_int, [c_void_p, c_int32, c_int64, i32p, f32p]),
+    "atmm_bypass_apply_group": (c_int, [c_void_p, c_int64, i64p, POINTER(c_void_p), c_int64, POINTER(c_void_p),
+                                        c_int64, c_int, c_float, c_void_p]),
     "atmm_merge_apply_layers": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int,
                                         c_float, c_void_p]),
     "atmm_plan_destroy": (None, [c_void_p]),

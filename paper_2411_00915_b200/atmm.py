@@ -382,6 +382,27 @@ class BypassPlan:
         _check(lib.atmm_bypass_apply(self._h, layer, x.data_ptr(), x.stride(0), y.data_ptr(), y.stride(0),
                                      BF16 if y.dtype == torch.bfloat16 else F32, float(scale), _stream_ptr(stream)))
 
+    def apply_group(self, xs, ys, layers, scale: float = 1.0, stream=None) -> None:
+        """Independent applications (xs[c], ys[c], layers[c]) in one launch
+        where the kernels allow it (include/atmm_b200.h atmm_bypass_apply_group)."""
+        import torch
+
+        if not (1 <= len(xs) == len(ys) == len(layers) <= 8):
+            raise ConfigError("apply_group takes 1..8 (x, y, layer) calls")
+        for x, y in zip(xs, ys):
+            if x.dtype != torch.bfloat16 or not x.is_cuda or x.shape != xs[0].shape or x.stride() != xs[0].stride():
+                raise ShapeError("every x must be a CUDA bfloat16 tensor of the same shape and strides")
+            if y.dtype != ys[0].dtype or not y.is_cuda or y.shape != ys[0].shape or y.stride() != ys[0].stride():
+                raise ShapeError("every y must be a CUDA tensor of the same dtype, shape and strides")
+        if xs[0].shape[0] != self.n or ys[0].shape[0] != self.n:
+            raise ShapeError(f"x/y must be 2-D with {self.n} rows")
+        lay = np.asarray(layers, np.int64)
+        xp = (ctypes.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+        yp = (ctypes.c_void_p * len(ys))(*[y.data_ptr() for y in ys])
+        _check(lib.atmm_bypass_apply_group(self._h, len(xs), _p(lay, i64p), xp, xs[0].stride(0), yp, ys[0].stride(0),
+                                           BF16 if ys[0].dtype == torch.bfloat16 else F32, float(scale),
+                                           _stream_ptr(stream)))
+
     def residual_host_bf16(self, x_host: np.ndarray, y_host: np.ndarray, layer: int = 0, scale: float = 1.0,
                            stream=None) -> None:
         """End-to-end: host bf16 (uint16) buffers in, y_host updated in place."""

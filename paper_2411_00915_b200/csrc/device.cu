@@ -31,7 +31,7 @@ cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensor
 int bypass_max_active_clusters(int C, size_t smem);
 cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t smem,
                          cudaStream_t stream);
-cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const BypassParams& p, int C, int num_tiles,
+cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassParams& p, int C, int num_tiles,
                               size_t smem, cudaStream_t stream);
 cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,
                          cudaStream_t stream);
@@ -747,8 +747,11 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
 // >= ctas * kTraceEvents uint64 filled by the next bypass launches.
 static uint64_t* g_trace = nullptr;
 
+// count > 1: independent calls (xs[c], ys[c], layers[c]) of one plan; the
+// all-to-all kernel runs them as ONE launch, other paths launch per call.
 static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
-                       int64_t ldy, int y_dtype, float scale, cudaStream_t stream) {
+                       int64_t ldy, int y_dtype, float scale, cudaStream_t stream, int count = 1,
+                       const int64_t* layers = nullptr, const void* const* xs = nullptr, void* const* ys = nullptr) {
   const atmm_registry* reg = p->reg;
   if (p->generation != reg->generation) fail(ATMM_ERR_CONFIG, "plan is stale: the registry changed after the plan was built");
   if (layer < 0 || layer >= reg->L) {
@@ -762,7 +765,22 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
   const int64_t ysz = y_dtype == ATMM_BF16 ? 2 : 4;
   if (ldy < reg->d_out) fail(ATMM_ERR_SHAPE, "Y row stride ldy must be >= d_out");
   if (reinterpret_cast<uintptr_t>(y) % ysz != 0) fail(ATMM_ERR_SHAPE, "Y is not element aligned");
-  const int32_t y_vec = ((ldy * ysz) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0) ? 1 : 0;
+  int32_t y_vec = ((ldy * ysz) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0) ? 1 : 0;
+  if (count > 1) {
+    if (count > kMaxGroup || !layers || !xs || !ys) fail(ATMM_ERR_CONFIG, "grouped apply: 1..8 calls with layers, xs, ys");
+    bool all_a2a = y_vec != 0;
+    for (int c = 0; c < count; ++c) {
+      if (layers[c] < 0 || layers[c] >= reg->L) fail(ATMM_ERR_CONFIG, "layer index out of range in grouped apply");
+      if (!xs[c] || !ys[c] || reinterpret_cast<uintptr_t>(xs[c]) % 16 != 0 || reinterpret_cast<uintptr_t>(ys[c]) % 16 != 0) {
+        all_a2a = false;
+      }
+    }
+    for (const LaunchGroup& g : p->groups) all_a2a = all_a2a && choose_path(g, y_dtype, true) == BypassPath::kA2a;
+    if (!all_a2a) {
+      for (int c = 0; c < count; ++c) apply_plan(p, layers[c], xs[c], ldx, ys[c], ldy, y_dtype, scale, stream);
+      return;
+    }
+  }
   const CUtensorMap tmap_x = make_x_map(x, p->n, reg->d_in, ldx);
   const CUtensorMap tmap_y = y_vec ? make_y_map(y, p->n, reg->d_out, ldy, y_dtype) : tmap_x;
 
@@ -860,7 +878,17 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       bp.off_mid = al.off_mid;
       bp.off_bar = al.off_bar;
       bp.tmem_cols = al.tmem_cols;
-      const cudaError_t e = launch_bypass_a2a(y_dtype, tmap_x, bp, g.cluster, static_cast<int>(g.num_tiles), al.smem, stream);
+      GroupArgs ga{};
+      ga.num_tiles = static_cast<int32_t>(g.num_tiles);
+      ga.count = count > 1 ? count : 1;
+      for (int c = 0; c < ga.count; ++c) {
+        const void* xc = count > 1 ? xs[c] : x;
+        ga.x_map[c] = count > 1 ? make_x_map(xc, p->n, reg->d_in, ldx) : tmap_x;
+        ga.x[c] = xc;
+        ga.y[c] = count > 1 ? ys[c] : y;
+        ga.layer[c] = static_cast<int32_t>(count > 1 ? layers[c] : layer);
+      }
+      const cudaError_t e = launch_bypass_a2a(y_dtype, ga, bp, g.cluster, static_cast<int>(g.num_tiles), al.smem, stream);
       if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
       continue;
     }
@@ -1241,6 +1269,17 @@ int atmm_bypass_apply(const atmm_plan* p, int64_t layer, const void* x, int64_t 
     if (!p) fail(ATMM_ERR_CONFIG, "null plan");
     DeviceGuard g(p->reg->device);
     apply_plan(p, layer, x, ldx, y, ldy, y_dtype, scale, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atmm_bypass_apply_group(const atmm_plan* p, int64_t count, const int64_t* layers, const void* const* xs,
+                            int64_t ldx, void* const* ys, int64_t ldy, int y_dtype, float scale, void* stream) {
+  return guarded([&] {
+    if (!p) fail(ATMM_ERR_CONFIG, "null plan");
+    if (count < 1 || count > kMaxGroup || !layers || !xs || !ys) fail(ATMM_ERR_CONFIG, "grouped apply: 1..8 calls");
+    DeviceGuard g(p->reg->device);
+    apply_plan(p, layers[0], xs[0], ldx, ys[0], ldy, y_dtype, scale, static_cast<cudaStream_t>(stream),
+               static_cast<int>(count), layers, xs, ys);
   });
 }
 

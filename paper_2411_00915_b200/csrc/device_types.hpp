@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include <cuda.h>
+
 namespace atmm {
 
 constexpr int kTileM = 128;   // tcgen05 M (TMEM lanes); a tile carries <= 128 valid rows
@@ -86,6 +88,20 @@ struct BypassParams {
 };
 
 constexpr int kTraceEvents = 32;
+
+// Independent calls (X_c, Y_c, layer_c) of one plan fused into ONE launch of
+// the all-to-all kernel (e.g. the q / k / v projections of a decoder layer):
+// cluster id = call * num_tiles + tile.  Passed as a __grid_constant__
+// parameter so the per-call X tensor maps live in parameter space.
+constexpr int kMaxGroup = 8;
+struct GroupArgs {
+  CUtensorMap x_map[kMaxGroup];
+  const void* x[kMaxGroup];
+  void* y[kMaxGroup];
+  int32_t layer[kMaxGroup];
+  int32_t count;
+  int32_t num_tiles;
+};
 
 // Split path (atmm_shrink_kernel + atmm_expand_kernel) for large batches.
 // Both kernels are persistent (one CTA per SM) over host-balanced ranges of a

@@ -876,7 +876,7 @@ __device__ __forceinline__ void a2a_epilogue(uint32_t tmem_base, uint32_t lane_a
 
 template <typename YT>
 __global__ void __launch_bounds__(kBypassThreads, 2)
-    atmm_bypass_a2a_kernel(const __grid_constant__ CUtensorMap tmap_x, const BypassParams p) {
+    atmm_bypass_a2a_kernel(const __grid_constant__ GroupArgs ga, const BypassParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -887,13 +887,17 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
 
   const uint32_t C = cluster_nctarank();
   const uint32_t crank = cluster_ctarank();
-  const TileDesc tile = p.tiles[cluster_id_x()];
+  const int call = static_cast<int>(cluster_id_x()) / ga.num_tiles;  // grouped launch: call, tile
+  const TileDesc tile = p.tiles[static_cast<int>(cluster_id_x()) - call * ga.num_tiles];
+  const CUtensorMap& tmap_x = ga.x_map[call];
+  const int layer = ga.layer[call];
+  uint8_t* const ycall = static_cast<uint8_t*>(ga.y[call]);
   const int rows = tile.rows;
   const int r_pad = tile.r_pad;
   const int rows16 = (rows + 15) & ~15;
   const int G = p.gcols;
-  const uint16_t* down_t = tile.down_t + static_cast<int64_t>(p.layer) * tile.down_layer_stride;
-  const uint16_t* up_t = tile.up_t + static_cast<int64_t>(p.layer) * tile.up_layer_stride;
+  const uint16_t* down_t = tile.down_t + static_cast<int64_t>(layer) * tile.down_layer_stride;
+  const uint16_t* up_t = tile.up_t + static_cast<int64_t>(layer) * tile.up_layer_stride;
   const int nkb = (p.d_in + kBK - 1) / kBK;
   const int kb_lo = (nkb * static_cast<int>(crank)) / static_cast<int>(C);
   const int kb_hi = (nkb * static_cast<int>(crank + 1)) / static_cast<int>(C);
@@ -1050,7 +1054,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     // 0..3 never wait behind these HBM reads.
     griddep_wait();
     const int cpr = ncols * kEsz / 16;  // 16-byte chunks per row
-    const uint8_t* ybase = reinterpret_cast<const uint8_t*>(p.y) + static_cast<int64_t>(n_lo) * kEsz;
+    const uint8_t* ybase = ycall + static_cast<int64_t>(n_lo) * kEsz;
     const int64_t ldy_b = p.ldy * kEsz;
     for (int q = static_cast<int>(lane); q < rows * cpr; q += 32) {
       const int r = q / cpr;
@@ -1188,7 +1192,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     const uint32_t lane_addr = (quad * 32u) << 16;
     const int m = static_cast<int>(quad * 32 + lane);
     const int half = static_cast<int>(warp >> 2);
-    uint8_t* ycols = reinterpret_cast<uint8_t*>(p.y) + static_cast<int64_t>(n_lo) * kEsz;
+    uint8_t* ycols = ycall + static_cast<int64_t>(n_lo) * kEsz;
     const int64_t ldy_b = p.ldy * kEsz;
     const uint32_t pitch = static_cast<uint32_t>(p.ypitch);
     const uint32_t rows_sa = smem_u32(rows_s);
@@ -2145,9 +2149,8 @@ template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant
 template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap,
                                                    const BypassParams);
-template __global__ void atmm_bypass_a2a_kernel<__nv_bfloat16>(const __grid_constant__ CUtensorMap,
-                                                               const BypassParams);
-template __global__ void atmm_bypass_a2a_kernel<float>(const __grid_constant__ CUtensorMap, const BypassParams);
+template __global__ void atmm_bypass_a2a_kernel<__nv_bfloat16>(const __grid_constant__ GroupArgs, const BypassParams);
+template __global__ void atmm_bypass_a2a_kernel<float>(const __grid_constant__ GroupArgs, const BypassParams);
 template __global__ void atmm_expand_kernel<__nv_bfloat16, 2>(const SplitParams);
 template __global__ void atmm_expand_kernel<__nv_bfloat16, 1>(const SplitParams);
 template __global__ void atmm_expand_kernel<float, 1>(const SplitParams);
@@ -2245,10 +2248,10 @@ cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensor
   return cudaLaunchKernelEx(&cfg, k, tmap_x, tmap_y, p);
 }
 
-cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const BypassParams& p, int C, int num_tiles,
+cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassParams& p, int C, int num_tiles,
                               size_t smem, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(C * num_tiles), 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(C * num_tiles * ga.count), 1, 1);
   cfg.blockDim = dim3(kBypassThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -2265,12 +2268,12 @@ cudaError_t launch_bypass_a2a(int y_dtype, const CUtensorMap& tmap_x, const Bypa
     auto k = atmm_bypass_a2a_kernel<__nv_bfloat16>;
     cudaError_t e = prepare(k, smem, C > 8);
     if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, k, tmap_x, p);
+    return cudaLaunchKernelEx(&cfg, k, ga, p);
   }
   auto k = atmm_bypass_a2a_kernel<float>;
   cudaError_t e = prepare(k, smem, C > 8);
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, k, tmap_x, p);
+  return cudaLaunchKernelEx(&cfg, k, ga, p);
 }
 
 cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,

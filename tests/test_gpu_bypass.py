@@ -226,3 +226,29 @@ def test_pipelined_host_residual(gpu, atmm, oracle):
     for want, yt in wants:
         got = yt.float().numpy()
         assert np.max(np.abs(got - want)) <= tol_for(want)
+
+
+def test_grouped_apply_matches_single_calls(gpu, atmm, oracle):
+    """atmm_bypass_apply_group: G independent (X, Y, layer) calls in one launch
+    give bit-identical results to G single applies."""
+    import torch
+
+    L, d, n = 3, 1024, 96
+    ranks = {1: 16, 2: 32, 3: 16}
+    reg, facs = _setup(atmm, oracle, d, d, ranks, L=L)
+    assignment = np.asarray([1 + (i * 5) % 3 for i in range(n)], np.int32)
+    plan = atmm.BypassPlan(reg, assignment)
+    xs = [torch.from_numpy(_x(oracle, n, d, seed=40 + c)).to("cuda", torch.bfloat16) for c in range(L)]
+    y0 = [torch.from_numpy(_x(oracle, n, d, seed=50 + c)).to("cuda", torch.bfloat16) for c in range(L)]
+    ya = [y.clone() for y in y0]
+    yb = [y.clone() for y in y0]
+    layers = [2, 0, 1]
+    plan.apply_group(xs, ya, layers, scale=0.5)
+    for c in range(L):
+        plan.apply(xs[c], yb[c], layer=layers[c], scale=0.5)
+    torch.cuda.synchronize()
+    for c in range(L):
+        assert torch.equal(ya[c], yb[c])
+        want = y0[c].float().cpu().numpy().astype(np.float64) + 0.5 * oracle.bypass_rows_f64(
+            xs[c].float().cpu().numpy(), assignment, {a: (f[0][layers[c]], f[1][layers[c]]) for a, f in facs.items()})
+        assert np.max(np.abs(ya[c].float().cpu().numpy() - want)) <= tol_for(want)
