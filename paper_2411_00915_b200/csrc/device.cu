@@ -471,7 +471,7 @@ struct SplitBufs {
   DevBuf<float> part;
   DevBuf<uint16_t> mid;
   DevBuf<int32_t> counter;
-  DevBuf<int32_t> tables;  // [s_begin | e_begin bf16 | e_begin fp32 (P+1 each) | seg_slot0 (P) | nseg | part_off (T) | red_off (T+1)]
+  DevBuf<int32_t> tables;  // [s_begin | e_begin bf16 | e_begin fp32 (P+1 each) | seg_slot0 (P) | nseg | part_off (T) | red_off (T+1) | red_tile0 (P)]
   int32_t grid = 0;
 };
 
@@ -724,6 +724,14 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     tables.insert(tables.end(), nseg.begin(), nseg.end());
     tables.insert(tables.end(), off.begin(), off.end());
     tables.insert(tables.end(), red_off.begin(), red_off.end());
+    {  // tile of each CTA's first reduction item (split_reduce_mid)
+      const int64_t total = red_off[static_cast<size_t>(T)];
+      for (int b = 0; b < P; ++b) {
+        const int32_t i = static_cast<int32_t>((total * b) / P);
+        const int t = static_cast<int>(std::upper_bound(red_off.begin(), red_off.end(), i) - red_off.begin()) - 1;
+        tables.push_back(std::clamp(t, 0, T - 1));
+      }
+    }
     auto& mb = plan->merged_bufs;
     mb = std::make_unique<SplitBufs>();
     mb->grid = P;
@@ -823,6 +831,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.nseg = sp.seg_slot0 + P;
       sp.part_off = sp.nseg + T;
       sp.red_off = sp.part_off + T;
+      sp.red_tile0 = sp.red_off + T + 1;
       sp.part = sb.part.p;
       sp.mid = sb.mid.p;
       sp.counter = sb.counter.p;

@@ -1261,6 +1261,22 @@ __device__ __forceinline__ void grid_barrier(int32_t* ctr, uint32_t nblocks) {
   __syncthreads();
 }
 
+// Single-thread form of grid_barrier (no __syncthreads; the caller publishes
+// completion to the rest of its CTA itself).
+__device__ __forceinline__ void grid_arrive_wait(int32_t* ctr, uint32_t nblocks) {
+  volatile int32_t* flag = ctr + 1;
+  const int32_t sense = *flag;
+  __threadfence();
+  if (atomicAdd(ctr, 1) == static_cast<int32_t>(nblocks) - 1) {
+    ctr[0] = 0;
+    __threadfence();
+    atomicExch(ctr + 1, sense ^ 1);
+  } else {
+    while (*flag == sense) __nanosleep(32);
+  }
+  __threadfence();
+}
+
 // Loader-side completion: after issuing item j (committed as one cp.async
 // group), the item D groups back has landed for every lane of the warp;
 // lane 0 publishes it (full barriers count one arrival per loader warp).
@@ -1278,6 +1294,77 @@ __device__ __forceinline__ void loader_drain(int n, int D, int S, uint64_t* full
   __syncwarp();
   if (lane == 0) {
     for (int j = max(0, n - D + 1); j < n; ++j) mbar_arrive(&full[j % S]);
+  }
+}
+
+// Fixed-order sum of the shrink's segment partials -> bf16 mid, a share of
+// the (tile, row, 4 columns) items per participating thread (rt of nthr per
+// CTA, all CTAs).  Summation order = slot order: deterministic.
+__device__ __forceinline__ void split_reduce_mid(const SplitParams& p, int rt, int nthr) {
+  // CTA b owns the contiguous item range [b N / P, (b + 1) N / P); its
+  // threads stride through it (consecutive threads -> consecutive 16-byte
+  // chunks of a row: coalesced); the tile of an item is found by walking
+  // forward from the CTA's first tile (host table red_tile0).
+  const int T = p.num_tiles;
+  const int total = p.red_off[T];
+  const int P = static_cast<int>(gridDim.x);
+  const int b = static_cast<int>(blockIdx.x);
+  const int i_lo = static_cast<int>((static_cast<int64_t>(total) * b) / P);
+  const int i_hi = static_cast<int>((static_cast<int64_t>(total) * (b + 1)) / P);
+  const int64_t seg_stride = static_cast<int64_t>(kTileM) * p.r_pad_max;
+  int t = p.red_tile0[b];
+  int t_next_off = p.red_off[t + 1];
+  constexpr int kB = 2;
+  for (int i0 = i_lo + rt; i0 < i_hi; i0 += nthr * kB) {
+    float4 acc[kB];
+    const float* src[kB];
+    uint8_t* dst[kB];
+    int ns[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int i = i0 + q * nthr;
+      ns[q] = 0;
+      src[q] = p.part;
+      dst[q] = nullptr;
+      if (i < i_hi) {
+        while (i >= t_next_off && t < T - 1) t_next_off = p.red_off[++t + 1];
+        const int r_pad = p.tiles[t].r_pad;
+        const int local = i - p.red_off[t];
+        const int rr = local / (r_pad / 4);
+        const int c4 = local - rr * (r_pad / 4);
+        ns[q] = p.nseg[t];
+        src[q] = p.part + static_cast<int64_t>(p.part_off[t]) * seg_stride + static_cast<int64_t>(rr) * p.r_pad_max + c4 * 4;
+        dst[q] = reinterpret_cast<uint8_t*>(p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max) +
+                 interleave_off(static_cast<uint32_t>(rr), static_cast<uint32_t>(c4 * 4), static_cast<uint32_t>(r_pad));
+      }
+    }
+    const int nmax = max(ns[0], ns[kB - 1]);
+    for (int sg0 = 0; sg0 < nmax; sg0 += 4) {
+      float4 v[kB][4];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[q][k] = sg0 + k < ns[q] ? __ldcg(reinterpret_cast<const float4*>(src[q] + (sg0 + k) * seg_stride))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc[q].x += v[q][k].x;
+          acc[q].y += v[q][k].y;
+          acc[q].z += v[q][k].z;
+          acc[q].w += v[q][k].w;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (dst[q]) *reinterpret_cast<uint2*>(dst[q]) = make_uint2(pack_bf16x2(acc[q].x, acc[q].y), pack_bf16x2(acc[q].z, acc[q].w));
+    }
   }
 }
 
@@ -1431,80 +1518,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
     }
   }
   if (tid == kSplitWarpEpi * 32) STRACE(2);
-  // ---- all partials written: grid-wide barrier, then every thread of every
-  // CTA sums a share of the (tile, row, 4 columns) items over the tile's
-  // segments in FIXED slot order -> bf16 mid.  (The grid is one CTA per SM,
-  // all co-resident, so the barrier cannot deadlock.) ----
   __threadfence();
-  __syncthreads();
-  grid_barrier(p.counter, gridDim.x);
-  {
-    const int T = p.num_tiles;
-    // tile lookup table in shared memory (the ring is dead now)
-    int32_t* red_off_s = reinterpret_cast<int32_t*>(smem);
-    for (int i = static_cast<int>(tid); i <= T; i += static_cast<int>(blockDim.x)) red_off_s[i] = p.red_off[i];
-    __syncthreads();
-    const int total = red_off_s[T];
-    const int64_t seg_stride = static_cast<int64_t>(kTileM) * p.r_pad_max;
-    const int gstride = static_cast<int>(gridDim.x * blockDim.x);
-    constexpr int kB = 2;
-    for (int i0 = static_cast<int>(blockIdx.x * blockDim.x + tid); i0 < total; i0 += gstride * kB) {
-      float4 acc[kB];
-      const float* src[kB];
-      uint8_t* dst[kB];
-      int ns[kB];
-#pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        acc[b] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int i = i0 + b * gstride;
-        ns[b] = 0;
-        src[b] = p.part;
-        dst[b] = nullptr;
-        if (i < total) {
-          int lo = 0, hi = T;  // tile t: red_off[t] <= i < red_off[t + 1]
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (red_off_s[mid] <= i) lo = mid; else hi = mid;
-          }
-          const int t = lo;
-          const int r_pad = p.tiles[t].r_pad;
-          const int local = i - red_off_s[t];
-          const int rr = local / (r_pad / 4);
-          const int c4 = local - rr * (r_pad / 4);
-          ns[b] = p.nseg[t];
-          src[b] = p.part + static_cast<int64_t>(p.part_off[t]) * seg_stride + static_cast<int64_t>(rr) * p.r_pad_max + c4 * 4;
-          dst[b] = reinterpret_cast<uint8_t*>(p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max) +
-                   interleave_off(static_cast<uint32_t>(rr), static_cast<uint32_t>(c4 * 4), static_cast<uint32_t>(r_pad));
-        }
-      }
-      const int nmax = max(ns[0], ns[kB - 1]);
-      for (int sg0 = 0; sg0 < nmax; sg0 += 4) {
-        float4 v[kB][4];
-#pragma unroll
-        for (int b = 0; b < kB; ++b) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            v[b][q] = sg0 + q < ns[b] ? __ldcg(reinterpret_cast<const float4*>(src[b] + (sg0 + q) * seg_stride))
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-#pragma unroll
-        for (int b = 0; b < kB; ++b) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            acc[b].x += v[b][q].x;
-            acc[b].y += v[b][q].y;
-            acc[b].z += v[b][q].z;
-            acc[b].w += v[b][q].w;
-          }
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        if (dst[b]) *reinterpret_cast<uint2*>(dst[b]) = make_uint2(pack_bf16x2(acc[b].x, acc[b].y), pack_bf16x2(acc[b].z, acc[b].w));
-      }
-    }
-  }
   __syncthreads();
   if (tid == 0) STRACE(3);
   griddep_launch_dependents();
@@ -1526,7 +1540,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   // interleave (no-swizzle) operands only need 16-byte alignment: align to 128
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
                                              ~static_cast<uintptr_t>(127));
-  __shared__ uint64_t bars[2 * 4 + 4];
+  __shared__ uint64_t bars[2 * 4 + 4 + 1];  // ... + mid_ready
   __shared__ uint32_t tmem_slot;
   constexpr int kEsz = static_cast<int>(sizeof(YT));
   constexpr int kCols = kTileM * G;  // output columns per item
@@ -1539,6 +1553,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   uint64_t* empty = bars + 4;      // [S], 256 epilogue arrivals
   uint64_t* acc_full = bars + 8;   // [2], MMA commit
   uint64_t* acc_empty = bars + 10; // [2], 256 epilogue arrivals
+  uint64_t* mid_ready = bars + 12; // grid-wide mid reduction done (1 arrival)
   const int rows16_max = (p.rows_max + 15) & ~15;
   const uint32_t up_bytes = static_cast<uint32_t>(kCols * p.r_pad_max * 2);
   const uint32_t mid_bytes = static_cast<uint32_t>((rows16_max * p.r_pad_max * 2 + 127) & ~127);
@@ -1555,7 +1570,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   const int nsl = (p.d_out + kCols - 1) / kCols;
 
   if (warp == 0) {
-    if (lane < 12) mbar_init(&bars[lane], lane < 4 ? kSplitLoaderWarps : ((lane < 8 || lane >= 10) ? 256u : 1u));
+    if (lane < 13) mbar_init(&bars[lane], lane < 4 ? kSplitLoaderWarps : ((lane < 8 || (lane >= 10 && lane < 12)) ? 256u : 1u));
     fence_mbar_init();
   }
   if (warp == kSplitWarpMMA) tmem_alloc(&tmem_slot, tcols);
@@ -1607,7 +1622,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
         cp_async16(Yb + static_cast<uint32_t>(r) * ypitch + c * 16, yb + static_cast<int64_t>(static_cast<int32_t>(ld_shared_u32(Rb + r * 4))) * ldy_b + c * 16, 16u);
       }
       if (!waited) {
-        griddep_wait();  // mid is produced by the shrink launch
+        mbar_wait(mid_ready, 0);  // mid is reduced by this launch's epilogue warps (grid barrier)
         waited = true;
         if (tid == 0) STRACE(12);
       }
@@ -1617,7 +1632,6 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       cp_async_commit();
       loader_publish(j, D, S, full, lane);
     }
-    if (!waited) griddep_wait();
     loader_drain(j, D, S, full, lane);
     if (tid == 0) STRACE(9);
   } else if (warp == kSplitWarpMMA) {
@@ -1652,6 +1666,20 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
     }
   } else {
     // ===================== epilogue (8 warps) =====================
+    // First: the shrink launch's partials -> bf16 mid, a share per CTA, then a
+    // grid-wide barrier; meanwhile the loaders already stream item 0's up^T
+    // and Y (which do not depend on mid).
+    {
+      const int et = static_cast<int>(tid) - static_cast<int>(kSplitWarpEpi) * 32;
+      griddep_wait();  // partials are produced by the shrink launch
+      split_reduce_mid(p, et, 256);
+      __threadfence();
+      named_bar_sync(3, 256);
+      if (et == 0) {
+        grid_arrive_wait(p.counter, gridDim.x);
+        mbar_arrive(mid_ready);
+      }
+    }
     // Warp w: TMEM lane quadrant w % 4, row blocks of RB rows alternating
     // between the two warps of a quadrant.
     constexpr int RB = 64 / G > 32 ? 32 : 64 / G;
