@@ -113,6 +113,18 @@ int atmm_default_candidates(size_t cache_budget_bytes, size_t scalar_width, int3
                             size_t cap, size_t* count);
 
 /* ===================================================================== */
+/* Fixture matrices (matrix.hpp:183-218): little-endian u32 rows, u32 cols, */
+/* u8 scalar width (4), row-major fp32 payload -- the reference's format.   */
+/* ===================================================================== */
+int atmm_matrix_save(const char* path, int64_t rows, int64_t cols, const float* data);
+/* out may be NULL (dims only); else capacity >= rows * cols floats. */
+int atmm_matrix_load(const char* path, int64_t* rows, int64_t* cols, float* out, int64_t capacity);
+/* A fixture directory's manifest.json (model_io.hpp:25-69 layout): layer
+ * count, hidden dim and the adapters' ids / ranks (first `capacity`). */
+int atmm_fixture_info(const char* dir, int64_t* num_layers, int64_t* hidden_dim, int64_t* num_adapters,
+                      int32_t* ids, int64_t* ranks, int64_t capacity);
+
+/* ===================================================================== */
 /* Adapter registry (adapter.hpp:18-110, device resident)                 */
 /* ===================================================================== */
 
@@ -130,6 +142,20 @@ void atmm_registry_destroy(atmm_registry* r);
  * Re-putting an id replaces it. */
 int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const float* down,
                       const float* up, float scale);
+/* Asynchronous adapter swap (serving.hpp:38-74 mode_switch, the paper's
+ * adapter swap): same factors and result as atmm_registry_put, but the H2D
+ * copy (pinned host memory for a truly async copy), the fp32 -> bf16
+ * operand-layout packing (a device kernel) and the release of a replaced
+ * slot's memory are all ordered on `stream`; work launched later on that
+ * stream sees the new factors. */
+int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, const float* down,
+                            const float* up, float scale, void* stream);
+/* load_model_fixture (model_io.hpp:71-114), adapter part: reads the
+ * fixture's manifest.json and binary matrix files (matrix.hpp:183-218) and
+ * puts every adapter (all layers) into the registry; the registry must match
+ * the fixture (num_layers, d_in == d_out == hidden_dim).  IoError on a bad or
+ * truncated file, ShapeError on mismatched factors. */
+int atmm_registry_load_fixture(atmm_registry* r, const char* dir, int64_t* num_adapters);
 int atmm_registry_remove(atmm_registry* r, int32_t adapter_id);
 /* Mixture / deLoRA branch (model.hpp:252-328): a slot whose
  * factors are the rank-concatenation of existing adapters,

@@ -256,6 +256,9 @@ class Reference:
         L.ref_table_lookup.argtypes = [i32p, i32p, c_size_t, i32p, c_uint64, c_uint64, c_uint64, i32p]
         L.ref_table_load_lookup.argtypes = [ctypes.c_char_p, c_uint64, c_uint64, c_uint64, i32p]
         L.ref_table_save.argtypes = [i32p, i32p, i64p, c_size_t, i32p, ctypes.c_char_p]
+        L.ref_save_matrix.argtypes = [ctypes.c_char_p, c_size_t, c_size_t, f32p]
+        L.ref_save_fixture.argtypes = [ctypes.c_char_p, c_size_t, c_size_t, c_size_t, c_uint64, c_size_t, i32p, i64p,
+                                       f32p]
         L.ref_plan_batch.restype = c_long
         L.ref_plan_batch.argtypes = [i32p, c_size_t, i32p, i64p, i64p]
         L.ref_ctx_new.restype = c_void_p

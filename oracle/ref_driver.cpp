@@ -23,6 +23,7 @@
 #include "loraserve/batch.hpp"
 #include "loraserve/matrix.hpp"
 #include "loraserve/model.hpp"
+#include "loraserve/model_io.hpp"
 #include "loraserve/random.hpp"
 #include "loraserve/tiling.hpp"
 
@@ -331,6 +332,48 @@ int ref_model_merge_cycle(float* w, size_t L, size_t d, size_t r, const float* d
     return 0;
   } catch (const std::exception& e) {
     return status_of(e);
+  }
+}
+
+// ---- fixture I/O (matrix.hpp:183-218, model_io.hpp:25-114) ----
+// save_matrix<float> of a rows x cols matrix; 0 = ok, 1 = IoError.
+int ref_save_matrix(const char* path, size_t rows, size_t cols, const float* data) {
+  try {
+    save_matrix<float>(ConstMatSpan<float>{data, rows, cols}, path);
+    return 0;
+  } catch (const Error&) {
+    return 1;
+  }
+}
+// save_model_fixture of a random model (seed) with the given adapters
+// (ids, ranks, factors [L][d x r] / [L][r x d] concatenated per adapter).
+int ref_save_fixture(const char* dir, size_t L, size_t d, size_t V, uint64_t seed, size_t num_adapters,
+                     const int32_t* ids, const int64_t* ranks, const float* factors) {
+  try {
+    BaseModel model = BaseModel::random(L, d, V, seed);
+    AdapterSet set;
+    const float* f = factors;
+    for (size_t a = 0; a < num_adapters; ++a) {
+      const size_t r = static_cast<size_t>(ranks[a]);
+      std::vector<Matrix<float>> down, up;
+      for (size_t l = 0; l < L; ++l) {
+        Matrix<float> m(d, r);
+        std::copy(f, f + d * r, m.data());
+        f += d * r;
+        down.push_back(std::move(m));
+      }
+      for (size_t l = 0; l < L; ++l) {
+        Matrix<float> m(r, d);
+        std::copy(f, f + r * d, m.data());
+        f += r * d;
+        up.push_back(std::move(m));
+      }
+      set.emplace(ids[a], LoraAdapter(ids[a], L, d, r, std::move(down), std::move(up), std::nullopt));
+    }
+    save_model_fixture(model, set, dir);
+    return 0;
+  } catch (const Error&) {
+    return 1;
   }
 }
 

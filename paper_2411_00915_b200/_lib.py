@@ -58,6 +58,11 @@ _SIGS = {
     "atmm_plan_create": (c_int, [c_void_p, i32p, c_int64, c_void_p, POINTER(c_void_p)]),
     "atmm_plan_create_mapped": (c_int, [c_void_p, i32p, i32p, c_int64, c_int64, c_void_p, POINTER(c_void_p)]),
     "atmm_registry_put_combined": (c_int, [c_void_p, c_int32, c_int64, i32p, f32p]),
+    "atmm_registry_put_async": (c_int, [c_void_p, c_int32, c_int64, f32p, f32p, c_float, c_void_p]),
+    "atmm_registry_load_fixture": (c_int, [c_void_p, c_char_p, i64p]),
+    "atmm_matrix_save": (c_int, [c_char_p, c_int64, c_int64, f32p]),
+    "atmm_matrix_load": (c_int, [c_char_p, i64p, i64p, f32p, c_int64]),
+    "atmm_fixture_info": (c_int, [c_char_p, i64p, i64p, i64p, i32p, i64p, c_int64]),
     "atmm_bypass_apply_group": (c_int, [c_void_p, c_int64, i64p, POINTER(c_void_p), c_int64, POINTER(c_void_p),
                                         c_int64, c_int, c_float, c_void_p]),
     "atmm_merge_apply_layers": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int,

@@ -277,6 +277,43 @@ class AdapterRegistry:
         for key in [k for k in combos if adapter_id in k]:
             lib.atmm_registry_remove(self._h, combos.pop(key))
 
+    def put_async(self, adapter_id: int, down, up, scale: float = 1.0, stream=None) -> None:
+        """Adapter swap ordered on `stream` (H2D + device-side packing,
+        atmm_registry_put_async).  down / up: numpy arrays or CPU torch tensors
+        (pinned for an asynchronous copy; keep them alive until the stream
+        has passed the copy)."""
+        def host(a):
+            try:
+                import torch
+
+                if isinstance(a, torch.Tensor):
+                    t = a.detach().to(torch.float32).contiguous()
+                    return t, ctypes.cast(t.data_ptr(), f32p), tuple(t.shape)
+            except ImportError:
+                pass
+            arr = _f32(a)
+            return arr, _p(arr, f32p), arr.shape
+
+        dkeep, dptr, dshape = host(down)
+        ukeep, uptr, ushape = host(up)
+        if len(dshape) == 2:
+            dshape = (1,) + tuple(dshape)
+        if len(ushape) == 2:
+            ushape = (1,) + tuple(ushape)
+        L, di, r = dshape
+        if L != self.num_layers or di != self.d_in or tuple(ushape) != (L, r, self.d_out):
+            raise ShapeError(f"adapter factor shapes {dshape} / {ushape} do not match registry")
+        _check(lib.atmm_registry_put_async(self._h, adapter_id, r, dptr, uptr, float(scale), _stream_ptr(stream)))
+        self._drop_combined(adapter_id)
+        self.__dict__.setdefault("_async_keep", []).append((dkeep, ukeep))
+
+    def load_fixture(self, directory: str) -> int:
+        """Every adapter of a reference fixture directory (manifest.json +
+        binary matrices, model_io.hpp) into the registry; returns the count."""
+        n = ctypes.c_int64(0)
+        _check(lib.atmm_registry_load_fixture(self._h, str(directory).encode(), ctypes.byref(n)))
+        return n.value
+
     def put_combined(self, new_id: int, parts: Sequence[Tuple[int, float]]) -> None:
         """A slot = rank-concatenation of existing adapters with signs folded
         into up (include/atmm_b200.h atmm_registry_put_combined): one fused
@@ -512,6 +549,35 @@ def merge_layers_into(registry: AdapterRegistry, adapter_id: int, w, sign: float
     _check(lib.atmm_merge_apply_layers(registry.handle, adapter_id, layer0, w.shape[0], w.data_ptr(), w.stride(1),
                                        w.stride(0), F32 if w.dtype == torch.float32 else BF16, float(sign),
                                        _stream_ptr(stream)))
+
+
+def save_matrix(path: str, m) -> None:
+    """save_matrix<float> (matrix.hpp:183-196): the reference's binary format."""
+    a = _f32(m)
+    if a.ndim != 2:
+        raise ShapeError("save_matrix takes a 2-D matrix")
+    _check(lib.atmm_matrix_save(str(path).encode(), a.shape[0], a.shape[1], _p(a, f32p)))
+
+
+def load_matrix(path: str) -> np.ndarray:
+    """load_matrix<float> (matrix.hpp:198-218)."""
+    r, c = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib.atmm_matrix_load(str(path).encode(), ctypes.byref(r), ctypes.byref(c), None, 0))
+    out = np.zeros((r.value, c.value), np.float32)
+    _check(lib.atmm_matrix_load(str(path).encode(), ctypes.byref(r), ctypes.byref(c), _p(out, f32p), out.size))
+    return out
+
+
+def fixture_info(directory: str) -> dict:
+    """manifest.json of a reference fixture: layers, hidden dim, adapter ids / ranks."""
+    L, d, n = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib.atmm_fixture_info(str(directory).encode(), ctypes.byref(L), ctypes.byref(d), ctypes.byref(n), None,
+                                 None, 0))
+    ids = np.zeros(n.value, np.int32)
+    ranks = np.zeros(n.value, np.int64)
+    _check(lib.atmm_fixture_info(str(directory).encode(), ctypes.byref(L), ctypes.byref(d), ctypes.byref(n),
+                                 _p(ids, i32p), _p(ranks, i64p), n.value))
+    return {"num_layers": L.value, "hidden_dim": d.value, "adapters": dict(zip(ids.tolist(), ranks.tolist()))}
 
 
 def atmm_multiply(a, b, config: Sequence[int]) -> np.ndarray:

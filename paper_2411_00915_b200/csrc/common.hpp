@@ -76,6 +76,21 @@ struct LaunchCfg {
   auto operator<=>(const LaunchCfg&) const = default;
 };
 
+// ---- reference fixture I/O (matrix.hpp:183-218, model_io.hpp:25-114) ----
+// Binary matrix: little-endian u32 rows, u32 cols, u8 scalar width, row-major payload.
+std::vector<float> load_matrix_f32(const std::string& path, int64_t& rows, int64_t& cols);
+void save_matrix_f32(const std::string& path, int64_t rows, int64_t cols, const float* data);
+struct FixtureAdapter {
+  int32_t id = 0;
+  int64_t rank = 0;
+  std::vector<std::string> down, up;  // per-layer matrix files (relative to the fixture dir)
+};
+struct FixtureManifest {
+  int64_t num_layers = 0, hidden_dim = 0;
+  std::vector<FixtureAdapter> adapters;
+};
+FixtureManifest read_fixture_manifest(const std::string& dir);
+
 struct TableEntry {
   TilingConfig config;
   int64_t measured_ns = 0;

@@ -41,6 +41,9 @@ cudaError_t launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t rows, in
                                int64_t lds, int64_t ldd, cudaStream_t stream);
 cudaError_t launch_scale_bf16_2d(uint16_t* base, int64_t rows, int64_t cols, int64_t ld, float f,
                                  cudaStream_t stream);
+cudaError_t launch_pack_factors(const float* down, const float* up, int64_t L, int64_t d_in, int64_t d_out,
+                                int64_t r, int64_t d_in_pad, int64_t d_out_pad, int64_t r_pad, uint16_t* down_t,
+                                uint16_t* up_t, cudaStream_t stream);
 
 namespace {
 
@@ -1147,6 +1150,87 @@ int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts
       r->slot_of[new_id] = idx;
     }
     r->sync_slots();
+  });
+}
+
+int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, const float* down,
+                            const float* up, float scale, void* stream) {
+  return guarded([&] {
+    if (!r) fail(ATMM_ERR_CONFIG, "null registry");
+    if (rank < 1 || rank > kMaxRank) fail(ATMM_ERR_CONFIG, "adapter rank must be in [1, 128]");
+    if (!down || !up) fail(ATMM_ERR_SHAPE, "null factors");
+    DeviceGuard g(r->device);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t r_pad = round_up(rank, 16);
+    const size_t dn = static_cast<size_t>(r->d_in_pad * r_pad) * static_cast<size_t>(r->L);
+    const size_t un = static_cast<size_t>(r->d_out_pad * r_pad) * static_cast<size_t>(r->L);
+    const size_t fd = static_cast<size_t>(r->L * r->d_in * rank), fu = static_cast<size_t>(r->L * rank * r->d_out);
+    Slot s;
+    s.id = adapter_id;
+    s.rank = rank;
+    s.r_pad = r_pad;
+    s.scale = scale;
+    s.live = true;
+    float* stage = nullptr;
+    CUDA_CHECK(cudaMallocAsync(&s.down_t, dn * 2, st));
+    CUDA_CHECK(cudaMallocAsync(&s.up_t, un * 2, st));
+    CUDA_CHECK(cudaMallocAsync(&stage, (fd + fu) * 4, st));
+    CUDA_CHECK(cudaMemcpyAsync(stage, down, fd * 4, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(stage + fd, up, fu * 4, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(launch_pack_factors(stage, stage + fd, r->L, r->d_in, r->d_out, rank, r->d_in_pad, r->d_out_pad, r_pad,
+                                   s.down_t, s.up_t, st));
+    CUDA_CHECK(cudaFreeAsync(stage, st));
+    auto it = r->slot_of.find(adapter_id);
+    if (it != r->slot_of.end()) {
+      Slot& old = r->slots[static_cast<size_t>(it->second)];
+      CUDA_CHECK(cudaFreeAsync(old.down_t, st));  // stream order: after every earlier use on this stream
+      CUDA_CHECK(cudaFreeAsync(old.up_t, st));
+      old = s;
+    } else {
+      int idx = -1;
+      for (size_t i = 0; i < r->slots.size(); ++i) {
+        if (!r->slots[i].live) {
+          idx = static_cast<int>(i);
+          break;
+        }
+      }
+      if (idx < 0) {
+        idx = static_cast<int>(r->slots.size());
+        r->slots.push_back(s);
+      } else {
+        r->slots[static_cast<size_t>(idx)] = s;
+      }
+      r->slot_of[adapter_id] = idx;
+    }
+    r->sync_slots();
+  });
+}
+
+int atmm_registry_load_fixture(atmm_registry* r, const char* dir, int64_t* num_adapters) {
+  return guarded([&] {
+    if (!r || !dir) fail(ATMM_ERR_CONFIG, "null registry or directory");
+    const FixtureManifest m = read_fixture_manifest(dir);
+    if (m.num_layers != r->L || m.hidden_dim != r->d_in || m.hidden_dim != r->d_out) {
+      fail(ATMM_ERR_SHAPE, "fixture (L=" + std::to_string(m.num_layers) + ", d=" + std::to_string(m.hidden_dim) +
+                               ") does not match the registry (L=" + std::to_string(r->L) + ", d_in=" +
+                               std::to_string(r->d_in) + ", d_out=" + std::to_string(r->d_out) + ")");
+    }
+    const std::string base(dir);
+    for (const FixtureAdapter& a : m.adapters) {
+      std::vector<float> down, up;
+      for (int64_t l = 0; l < m.num_layers; ++l) {
+        int64_t rr = 0, cc = 0;
+        std::vector<float> dm = load_matrix_f32(base + "/" + a.down[static_cast<size_t>(l)], rr, cc);
+        if (rr != r->d_in || cc != a.rank) fail(ATMM_ERR_SHAPE, "adapter " + std::to_string(a.id) + " down factor must be d x r");
+        down.insert(down.end(), dm.begin(), dm.end());
+        std::vector<float> um = load_matrix_f32(base + "/" + a.up[static_cast<size_t>(l)], rr, cc);
+        if (rr != a.rank || cc != r->d_out) fail(ATMM_ERR_SHAPE, "adapter " + std::to_string(a.id) + " up factor must be r x d");
+        up.insert(up.end(), um.begin(), um.end());
+      }
+      const int st = atmm_registry_put(r, a.id, a.rank, down.data(), up.data(), 1.0f);
+      if (st != ATMM_OK) fail(st, atmm_last_error());
+    }
+    if (num_adapters) *num_adapters = static_cast<int64_t>(m.adapters.size());
   });
 }
 

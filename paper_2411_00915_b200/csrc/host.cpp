@@ -427,6 +427,85 @@ BatchPlan plan_batch(const int32_t* assignment, int64_t n) {
   return p;
 }
 
+// ---- reference fixture I/O ----
+std::vector<float> load_matrix_f32(const std::string& path, int64_t& rows, int64_t& cols) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(ATMM_ERR_IO, "cannot open for read: " + path);
+  uint32_t r = 0, c = 0;
+  uint8_t width = 0;
+  in.read(reinterpret_cast<char*>(&r), 4);
+  in.read(reinterpret_cast<char*>(&c), 4);
+  in.read(reinterpret_cast<char*>(&width), 1);
+  if (!in) fail(ATMM_ERR_IO, "truncated header: " + path);
+  if (width != sizeof(float)) {
+    fail(ATMM_ERR_IO, "scalar width mismatch in " + path + ": file has " + std::to_string(width) + ", expected 4");
+  }
+  rows = r;
+  cols = c;
+  std::vector<float> out(static_cast<size_t>(r) * c);
+  in.read(reinterpret_cast<char*>(out.data()), static_cast<std::streamsize>(out.size() * sizeof(float)));
+  if (!in) fail(ATMM_ERR_IO, "truncated payload: " + path);
+  return out;
+}
+
+void save_matrix_f32(const std::string& path, int64_t rows, int64_t cols, const float* data) {
+  if (rows < 0 || cols < 0 || rows > 0xffffffffLL || cols > 0xffffffffLL) fail(ATMM_ERR_SHAPE, "matrix too large for the u32 header");
+  std::ofstream out(path, std::ios::binary);
+  if (!out) fail(ATMM_ERR_IO, "cannot open for write: " + path);
+  const uint32_t r = static_cast<uint32_t>(rows), c = static_cast<uint32_t>(cols);
+  const uint8_t width = sizeof(float);
+  out.write(reinterpret_cast<const char*>(&r), 4);
+  out.write(reinterpret_cast<const char*>(&c), 4);
+  out.write(reinterpret_cast<const char*>(&width), 1);
+  out.write(reinterpret_cast<const char*>(data), static_cast<std::streamsize>(sizeof(float) * rows * cols));
+  if (!out) fail(ATMM_ERR_IO, "short write: " + path);
+}
+
+FixtureManifest read_fixture_manifest(const std::string& dir) {
+  std::ifstream in(dir + "/manifest.json");
+  if (!in) fail(ATMM_ERR_IO, "cannot read manifest in " + dir);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  const std::string text = ss.str();
+  json::Value root;
+  try {
+    root = json::Parser(text).parse();
+  } catch (const Failure& e) {
+    fail(ATMM_ERR_IO, std::string("bad manifest: ") + e.what());
+  }
+  if (!root.is_obj()) fail(ATMM_ERR_IO, "bad manifest: root must be an object");
+  auto need = [&](const json::Object& o, const char* key) -> const json::Value& {
+    auto it = o.find(key);
+    if (it == o.end()) fail(ATMM_ERR_IO, std::string("bad manifest: missing key '") + key + "'");
+    return it->second;
+  };
+  auto as_str = [](const json::Value& v) -> std::string {
+    if (!std::holds_alternative<std::string>(v.v)) fail(ATMM_ERR_IO, "bad manifest: file names must be strings");
+    return std::get<std::string>(v.v);
+  };
+  FixtureManifest m;
+  m.num_layers = json::as_int(need(root.obj(), "num_layers"), "num_layers");
+  m.hidden_dim = json::as_int(need(root.obj(), "hidden_dim"), "hidden_dim");
+  const json::Value& ads = need(root.obj(), "adapters");
+  if (!ads.is_arr()) fail(ATMM_ERR_IO, "bad manifest: adapters must be an array");
+  for (const json::Value& av : ads.arr()) {
+    if (!av.is_obj()) fail(ATMM_ERR_IO, "bad manifest: adapter entries must be objects");
+    FixtureAdapter a;
+    a.id = static_cast<int32_t>(json::as_int(need(av.obj(), "id"), "adapter id"));
+    a.rank = json::as_int(need(av.obj(), "rank"), "adapter rank");
+    for (const char* key : {"down", "up"}) {
+      const json::Value& files = need(av.obj(), key);
+      if (!files.is_arr()) fail(ATMM_ERR_IO, std::string("bad manifest: adapter ") + key + " must be an array");
+      for (const json::Value& f : files.arr()) (key[0] == 'd' ? a.down : a.up).push_back(as_str(f));
+    }
+    if (static_cast<int64_t>(a.down.size()) != m.num_layers || static_cast<int64_t>(a.up.size()) != m.num_layers) {
+      fail(ATMM_ERR_IO, "manifest lists wrong layer count for adapter " + std::to_string(a.id));
+    }
+    m.adapters.push_back(std::move(a));
+  }
+  return m;
+}
+
 }  // namespace atmm
 
 // =========================================================================
@@ -435,6 +514,42 @@ BatchPlan plan_batch(const int32_t* assignment, int64_t n) {
 using namespace atmm;
 
 extern "C" {
+
+int atmm_matrix_save(const char* path, int64_t rows, int64_t cols, const float* data) {
+  return guarded([&] {
+    if (!path || (!data && rows * cols > 0)) fail(ATMM_ERR_CONFIG, "null path or data");
+    save_matrix_f32(path, rows, cols, data);
+  });
+}
+
+int atmm_fixture_info(const char* dir, int64_t* num_layers, int64_t* hidden_dim, int64_t* num_adapters,
+                      int32_t* ids, int64_t* ranks, int64_t capacity) {
+  return guarded([&] {
+    if (!dir) fail(ATMM_ERR_CONFIG, "null directory");
+    const FixtureManifest m = read_fixture_manifest(dir);
+    if (num_layers) *num_layers = m.num_layers;
+    if (hidden_dim) *hidden_dim = m.hidden_dim;
+    if (num_adapters) *num_adapters = static_cast<int64_t>(m.adapters.size());
+    for (size_t i = 0; i < m.adapters.size() && static_cast<int64_t>(i) < capacity; ++i) {
+      if (ids) ids[i] = m.adapters[i].id;
+      if (ranks) ranks[i] = m.adapters[i].rank;
+    }
+  });
+}
+
+int atmm_matrix_load(const char* path, int64_t* rows, int64_t* cols, float* out, int64_t capacity) {
+  return guarded([&] {
+    if (!path || !rows || !cols) fail(ATMM_ERR_CONFIG, "null path or dims");
+    int64_t r = 0, c = 0;
+    std::vector<float> m = load_matrix_f32(path, r, c);
+    *rows = r;
+    *cols = c;
+    if (out) {
+      if (capacity < r * c) fail(ATMM_ERR_SHAPE, "output buffer too small");
+      std::copy(m.begin(), m.end(), out);
+    }
+  });
+}
 
 const char* atmm_last_error(void) { return g_last_error.c_str(); }
 int atmm_abi_version(void) { return ATMM_ABI_VERSION; }

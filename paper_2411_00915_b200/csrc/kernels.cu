@@ -2170,6 +2170,38 @@ __global__ void scale_bf16_2d_kernel(uint16_t* __restrict__ base, int64_t rows, 
   }
 }
 
+// Device-side packing of host fp32 factors into the registry's tcgen05
+// operand layouts (bit-identical to pack_down_t / pack_up_t in device.cu):
+//   down [L][d_in x r] -> down^T [L][kb][g = r_pad/8][c = 8][8 rank][8 d_in]
+//   up   [L][r x d_out] -> up^T  [L][g = d_out_pad/8][c = r_pad/8][8 n][8 rank]
+__global__ void pack_factors_kernel(const float* __restrict__ down, const float* __restrict__ up, int64_t L,
+                                    int64_t d_in, int64_t d_out, int64_t r, int64_t d_in_pad, int64_t d_out_pad,
+                                    int64_t r_pad, uint16_t* __restrict__ down_t, uint16_t* __restrict__ up_t) {
+  const int64_t dn = d_in_pad * r_pad, un = d_out_pad * r_pad;
+  const int64_t total = L * (dn + un);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float v = 0.0f;
+    if (e < L * dn) {
+      const int64_t l = e / dn, q = e - l * dn;
+      const int64_t kb = q / (r_pad * 64), rem = q - kb * (r_pad * 64);
+      const int64_t g = rem >> 9, rem2 = rem & 511;
+      const int64_t c = rem2 >> 6, rr = (rem2 >> 3) & 7, cc = rem2 & 7;
+      const int64_t i = kb * 64 + c * 8 + cc, j = g * 8 + rr;
+      if (i < d_in && j < r) v = down[(l * d_in + i) * r + j];
+      down_t[e] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    } else {
+      const int64_t e2 = e - L * dn;
+      const int64_t l = e2 / un, q = e2 - l * un;
+      const int64_t g = q / (r_pad * 8), rem = q - g * (r_pad * 8);
+      const int64_t c = rem >> 6, rr = (rem >> 3) & 7, cc = rem & 7;
+      const int64_t n = g * 8 + rr, j = c * 8 + cc;
+      if (n < d_out && j < r) v = up[(l * r + j) * d_out + n];
+      up_t[e2] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    }
+  }
+}
+
 // Explicit instantiations reachable from the host launcher.
 template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant__ CUtensorMap,
                                                            const __grid_constant__ CUtensorMap,
@@ -2388,6 +2420,16 @@ cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const Merge
   cudaError_t e = prepare(k, smem, false);
   if (e != cudaSuccess) return e;
   k<<<grid, kMergeThreads, smem, stream>>>(tmap_w, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_factors(const float* down, const float* up, int64_t L, int64_t d_in, int64_t d_out,
+                                int64_t r, int64_t d_in_pad, int64_t d_out_pad, int64_t r_pad, uint16_t* down_t,
+                                uint16_t* up_t, cudaStream_t stream) {
+  const int64_t total = L * (d_in_pad + d_out_pad) * r_pad;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+  pack_factors_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(down, up, L, d_in, d_out, r, d_in_pad, d_out_pad,
+                                                                   r_pad, down_t, up_t);
   return cudaGetLastError();
 }
 
