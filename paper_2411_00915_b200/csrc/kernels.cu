@@ -874,7 +874,7 @@ __device__ __forceinline__ void a2a_epilogue(uint32_t tmem_base, uint32_t lane_a
   }
 }
 
-template <typename YT>
+template <typename YT, int G>
 __global__ void __launch_bounds__(kBypassThreads, 2)
     atmm_bypass_a2a_kernel(const __grid_constant__ GroupArgs ga, const BypassParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -895,7 +895,6 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
   const int rows = tile.rows;
   const int r_pad = tile.r_pad;
   const int rows16 = (rows + 15) & ~15;
-  const int G = p.gcols;
   const uint16_t* down_t = tile.down_t + static_cast<int64_t>(layer) * tile.down_layer_stride;
   const uint16_t* up_t = tile.up_t + static_cast<int64_t>(layer) * tile.up_layer_stride;
   const int nkb = (p.d_in + kBK - 1) / kBK;
@@ -941,7 +940,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  cluster_arrive();  // phase 1: barrier inits visible to peers
+  cluster_arrive_relaxed();  // phase 1: barrier inits (fenced above) visible to peers
   if (threadIdx.x == 0) TRACE(1);
 
   const uint32_t ybuf_s = smem_u32(ybuf);
@@ -1176,7 +1175,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
   } else {
     mbar_wait_cluster(red_full, 0);
   }
-  cluster_arrive();
+  cluster_arrive_relaxed();
 
   // ===================== all warps: Y[rows, cols] += s * acc =====================
   {
@@ -1196,12 +1195,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     const int64_t ldy_b = p.ldy * kEsz;
     const uint32_t pitch = static_cast<uint32_t>(p.ypitch);
     const uint32_t rows_sa = smem_u32(rows_s);
-    switch (G) {
-      case 1: a2a_epilogue<YT, 1>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
-      case 2: a2a_epilogue<YT, 2>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
-      case 4: a2a_epilogue<YT, 4>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
-      default: a2a_epilogue<YT, 8>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s); break;
-    }
+    a2a_epilogue<YT, G>(tmem_base, lane_addr, half, rows, rows16, m, ncols, ybuf_s, pitch, ycols, rows_sa, ldy_b, s);
     if (tracer) TRACE(12);
   }
   tc_fence_before();
@@ -2209,8 +2203,6 @@ template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant
 template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap,
                                                    const BypassParams);
-template __global__ void atmm_bypass_a2a_kernel<__nv_bfloat16>(const __grid_constant__ GroupArgs, const BypassParams);
-template __global__ void atmm_bypass_a2a_kernel<float>(const __grid_constant__ GroupArgs, const BypassParams);
 template __global__ void atmm_expand_kernel<__nv_bfloat16, 2>(const SplitParams);
 template __global__ void atmm_expand_kernel<__nv_bfloat16, 1>(const SplitParams);
 template __global__ void atmm_expand_kernel<float, 1>(const SplitParams);
@@ -2308,6 +2300,15 @@ cudaError_t launch_bypass(int y_dtype, const CUtensorMap& tmap_x, const CUtensor
   return cudaLaunchKernelEx(&cfg, k, tmap_x, tmap_y, p);
 }
 
+template <typename YT, int G>
+static cudaError_t launch_a2a_typed(const cudaLaunchConfig_t& cfg, const GroupArgs& ga, const BypassParams& p, size_t smem,
+                                    bool nonportable) {
+  auto k = atmm_bypass_a2a_kernel<YT, G>;
+  cudaError_t e = prepare(k, smem, nonportable);
+  if (e != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, k, ga, p);
+}
+
 cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassParams& p, int C, int num_tiles,
                               size_t smem, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
@@ -2324,16 +2325,22 @@ cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassPara
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const bool np = C > 8;
+  // one instantiation per (Y type, columns per epilogue thread): small hot code
   if (y_dtype == 0) {
-    auto k = atmm_bypass_a2a_kernel<__nv_bfloat16>;
-    cudaError_t e = prepare(k, smem, C > 8);
-    if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, k, ga, p);
+    switch (p.gcols) {
+      case 1: return launch_a2a_typed<__nv_bfloat16, 1>(cfg, ga, p, smem, np);
+      case 2: return launch_a2a_typed<__nv_bfloat16, 2>(cfg, ga, p, smem, np);
+      case 4: return launch_a2a_typed<__nv_bfloat16, 4>(cfg, ga, p, smem, np);
+      default: return launch_a2a_typed<__nv_bfloat16, 8>(cfg, ga, p, smem, np);
+    }
   }
-  auto k = atmm_bypass_a2a_kernel<float>;
-  cudaError_t e = prepare(k, smem, C > 8);
-  if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, k, ga, p);
+  switch (p.gcols) {
+    case 1: return launch_a2a_typed<float, 1>(cfg, ga, p, smem, np);
+    case 2: return launch_a2a_typed<float, 2>(cfg, ga, p, smem, np);
+    case 4: return launch_a2a_typed<float, 4>(cfg, ga, p, smem, np);
+    default: return launch_a2a_typed<float, 8>(cfg, ga, p, smem, np);
+  }
 }
 
 cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,
