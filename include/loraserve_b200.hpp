@@ -17,6 +17,7 @@
 #pragma once
 
 #include <array>
+#include <map>
 #include <compare>
 #include <cstdint>
 #include <stdexcept>
@@ -160,6 +161,29 @@ class AdapterRegistry {
   void put(int adapter_id, std::size_t rank, const float* down, const float* up, float scale = 1.0f) {
     check(atmm_registry_put(h_, adapter_id, static_cast<int64_t>(rank), down, up, scale));
   }
+  // mode_switch's adapter swap, ordered on `stream` (pinned host memory for
+  // an asynchronous copy); same result as put().
+  void put_async(int adapter_id, std::size_t rank, const float* down, const float* up, float scale = 1.0f,
+                 void* stream = nullptr) {
+    check(atmm_registry_put_async(h_, adapter_id, static_cast<int64_t>(rank), down, up, scale, stream));
+  }
+  // A slot = rank-concatenation of existing adapters with signs folded into
+  // up: one bypass then adds sum_i sign_i s_i (x.down_i).up_i.
+  void put_combined(int new_id, const std::vector<std::pair<int, float>>& parts) {
+    std::vector<int32_t> ids;
+    std::vector<float> signs;
+    for (const auto& [id, sign] : parts) {
+      ids.push_back(id);
+      signs.push_back(sign);
+    }
+    check(atmm_registry_put_combined(h_, new_id, static_cast<int64_t>(ids.size()), ids.data(), signs.data()));
+  }
+  // load_model_fixture's adapters (model_io.hpp:71-114); returns the count.
+  std::size_t load_fixture(const std::string& dir) {
+    int64_t n = 0;
+    check(atmm_registry_load_fixture(h_, dir.c_str(), &n));
+    return static_cast<std::size_t>(n);
+  }
   bool contains(int adapter_id) const { return atmm_registry_contains(h_, adapter_id) == 1; }
   atmm_registry* handle() const { return h_; }
   std::size_t d_in() const { return d_in_; }
@@ -200,6 +224,73 @@ inline void unmerge_into(const AdapterRegistry& reg, int adapter_id, std::size_t
                          std::size_t ldw, int w_dtype, void* stream = nullptr) {
   check(atmm_merge_apply(reg.handle(), adapter_id, static_cast<int64_t>(layer), w_device,
                          static_cast<int64_t>(ldw), w_dtype, -1.0f, stream));
+}
+
+// merge / unmerge every layer [layer0, layer0 + num_layers) in ONE launch;
+// layer l's W at w_device + (l - layer0) * w_layer_stride elements.
+inline void merge_layers_into(const AdapterRegistry& reg, int adapter_id, std::size_t layer0, std::size_t num_layers,
+                              void* w_device, std::size_t ldw, std::size_t w_layer_stride, int w_dtype, float sign,
+                              void* stream = nullptr) {
+  check(atmm_merge_apply_layers(reg.handle(), adapter_id, static_cast<int64_t>(layer0),
+                                static_cast<int64_t>(num_layers), w_device, static_cast<int64_t>(ldw),
+                                static_cast<int64_t>(w_layer_stride), w_dtype, sign, stream));
+}
+
+// forward_mixture's per-layer bypass (model.hpp:252-328) on device buffers:
+// guest rows (adapter != merged_id) get (x.down_a).up_a - (x.down_m).up_m in
+// ONE launch through combined slots (ids combined_base - k); merged rows are
+// untouched.  X: n x d_in bf16, Y: n x d_out (y_dtype).
+class MixturePlan {
+ public:
+  MixturePlan(AdapterRegistry& reg, const std::vector<int>& assignment, int merged_id, int combined_base = -(1 << 20)) {
+    if (!reg.contains(merged_id)) throw ModeError("mixture integrity: subtraction branch missing");
+    std::vector<int32_t> guest_rows, virt;
+    std::map<int, int> combo;
+    for (std::size_t row = 0; row < assignment.size(); ++row) {
+      const int a = assignment[row];
+      if (a == merged_id) continue;
+      auto it = combo.find(a);
+      if (it == combo.end()) {
+        const int vid = combined_base - static_cast<int>(combo.size());
+        reg.put_combined(vid, {{a, 1.0f}, {merged_id, -1.0f}});
+        it = combo.emplace(a, vid).first;
+      }
+      guest_rows.push_back(static_cast<int32_t>(row));
+      virt.push_back(it->second);
+    }
+    if (!guest_rows.empty()) {
+      check(atmm_plan_create_mapped(reg.handle(), virt.data(), guest_rows.data(), static_cast<int64_t>(virt.size()),
+                                    static_cast<int64_t>(assignment.size()), nullptr, &plan_));
+    }
+  }
+  ~MixturePlan() { atmm_plan_destroy(plan_); }
+  MixturePlan(const MixturePlan&) = delete;
+  MixturePlan& operator=(const MixturePlan&) = delete;
+  void apply(std::size_t layer, const void* x, std::size_t ldx, void* y, std::size_t ldy, int y_dtype,
+             float scale = 1.0f, void* stream = nullptr) const {
+    if (!plan_) return;
+    check(atmm_bypass_apply(plan_, static_cast<int64_t>(layer), x, static_cast<int64_t>(ldx), y,
+                            static_cast<int64_t>(ldy), y_dtype, scale, stream));
+  }
+
+ private:
+  atmm_plan* plan_ = nullptr;
+};
+
+// ------------------------------------------------------------- fixtures --
+// save_matrix / load_matrix<float> (matrix.hpp:183-218), the reference's format.
+inline void save_matrix(const std::string& path, std::size_t rows, std::size_t cols, const std::vector<float>& m) {
+  if (m.size() != rows * cols) throw ShapeError("save_matrix: data must be rows x cols");
+  check(atmm_matrix_save(path.c_str(), static_cast<int64_t>(rows), static_cast<int64_t>(cols), m.data()));
+}
+inline std::vector<float> load_matrix(const std::string& path, std::size_t* rows, std::size_t* cols) {
+  int64_t r = 0, c = 0;
+  check(atmm_matrix_load(path.c_str(), &r, &c, nullptr, 0));
+  std::vector<float> out(static_cast<std::size_t>(r * c));
+  check(atmm_matrix_load(path.c_str(), &r, &c, out.data(), r * c));
+  if (rows) *rows = static_cast<std::size_t>(r);
+  if (cols) *cols = static_cast<std::size_t>(c);
+  return out;
 }
 
 // atmm_multiply (atmm.hpp:144-154): host fp32 a (m x k) . b (k x n).

@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "loraserve_b200.hpp"
 
 using namespace loraserve_b200;
@@ -87,6 +89,15 @@ static void host_checks() {
   CHECK((back.lookup(256, 4096, 32) == TilingConfig{64, 32, 32, 32, 32, 32}));
   CHECK((back.lookup(8192, 4096, 128) == TilingConfig{64, 64, 64, 32, 64, 64}));
   CHECK_THROWS_AS(TilingTable::load("/nonexistent/table.json"), IoError);
+
+  // matrix.hpp:183-218 -- binary fixture round trip and errors
+  const std::vector<float> m = {1.f, -2.5f, 3.25f, 0.f, 7.f, -0.125f};
+  save_matrix("/tmp/loraserve_b200_shim_m.bin", 2, 3, m);
+  std::size_t mr = 0, mc = 0;
+  CHECK(load_matrix("/tmp/loraserve_b200_shim_m.bin", &mr, &mc) == m);
+  CHECK(mr == 2 && mc == 3);
+  CHECK_THROWS_AS(load_matrix("/nonexistent/m.bin", nullptr, nullptr), IoError);
+  CHECK_THROWS_AS(save_matrix("/tmp/loraserve_b200_shim_m.bin", 4, 3, m), ShapeError);
 }
 
 static void gpu_checks() {
@@ -155,6 +166,46 @@ static void gpu_checks() {
   for (float v : dw) sum += std::fabs(v);
   CHECK(dw[3 * 64 + 5] == 1.f);
   CHECK(sum == 1.0);
+
+  // put_async == put (device-side packing), then the mixture plan on device
+  // buffers: guest rows get own - merged, merged rows stay untouched.
+  AdapterRegistry r2(0, 1, d, d);
+  r2.put_async(1, ranks[0], downs[0].data(), ups[0].data());
+  r2.put(2, ranks[1], downs[1].data(), ups[1].data());
+  CHECK(cudaDeviceSynchronize() == cudaSuccess);
+  std::vector<float> own = run_bypass(r2, x, std::vector<int>(n, 1), 0);
+  std::vector<float> ref1 = run_bypass(reg, x, std::vector<int>(n, 1), 0);
+  CHECK(own == ref1);
+  std::vector<int> mix(n);
+  for (std::size_t i = 0; i < n; ++i) mix[i] = 1 + static_cast<int>(i % 2);
+  MixturePlan mp(r2, mix, /*merged*/ 2);
+  std::vector<uint16_t> xb(n * d);
+  for (std::size_t i = 0; i < n * d; ++i) {
+    uint32_t bits;
+    std::memcpy(&bits, &x[i], 4);
+    xb[i] = static_cast<uint16_t>(bits >> 16);  // x is bf16-exact
+  }
+  void *xd = nullptr, *yd = nullptr;
+  CHECK(cudaMalloc(&xd, n * d * 2) == cudaSuccess);
+  CHECK(cudaMalloc(&yd, n * d * 4) == cudaSuccess);
+  CHECK(cudaMemcpy(xd, xb.data(), n * d * 2, cudaMemcpyHostToDevice) == cudaSuccess);
+  CHECK(cudaMemset(yd, 0, n * d * 4) == cudaSuccess);
+  mp.apply(0, xd, d, yd, d, ATMM_F32);
+  std::vector<float> y(n * d);
+  CHECK(cudaMemcpy(y.data(), yd, n * d * 4, cudaMemcpyDeviceToHost) == cudaSuccess);
+  std::vector<float> cancel = run_bypass(r2, x, std::vector<int>(n, 2), 0);
+  double mworst = 0, mscale = 1;
+  for (std::size_t row = 0; row < n; ++row) {
+    for (std::size_t c2 = 0; c2 < d; ++c2) {
+      const double want = mix[row] == 2 ? 0.0 : double(own[row * d + c2]) - cancel[row * d + c2];
+      mworst = std::max(mworst, std::fabs(want - y[row * d + c2]));
+      mscale = std::max(mscale, std::fabs(want));
+      if (mix[row] == 2) CHECK(y[row * d + c2] == 0.f);
+    }
+  }
+  CHECK(mworst <= 1e-2 * mscale);
+  cudaFree(xd);
+  cudaFree(yd);
 }
 
 int main(int argc, char** argv) {

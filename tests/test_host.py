@@ -229,8 +229,10 @@ def test_compute_fails_loudly_without_device(atmm):
 
 def _build_shim(tmp_path):
     exe = tmp_path / "shim_test"
-    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp", "shim_test.cpp"),
-           "-L", os.path.dirname(LIB), "-l:libatmm_b200.so", f"-Wl,-rpath,{os.path.dirname(LIB)}", "-o", str(exe)]
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tests", "cpp", "shim_test.cpp"),
+           "-L", os.path.dirname(LIB), "-l:libatmm_b200.so", f"-Wl,-rpath,{os.path.dirname(LIB)}",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", str(exe)]
     subprocess.run(cmd, check=True, capture_output=True)
     return exe
 
