@@ -163,8 +163,8 @@ def max_over_ranks(v: float, world: int) -> float:
 
 # -------------------------------------------------- reference (CPU) -------
 def reference_batch_fn(w, seed: int):
-    """Returns (fn, flops): fn() runs the reference's run_bypass + add_inplace
-    (model.hpp:239-241) on one fp32 batch and returns elapsed seconds."""
+    """Returns (fn, flops): fn() runs the reference's run_bypass (batch.hpp:48)
+    on one fp32 batch."""
     from oracle.oracle import Reference
 
     ref = Reference()
@@ -176,11 +176,10 @@ def reference_batch_fn(w, seed: int):
                        rng.uniform(-s, s, (r, w.d_out)).astype(np.float32))
     ctx = ref.ctx(w.d_in, adapters)
     x = rng.uniform(-1, 1, (w.tokens, w.d_in)).astype(np.float32)
-    y = np.zeros((w.tokens, w.d_out), np.float32)
     a = np.ascontiguousarray(w.assignment, np.int32)
 
     def fn():
-        return ctx.bypass_residual(x, a, y) * 1e-9
+        return ctx.run_bypass(x, a)  # batch.hpp:48 run_bypass: a fresh n x d_out bypass
 
     return fn, w.flops()
 
@@ -234,7 +233,7 @@ def impl_reference(args, w):
     cfg = {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens, "adapters": len(w.ranks),
            "ranks": sorted(set(w.ranks.values())), "dtype_ref": "f32"}
     sample = (f"{args.steps} steps x {threads} concurrent {w.name} batches (one per host thread) through the "
-              f"reference's run_bypass + add_inplace, fp32")
+              f"reference's run_bypass (batch.hpp:48), fp32")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
@@ -361,13 +360,16 @@ def impl_ours_bypass(args, w):
     achieved_gbs = step_bytes / (kernel_us * 1e-6) / 1e9
 
     # ---- end to end through the C ABI with pinned host buffers ----
-    # Every step: H2D of that step's X and Y from pinned host memory, the
-    # fused kernel, D2H of the updated Y; steps are independent micro-batches
-    # pipelined over two streams (atmm_bypass_residual_host_bf16_pipelined).
+    # run_bypass (batch.hpp:48) semantics, the reference's own call: every
+    # step H2D of that step's X from pinned host memory, the bypass into a
+    # fresh output, D2H of the output; independent batches pipelined over
+    # three streams (atmm_run_bypass_host_bf16_pipelined).  The residual
+    # form (Y in, Y += bypass, Y out) is reported beside it.
     e2e = None
+    e2e_res = None
     if not args.no_e2e:
         e2e_steps = max(3, min(args.steps, 64))
-        nbuf = 4
+        nbuf = 6
         xh = [torch.empty(w.tokens, w.d_in, dtype=torch.bfloat16).uniform_(-1, 1).pin_memory() for _ in range(nbuf)]
         yh = [torch.zeros(w.tokens, w.d_out, dtype=torch.bfloat16).pin_memory() for _ in range(nbuf)]
         xs = [t.view(torch.int16).numpy().view(np.uint16) for t in xh]
@@ -375,19 +377,28 @@ def impl_ours_bypass(args, w):
         seq_x = [xs[i % nbuf] for i in range(e2e_steps)]
         seq_y = [ys[i % nbuf] for i in range(e2e_steps)]
         seq_l = [i % layers for i in range(e2e_steps)]
-        atmm.residual_host_bf16_pipelined(plan, seq_x[:2], seq_y[:2], seq_l[:2])  # warm-up
-        barrier(world)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        atmm.residual_host_bf16_pipelined(plan, seq_x, seq_y, seq_l)
-        torch.cuda.synchronize()
-        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+
+        def timed(fn):
+            fn(seq_x[:3], seq_y[:3], seq_l[:3])  # warm-up
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn(seq_x, seq_y, seq_l)
+            torch.cuda.synchronize()
+            return max_over_ranks(time.perf_counter() - t0, world)
+
+        e2e_s = timed(lambda a, b, c: atmm.run_bypass_host_bf16_pipelined(plan, a, b, c))
         e2e = {"value": world * flops_step * e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": int(w.tokens * (w.d_in + w.d_out) * 2),
+               "h2d_bytes_per_step": int(w.tokens * w.d_in * 2),
                "d2h_bytes_per_step": int(w.tokens * w.d_out * 2),
                "us_per_batch": e2e_s / e2e_steps * 1e6, "steps": e2e_steps,
-               "path": "atmm_bypass_residual_host_bf16_pipelined (pinned bf16 host X,Y -> H2D, fused kernel, "
-                       "D2H Y; 2 streams)"}
+               "path": "atmm_run_bypass_host_bf16_pipelined = run_bypass (batch.hpp:48) on pinned bf16 host "
+                       "buffers: H2D X, fused kernel into a fresh output, D2H; 3 streams"}
+        r_s = timed(lambda a, b, c: atmm.residual_host_bf16_pipelined(plan, a, b, c))
+        e2e_res = {"value": world * flops_step * e2e_steps / r_s / 1e12, "unit": "TFLOP/s",
+                   "h2d_bytes_per_step": int(w.tokens * (w.d_in + w.d_out) * 2),
+                   "d2h_bytes_per_step": int(w.tokens * w.d_out * 2), "us_per_batch": r_s / e2e_steps * 1e6,
+                   "path": "atmm_bypass_residual_host_bf16_pipelined: H2D X and Y, Y += bypass, D2H Y"}
 
     # ---- CPU baseline: the reference itself, bounded sample, rank 0, N=1 ----
     cpu = None
@@ -399,7 +410,7 @@ def impl_ours_bypass(args, w):
             cpu = {"value": w.flops() * batches / el / 1e12, "unit": "TFLOP/s", "cores": threads,
                    "kind": "reference",
                    "sample": f"{batches} {w.name} batches in {el:.1f} s, {threads} concurrent batches "
-                             f"(one per host thread) through the reference run_bypass + add_inplace (fp32), "
+                             f"(one per host thread) through the reference run_bypass (batch.hpp:48, fp32), "
                              f"oracle/_ref built from the reference headers"}
         except FileNotFoundError as e:
             cpu = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
@@ -425,6 +436,7 @@ def impl_ours_bypass(args, w):
                          "step_us": kernel_us, "algorithmic_bytes_per_step": step_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_residual": e2e_res,
             "grouped": grouped,
             "clocks": clocks,
             "gpu_launches": int(args.steps * launches_per_step),

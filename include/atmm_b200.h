@@ -237,6 +237,13 @@ int atmm_bypass_residual_host_bf16_pipelined(const atmm_plan* p, const int64_t* 
                                              const uint16_t* const* x_hosts,
                                              uint16_t* const* y_hosts, int64_t count,
                                              float scale);
+/* run_bypass (batch.hpp:48) end to end with bf16 HOST buffers, `count`
+ * independent batches pipelined (H2D of one, compute of another, D2H of a
+ * third): out_hosts[i] = bypass(x_hosts[i]) for layer layers[i] (a fresh
+ * output, like run_bypass's returned matrix).  Pinned host memory for
+ * overlap. */
+int atmm_run_bypass_host_bf16_pipelined(const atmm_plan* p, const int64_t* layers, const uint16_t* const* x_hosts,
+                                        uint16_t* const* out_hosts, int64_t count);
 
 /* ===================================================================== */
 /* Merge / unmerge  W +-= s . down . up   (model.hpp:120-188)             */

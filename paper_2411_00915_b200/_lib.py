@@ -63,6 +63,7 @@ _SIGS = {
     "atmm_matrix_save": (c_int, [c_char_p, c_int64, c_int64, f32p]),
     "atmm_matrix_load": (c_int, [c_char_p, i64p, i64p, f32p, c_int64]),
     "atmm_fixture_info": (c_int, [c_char_p, i64p, i64p, i64p, i32p, i64p, c_int64]),
+    "atmm_run_bypass_host_bf16_pipelined": (c_int, [c_void_p, i64p, POINTER(c_void_p), POINTER(c_void_p), c_int64]),
     "atmm_bypass_apply_group": (c_int, [c_void_p, c_int64, i64p, POINTER(c_void_p), c_int64, POINTER(c_void_p),
                                         c_int64, c_int, c_float, c_void_p]),
     "atmm_merge_apply_layers": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int,

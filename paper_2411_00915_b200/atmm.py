@@ -486,6 +486,22 @@ class MixturePlan:
             self.plan.apply(x, y, layer, scale, stream)
 
 
+def run_bypass_host_bf16_pipelined(plan: "BypassPlan", xs, outs, layers) -> None:
+    """run_bypass (batch.hpp:48) end to end from bf16 host buffers (uint16
+    numpy views, pinned for overlap): outs[i] = bypass(xs[i]) at layers[i],
+    batches pipelined over H2D / compute / D2H."""
+    n = len(xs)
+    if not (n == len(outs) == len(layers)):
+        raise ShapeError("xs, outs and layers must have the same length")
+    for a in list(xs) + list(outs):
+        if a.dtype != np.uint16 or not a.flags.c_contiguous:
+            raise ShapeError("host buffers must be C-contiguous uint16 (bf16 bits)")
+    lay = np.asarray(layers, np.int64)
+    xp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in xs])
+    op = (ctypes.c_void_p * n)(*[a.ctypes.data for a in outs])
+    _check(lib.atmm_run_bypass_host_bf16_pipelined(plan.handle, _p(lay, i64p), xp, op, n))
+
+
 def residual_host_bf16_pipelined(plan: "BypassPlan", xs, ys, layers, scale: float = 1.0) -> None:
     """Serving form: one micro-batch per (x, y) host pair (uint16 bf16 bit
     patterns, pinned for overlap), pipelined H2D / kernel / D2H."""

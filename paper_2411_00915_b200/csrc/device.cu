@@ -1456,6 +1456,53 @@ int atmm_bypass_residual_host_bf16_pipelined(const atmm_plan* p, const int64_t* 
   });
 }
 
+int atmm_run_bypass_host_bf16_pipelined(const atmm_plan* p, const int64_t* layers, const uint16_t* const* x_hosts,
+                                        uint16_t* const* out_hosts, int64_t count) {
+  return guarded([&] {
+    if (!p || !layers || !x_hosts || !out_hosts || count < 0) fail(ATMM_ERR_CONFIG, "null plan or buffers");
+    const atmm_registry* r = p->reg;
+    DeviceGuard g(r->device);
+    const int64_t ldx = round_up(r->d_in, 8), ldy = round_up(r->d_out, 8);
+    const size_t nx = static_cast<size_t>(p->n * ldx), ny = static_cast<size_t>(p->n * ldy);
+    struct Slot {
+      DevBuf<uint16_t> x, y;
+      cudaStream_t s = nullptr;
+    };
+    // Three independent batches in flight: one H2D, one on the SMs, one D2H
+    // (the copy engines run both directions at once).
+    constexpr size_t kSlots = 4;
+    thread_local std::vector<std::unique_ptr<Slot>> slots;
+    thread_local int slots_dev = -1;
+    if (slots_dev != r->device) slots.clear();
+    slots_dev = r->device;
+    while (slots.size() < kSlots) {
+      auto s = std::make_unique<Slot>();
+      CUDA_CHECK(cudaStreamCreateWithFlags(&s->s, cudaStreamNonBlocking));
+      slots.push_back(std::move(s));
+    }
+    for (auto& s : slots) {
+      if (s->x.n < nx) s->x.alloc(nx);
+      if (s->y.n < ny) s->y.alloc(ny);
+    }
+    for (int64_t i = 0; i < count; ++i) {
+      Slot& s = *slots[static_cast<size_t>(i) % kSlots];
+      if (ldx == r->d_in) {
+        CUDA_CHECK(cudaMemcpyAsync(s.x.p, x_hosts[i], nx * 2, cudaMemcpyHostToDevice, s.s));
+      } else {
+        CUDA_CHECK(cudaMemcpy2DAsync(s.x.p, ldx * 2, x_hosts[i], r->d_in * 2, r->d_in * 2, p->n, cudaMemcpyHostToDevice, s.s));
+      }
+      CUDA_CHECK(cudaMemsetAsync(s.y.p, 0, ny * 2, s.s));  // fresh output: out = 0 + bypass
+      apply_plan(p, layers[i], s.x.p, ldx, s.y.p, ldy, ATMM_BF16, 1.0f, s.s);
+      if (ldy == r->d_out) {
+        CUDA_CHECK(cudaMemcpyAsync(out_hosts[i], s.y.p, ny * 2, cudaMemcpyDeviceToHost, s.s));
+      } else {
+        CUDA_CHECK(cudaMemcpy2DAsync(out_hosts[i], r->d_out * 2, s.y.p, ldy * 2, r->d_out * 2, p->n, cudaMemcpyDeviceToHost, s.s));
+      }
+    }
+    for (auto& s : slots) CUDA_CHECK(cudaStreamSynchronize(s->s));
+  });
+}
+
 int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* w, int64_t ldw,
                      int w_dtype, float sign, void* stream) {
   return guarded([&] {
