@@ -135,6 +135,7 @@ LaunchCfg heuristic_launch(int64_t m, int64_t d_in, int64_t rank, int64_t d_out)
   l.tile_m = 128;
   l.cluster = static_cast<int32_t>(std::clamp<int64_t>((d_in + 511) / 512, 1, 16));
   if (const char* e = std::getenv("ATMM_CLUSTER")) l.cluster = std::clamp(std::atoi(e), 1, 16);  // A/B runs
+  if (const char* e = std::getenv("ATMM_TILE_M")) l.tile_m = std::clamp(std::atoi(e), 1, 128);   // A/B runs
   // Small segments are latency bound: 128-column chunks keep TMEM at 256
   // columns so two CTAs fit per SM (see resolve_group).
   l.bn = (m <= 64 || rank > 32) ? 128 : 256;

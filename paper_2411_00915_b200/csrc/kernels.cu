@@ -1387,7 +1387,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
   if (tid == 0) STRACE(0);
 
   if (warp == 0) {
-    if (lane < 2 * 8 + 4) mbar_init(&bars[lane], lane < 8 ? kSplitLoaderWarps : (lane >= 18 ? 128u : 1u));
+    // full: the 8 loader warps + the down^T bulk copy's expect_tx arrival
+    if (lane < 2 * 8 + 4) mbar_init(&bars[lane], lane < 8 ? kSplitLoaderWarps + 1u : (lane >= 18 ? 128u : 1u));
     fence_mbar_init();
   }
   if (warp == kSplitWarpMMA) tmem_alloc(&tmem_slot, tcols);
@@ -1433,9 +1434,13 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
         const int r = r0 + kRowStep * i;
         if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], 16u);
       }
-      const uint16_t* dk = down_t + static_cast<int64_t>(kb) * r_pad * kBK;
-      for (int q = static_cast<int>(tid); q < r_pad * 8; q += kSplitLoaders) cp_async16(A + a_bytes + q * 16, dk + q * 8, 16u);
+      if (tid == 0) {  // the down^T block is one contiguous run: one TMA bulk copy
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(r_pad * kBK * 2));
+        bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes + a_bytes, down_t + static_cast<int64_t>(kb) * r_pad * kBK,
+                 static_cast<uint32_t>(r_pad * kBK * 2), &full[st]);
+      }
       cp_async_commit();
+      if (tid == 0 && j < 12) STRACE(16 + j);
       loader_publish(j, D, S, full, lane);
     }
     loader_drain(j, D, S, full, lane);
@@ -1454,6 +1459,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
       const int st = j % S;
       mbar_wait(&full[st], static_cast<uint32_t>((j / S) & 1));
       tc_fence_after();
+      if (lane == 0 && j < 2) STRACE(4 + j);
       if (elect_one()) {
         const uint32_t A = smem0 + static_cast<uint32_t>(st) * stage_bytes;
         const uint64_t ad0 = smem_desc(A, 16u, 1024u, kLayoutSW128);
@@ -1564,7 +1570,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   const int nsl = (p.d_out + kCols - 1) / kCols;
 
   if (warp == 0) {
-    if (lane < 13) mbar_init(&bars[lane], lane < 4 ? kSplitLoaderWarps : ((lane < 8 || (lane >= 10 && lane < 12)) ? 256u : 1u));
+    // full: the 8 loader warps + the mid bulk copy's expect_tx arrival
+    if (lane < 13) mbar_init(&bars[lane], lane < 4 ? kSplitLoaderWarps + 1u : ((lane < 8 || (lane >= 10 && lane < 12)) ? 256u : 1u));
     fence_mbar_init();
   }
   if (warp == kSplitWarpMMA) tmem_alloc(&tmem_slot, tcols);
@@ -1622,7 +1629,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       }
       const uint16_t* ms = p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max;
       const int rows16 = (rows + 15) & ~15;
-      for (int q = static_cast<int>(tid); q < rows16 * r_pad / 8; q += kSplitLoaders) cp_async16(M + q * 16, ms + q * 8, 16u);
+      if (tid == 0) {  // mid is one contiguous bf16 run: one TMA bulk copy
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows16 * r_pad * 2));
+        bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes + up_bytes, ms, static_cast<uint32_t>(rows16 * r_pad * 2),
+                 &full[st]);
+      }
       cp_async_commit();
       loader_publish(j, D, S, full, lane);
     }
@@ -2357,8 +2368,12 @@ cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t sme
   cfg.dynamicSmemBytes = smem_s;
   cudaError_t e = prepare(atmm_shrink_kernel, smem_s, false);
   if (e != cudaSuccess) return e;
-  e = cudaLaunchKernelEx(&cfg, atmm_shrink_kernel, p);
-  if (e != cudaSuccess) return e;
+  static const int only = std::getenv("ATMM_SPLIT_ONLY") ? std::atoi(std::getenv("ATMM_SPLIT_ONLY")) : 0;  // A/B: 1 shrink, 2 expand
+  if (only != 2) {
+    e = cudaLaunchKernelEx(&cfg, atmm_shrink_kernel, p);
+    if (e != cudaSuccess) return e;
+  }
+  if (only == 1) return cudaSuccess;
   cfg.blockDim = dim3(kExpandThreads, 1, 1);
   cfg.dynamicSmemBytes = smem_e;
   if (y_dtype == 0 && p.expand_g == 1) {
