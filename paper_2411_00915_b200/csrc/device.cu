@@ -16,6 +16,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <new>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -82,6 +83,14 @@ struct DeviceGuard {
   explicit DeviceGuard(int dev) {
     cudaGetDevice(&prev);
     if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+  }
+  // Destructor paths (plan / registry teardown, possibly during process
+  // exit after the CUDA runtime shut down) must never throw.
+  DeviceGuard(int dev, std::nothrow_t) {
+    if (cudaGetDevice(&prev) != cudaSuccess || (prev != dev && cudaSetDevice(dev) != cudaSuccess)) {
+      cudaGetLastError();
+      prev = -1;
+    }
   }
   ~DeviceGuard() {
     int cur = -1;
@@ -241,7 +250,7 @@ struct atmm_registry {
   uint64_t generation = 0;
 
   ~atmm_registry() {
-    DeviceGuard g(device);
+    DeviceGuard g(device, std::nothrow);
     for (auto& s : slots) {
       if (s.down_t) cudaFree(s.down_t);
       if (s.up_t) cudaFree(s.up_t);
@@ -1293,7 +1302,7 @@ int atmm_plan_create_mapped(atmm_registry* r, const int32_t* assignment, const i
 
 void atmm_plan_destroy(atmm_plan* p) {
   if (!p) return;
-  DeviceGuard g(p->reg->device);
+  DeviceGuard g(p->reg->device, std::nothrow);
   delete p;
 }
 

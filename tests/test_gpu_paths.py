@@ -102,3 +102,41 @@ def test_split_path_is_chosen_for_large_tiles(gpu, atmm, oracle, monkeypatch):
     small = np.repeat(np.asarray(sorted(ranks), np.int32), 16)
     groups = atmm.BypassPlan(reg, small).describe()
     assert all(g["path_bf16"] == "a2a" for g in groups), groups
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_shapes_all_paths(gpu, atmm, oracle, monkeypatch, seed):
+    """Random d_in / d_out (incl. not multiples of 8 or 64), ranks 1..128,
+    ragged segments down to 1 row, bf16 and fp32 Y: every kernel path the
+    launcher can take matches the oracle."""
+    import torch
+
+    rng = np.random.default_rng(1000 + seed)
+    d_in = int(rng.integers(16, 1200))
+    d_out = int(rng.choice([int(rng.integers(8, 1200)) // 8 * 8, int(rng.integers(9, 700))]))
+    n_ad = int(rng.integers(1, 6))
+    ranks = {int(a): int(rng.choice([1, 7, 16, 33, 64, 100, 128])) for a in rng.choice(50, n_ad, replace=False)}
+    lens = [int(v) for v in rng.integers(1, 150, n_ad)]
+    facs, assignment, x, y0 = _inputs(oracle, d_in, d_out, ranks, lens, seed=seed)
+    reg = atmm.AdapterRegistry(1, d_in, d_out)
+    for a, (down, up) in facs.items():
+        reg.put(a, down, up)
+    want_b = oracle.bypass_rows_f64(x, assignment, facs)
+    # X rows must be 16-byte aligned (ldx % 8 == 0): pad the row stride, as a caller would
+    ldx = (d_in + 7) // 8 * 8
+    xpad = torch.zeros(x.shape[0], ldx, dtype=torch.bfloat16, device="cuda")
+    xpad[:, :d_in] = torch.from_numpy(x).to("cuda", torch.bfloat16)
+    xt = xpad[:, :d_in]
+    for path in ("auto", "a2a", "split", "fused"):
+        if path == "auto":
+            monkeypatch.delenv("ATMM_PATH", raising=False)
+        else:
+            monkeypatch.setenv("ATMM_PATH", path)
+        plan = atmm.BypassPlan(reg, assignment)
+        for dt in (torch.bfloat16, torch.float32):
+            yt = torch.from_numpy(y0).to("cuda", dt)
+            plan.apply(xt, yt)
+            torch.cuda.synchronize()
+            want = y0.astype(np.float64) + want_b
+            got = yt.float().cpu().numpy()
+            assert np.max(np.abs(got - want)) <= tol_for(want), (path, dt, d_in, d_out, ranks, lens)
