@@ -296,6 +296,42 @@ int atmm_shard_rows(const int32_t* assignment, int64_t n, const int32_t* adapter
                     const int64_t* adapter_ranks, int64_t num_adapters, int64_t d_in,
                     int64_t d_out, int32_t num_shards, int32_t* shard_of_row);
 
+/* ===================================================================== */
+/* Layer forward (model.hpp:192-328)                                      */
+/* ===================================================================== */
+
+/* The serving model's stack forward on device, replacing forward_unmerged
+ * (model.hpp:216-246), forward_mixture (model.hpp:251-328) and
+ * forward_merged (model.hpp:192-211):
+ *     cur <- tanh(cur . W_l + bypass_l(cur)),  l = 0 .. num_layers-1
+ * bypass_l is the plan's batched LoRA at layer l (run_bypass,
+ * batch.hpp:48-81).  A mixture plan (combined slots over the guest rows, see
+ * atmm_plan_create_mapped) gives forward_mixture over merged weights; a NULL
+ * plan gives forward_merged.  The bypass rides the base GEMM as extra K
+ * blocks of the same tcgen05 accumulator; bf16 activations and weights,
+ * fp32 accumulation, tanh, bf16 out.
+ *
+ * create: plan may be NULL (then device, n and hidden_dim give the shape;
+ * otherwise they may be 0 or must match the plan).  The forward owns its
+ * workspace (two n x d activation buffers, the K-extension images) and
+ * references the plan's registry: replacing an adapter makes it stale
+ * (ATMM_ERR_CONFIG at run).
+ * run: W is num_layers x [d][d] bf16 (row stride ldw, layer stride
+ * w_layer_stride elements, the reference's BaseModel layer layout), X and
+ * out are n x d bf16 (row strides ldx / ldo, multiples of 8; 16-byte aligned
+ * bases; out must not overlap X).  Stream-ordered on `stream`.
+ * num_layers = 0 copies X. */
+typedef struct atmm_forward atmm_forward;
+int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hidden_dim,
+                        atmm_forward** out);
+void atmm_forward_destroy(atmm_forward* f);
+int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_layer_stride,
+                     int64_t num_layers, const void* x, int64_t ldx, void* out, int64_t ldo,
+                     void* stream);
+/* {n, d, bn, tiles, grid, ext blocks, shrink items, shrink K split, sorted,
+ *  GEMM stages, shrink stages}: the first min(cap, 11) are written. */
+int atmm_forward_stats(const atmm_forward* f, int64_t* out, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,7 @@ import os
 from ctypes import POINTER, c_double, c_float, c_int, c_int32, c_int64, c_long, c_size_t, c_uint64, c_void_p
 
 import numpy as np
+from typing import Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
@@ -73,6 +74,8 @@ class Oracle:
                                           c_void_p, f64p]
         L.orc_delta_w.argtypes = [f32p, f32p, c_size_t, c_size_t, c_size_t, f32p]
         L.orc_merge.argtypes = [f32p, c_size_t, c_size_t, c_size_t, c_size_t, f32p, f32p, c_int]
+        L.orc_forward_f64.argtypes = [f32p, c_size_t, c_size_t, c_size_t, f32p, c_int, i32p, ctypes.c_int32, c_size_t,
+                                      i32p, i64p, c_void_p, c_void_p, c_int, f64p]
 
     # ---- RNG ----
     def rng(self, seed: int):
@@ -203,6 +206,30 @@ class Oracle:
             raise KeyError(f"oracle status {st}")
         return out
 
+    def forward_f64(self, x, w, mode: str = "unmerged", assignment=None, adapters: Optional[dict] = None,
+                    merged_id: int = -1, round_act: bool = True) -> np.ndarray:
+        """Stack forward (model.hpp:192-328), mode 'unmerged' | 'merged' |
+        'mixture'.  w: [L][d][d]; adapters: {id: (down [L][d][r], up [L][r][d])};
+        for 'mixture' w must already hold the merged adapter."""
+        x = np.ascontiguousarray(x, np.float32)
+        w = np.ascontiguousarray(w, np.float32)
+        n, d = x.shape
+        L = w.shape[0]
+        m = {"unmerged": 0, "merged": 1, "mixture": 2}[mode]
+        adapters = adapters or {}
+        ids = np.asarray(sorted(adapters), np.int32)
+        downs = [np.ascontiguousarray(adapters[i][0], np.float32) for i in ids]
+        ups = [np.ascontiguousarray(adapters[i][1], np.float32) for i in ids]
+        ranks = np.asarray([dn.shape[-1] for dn in downs], np.int64)
+        a = np.ascontiguousarray(np.asarray(assignment if assignment is not None else np.zeros(n), np.int32))
+        out = np.zeros((n, d), np.float64)
+        st = self.L.orc_forward_f64(_p(x, f32p), n, d, L, _p(w, f32p), m, _p(a, i32p), merged_id, len(ids),
+                                    _p(ids, i32p), _p(ranks, i64p), _ptr_array(downs), _ptr_array(ups),
+                                    1 if round_act else 0, _p(out, f64p))
+        if st != 0:
+            raise KeyError(f"oracle status {st}")
+        return out
+
     def delta_w(self, down, up) -> np.ndarray:
         down = np.ascontiguousarray(down, np.float32)
         up = np.ascontiguousarray(up, np.float32)
@@ -268,6 +295,8 @@ class Reference:
         L.ref_ctx_bypass_residual.argtypes = [c_void_p, f32p, c_size_t, i32p, f32p, i64p]
         L.ref_merge_rect.argtypes = [f32p, c_size_t, c_size_t, c_size_t, f32p, f32p, c_int, f32p, i64p]
         L.ref_model_merge_cycle.argtypes = [f32p, c_size_t, c_size_t, c_size_t, f32p, f32p, c_int]
+        L.ref_forward.argtypes = [c_int, c_size_t, c_size_t, f32p, c_size_t, i32p, i64p, c_void_p, c_void_p, f32p,
+                                  c_size_t, i32p, ctypes.c_int32, f32p]
 
     def fill_uniform(self, seed: int, count: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
         h = self.L.ref_rng_new(seed)
@@ -350,6 +379,28 @@ class Reference:
 
     def ctx(self, d: int, adapters: dict) -> "Reference.Ctx":
         return Reference.Ctx(self, d, adapters)
+
+    def forward(self, x, w, mode: str = "unmerged", assignment=None, adapters: Optional[dict] = None,
+                merged_id: int = -1):
+        """The reference's forward_unmerged / forward_merged / forward_mixture.
+        Returns (out fp32, weights after the call: merged for 'mixture')."""
+        x = np.ascontiguousarray(x, np.float32)
+        w = np.array(w, np.float32, copy=True, order="C")
+        n, d = x.shape
+        L = w.shape[0]
+        m = {"unmerged": 0, "merged": 1, "mixture": 2}[mode]
+        adapters = adapters or {}
+        ids = np.asarray(sorted(adapters), np.int32)
+        downs = [np.ascontiguousarray(adapters[i][0], np.float32) for i in ids]
+        ups = [np.ascontiguousarray(adapters[i][1], np.float32) for i in ids]
+        ranks = np.asarray([dn.shape[-1] for dn in downs], np.int64)
+        a = np.ascontiguousarray(np.asarray(assignment if assignment is not None else np.zeros(n), np.int32))
+        out = np.zeros((n, d), np.float32)
+        st = self.L.ref_forward(m, L, d, _p(w, f32p), len(ids), _p(ids, i32p), _p(ranks, i64p), _ptr_array(downs),
+                                _ptr_array(ups), _p(x, f32p), n, _p(a, i32p), merged_id, _p(out, f32p))
+        if st != 0:
+            raise ValueError(f"reference status {st}")
+        return out, w
 
     def merge_rect(self, w, down, up, sign: int = 1):
         """In place on w (d_in x d_out fp32); returns elapsed ns."""

@@ -25,6 +25,7 @@
 #include "loraserve/model.hpp"
 #include "loraserve/model_io.hpp"
 #include "loraserve/random.hpp"
+#include "loraserve/serving.hpp"
 #include "loraserve/tiling.hpp"
 
 using namespace loraserve;
@@ -374,6 +375,56 @@ int ref_save_fixture(const char* dir, size_t L, size_t d, size_t V, uint64_t see
     return 0;
   } catch (const Error&) {
     return 1;
+  }
+}
+
+
+// The stack forward through BaseModel + ModelState (model.hpp:192-328):
+// mode 0 forward_unmerged, 1 forward_merged (W used as given), 2
+// forward_mixture: the reference merges adapter merged_id into W (merge,
+// model.hpp:144), attaches the subtraction branch (init_delora) and runs
+// forward_mixture; w then holds the merged weights on return.
+// w is [L][d*d]; downs[a] / ups[a] are [L][d*r] / [L][r*d].
+int ref_forward(int mode, size_t L, size_t d, float* w, size_t num_adapters, const int32_t* ids,
+                const int64_t* ranks, const float* const* downs, const float* const* ups, const float* x,
+                size_t n, const int32_t* assignment, int32_t merged_id, float* out) {
+  try {
+    BaseModel model(L, d, 2);
+    for (size_t l = 0; l < L; ++l) std::memcpy(model.layer(l).data, w + l * d * d, d * d * 4);
+    AdapterSet adapters;
+    for (size_t i = 0; i < num_adapters; ++i) {
+      const size_t r = static_cast<size_t>(ranks[i]);
+      std::vector<Matrix<float>> dn, u;
+      for (size_t l = 0; l < L; ++l) {
+        Matrix<float> dm(d, r), um(r, d);
+        std::memcpy(dm.data(), downs[i] + l * d * r, d * r * 4);
+        std::memcpy(um.data(), ups[i] + l * r * d, r * d * 4);
+        dn.push_back(std::move(dm));
+        u.push_back(std::move(um));
+      }
+      adapters.emplace(ids[i], LoraAdapter(ids[i], L, d, r, std::move(dn), std::move(u)));
+    }
+    TilingTable table;
+    ModelState state;
+    ConstMatSpan<float> xs(x, n, d);
+    std::vector<int> a(assignment ? assignment : nullptr, assignment ? assignment + n : nullptr);
+    Matrix<float> res(1, 1);
+    if (mode == 0) {
+      res = forward_unmerged(model, state, xs, std::span<const int>(a.data(), a.size()), adapters, table);
+    } else if (mode == 1) {
+      state.mode = InferMode::Merged;
+      res = forward_merged(model, state, xs, table);
+    } else {
+      merge(model, state, adapter_at(adapters, merged_id), table);
+      init_delora(state, adapter_at(adapters, merged_id));
+      state.mode = InferMode::Mixture;
+      res = forward_mixture(model, state, xs, std::span<const int>(a.data(), a.size()), adapters, table);
+      for (size_t l = 0; l < L; ++l) std::memcpy(w + l * d * d, model.layer(l).data, d * d * 4);
+    }
+    std::memcpy(out, res.data(), n * d * 4);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
   }
 }
 

@@ -69,6 +69,11 @@ _SIGS = {
     "atmm_merge_apply_layers": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int,
                                         c_float, c_void_p]),
     "atmm_plan_destroy": (None, [c_void_p]),
+    "atmm_forward_create": (c_int, [c_void_p, c_int, c_int64, c_int64, POINTER(c_void_p)]),
+    "atmm_forward_destroy": (None, [c_void_p]),
+    "atmm_forward_run": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                 c_void_p]),
+    "atmm_forward_stats": (c_int, [c_void_p, i64p, c_int64]),
     "atmm_plan_routing": (c_int, [c_void_p, i32p, i64p, i64p, i64p]),
     "atmm_plan_stats": (c_int, [c_void_p, i64p, i64p, i64p]),
     "atmm_plan_describe": (c_int, [c_void_p, ctypes.c_char_p, c_size_t]),

@@ -486,6 +486,80 @@ class MixturePlan:
             self.plan.apply(x, y, layer, scale, stream)
 
 
+class LayerForward:
+    """The serving model's stack forward on device (model.hpp:192-328):
+    cur <- tanh(cur @ W_l + bypass_l(cur)) for every layer, the bypass riding
+    the base GEMM as extra K blocks of the same tensor-core accumulator.
+
+    plan: a BypassPlan (forward_unmerged), a MixturePlan over merged weights
+    (forward_mixture) or None (forward_merged; then n and hidden_dim give
+    the shape).  bf16 activations / weights, fp32 accumulation, bf16 out."""
+
+    STATS = ("n", "d", "bn", "tiles", "grid", "ext_blocks", "shrink_items", "shrink_ks", "sorted", "gemm_stages",
+             "shrink_stages")
+
+    def __init__(self, plan=None, n: Optional[int] = None, hidden_dim: Optional[int] = None, device: int = 0):
+        if isinstance(plan, MixturePlan):
+            n = plan.n if n is None else n
+            if hidden_dim is None and plan.plan is not None:
+                hidden_dim = plan.plan.registry.d_in
+            plan = plan.plan
+        h = ctypes.c_void_p()
+        _check(lib.atmm_forward_create(plan.handle if plan is not None else None, int(device), int(n or 0),
+                                       int(hidden_dim or 0), ctypes.byref(h)))
+        self._h = h
+        self.plan = plan  # keeps the plan (and its registry) alive
+        st = self.stats()
+        self.n, self.d = st["n"], st["d"]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.atmm_forward_destroy(h)
+            self._h = None
+
+    def stats(self) -> dict:
+        v = np.zeros(len(self.STATS), np.int64)
+        _check(lib.atmm_forward_stats(self._h, _p(v, i64p), v.size))
+        return {k: int(x) for k, x in zip(self.STATS, v)}
+
+    def run(self, w, x, out=None, num_layers: Optional[int] = None, stream=None):
+        """w: [L, d, d] bf16 CUDA tensor (rows contiguous); x: [n, d] bf16 CUDA
+        tensor; returns out ([n, d] bf16, allocated when not given)."""
+        import torch
+
+        if w.dim() != 3 or w.dtype != torch.bfloat16 or not w.is_cuda or w.stride(2) != 1:
+            raise ShapeError("w must be an [L, d, d] bfloat16 CUDA tensor with contiguous rows")
+        if x.dim() != 2 or x.dtype != torch.bfloat16 or not x.is_cuda or x.stride(1) != 1:
+            raise ShapeError("x must be an [n, d] bfloat16 CUDA tensor with contiguous rows")
+        if tuple(x.shape) != (self.n, self.d) or tuple(w.shape[1:]) != (self.d, self.d):
+            raise ShapeError(f"x {tuple(x.shape)} / w {tuple(w.shape)} do not match n={self.n}, d={self.d}")
+        if out is None:
+            out = torch.empty((self.n, self.d), dtype=torch.bfloat16, device=x.device)
+        L = w.shape[0] if num_layers is None else int(num_layers)
+        _check(lib.atmm_forward_run(self._h, w.data_ptr(), w.stride(1), w.stride(0), L, x.data_ptr(), x.stride(0),
+                                    out.data_ptr(), out.stride(0), _stream_ptr(stream)))
+        return out
+
+
+def forward_unmerged(w, x, assignment: Sequence[int], registry: AdapterRegistry, table=None):
+    """forward_unmerged (model.hpp:216-246) on device tensors."""
+    return LayerForward(BypassPlan(registry, assignment, table)).run(w, x)
+
+
+def forward_mixture(w_merged, x, assignment: Sequence[int], registry: AdapterRegistry, merged_id: int, table=None):
+    """forward_mixture (model.hpp:251-328): w_merged already holds adapter
+    merged_id (merge_layers_into); guest rows get own - merged bypass."""
+    mp = MixturePlan(registry, assignment, merged_id, table)
+    return LayerForward(mp, n=mp.n, hidden_dim=registry.d_in).run(w_merged, x)
+
+
+def forward_merged(w, x, device: Optional[int] = None):
+    """forward_merged (model.hpp:192-211): no bypass."""
+    dev = x.device.index if device is None else device
+    return LayerForward(None, n=x.shape[0], hidden_dim=x.shape[1], device=dev or 0).run(w, x)
+
+
 def run_bypass_host_bf16_pipelined(plan: "BypassPlan", xs, outs, layers) -> None:
     """run_bypass (batch.hpp:48) end to end from bf16 host buffers (uint16
     numpy views, pinned for overlap): outs[i] = bypass(xs[i]) at layers[i],

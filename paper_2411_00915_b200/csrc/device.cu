@@ -42,6 +42,11 @@ cudaError_t launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t rows, in
                                int64_t lds, int64_t ldd, cudaStream_t stream);
 cudaError_t launch_scale_bf16_2d(uint16_t* base, int64_t rows, int64_t cols, int64_t ld, float f,
                                  cudaStream_t stream);
+cudaError_t launch_fwd_gather(const uint16_t* x, int64_t ldx, uint16_t* dst, int64_t ldd, const int32_t* order,
+                              int64_t n, int64_t d, cudaStream_t stream);
+cudaError_t launch_fwd_shrink(const CUtensorMap& xmap, const FwdParams& p, size_t smem, cudaStream_t stream);
+cudaError_t launch_fwd_gemm(const CUtensorMap& xmap, const CUtensorMap& wmap, const FwdParams& p, int grid, size_t smem,
+                            cudaStream_t stream);
 cudaError_t launch_pack_factors(const float* down, const float* up, int64_t L, int64_t d_in, int64_t d_out,
                                 int64_t r, int64_t d_in_pad, int64_t d_out_pad, int64_t r_pad, uint16_t* down_t,
                                 uint16_t* up_t, cudaStream_t stream);
@@ -500,6 +505,7 @@ struct atmm_plan {
   LaunchGroup merged;
   std::unique_ptr<SplitBufs> merged_bufs;
   DevBuf<int32_t> d_rows;
+  std::vector<int32_t> rows_host;  // routed entry (plan order) -> X / Y row
   DevBuf<TileDesc> d_tiles;
   int64_t total_ctas = 0;
 };
@@ -757,6 +763,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
   }
   plan->d_rows.alloc(rows32.size());
   CUDA_CHECK(cudaMemcpy(plan->d_rows.p, rows32.data(), rows32.size() * 4, cudaMemcpyHostToDevice));
+  plan->rows_host = std::move(rows32);
   plan->d_tiles.alloc(all_tiles.size());
   CUDA_CHECK(cudaMemcpy(plan->d_tiles.p, all_tiles.data(), all_tiles.size() * sizeof(TileDesc),
                         cudaMemcpyHostToDevice));
@@ -1666,3 +1673,262 @@ int atmm_bench_launches(int device, int64_t m, int64_t d_in, int64_t rank, int64
 }
 
 }  // extern "C"
+
+// =========================================================================
+// Layer forward (model.hpp:192-328): cur <- tanh(cur . W_l + bypass_l(cur))
+// over L layers; two launches per layer (forward_kernels.cu).
+// =========================================================================
+struct atmm_forward {
+  atmm_registry* reg = nullptr;  // null: forward_merged (no bypass)
+  uint64_t generation = 0;
+  int device = 0;
+  int64_t n = 0, d = 0;
+  bool sorted = false;  // rows run in plan order (gathered in, scattered out)
+  int32_t row_tiles = 0, bn = 128, ntn = 0, num_tiles = 0, nkb = 0, ks = 1, num_items = 0, num_ext = 0;
+  int32_t stages_g = 0, stages_s = 0, grid = 0;
+  size_t smem_g = 0, smem_s = 0;
+  DevBuf<uint16_t> buf[2];
+  DevBuf<uint8_t> ext;
+  DevBuf<FwdExt> exts;
+  DevBuf<int32_t> ext_begin, order;
+  DevBuf<FwdItem> items;
+  CUtensorMap bmap[2];
+};
+
+namespace atmm {
+namespace {
+// Activations (rows x d bf16, row stride ld): box = 128 rows x one 64-wide K block, 128-byte swizzle.
+CUtensorMap make_act_map(const void* x, int64_t rows, int64_t d, int64_t ld) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[2] = {kBK, kTileM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(activations) failed: " + std::to_string(r));
+  return m;
+}
+// Layer weights W_l (d x d bf16, [k][n], row stride ldw, layer stride w_ls):
+// box = 64 K rows x 64 N columns, 128-byte swizzle = the MN-major B operand.
+CUtensorMap make_layer_w_map(const void* w, int64_t d, int64_t ldw, int64_t L, int64_t w_ls) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(L)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldw) * 2, static_cast<cuuint64_t>(L > 1 ? w_ls : ldw * d) * 2};
+  const cuuint32_t box[3] = {kBK, kBK, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(layer W) failed: " + std::to_string(r));
+  return m;
+}
+void require_aligned16(const void* p, const char* what) {
+  if (reinterpret_cast<uintptr_t>(p) % 16 != 0) fail(ATMM_ERR_SHAPE, std::string(what) + " must be 16-byte aligned");
+}
+}  // namespace
+}  // namespace atmm
+
+int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hidden_dim, atmm_forward** out) {
+  return guarded([&] {
+    if (!out) fail(ATMM_ERR_CONFIG, "null output");
+    auto f = std::make_unique<atmm_forward>();
+    if (plan) {
+      atmm_registry* reg = plan->reg;
+      if (plan->generation != reg->generation) fail(ATMM_ERR_CONFIG, "plan is stale: the registry changed since it was built");
+      if (reg->d_in != reg->d_out) fail(ATMM_ERR_SHAPE, "the layer forward needs square layers (d_in == d_out)");
+      if (hidden_dim > 0 && hidden_dim != reg->d_in) fail(ATMM_ERR_SHAPE, "hidden_dim does not match the registry");
+      if (n > 0 && n != plan->n) fail(ATMM_ERR_SHAPE, "row count does not match the plan");
+      f->reg = reg;
+      f->generation = reg->generation;
+      f->device = reg->device;
+      f->n = plan->n;
+      f->d = reg->d_in;
+    } else {
+      f->device = device;
+      f->n = n;
+      f->d = hidden_dim;
+    }
+    if (f->n < 1 || f->d < 1) fail(ATMM_ERR_SHAPE, "rows and hidden_dim must be >= 1");
+    if (f->d % 8 != 0) fail(ATMM_ERR_SHAPE, "hidden_dim must be a multiple of 8 (16-byte activation rows)");
+    if (f->n > std::numeric_limits<int32_t>::max() / 2) fail(ATMM_ERR_SHAPE, "batch too large");
+    require_device(f->device);
+    DeviceGuard g(f->device);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, f->device);
+    const int64_t n_ = f->n, d = f->d;
+    f->nkb = static_cast<int32_t>((d + kBK - 1) / kBK);
+    f->row_tiles = static_cast<int32_t>((n_ + kTileM - 1) / kTileM);
+    f->bn = int64_t(f->row_tiles) * ((d + 255) / 256) >= sms ? 256 : 128;
+    if (const char* e = std::getenv("ATMM_FWD_BN")) f->bn = std::atoi(e) == 256 ? 256 : 128;
+    f->ntn = static_cast<int32_t>((d + f->bn - 1) / f->bn);
+    f->num_tiles = f->row_tiles * f->ntn;
+    f->grid = std::min(f->num_tiles, sms);
+    const size_t gstage = 16384 + static_cast<size_t>(f->bn) * 128;
+    f->stages_g = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 1024) / gstage));
+    f->smem_g = 1024 + f->stages_g * gstage;
+
+    std::vector<int32_t> order;
+    std::vector<FwdExt> exts;
+    std::vector<int32_t> ext_begin{0};
+    std::vector<FwdItem> items;
+    if (plan && !plan->bp.seg_adapter.empty()) {
+      atmm_registry* reg = plan->reg;
+      f->sorted = true;
+      order = plan->rows_host;
+      std::vector<char> covered(static_cast<size_t>(n_), 0);
+      for (int32_t r : order) covered[static_cast<size_t>(r)] = 1;
+      for (int64_t r = 0; r < n_; ++r)
+        if (!covered[static_cast<size_t>(r)]) order.push_back(static_cast<int32_t>(r));
+      const auto& off = plan->bp.seg_offsets;
+      const size_t S = plan->bp.seg_adapter.size();
+      int64_t a_off = 0;
+      for (int32_t t = 0; t < f->row_tiles; ++t) {
+        const int64_t t0 = int64_t(t) * kTileM, t1 = std::min<int64_t>(t0 + kTileM, n_);
+        const size_t first = exts.size();
+        for (size_t s = 0; s < S; ++s) {
+          const int64_t b = std::max<int64_t>(off[s], t0), e = std::min<int64_t>(off[s + 1], t1);
+          if (e <= b) continue;
+          const Slot& sl = reg->at(plan->bp.seg_adapter[s]);
+          for (int32_t kc = 0; kc * 32 < sl.r_pad; ++kc) {
+            FwdExt x{};
+            x.down_t = sl.down_t;
+            x.up_t = sl.up_t;
+            x.down_ls = reg->d_in_pad * sl.r_pad;
+            x.up_ls = reg->d_out_pad * sl.r_pad;
+            x.a_off = a_off;
+            x.r_pad = static_cast<int32_t>(sl.r_pad);
+            x.kc = kc;
+            x.kk = static_cast<int32_t>(std::min<int64_t>(32, sl.r_pad - 32 * kc));
+            x.lo = static_cast<int32_t>(b - t0);
+            x.hi = static_cast<int32_t>(e - t0);
+            x.scale = sl.scale;
+            a_off += int64_t(x.kk) * 512;  // 128 rows x [mid_hi | mid_lo]
+            exts.push_back(x);
+          }
+        }
+        // shrink items: consecutive chunks of the tile, <= 128 rank columns each
+        for (size_t i = first; i < exts.size();) {
+          FwdItem it{t, static_cast<int32_t>(i), static_cast<int32_t>(i), 0};
+          while (i < exts.size() && it.ncols + exts[i].kk <= 128) {
+            exts[i].col = it.ncols;
+            it.ncols += exts[i].kk;
+            ++i;
+          }
+          it.e_end = static_cast<int32_t>(i);
+          items.push_back(it);
+        }
+        ext_begin.push_back(static_cast<int32_t>(exts.size()));
+      }
+      f->num_ext = static_cast<int32_t>(exts.size());
+      f->num_items = static_cast<int32_t>(items.size());
+      f->ks = 1;
+      while (f->ks < 8 && int64_t(f->num_items) * f->ks * 2 <= sms && f->ks * 2 <= f->nkb) f->ks *= 2;
+      if (const char* e = std::getenv("ATMM_FWD_KS")) f->ks = std::clamp(std::atoi(e), 1, 8);
+      while (f->ks > 1 && f->ks > f->nkb) f->ks /= 2;  // every K slice gets >= 1 K block
+      const size_t red = f->ks > 1 ? size_t(kTileM) * (128 + 4) * 4 : 0;
+      f->stages_s = static_cast<int32_t>(std::min<size_t>(4, (kSmemLimit - 1024 - red) / 32768));
+      f->smem_s = 1024 + f->stages_s * 32768 + red;
+      f->ext.alloc(static_cast<size_t>(a_off));
+      f->exts.alloc(exts.size());
+      f->ext_begin.alloc(ext_begin.size());
+      f->items.alloc(items.size());
+      f->order.alloc(order.size());
+      CUDA_CHECK(cudaMemset(f->ext.p, 0, f->ext.n));
+      CUDA_CHECK(cudaMemcpy(f->exts.p, exts.data(), exts.size() * sizeof(FwdExt), cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(f->ext_begin.p, ext_begin.data(), ext_begin.size() * 4, cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(f->items.p, items.data(), items.size() * sizeof(FwdItem), cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(f->order.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice));
+    }
+    for (int b = 0; b < 2; ++b) {
+      f->buf[b].alloc(static_cast<size_t>(n_ * d));
+      f->bmap[b] = make_act_map(f->buf[b].p, n_, d, d);
+    }
+    *out = f.release();
+  });
+}
+
+void atmm_forward_destroy(atmm_forward* f) {
+  if (!f) return;
+  DeviceGuard g(f->device, std::nothrow);
+  delete f;
+}
+
+int atmm_forward_stats(const atmm_forward* f, int64_t* out, int64_t cap) {
+  return guarded([&] {
+    if (!f || !out) fail(ATMM_ERR_CONFIG, "null forward or output");
+    const int64_t v[] = {f->n, f->d, f->bn, f->num_tiles, f->grid, f->num_ext, f->num_items, f->ks, f->sorted ? 1 : 0,
+                         f->stages_g, f->stages_s};
+    const int64_t k = std::min<int64_t>(cap, static_cast<int64_t>(sizeof(v) / sizeof(v[0])));
+    for (int64_t i = 0; i < k; ++i) out[i] = v[i];
+  });
+}
+
+int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_layer_stride, int64_t num_layers,
+                     const void* x, int64_t ldx, void* out, int64_t ldo, void* stream) {
+  return guarded([&] {
+    if (!f || !w || !x || !out) fail(ATMM_ERR_CONFIG, "null forward, W, X or output");
+    if (f->reg && f->reg->generation != f->generation) {
+      fail(ATMM_ERR_CONFIG, "forward is stale: the registry changed since it was created");
+    }
+    const int64_t d = f->d, n = f->n;
+    if (num_layers < 0) fail(ATMM_ERR_SHAPE, "num_layers must be >= 0");
+    if (f->reg && num_layers > f->reg->L) fail(ATMM_ERR_SHAPE, "more layers than the adapters carry");
+    if (ldw < d || ldw % 8 != 0) fail(ATMM_ERR_SHAPE, "W row stride must be >= hidden_dim and a multiple of 8");
+    if (num_layers > 1 && (w_layer_stride < ldw * d || w_layer_stride % 8 != 0)) {
+      fail(ATMM_ERR_SHAPE, "W layer stride must be >= ldw * hidden_dim and a multiple of 8");
+    }
+    if (ldx < d || ldx % 8 != 0) fail(ATMM_ERR_SHAPE, "X row stride must be >= hidden_dim and a multiple of 8");
+    if (ldo < d || ldo % 8 != 0) fail(ATMM_ERR_SHAPE, "output row stride must be >= hidden_dim and a multiple of 8");
+    require_aligned16(w, "W");
+    require_aligned16(x, "X");
+    require_aligned16(out, "the output");
+    DeviceGuard g(f->device);
+    const auto st = static_cast<cudaStream_t>(stream);
+    if (num_layers == 0) {
+      CUDA_CHECK(cudaMemcpy2DAsync(out, ldo * 2, x, ldx * 2, d * 2, n, cudaMemcpyDeviceToDevice, st));
+      return;
+    }
+    const CUtensorMap wmap = make_layer_w_map(w, d, ldw, num_layers, w_layer_stride);
+    CUtensorMap xm;
+    int cur = -1;  // -1: the caller's X
+    if (f->sorted) {
+      CUDA_CHECK(launch_fwd_gather(static_cast<const uint16_t*>(x), ldx, f->buf[0].p, d, f->order.p, n, d, st));
+      cur = 0;
+      xm = f->bmap[0];
+    } else {
+      xm = make_act_map(x, n, d, ldx);
+    }
+    FwdParams p{};
+    const bool bypass = f->num_ext > 0;
+    p.ext = f->ext.p;
+    p.exts = bypass ? f->exts.p : nullptr;
+    p.ext_begin = f->ext_begin.p;
+    p.items = f->items.p;
+    p.n = n;
+    p.d = d;
+    p.bn = f->bn;
+    p.ntn = f->ntn;
+    p.num_tiles = f->num_tiles;
+    p.nkb = f->nkb;
+    p.ks = f->ks;
+    p.num_items = f->num_items;
+    for (int64_t l = 0; l < num_layers; ++l) {
+      const bool last = l + 1 == num_layers;
+      const int nxt = cur == 0 ? 1 : 0;
+      p.layer = static_cast<int32_t>(l);
+      p.out = last ? static_cast<uint16_t*>(out) : f->buf[nxt].p;
+      p.ldo = last ? ldo : d;
+      p.out_rows = last && f->sorted ? f->order.p : nullptr;
+      if (bypass) {
+        p.stages = f->stages_s;
+        CUDA_CHECK(launch_fwd_shrink(xm, p, f->smem_s, st));
+      }
+      p.stages = f->stages_g;
+      CUDA_CHECK(launch_fwd_gemm(xm, wmap, p, f->grid, f->smem_g, st));
+      cur = nxt;
+      xm = f->bmap[nxt];
+    }
+  });
+}

@@ -177,4 +177,49 @@ struct MergeParams {
   int64_t b_layer_stride;
 };
 
+// ---- layer forward (model.hpp:192-328): tanh(cur . W_l + bypass_l(cur)) ----
+// Rows run in segment-sorted order (plan order, then the rows no segment
+// covers) so a 128-row tile meets few adapters.  The bypass rides the base
+// GEMM as extra K blocks: for every (tile, segment, 32-rank chunk) a
+// "K-extension" block D += mid_chunk . up_chunk^T, where mid_chunk is the
+// 128 x kk bf16 A image (rows outside the segment zero) written by the
+// shrink launch and up_chunk is read straight from the registry.  Chunks
+// are 32 ranks wide so the [hi | lo] A image (128 x 64 bf16) and the up^T
+// slice (bn x 32 bf16) each fit one pipeline stage.
+struct FwdExt {
+  const uint16_t* down_t;  // slot down^T (layer 0), [kb][g][c][8x8]
+  const uint16_t* up_t;    // slot up^T (layer 0),   [g][c][8x8]
+  int64_t down_ls;         // elements per layer
+  int64_t up_ls;
+  int64_t a_off;           // byte offset of the A image in the ext buffer
+  int32_t r_pad;
+  int32_t kc;              // rank chunk: ranks [32 kc, 32 kc + kk)
+  int32_t kk;              // 16 | 32
+  int32_t lo, hi;          // tile-local rows [lo, hi) of the segment
+  int32_t col;             // first TMEM / B-image column in its shrink item
+  float scale;             // slot scale
+  int32_t pad;
+};
+struct FwdItem {           // one shrink work item: a tile's chunks [e_begin, e_end)
+  int32_t tile, e_begin, e_end, ncols;
+};
+struct FwdParams {
+  uint8_t* ext;            // A images
+  const FwdExt* exts;
+  const int32_t* ext_begin;  // [row tiles + 1]
+  const FwdItem* items;
+  const int32_t* out_rows;   // sorted row -> output row (nullptr: identity)
+  uint16_t* out;
+  int64_t ldo;
+  int64_t n, d;
+  int32_t layer;
+  int32_t bn;              // GEMM N tile (128 | 256)
+  int32_t ntn;             // N tiles per row tile
+  int32_t num_tiles;       // row tiles x ntn
+  int32_t nkb;             // K blocks of the base GEMM (ceil(d / 64))
+  int32_t ks;              // shrink K split (cluster size)
+  int32_t num_items;
+  int32_t stages;
+};
+
 }  // namespace atmm

@@ -1,0 +1,492 @@
+// forward_kernels.cu -- the layer forward of the serving model on sm_100a:
+//   cur_{l+1} = tanh(cur_l . W_l + bypass_l(cur_l))        (model.hpp:213-246)
+// (forward_merged, model.hpp:192-211, is the same launch without bypass;
+// forward_mixture, model.hpp:248-328, uses combined mixture slots).
+//
+// Two launches per layer, chained with programmatic dependent launch:
+//   fwd_shrink_kernel  mid = scale * cur . down_a for every (row tile,
+//                      segment, 32-rank chunk), written as the bf16 A image
+//                      of a K-extension block (rows outside the segment 0).
+//                      K split over a thread-block cluster, fixed-order DSMEM
+//                      reduction (bit-identical reruns).
+//   fwd_gemm_kernel    persistent tcgen05 GEMM, 128 x bn tiles, TMA ring of
+//                      64-wide K blocks (X K-major SW128, W MN-major SW128),
+//                      then the tile's K-extension blocks (mid . up^T, up^T
+//                      read straight from the registry) into the SAME TMEM
+//                      accumulator, tanh + bf16 in the epilogue.  Double-
+//                      buffered TMEM so tile i's epilogue overlaps tile i+1's
+//                      MMAs.  The last layer scatters rows back to the
+//                      caller's order.
+// Rows run in segment-sorted order ("Layer forward").
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "device_types.hpp"
+#include "ptx.cuh"
+
+namespace atmm {
+using namespace ptx;
+
+namespace {
+
+constexpr int kFwdThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr uint32_t kFwdA = 16384;  // 128 rows x 64 bf16 (one K block of X)
+constexpr uint32_t kShrinkB = 16384;  // <= 128 rank columns x 64 bf16
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// mid = hi + lo with hi = bf16(mid), lo = bf16(mid - hi): the K-extension
+// carries mid to ~16 mantissa bits (two bf16 MMAs against the same up^T),
+// so rounding mid costs nothing next to the fp32 GEMM accumulation.
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat16 ha = __float2bfloat16_rn(a), hb = __float2bfloat16_rn(b);
+  const __nv_bfloat162 h2(ha, hb);
+  hi = *reinterpret_cast<const uint32_t*>(&h2);
+  lo = pack_bf16x2(a - __bfloat162float(ha), b - __bfloat162float(hb));
+}
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ void st_global_v2(void* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global.v2.b32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// Element offset of (row, col) in a K-extension A image: 128 x kk bf16 in
+// 8x8 core matrices, [row / 8][col / 8][row % 8][col % 8] (K-major,
+// no swizzle: LBO 128 B, SBO kk * 16 B).  The images hold [mid_hi | mid_lo],
+// i.e. kk = 2 x the rank chunk.
+__device__ __forceinline__ int64_t ext_a_index(int row, int col, int kk) {
+  return (static_cast<int64_t>(row >> 3) * (kk >> 3) + (col >> 3)) * 64 + (row & 7) * 8 + (col & 7);
+}
+
+}  // namespace
+
+// -------------------------------------------------------------------------
+// Shrink: one CTA per (K slice, work item); the K slices of an item form a
+// cluster and reduce through DSMEM in rank order.
+// smem: [stages x (A 16 KB | B 16 KB)] [red: 128 x (ncols + 4) fp32]
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    fwd_shrink_kernel(const __grid_constant__ CUtensorMap xmap, const FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = align1024(smem_raw);
+  __shared__ uint64_t full[8], empty[8], done;
+  __shared__ uint32_t tslot;
+  constexpr uint32_t kStage = kFwdA + kShrinkB;
+  const int S = p.stages;
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  const FwdItem item = p.items[blockIdx.y];
+  const int ks = p.ks, kr = static_cast<int>(blockIdx.x);
+  const int kb0 = static_cast<int>(int64_t(p.nkb) * kr / ks);
+  const int kb1 = static_cast<int>(int64_t(p.nkb) * (kr + 1) / ks);
+  const int ncols = item.ncols;
+  const int pitch = ncols + 4;  // fp32 words per red row (16-byte skew)
+  float* red = reinterpret_cast<float*>(sm + S * kStage);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&xmap);
+  }
+  if (warp == 1) tmem_alloc(&tslot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      griddep_wait();  // cur is the previous launch's output
+      griddep_launch_dependents();
+      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+        const int s = i % S;
+        const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* a = sm + s * kStage;
+        uint8_t* b = a + kFwdA;
+        mbar_arrive_expect_tx(&full[s], kFwdA + static_cast<uint32_t>(ncols) * 128u);
+        tma_load_2d(a, &xmap, &full[s], kb * kBK, item.tile * kTileM);
+        for (int e = item.e_begin; e < item.e_end; ++e) {
+          const FwdExt& x = p.exts[e];
+          const uint16_t* src = x.down_t + int64_t(p.layer) * x.down_ls + int64_t(kb) * x.r_pad * kBK + x.kc * 2048;
+          bulk_g2s(b + x.col * 128, src, static_cast<uint32_t>(x.kk) * 128u, &full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t idesc = idesc_bf16(128, static_cast<uint32_t>(ncols));
+      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+        const int s = i % S;
+        const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          mma_bf16(tmem, smem_desc(a + k * 32, 16, 1024, kLayoutSW128), smem_desc(b + k * 256, 128, 1024, kLayoutNone),
+                   idesc, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(&done);
+    }
+    __syncwarp();
+  } else {
+    // Epilogue warps: warp w reads TMEM lanes 32 (w % 4) .. +32 = tile rows.
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    mbar_wait_sleep(&done, 0, 64);
+    tc_fence_after();
+    for (int e = item.e_begin; e < item.e_end; ++e) {
+      const FwdExt x = p.exts[e];
+      const bool valid = row >= x.lo && row < x.hi;
+      for (int cc = 0; cc < x.kk; cc += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(x.col + cc), v);
+        tmem_wait_ld();
+        if (kb1 <= kb0) {  // empty K slice (never planned): a zero partial
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0u;
+        }
+        if (ks == 1) {
+          uint16_t* img = reinterpret_cast<uint16_t*>(p.ext + x.a_off);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float f0 = valid ? __uint_as_float(v[h * 8 + 2 * j]) * x.scale : 0.f;
+              const float f1 = valid ? __uint_as_float(v[h * 8 + 2 * j + 1]) * x.scale : 0.f;
+              split_bf16x2(f0, f1, hi[j], lo[j]);
+            }
+            st_global_v4(img + ext_a_index(row, cc + h * 8, 2 * x.kk), hi[0], hi[1], hi[2], hi[3]);
+            st_global_v4(img + ext_a_index(row, x.kk + cc + h * 8, 2 * x.kk), lo[0], lo[1], lo[2], lo[3]);
+          }
+        } else {
+          const uint32_t dst = smem_u32(red + row * pitch + x.col + cc);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) st_shared_v4(dst + j * 16, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+      }
+    }
+  }
+
+  if (ks > 1) {
+    // Fixed-order cluster reduction: CTA kr finalises rows [kr*rows, +rows).
+    cluster_sync();
+    if (warp >= 2) {
+      const int tid = static_cast<int>(threadIdx.x) - 64;
+      const int rows = kTileM / ks;
+      const int groups = ncols / 4;
+      const uint32_t red_base = smem_u32(red);
+      for (int u = tid; u < rows * groups; u += 128) {
+        const int row = kr * rows + u / groups;
+        const int c = (u % groups) * 4;
+        const uint32_t off = red_base + static_cast<uint32_t>(row * pitch + c) * 4u;
+        float4 acc = ld_cluster_f4(map_cta(off, 0));
+        for (int peer = 1; peer < ks; ++peer) {
+          const float4 v = ld_cluster_f4(map_cta(off, static_cast<uint32_t>(peer)));
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
+        }
+        int e = item.e_begin;
+        while (e + 1 < item.e_end && p.exts[e + 1].col <= c) ++e;
+        const FwdExt& x = p.exts[e];
+        const bool valid = row >= x.lo && row < x.hi;
+        const float s = valid ? x.scale : 0.f;
+        uint16_t* img = reinterpret_cast<uint16_t*>(p.ext + x.a_off);
+        uint32_t hi0, lo0, hi1, lo1;
+        split_bf16x2(acc.x * s, acc.y * s, hi0, lo0);
+        split_bf16x2(acc.z * s, acc.w * s, hi1, lo1);
+        st_global_v2(img + ext_a_index(row, c - x.col, 2 * x.kk), hi0, hi1);
+        st_global_v2(img + ext_a_index(row, x.kk + c - x.col, 2 * x.kk), lo0, lo1);
+      }
+    }
+    cluster_sync();  // peers' red buffers stay alive until every read is done
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
+// -------------------------------------------------------------------------
+// Persistent base GEMM + K-extension bypass + tanh.
+// smem: [stages x (A 16 KB | B bn x 128 B)]
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    fwd_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+                    const FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = align1024(smem_raw);
+  __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2];
+  __shared__ uint32_t tslot;
+  const int S = p.stages, bn = p.bn;
+  const uint32_t kStage = kFwdA + static_cast<uint32_t>(bn) * 128u;
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&xmap);
+    tma_prefetch_desc(&wmap);
+  }
+  if (warp == 1) tmem_alloc(&tslot, static_cast<uint32_t>(2 * bn));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // Without a bypass the previous launch is the previous layer's GEMM,
+      // which releases its dependents before its epilogue is done.  With one,
+      // the shrink launch in between only released this grid after its own
+      // griddep_wait, so cur is complete; the A images are waited for below.
+      bool waited = p.exts == nullptr;
+      if (waited) griddep_wait();
+      int i = 0;
+      for (int tile = static_cast<int>(blockIdx.x); tile < p.num_tiles; tile += static_cast<int>(gridDim.x)) {
+        const int t = tile / p.ntn;
+        const int n0 = (tile % p.ntn) * bn;
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          const int s = i % S;
+          const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* a = sm + s * kStage;
+          uint8_t* b = a + kFwdA;
+          mbar_arrive_expect_tx(&full[s], kStage);
+          tma_load_2d(a, &xmap, &full[s], kb * kBK, t * kTileM);
+          for (int c = 0; c < bn; c += 64) tma_load_3d(b + c * 128, &wmap, &full[s], n0 + c, kb * kBK, p.layer);
+        }
+        if (p.exts == nullptr) continue;
+        for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
+          if (!waited) {
+            griddep_wait();  // the A images are the shrink launch's output
+            waited = true;
+          }
+          const FwdExt& x = p.exts[e];
+          const int s = i % S;
+          const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* a = sm + s * kStage;
+          uint8_t* b = a + kFwdA;
+          const int g_pad = static_cast<int>(x.up_ls / x.r_pad / 8);  // up^T row groups in the registry
+          const int g_n = min(bn / 8, g_pad - n0 / 8);
+          const uint32_t a_bytes = static_cast<uint32_t>(x.kk) * 512u;  // [hi | lo]
+          const uint32_t g_bytes = static_cast<uint32_t>(x.kk) * 16u;
+          mbar_arrive_expect_tx(&full[s], a_bytes + g_bytes * static_cast<uint32_t>(g_n));
+          bulk_g2s(a, p.ext + x.a_off, a_bytes, &full[s]);
+          const uint16_t* ub = x.up_t + int64_t(p.layer) * x.up_ls + int64_t(n0 / 8) * x.r_pad * 8 + x.kc * 256;
+          if (x.kk == x.r_pad) {
+            bulk_g2s(b, ub, g_bytes * static_cast<uint32_t>(g_n), &full[s]);
+          } else {
+            for (int g = 0; g < g_n; ++g) bulk_g2s(b + g * g_bytes, ub + int64_t(g) * x.r_pad * 8, g_bytes, &full[s]);
+          }
+        }
+      }
+      griddep_launch_dependents();
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t idesc_main = idesc_bf16(128, static_cast<uint32_t>(bn), 0, 1);
+      const uint32_t idesc_ext = idesc_bf16(128, static_cast<uint32_t>(bn));
+      int i = 0, it = 0;
+      for (int tile = static_cast<int>(blockIdx.x); tile < p.num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+        const int t = tile / p.ntn;
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          const int s = i % S;
+          mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
+          tc_fence_after();
+          const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            mma_bf16(d, smem_desc(a + k * 32, 16, 1024, kLayoutSW128), smem_desc(b + k * 2048, 8192, 1024, kLayoutSW128),
+                     idesc_main, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+        }
+        if (p.exts != nullptr) {
+          for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
+            const int kk = p.exts[e].kk;
+            const int s = i % S;
+            mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
+            tc_fence_after();
+            const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
+            const uint32_t sbo_a = static_cast<uint32_t>(kk) * 32u, sbo_b = static_cast<uint32_t>(kk) * 16u;
+            for (int k = 0; k < kk / 16; ++k) {
+              const uint64_t bd = smem_desc(b + k * 256, 128, sbo_b, kLayoutNone);
+              mma_bf16(d, smem_desc(a + k * 256, 128, sbo_a, kLayoutNone), bd, idesc_ext, 1u);
+              mma_bf16(d, smem_desc(a + kk * 16 + k * 256, 128, sbo_a, kLayoutNone), bd, idesc_ext, 1u);
+            }
+            mma_commit(&empty[s]);
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = static_cast<int>(blockIdx.x); tile < p.num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+      const int t = tile / p.ntn;
+      const int n0 = (tile % p.ntn) * bn;
+      const int acc = it & 1;
+      const int64_t srow = int64_t(t) * kTileM + q * 32 + lane;
+      const bool rv = srow < p.n;
+      const int64_t orow = rv && p.out_rows ? p.out_rows[srow] : srow;
+      uint16_t* dst = p.out + orow * p.ldo + n0;
+      mbar_wait_sleep(&tfull[acc], static_cast<uint32_t>(it >> 1) & 1u, 32);
+      tc_fence_after();
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * bn);
+      for (int c = 0; c < bn; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+        tmem_wait_ld();
+        uint32_t h[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) h[j] = pack_bf16x2(tanh_fast(__uint_as_float(v[2 * j])), tanh_fast(__uint_as_float(v[2 * j + 1])));
+        if (rv) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (n0 + c + 8 * g < p.d) st_global_v4(dst + c + 8 * g, h[4 * g], h[4 * g + 1], h[4 * g + 2], h[4 * g + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, static_cast<uint32_t>(2 * bn));
+  }
+}
+
+// Row gather into segment-sorted order: dst[i] = x[order[i]] (one warp per row).
+__global__ void fwd_gather_rows_kernel(const uint16_t* __restrict__ x, int64_t ldx, uint16_t* __restrict__ dst,
+                                       int64_t ldd, const int32_t* __restrict__ order, int64_t n, int64_t d) {
+  griddep_wait();
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  for (int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + int64_t(order[r]) * ldx);
+    uint4* out = reinterpret_cast<uint4*>(dst + r * ldd);
+    for (int64_t c = lane; c < d / 8; c += 32) out[c] = src[c];
+  }
+  griddep_launch_dependents();
+}
+
+// ------------------------------------------------------------- launchers --
+namespace {
+template <typename K>
+cudaError_t set_smem(K kernel, size_t smem) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+}
+bool fwd_pdl() {
+  static const bool on = std::getenv("ATMM_NO_PDL") == nullptr;
+  return on;
+}
+}  // namespace
+
+cudaError_t launch_fwd_gather(const uint16_t* x, int64_t ldx, uint16_t* dst, int64_t ldd, const int32_t* order,
+                              int64_t n, int64_t d, cudaStream_t stream) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>((n + 7) / 8, 148 * 8)), 1, 1);
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = fwd_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fwd_gather_rows_kernel, x, ldx, dst, ldd, order, n, d);
+}
+
+cudaError_t launch_fwd_shrink(const CUtensorMap& xmap, const FwdParams& p, size_t smem, cudaStream_t stream) {
+  cudaError_t e = set_smem(fwd_shrink_kernel, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(p.ks);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kFwdThreads, 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(p.ks), static_cast<unsigned>(p.num_items), 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = fwd_pdl() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, fwd_shrink_kernel, xmap, p);
+}
+
+cudaError_t launch_fwd_gemm(const CUtensorMap& xmap, const CUtensorMap& wmap, const FwdParams& p, int grid, size_t smem,
+                            cudaStream_t stream) {
+  cudaError_t e = set_smem(fwd_gemm_kernel, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kFwdThreads, 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = fwd_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fwd_gemm_kernel, xmap, wmap, p);
+}
+
+}  // namespace atmm

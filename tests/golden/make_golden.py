@@ -8,6 +8,7 @@ against reference outputs even where the reference is not mounted.
 
     python tests/golden/make_golden.py
 """
+import ctypes
 import json
 import os
 import sys
@@ -86,6 +87,28 @@ def main():
     ref.merge_rect(wm, down, up, -1)
     out["merge_w_roundtrip"] = wm
 
+
+    # stack forward (model.hpp:192-328): the mode-equivalence setting of
+    # verify.hpp:63-100 -- L = 3, d = 64, rank 16, adapters 1 and 2, 6 rows
+    L, d = 3, 64
+    w = np.zeros((L, d, d), np.float32)
+    ref.L.ref_model_random(L, d, 64, 2024, w.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+    fwd_adapters = {}
+    for a in (1, 2):
+        dn, u = ref.adapter_random(a, L, d, 16, 2024 * 31 + a)
+        fwd_adapters[a] = (dn, u)
+        out[f"fwd_down_{a}"] = dn
+        out[f"fwd_up_{a}"] = u
+    x = ref.fill_uniform(2024 ^ 0xABCD, 6 * d).reshape(6, d)
+    assignment = np.asarray([1, 2, 1, 2, 2, 1], np.int32)
+    out["fwd_w"] = w
+    out["fwd_x"] = x
+    out["fwd_assignment"] = assignment
+    out["fwd_unmerged"], _ = ref.forward(x, w, "unmerged", assignment, fwd_adapters)
+    out["fwd_mixture"], wm = ref.forward(x, w, "mixture", assignment, fwd_adapters, merged_id=1)
+    out["fwd_w_merged"] = wm
+    out["fwd_merged"], _ = ref.forward(x, wm, "merged")
+
     np.savez_compressed(os.path.join(HERE, "reference_vectors.npz"), **out)
 
     # tiling-table lookups (tiling.hpp:181-199) incl. the test_tiling.cpp KATs
@@ -97,8 +120,6 @@ def main():
     queries = [(33, 256, 16), (90, 256, 16), (96, 256, 16), (200, 256, 16), (64, 128, 16), (256, 4096, 32),
                (8192, 4096, 128), (8000, 4096, 128), (1, 256, 16), (160, 256, 16)]
     res = []
-    import ctypes
-
     for (m, k, nn) in queries:
         o = np.zeros(6, np.int32)
         ref.L.ref_table_lookup(keys.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),

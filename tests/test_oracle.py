@@ -219,3 +219,50 @@ def test_run_bypass_live_cfg1_shape(oracle, reference):
     assignment = np.asarray(oracle.seeded_shuffle(oracle.rng(3), np.repeat(np.arange(4), 16)), np.int32)
     ctx = reference.ctx(d, adapters)
     assert np.array_equal(oracle.run_bypass(x, assignment, adapters), ctx.run_bypass(x, assignment))
+
+
+# ------------------------------------------------------- stack forward ---
+
+
+def _fwd_gold_adapters(gold):
+    return {a: (gold[f"fwd_down_{a}"], gold[f"fwd_up_{a}"]) for a in (1, 2)}
+
+
+@pytest.mark.parametrize("mode", ["unmerged", "mixture", "merged"])
+def test_forward_matches_reference_golden(oracle, gold, mode):
+    """orc_forward_f64 restates forward_unmerged / forward_mixture /
+    forward_merged (model.hpp:192-328); pinned to the reference's own outputs
+    in the mode-equivalence setting of verify.hpp:63-100."""
+    ads = _fwd_gold_adapters(gold)
+    w = gold["fwd_w"] if mode == "unmerged" else gold["fwd_w_merged"]
+    got = oracle.forward_f64(gold["fwd_x"], w, mode, gold["fwd_assignment"], ads, merged_id=1, round_act=False)
+    want = gold[f"fwd_{mode}"]
+    assert np.max(np.abs(got - want)) <= 1e-4 * max(1.0, float(np.max(np.abs(want))))
+
+
+def test_forward_mode_equivalence_golden(gold):
+    """verify.hpp:89-100: mixture rows of the merged adapter equal the merged
+    forward, every other row equals the unmerged forward."""
+    a = gold["fwd_assignment"]
+    tol = 1e-4 * max(1.0, float(np.max(np.abs(gold["fwd_unmerged"]))))
+    for row in range(a.size):
+        other = gold["fwd_merged"] if a[row] == 1 else gold["fwd_unmerged"]
+        assert np.max(np.abs(gold["fwd_mixture"][row] - other[row])) <= tol
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_forward_live(oracle, reference, seed):
+    rng = np.random.default_rng(seed)
+    L, d, n = 2, 96, 13
+    w = oracle.model_random(seed, L, d)
+    ads = {}
+    for a, r in {3: 8, 4: 24, 9: 16}.items():
+        ads[a] = oracle.adapter_random(100 * seed + a, L, d, r)
+    x = rng.uniform(-1, 1, (n, d)).astype(np.float32)
+    assignment = rng.choice([3, 4, 9], n).astype(np.int32)
+    want, _ = reference.forward(x, w, "unmerged", assignment, ads)
+    got = oracle.forward_f64(x, w, "unmerged", assignment, ads, round_act=False)
+    assert np.max(np.abs(got - want)) <= 1e-4
+    want, wm = reference.forward(x, w, "mixture", assignment, ads, merged_id=4)
+    got = oracle.forward_f64(x, wm, "mixture", assignment, ads, merged_id=4, round_act=False)
+    assert np.max(np.abs(got - want)) <= 1e-4
