@@ -1685,7 +1685,7 @@ struct atmm_forward {
   int64_t n = 0, d = 0;
   bool sorted = false;  // rows run in plan order (gathered in, scattered out)
   int32_t row_tiles = 0, bn = 128, ntn = 0, num_tiles = 0, nkb = 0, ks = 1, num_items = 0, num_ext = 0;
-  int32_t stages_g = 0, stages_s = 0, grid = 0;
+  int32_t stages_g = 0, stages_s = 0, grid = 0, sbytes = 0;
   size_t smem_g = 0, smem_s = 0;
   DevBuf<uint16_t> buf[2];
   DevBuf<uint8_t> ext;
@@ -1766,7 +1766,7 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
     f->num_tiles = f->row_tiles * f->ntn;
     f->grid = std::min(f->num_tiles, sms);
     const size_t gstage = 16384 + static_cast<size_t>(f->bn) * 128;
-    f->stages_g = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 1024) / gstage));
+    f->stages_g = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage));
     f->smem_g = 1024 + f->stages_g * gstage;
 
     std::vector<int32_t> order;
@@ -1808,10 +1808,11 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
             exts.push_back(x);
           }
         }
-        // shrink items: consecutive chunks of the tile, <= 128 rank columns each
+        // shrink items: consecutive chunks of the tile, <= 64 rank columns each
+        // (keeps >= 4 pipeline stages beside the two reduction buffers)
         for (size_t i = first; i < exts.size();) {
           FwdItem it{t, static_cast<int32_t>(i), static_cast<int32_t>(i), 0};
-          while (i < exts.size() && it.ncols + exts[i].kk <= 128) {
+          while (i < exts.size() && it.ncols + exts[i].kk <= 64) {
             exts[i].col = it.ncols;
             it.ncols += exts[i].kk;
             ++i;
@@ -1827,9 +1828,13 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       while (f->ks < 8 && int64_t(f->num_items) * f->ks * 2 <= sms && f->ks * 2 <= f->nkb) f->ks *= 2;
       if (const char* e = std::getenv("ATMM_FWD_KS")) f->ks = std::clamp(std::atoi(e), 1, 8);
       while (f->ks > 1 && f->ks > f->nkb) f->ks /= 2;  // every K slice gets >= 1 K block
-      const size_t red = f->ks > 1 ? size_t(kTileM) * (128 + 4) * 4 : 0;
-      f->stages_s = static_cast<int32_t>(std::min<size_t>(4, (kSmemLimit - 1024 - red) / 32768));
-      f->smem_s = 1024 + f->stages_s * 32768 + red;
+      int32_t max_cols = 16;
+      for (const FwdItem& it : items) max_cols = std::max(max_cols, it.ncols);
+      f->sbytes = max_cols * 128;
+      const size_t red = f->ks > 1 ? 2 * size_t(kTileM) * (max_cols + 4) * 4 : 0;  // partial + receive slots
+      const size_t sstage = 16384 + static_cast<size_t>(f->sbytes);
+      f->stages_s = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048 - red) / sstage));  // 1 KiB static
+      f->smem_s = 1024 + f->stages_s * sstage + red;
       f->ext.alloc(static_cast<size_t>(a_off));
       f->exts.alloc(exts.size());
       f->ext_begin.alloc(ext_begin.size());
@@ -1914,6 +1919,8 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     p.nkb = f->nkb;
     p.ks = f->ks;
     p.num_items = f->num_items;
+    p.sbytes = f->sbytes;
+    p.trace = g_trace;
     for (int64_t l = 0; l < num_layers; ++l) {
       const bool last = l + 1 == num_layers;
       const int nxt = cur == 0 ? 1 : 0;
@@ -1926,7 +1933,8 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
         CUDA_CHECK(launch_fwd_shrink(xm, p, f->smem_s, st));
       }
       p.stages = f->stages_g;
-      CUDA_CHECK(launch_fwd_gemm(xm, wmap, p, f->grid, f->smem_g, st));
+      static const int only = std::getenv("ATMM_FWD_ONLY") ? std::atoi(std::getenv("ATMM_FWD_ONLY")) : 0;  // A/B: 1 = shrink only
+      if (only != 1) CUDA_CHECK(launch_fwd_gemm(xm, wmap, p, f->grid, f->smem_g, st));
       cur = nxt;
       xm = f->bmap[nxt];
     }

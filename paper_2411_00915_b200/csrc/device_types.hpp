@@ -220,6 +220,9 @@ struct FwdParams {
   int32_t ks;              // shrink K split (cluster size)
   int32_t num_items;
   int32_t stages;
+  int32_t sbytes;            // shrink: B bytes per stage (max item columns x 128)
+  int32_t pad;
+  uint64_t* trace;           // debug: per-CTA %globaltimer events (atmm_debug_set_trace)
 };
 
 }  // namespace atmm

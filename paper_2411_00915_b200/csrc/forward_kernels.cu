@@ -36,7 +36,6 @@ namespace {
 
 constexpr int kFwdThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 constexpr uint32_t kFwdA = 16384;  // 128 rows x 64 bf16 (one K block of X)
-constexpr uint32_t kShrinkB = 16384;  // <= 128 rank columns x 64 bf16
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
@@ -69,8 +68,7 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr)
-               : "memory");
+               : "r"(addr));
   return v;
 }
 
@@ -82,20 +80,32 @@ __device__ __forceinline__ int64_t ext_a_index(int row, int col, int kk) {
   return (static_cast<int64_t>(row >> 3) * (kk >> 3) + (col >> 3)) * 64 + (row & 7) * 8 + (col & 7);
 }
 
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Debug trace: shrink CTAs at [0, 4096) x 16 events, GEMM CTAs after them.
+#define FTRACE(base, ev)                                                                      \
+  do {                                                                                        \
+    if (p.trace) p.trace[(static_cast<size_t>(base) + blockIdx.y * gridDim.x + blockIdx.x) * 16 + (ev)] = gtime(); \
+  } while (0)
+
 }  // namespace
 
 // -------------------------------------------------------------------------
 // Shrink: one CTA per (K slice, work item); the K slices of an item form a
 // cluster and reduce through DSMEM in rank order.
-// smem: [stages x (A 16 KB | B 16 KB)] [red: 128 x (ncols + 4) fp32]
+// smem: [stages x (A 16 KB | B sbytes = max ncols x 128 B)] [red: 128 x (ncols + 4) fp32]
 // -------------------------------------------------------------------------
 __global__ void __launch_bounds__(kFwdThreads, 1)
     fwd_shrink_kernel(const __grid_constant__ CUtensorMap xmap, const FwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  __shared__ uint64_t full[8], empty[8], done;
+  __shared__ uint64_t full[8], empty[8], done, recv_bar;
   __shared__ uint32_t tslot;
-  constexpr uint32_t kStage = kFwdA + kShrinkB;
+  __shared__ FwdExt sx[8];  // the item's chunks (<= 128 columns, >= 16 each)
+  const uint32_t kStage = kFwdA + static_cast<uint32_t>(p.sbytes);
   const int S = p.stages;
   const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   const FwdItem item = p.items[blockIdx.y];
@@ -104,7 +114,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int kb1 = static_cast<int>(int64_t(p.nkb) * (kr + 1) / ks);
   const int ncols = item.ncols;
   const int pitch = ncols + 4;  // fp32 words per red row (16-byte skew)
-  float* red = reinterpret_cast<float*>(sm + S * kStage);
+  float* red = reinterpret_cast<float*>(sm + S * kStage);  // this CTA's partial, 128 x pitch
+  const int rows_per = kTileM / ks;                        // rows each cluster rank finalises
+  const uint32_t slot_bytes = static_cast<uint32_t>(rows_per * pitch) * 4u;
+  float* recv = red + kTileM * pitch;                      // ks slots: the senders' partials of my rows
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -112,33 +125,64 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(&done, 1);
+    mbar_init(&recv_bar, 1);
     fence_mbar_init();
     tma_prefetch_desc(&xmap);
+    if (ks > 1) mbar_arrive_expect_tx(&recv_bar, static_cast<uint32_t>(ks) * slot_bytes);
   }
   if (warp == 1) tmem_alloc(&tslot, 128);
+  const int ne = item.e_end - item.e_begin;
+  if (warp == 2 && lane < ne) sx[lane] = p.exts[item.e_begin + lane];
   tc_fence_before();
-  __syncthreads();
+  if (ks > 1) {
+    cluster_sync();  // every rank's recv_bar is initialised before any partial is pushed
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem = tslot;
 
+  if (threadIdx.x == 0) FTRACE(0, 0);
+  // Release the GEMM launch once the previous grid (which wrote cur) is
+  // complete: the GEMM's main loop reads cur without a wait of its own.
+  griddep_wait();
+  griddep_launch_dependents();
   if (warp == 0) {
     if (elect_one()) {
       griddep_wait();  // cur is the previous launch's output
-      griddep_launch_dependents();
+      FTRACE(0, 1);
+      // per-chunk invariants in registers: source at K block kb0, bytes per K block
+      const uint16_t* src[8];
+      uint32_t dst_off[8], bytes[8], kstep[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (e < ne) {
+          const FwdExt& x = sx[e];
+          src[e] = x.down_t + int64_t(p.layer) * x.down_ls + int64_t(kb0) * x.r_pad * kBK + x.kc * 2048;
+          kstep[e] = static_cast<uint32_t>(x.r_pad) * kBK;
+          dst_off[e] = static_cast<uint32_t>(x.col) * 128u;
+          bytes[e] = static_cast<uint32_t>(x.kk) * 128u;
+        }
+      }
+      const uint32_t tx = kFwdA + static_cast<uint32_t>(ncols) * 128u;
+      const int row0 = item.tile * kTileM;
       for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
         const int s = i % S;
         const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         uint8_t* a = sm + s * kStage;
         uint8_t* b = a + kFwdA;
-        mbar_arrive_expect_tx(&full[s], kFwdA + static_cast<uint32_t>(ncols) * 128u);
-        tma_load_2d(a, &xmap, &full[s], kb * kBK, item.tile * kTileM);
-        for (int e = item.e_begin; e < item.e_end; ++e) {
-          const FwdExt& x = p.exts[e];
-          const uint16_t* src = x.down_t + int64_t(p.layer) * x.down_ls + int64_t(kb) * x.r_pad * kBK + x.kc * 2048;
-          bulk_g2s(b + x.col * 128, src, static_cast<uint32_t>(x.kk) * 128u, &full[s]);
+        mbar_arrive_expect_tx(&full[s], tx);
+        tma_load_2d(a, &xmap, &full[s], kb * kBK, row0);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (e < ne) {
+            bulk_g2s(b + dst_off[e], src[e], bytes[e], &full[s]);
+            src[e] += kstep[e];
+          }
         }
       }
+      FTRACE(0, 2);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -148,6 +192,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int s = i % S;
         const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
         mbar_wait(&full[s], ph);
+        if (i == 0) FTRACE(0, 3);
         tc_fence_after();
         const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
 #pragma unroll
@@ -157,6 +202,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         mma_commit(&empty[s]);
       }
+      FTRACE(0, 4);
       mma_commit(&done);
     }
     __syncwarp();
@@ -165,9 +211,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     mbar_wait_sleep(&done, 0, 64);
+    if (threadIdx.x == 64) FTRACE(0, 5);
     tc_fence_after();
-    for (int e = item.e_begin; e < item.e_end; ++e) {
-      const FwdExt x = p.exts[e];
+    for (int e = 0; e < ne; ++e) {
+      const FwdExt& x = sx[e];
       const bool valid = row >= x.lo && row < x.hi;
       for (int cc = 0; cc < x.kk; cc += 16) {
         uint32_t v[16];
@@ -198,43 +245,70 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
     }
+    if (ks > 1) {
+      // Push rows [q*rows_per, +rows_per) of the partial to rank q's slot kr
+      // (one bulk DSMEM copy per rank), then wait for the ks slots of mine.
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 64) {
+        const uint32_t src0 = smem_u32(red), dst0 = smem_u32(recv) + static_cast<uint32_t>(kr) * slot_bytes;
+        for (int q2 = 0; q2 < ks; ++q2) {
+          bulk_s2cluster(map_cta(dst0, static_cast<uint32_t>(q2)), src0 + static_cast<uint32_t>(q2) * slot_bytes, slot_bytes,
+                         map_cta(smem_u32(&recv_bar), static_cast<uint32_t>(q2)));
+        }
+      }
+      mbar_wait_cluster(&recv_bar, 0);
+    }
   }
 
+  if (threadIdx.x == 64) FTRACE(0, 6);
   if (ks > 1) {
-    // Fixed-order cluster reduction: CTA kr finalises rows [kr*rows, +rows).
-    cluster_sync();
+    // Fixed-order reduction of my rows over the ks received slots; the
+    // cluster barrier (arrive now, wait at exit) keeps every rank's partial
+    // alive until all pushes out of it have landed.
+    cluster_arrive();
+    if (threadIdx.x == 64) FTRACE(0, 7);
     if (warp >= 2) {
       const int tid = static_cast<int>(threadIdx.x) - 64;
-      const int rows = kTileM / ks;
       const int groups = ncols / 4;
-      const uint32_t red_base = smem_u32(red);
-      for (int u = tid; u < rows * groups; u += 128) {
-        const int row = kr * rows + u / groups;
+      const uint32_t recv_base = smem_u32(recv);
+      for (int u = tid; u < rows_per * groups; u += 128) {
+        const int lr = u / groups;
+        const int row = kr * rows_per + lr;
         const int c = (u % groups) * 4;
-        const uint32_t off = red_base + static_cast<uint32_t>(row * pitch + c) * 4u;
-        float4 acc = ld_cluster_f4(map_cta(off, 0));
-        for (int peer = 1; peer < ks; ++peer) {
-          const float4 v = ld_cluster_f4(map_cta(off, static_cast<uint32_t>(peer)));
-          acc.x += v.x;
-          acc.y += v.y;
-          acc.z += v.z;
-          acc.w += v.w;
+        const uint32_t off = recv_base + static_cast<uint32_t>(lr * pitch + c) * 4u;
+        uint4 v[8];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2)
+          if (q2 < ks) v[q2] = ld_shared_v4(off + static_cast<uint32_t>(q2) * slot_bytes);
+        float4 acc = make_float4(__uint_as_float(v[0].x), __uint_as_float(v[0].y), __uint_as_float(v[0].z),
+                                 __uint_as_float(v[0].w));
+#pragma unroll
+        for (int q2 = 1; q2 < 8; ++q2) {
+          if (q2 < ks) {
+            acc.x += __uint_as_float(v[q2].x);
+            acc.y += __uint_as_float(v[q2].y);
+            acc.z += __uint_as_float(v[q2].z);
+            acc.w += __uint_as_float(v[q2].w);
+          }
         }
-        int e = item.e_begin;
-        while (e + 1 < item.e_end && p.exts[e + 1].col <= c) ++e;
-        const FwdExt& x = p.exts[e];
+        int e = 0;
+        while (e + 1 < ne && sx[e + 1].col <= c) ++e;
+        const FwdExt& x = sx[e];
         const bool valid = row >= x.lo && row < x.hi;
-        const float s = valid ? x.scale : 0.f;
+        const float sc = valid ? x.scale : 0.f;
         uint16_t* img = reinterpret_cast<uint16_t*>(p.ext + x.a_off);
         uint32_t hi0, lo0, hi1, lo1;
-        split_bf16x2(acc.x * s, acc.y * s, hi0, lo0);
-        split_bf16x2(acc.z * s, acc.w * s, hi1, lo1);
+        split_bf16x2(acc.x * sc, acc.y * sc, hi0, lo0);
+        split_bf16x2(acc.z * sc, acc.w * sc, hi1, lo1);
         st_global_v2(img + ext_a_index(row, c - x.col, 2 * x.kk), hi0, hi1);
         st_global_v2(img + ext_a_index(row, x.kk + c - x.col, 2 * x.kk), lo0, lo1);
       }
     }
-    cluster_sync();  // peers' red buffers stay alive until every read is done
+    if (threadIdx.x == 64) FTRACE(0, 8);
+    cluster_wait();
   }
+  if (threadIdx.x == 64) FTRACE(0, 9);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -271,6 +345,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tma_prefetch_desc(&xmap);
     tma_prefetch_desc(&wmap);
   }
+  if (threadIdx.x == 0) FTRACE(4096, 0);
+  if (threadIdx.x == 0 && p.trace) p.trace[(4096 + blockIdx.x) * 16 + 14] = clock64();
   if (warp == 1) tmem_alloc(&tslot, static_cast<uint32_t>(2 * bn));
   tc_fence_before();
   __syncthreads();
@@ -303,6 +379,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
           if (!waited) {
             griddep_wait();  // the A images are the shrink launch's output
+            FTRACE(4096, 3);
             waited = true;
           }
           const FwdExt& x = p.exts[e];
@@ -342,6 +419,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int kb = 0; kb < p.nkb; ++kb, ++i) {
           const int s = i % S;
           mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
+          if (it == 0 && kb == 0) FTRACE(4096, 1);
           tc_fence_after();
           const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
 #pragma unroll
@@ -367,6 +445,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             mma_commit(&empty[s]);
           }
         }
+        if (it == 0) FTRACE(4096, 2);
         mma_commit(&tfull[acc]);
       }
     }
@@ -383,6 +462,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int64_t orow = rv && p.out_rows ? p.out_rows[srow] : srow;
       uint16_t* dst = p.out + orow * p.ldo + n0;
       mbar_wait_sleep(&tfull[acc], static_cast<uint32_t>(it >> 1) & 1u, 32);
+      if (it == 0 && threadIdx.x == 64) FTRACE(4096, 4);
       tc_fence_after();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * bn);
       for (int c = 0; c < bn; c += 32) {
@@ -402,8 +482,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (it == 0 && threadIdx.x == 64) FTRACE(4096, 5);
     }
   }
+  if (threadIdx.x == 64) FTRACE(4096, 6);
+  if (threadIdx.x == 64 && p.trace) p.trace[(4096 + blockIdx.x) * 16 + 15] = clock64();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
