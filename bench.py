@@ -51,6 +51,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--soak-s", type=float, default=1.0, help="load before the timed region while clocks are sampled")
     ap.add_argument("--group", type=int, default=3, help="extra measurement: steps per grouped launch (1 = off)")
+    ap.add_argument("--no-forward", action="store_true", help="skip the layer-forward side measurement")
     return ap.parse_args()
 
 
@@ -246,6 +247,81 @@ def impl_reference(args, w):
 
 
 # -------------------------------------------------------- ours (GPU) ------
+def measure_forward(atmm, plan, w, x, stream, reps=10, num_layers=2):
+    """Side measurement (not the headline): the model's layer forward
+    tanh(x W_l + bypass_l(x)) (model.hpp:216-246) on this batch through
+    LayerForward (bypass fused into the base GEMM as extra K blocks), beside
+    the unfused composition cuBLAS x @ W + our bypass kernel + tanh, and
+    cuBLAS alone.  CUDA graph of `reps` forwards, per-layer us."""
+    import torch
+
+    d = w.d_in
+    W = (torch.rand(num_layers, d, d, device=x.device) * 2 - 1).mul_(1.0 / np.sqrt(d)).to(torch.bfloat16)
+    fw = atmm.LayerForward(plan)
+    out = torch.empty_like(x)
+    bufs = [torch.empty_like(x) for _ in range(2)]
+
+    def fused():
+        fw.run(W, x, out, stream=stream)
+
+    def unfused():
+        cur = x
+        for l in range(num_layers):
+            y = bufs[l % 2]
+            torch.mm(cur, W[l], out=y)
+            plan.apply(cur, y, layer=l, stream=stream)
+            torch.tanh_(y)
+            cur = y
+
+    def cublas():
+        cur = x
+        for l in range(num_layers):
+            torch.mm(cur, W[l], out=bufs[l % 2])
+            cur = bufs[l % 2]
+
+    def per_layer_us(fn):
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+            for _ in range(reps):
+                fn()
+        best = float("inf")
+        with torch.cuda.stream(stream):
+            g.replay()
+            torch.cuda.synchronize()
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1) * 1e3 / (reps * num_layers))
+        return best
+
+    t_f, t_u, t_c = per_layer_us(fused), per_layer_us(unfused), per_layer_us(cublas)
+    flops = 2 * w.tokens * d * d + w.flops()
+    peak = measured_bf16_peak()
+    st = fw.stats()
+    return {"us_per_layer": t_f, "tflops": flops / (t_f * 1e-6) / 1e12,
+            "roofline": {"bound": "tensor", "peak": peak, "unit": "TFLOP/s",
+                         "frac": flops / (t_f * 1e-6) / 1e12 / peak if peak else None},
+            "unfused_us_per_layer": t_u, "cublas_mm_only_us_per_layer": t_c,
+            "layers": num_layers, "launches_per_layer": 2, "gemm_tile_n": st["bn"], "shrink_k_split": st["shrink_ks"],
+            "note": "side measurement: tanh(x W + bypass) per layer, fused forward (fwd_shrink + fwd_gemm) vs "
+                    "cuBLAS x@W + bypass kernel + tanh; W bf16 random, not the headline"}
+
+
+def measured_bf16_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f).get("bf16_tflops") or 0) or None
+    return 2250.0
+
+
 def impl_ours_bypass(args, w):
     import torch
 
@@ -345,6 +421,10 @@ def impl_ours_bypass(args, w):
                    "roofline_frac": step_bytes / (gms * 1e-3 / gsteps) / 1e9 / measured_peaks()[0],
                    "note": "same steps, G independent (X, Y, layer) calls per launch; not the headline"}
 
+    layer_fwd = None
+    if not args.no_forward and w.d_in == w.d_out:
+        layer_fwd = measure_forward(atmm, plan, w, xs[0], stream, reps=10)
+
     flops_step = w.flops()
     value = world * flops_step * args.steps / (ms * 1e-3) / 1e12
     ms_per_step = ms / args.steps
@@ -438,6 +518,7 @@ def impl_ours_bypass(args, w):
             "e2e": e2e,
             "e2e_residual": e2e_res,
             "grouped": grouped,
+            "layer_forward": layer_fwd,
             "clocks": clocks,
             "gpu_launches": int(args.steps * launches_per_step),
         }

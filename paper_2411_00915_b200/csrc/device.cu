@@ -1824,8 +1824,13 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       }
       f->num_ext = static_cast<int32_t>(exts.size());
       f->num_items = static_cast<int32_t>(items.size());
+      // K split of the shrink: when the GEMM grid leaves room, keep shrink +
+      // GEMM co-resident (the GEMM's main loop then hides the shrink, which
+      // only gates its final K-extension blocks); otherwise fill the SMs.
       f->ks = 1;
-      while (f->ks < 8 && int64_t(f->num_items) * f->ks * 2 <= sms && f->ks * 2 <= f->nkb) f->ks *= 2;
+      const int64_t room = sms - f->grid;
+      const int64_t cap = room >= f->num_items ? room : sms;
+      while (f->ks < 8 && int64_t(f->num_items) * f->ks * 2 <= cap && f->ks * 2 <= f->nkb) f->ks *= 2;
       if (const char* e = std::getenv("ATMM_FWD_KS")) f->ks = std::clamp(std::atoi(e), 1, 8);
       while (f->ks > 1 && f->ks > f->nkb) f->ks /= 2;  // every K slice gets >= 1 K block
       int32_t max_cols = 16;
