@@ -273,8 +273,49 @@ class MixturePlan {
                             static_cast<int64_t>(ldy), y_dtype, scale, stream));
   }
 
+  const atmm_plan* handle() const { return plan_; }  // null: every row is the merged adapter's
+
  private:
   atmm_plan* plan_ = nullptr;
+};
+
+// --------------------------------------------------------- layer forward --
+// forward_unmerged / forward_mixture / forward_merged (model.hpp:192-328) on
+// device buffers: cur <- tanh(cur . W_l + bypass_l(cur)) over num_layers.
+// W: num_layers x [d][d] bf16 (row stride ldw, layer stride w_layer_stride);
+// x / out: n x d bf16.  The bypass runs as extra K blocks of the base GEMM.
+class LayerForward {
+ public:
+  // forward_unmerged: every row's own adapter.
+  LayerForward(AdapterRegistry& reg, const std::vector<int>& assignment) {
+    std::vector<int32_t> a(assignment.begin(), assignment.end());
+    check(atmm_plan_create(reg.handle(), a.data(), static_cast<int64_t>(a.size()), nullptr, &plan_));
+    check(atmm_forward_create(plan_, 0, 0, 0, &f_));
+  }
+  // forward_mixture over merged weights (the plan's registry must outlive this).
+  LayerForward(const MixturePlan& mp, int device, std::size_t n, std::size_t hidden_dim) {
+    check(atmm_forward_create(mp.handle(), device, static_cast<int64_t>(n), static_cast<int64_t>(hidden_dim), &f_));
+  }
+  // forward_merged: no bypass.
+  LayerForward(int device, std::size_t n, std::size_t hidden_dim) {
+    check(atmm_forward_create(nullptr, device, static_cast<int64_t>(n), static_cast<int64_t>(hidden_dim), &f_));
+  }
+  ~LayerForward() {
+    atmm_forward_destroy(f_);
+    atmm_plan_destroy(plan_);
+  }
+  LayerForward(const LayerForward&) = delete;
+  LayerForward& operator=(const LayerForward&) = delete;
+  void run(const void* w, std::size_t ldw, std::size_t w_layer_stride, std::size_t num_layers, const void* x,
+           std::size_t ldx, void* out, std::size_t ldo, void* stream = nullptr) {
+    check(atmm_forward_run(f_, w, static_cast<int64_t>(ldw), static_cast<int64_t>(w_layer_stride),
+                           static_cast<int64_t>(num_layers), x, static_cast<int64_t>(ldx), out,
+                           static_cast<int64_t>(ldo), stream));
+  }
+
+ private:
+  atmm_plan* plan_ = nullptr;
+  atmm_forward* f_ = nullptr;
 };
 
 // ------------------------------------------------------------- fixtures --

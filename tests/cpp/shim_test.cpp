@@ -204,6 +204,28 @@ static void gpu_checks() {
     }
   }
   CHECK(mworst <= 1e-2 * mscale);
+  // LayerForward (model.hpp:216-246) with W = 0: out = tanh(own bypass)
+  void *wd = nullptr, *od = nullptr;
+  CHECK(cudaMalloc(&wd, d * d * 2) == cudaSuccess);
+  CHECK(cudaMalloc(&od, n * d * 2) == cudaSuccess);
+  CHECK(cudaMemset(wd, 0, d * d * 2) == cudaSuccess);
+  {
+    LayerForward fw(r2, std::vector<int>(n, 1));
+    fw.run(wd, d, d * d, 1, xd, d, od, d);
+    std::vector<uint16_t> ob(n * d);
+    CHECK(cudaMemcpy(ob.data(), od, n * d * 2, cudaMemcpyDeviceToHost) == cudaSuccess);
+    double fworst = 0;
+    for (std::size_t i = 0; i < n * d; ++i) {
+      const uint32_t bits = static_cast<uint32_t>(ob[i]) << 16;
+      float got;
+      std::memcpy(&got, &bits, 4);
+      fworst = std::max(fworst, std::fabs(double(got) - std::tanh(double(own[i]))));
+    }
+    CHECK(fworst <= 2e-2);  // bf16 output + bf16-rounded mid in run_bypass
+    CHECK_THROWS_AS(fw.run(wd, d, d * d, 2, xd, d, od, d), ShapeError);  // the adapters carry one layer
+  }
+  cudaFree(wd);
+  cudaFree(od);
   cudaFree(xd);
   cudaFree(yd);
 }

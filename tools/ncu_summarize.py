@@ -55,6 +55,28 @@ def raw(rep):
     return d
 
 
+def raw_rows(rep):
+    """Per-launch metric rows of a report (the forward's shrink and GEMM separately)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return []
+    hdr, units = rows[0], rows[1]
+    res = []
+    for vals in rows[2:]:
+        d = {}
+        for h, u, v in zip(hdr, units, vals):
+            if h == "Kernel Name":
+                d["kernel"] = (v.split("(")[0].replace("void ", "")[:40], "")
+            if h in METRICS:
+                try:
+                    d[METRICS[h]] = (float(v.replace(",", "")), u)
+                except ValueError:
+                    pass
+        res.append(d)
+    return res
+
+
 def to_bytes(v, u):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6}.get(u, 1)
     return v * scale
@@ -96,6 +118,30 @@ def main():
                   f"{entry.get('dram_pct', float('nan')):.1f} | {entry.get('tensor_pct', float('nan')):.2f} | "
                   f"{entry.get('registers', '')} | {entry.get('smem_dynamic', 0) / 1024:.0f} | {entry.get('grid', '')} | "
                   f"{entry.get('cluster', '')} |")
+    # layer forward: one full capture of the shrink and the GEMM per config
+    fwd_rows = []
+    for cfg in ("cfg2", "cfg5"):
+        rep = os.path.join(src, f"prof_fwd_{cfg}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        for d in raw_rows(rep):
+            if "duration" not in d:
+                continue
+            e = {"kernel": d["kernel"][0], "duration_us": to_us(*d["duration"]),
+                 "dram_read_bytes": to_bytes(*d["dram_read"]), "dram_write_bytes": to_bytes(*d["dram_write"])}
+            for k in ("dram_pct", "tensor_pct", "sm_pct", "registers", "grid", "cluster"):
+                if k in d:
+                    e[k] = d[k][0]
+            if "l2_bytes" in d:
+                e["l2_bytes"] = to_bytes(*d["l2_bytes"])
+            summary.setdefault(f"forward_{cfg}", []).append(e)
+            fwd_rows.append(f"| {cfg} | {e['kernel']} | {e['duration_us']:.1f} | {e['dram_read_bytes'] / 1e6:.1f} | "
+                            f"{e['dram_write_bytes'] / 1e6:.1f} | {e.get('l2_bytes', 0) / 1e6:.0f} | "
+                            f"{e.get('tensor_pct', float('nan')):.1f} | {e.get('grid', '')} | {e.get('cluster', '')} |")
+    if fwd_rows:
+        md += ["", "## Layer forward (tools/fwd_bench.py, one layer): one capture per kernel", "",
+               "| config | kernel | duration us | DRAM read MB | DRAM write MB | L2 MB | tensor % | grid | cluster |",
+               "|---|---|---|---|---|---|---|---|---|"] + fwd_rows
     # launch list of the bench command
     lpath = os.path.join(src, "launches_bench.csv")
     if os.path.exists(lpath):
