@@ -47,6 +47,9 @@ cudaError_t launch_fwd_gather(const uint16_t* x, int64_t ldx, uint16_t* dst, int
 cudaError_t launch_fwd_shrink(const CUtensorMap& xmap, const FwdParams& p, size_t smem, cudaStream_t stream);
 cudaError_t launch_fwd_gemm(const CUtensorMap& xmap, const CUtensorMap& wmap, const FwdParams& p, int grid, size_t smem,
                             cudaStream_t stream);
+cudaError_t launch_fwd_gemm_pair(const CUtensorMap& xmap, const CUtensorMap& wmap, const CUtensorMap& amap,
+                                 const FwdParams& p, int grid, size_t smem, cudaStream_t stream);
+int fwd_gemm_pair_max_clusters(size_t smem);
 cudaError_t launch_pack_factors(const float* down, const float* up, int64_t L, int64_t d_in, int64_t d_out,
                                 int64_t r, int64_t d_in_pad, int64_t d_out_pad, int64_t r_pad, uint16_t* down_t,
                                 uint16_t* up_t, cudaStream_t stream);
@@ -1686,6 +1689,11 @@ struct atmm_forward {
   bool sorted = false;  // rows run in plan order (gathered in, scattered out)
   int32_t row_tiles = 0, bn = 128, ntn = 0, num_tiles = 0, nkb = 0, ks = 1, num_items = 0, num_ext = 0;
   int32_t stages_g = 0, stages_s = 0, grid = 0, sbytes = 0;
+  bool pair = false;  // GEMM as 2-SM CTA pairs (fwd_gemm_pair_kernel)
+  int64_t zero_off = 0;
+  CUtensorMap amap;            // pair GEMM: the A images, 16 KB slots
+  DevBuf<CUtensorMap> umaps;   // pair GEMM: per-slot up^T maps
+  DevBuf<int32_t> pext, pext_begin;
   size_t smem_g = 0, smem_s = 0;
   DevBuf<uint16_t> buf[2];
   DevBuf<uint8_t> ext;
@@ -1760,19 +1768,39 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
     const int64_t n_ = f->n, d = f->d;
     f->nkb = static_cast<int32_t>((d + kBK - 1) / kBK);
     f->row_tiles = static_cast<int32_t>((n_ + kTileM - 1) / kTileM);
-    f->bn = int64_t(f->row_tiles) * ((d + 255) / 256) >= sms ? 256 : 128;
+    // 2-SM CTA pairs (cta_group::2, M = 256) whenever there are two row tiles:
+    // each SM then stages half of every W block (ATMM_FWD_PAIR=0: 1-SM tiles).
+    // With a bypass, pairs pay for the union of two row tiles' extension
+    // chunks; they are taken when the GEMM is large enough to amortise it
+    // (measured: cfg5-sized batches win, cfg2/cfg3-sized ones lose).
+    const bool bypass_plan = plan && !plan->bp.seg_adapter.empty();
+    const int64_t pair_tiles = int64_t((f->row_tiles + 1) / 2) * ((d + 255) / 256);
+    f->pair = f->row_tiles >= 2 && (!bypass_plan || pair_tiles >= 2 * sms);
+    if (const char* e = std::getenv("ATMM_FWD_PAIR")) f->pair = f->row_tiles >= 2 && std::atoi(e) != 0;
+    const int64_t mtiles = f->pair ? (f->row_tiles + 1) / 2 : f->row_tiles;
+    const int64_t units = f->pair ? sms / 2 : sms;
+    f->bn = mtiles * ((d + 255) / 256) >= units ? 256 : 128;
     if (const char* e = std::getenv("ATMM_FWD_BN")) f->bn = std::atoi(e) == 256 ? 256 : 128;
     f->ntn = static_cast<int32_t>((d + f->bn - 1) / f->bn);
-    f->num_tiles = f->row_tiles * f->ntn;
-    f->grid = std::min(f->num_tiles, sms);
-    const size_t gstage = 16384 + static_cast<size_t>(f->bn) * 128;
+    f->num_tiles = static_cast<int32_t>(mtiles) * f->ntn;
+    const size_t gstage = 16384 + static_cast<size_t>(f->pair ? f->bn / 2 : f->bn) * 128;
     f->stages_g = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage));
     f->smem_g = 1024 + f->stages_g * gstage;
+    if (f->pair) {
+      int clusters = fwd_gemm_pair_max_clusters(f->smem_g);
+      if (clusters <= 0) clusters = sms / 2;
+      f->grid = std::min(f->num_tiles, clusters) * 2;
+    } else {
+      f->grid = std::min(f->num_tiles, sms);
+    }
 
     std::vector<int32_t> order;
     std::vector<FwdExt> exts;
     std::vector<int32_t> ext_begin{0};
     std::vector<FwdItem> items;
+    std::vector<int64_t> ext_key;  // (segment, chunk) of each ext, for the pair unions
+    std::map<const uint16_t*, int32_t> umap_of;
+    std::vector<const Slot*> umap_slots;
     if (plan && !plan->bp.seg_adapter.empty()) {
       atmm_registry* reg = plan->reg;
       f->sorted = true;
@@ -1804,8 +1832,15 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
             x.lo = static_cast<int32_t>(b - t0);
             x.hi = static_cast<int32_t>(e - t0);
             x.scale = sl.scale;
-            a_off += int64_t(x.kk) * 512;  // 128 rows x [mid_hi | mid_lo]
+            a_off += 16384;  // one 16 KB slot per image: 128 rows x [mid_hi | mid_lo] (<= 64 columns)
+            auto um = umap_of.find(sl.up_t);
+            if (um == umap_of.end()) {
+              um = umap_of.emplace(sl.up_t, static_cast<int32_t>(umap_slots.size())).first;
+              umap_slots.push_back(&sl);
+            }
+            x.umap = um->second;
             exts.push_back(x);
+            ext_key.push_back(int64_t(s) * 16 + kc);
           }
         }
         // shrink items: consecutive chunks of the tile, <= 64 rank columns each
@@ -1840,7 +1875,58 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       const size_t sstage = 16384 + static_cast<size_t>(f->sbytes);
       f->stages_s = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048 - red) / sstage));  // 1 KiB static
       f->smem_s = 1024 + f->stages_s * sstage + red;
+      if (f->pair) {  // per pair: the union of both row tiles' chunks, in (segment, chunk) order
+        std::vector<int32_t> pe, pb{0};
+        for (int32_t pi = 0; pi < (f->row_tiles + 1) / 2; ++pi) {
+          const int32_t t0 = 2 * pi, t1 = 2 * pi + 1;
+          int32_t i0 = ext_begin[static_cast<size_t>(t0)], e0 = ext_begin[static_cast<size_t>(t0) + 1];
+          int32_t i1 = t1 < f->row_tiles ? ext_begin[static_cast<size_t>(t1)] : 0;
+          const int32_t e1 = t1 < f->row_tiles ? ext_begin[static_cast<size_t>(t1) + 1] : 0;
+          while (i0 < e0 || i1 < e1) {
+            const int64_t k0 = i0 < e0 ? ext_key[static_cast<size_t>(i0)] : INT64_MAX;
+            const int64_t k1 = i1 < e1 ? ext_key[static_cast<size_t>(i1)] : INT64_MAX;
+            pe.push_back(k0 <= k1 ? i0 : -1);
+            pe.push_back(k1 <= k0 ? i1 : -1);
+            if (k0 <= k1) ++i0;
+            if (k1 <= k0) ++i1;
+          }
+          pb.push_back(static_cast<int32_t>(pe.size() / 2));
+        }
+        f->pext.alloc(std::max<size_t>(pe.size(), 2));
+        f->pext_begin.alloc(pb.size());
+        if (!pe.empty()) CUDA_CHECK(cudaMemcpy(f->pext.p, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice));
+        CUDA_CHECK(cudaMemcpy(f->pext_begin.p, pb.data(), pb.size() * 4, cudaMemcpyHostToDevice));
+      }
+      f->zero_off = a_off;
+      a_off += 16384;  // a zero A image for pair members without rows in a chunk
       f->ext.alloc(static_cast<size_t>(a_off));
+      if (f->pair) {
+        const int64_t images = a_off / 16384;
+        const cuuint64_t adims[2] = {64, static_cast<cuuint64_t>(images * kTileM)};
+        const cuuint64_t astr[1] = {128};
+        const cuuint32_t abox[2] = {64, static_cast<cuuint32_t>(kTileM)};
+        const cuuint32_t ones[3] = {1, 1, 1};
+        CUresult r = encode_fn()(&f->amap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, f->ext.p, adims, astr, abox, ones,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(A images) failed: " + std::to_string(r));
+        std::vector<CUtensorMap> um(umap_slots.size());
+        const int64_t hb = f->bn / 2;
+        for (size_t i = 0; i < umap_slots.size(); ++i) {
+          const Slot& sl = *umap_slots[i];
+          const cuuint64_t udims[3] = {64, static_cast<cuuint64_t>(sl.r_pad / 8),
+                                       static_cast<cuuint64_t>(reg->L * reg->d_out_pad / 8)};
+          const cuuint64_t ustr[2] = {128, static_cast<cuuint64_t>(sl.r_pad) * 16};
+          const cuuint32_t ubox[3] = {64, static_cast<cuuint32_t>(std::min<int64_t>(4, sl.r_pad / 8)),
+                                      static_cast<cuuint32_t>(hb / 8)};
+          r = encode_fn()(&um[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, sl.up_t, udims, ustr, ubox, ones,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(up^T) failed: " + std::to_string(r));
+        }
+        f->umaps.alloc(std::max<size_t>(um.size(), 1));
+        if (!um.empty()) CUDA_CHECK(cudaMemcpy(f->umaps.p, um.data(), um.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+      }
       f->exts.alloc(exts.size());
       f->ext_begin.alloc(ext_begin.size());
       f->items.alloc(items.size());
@@ -1869,7 +1955,7 @@ int atmm_forward_stats(const atmm_forward* f, int64_t* out, int64_t cap) {
   return guarded([&] {
     if (!f || !out) fail(ATMM_ERR_CONFIG, "null forward or output");
     const int64_t v[] = {f->n, f->d, f->bn, f->num_tiles, f->grid, f->num_ext, f->num_items, f->ks, f->sorted ? 1 : 0,
-                         f->stages_g, f->stages_s};
+                         f->stages_g, f->stages_s, f->pair ? 2 : 1};
     const int64_t k = std::min<int64_t>(cap, static_cast<int64_t>(sizeof(v) / sizeof(v[0])));
     for (int64_t i = 0; i < k; ++i) out[i] = v[i];
   });
@@ -1925,6 +2011,13 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     p.ks = f->ks;
     p.num_items = f->num_items;
     p.sbytes = f->sbytes;
+    p.pair = f->pair ? 1 : 0;
+    p.dbg = std::getenv("ATMM_FWD_DBG") ? std::atoi(std::getenv("ATMM_FWD_DBG")) : 0;
+    p.pext = f->pext.p;
+    p.pext_begin = f->pext_begin.p;
+    p.zero_a = f->ext.p ? f->ext.p + f->zero_off : nullptr;
+    p.umaps = f->umaps.p;
+    p.zero_img = static_cast<int32_t>(f->zero_off / 16384);
     p.trace = g_trace;
     for (int64_t l = 0; l < num_layers; ++l) {
       const bool last = l + 1 == num_layers;
@@ -1939,7 +2032,13 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
       }
       p.stages = f->stages_g;
       static const int only = std::getenv("ATMM_FWD_ONLY") ? std::atoi(std::getenv("ATMM_FWD_ONLY")) : 0;  // A/B: 1 = shrink only
-      if (only != 1) CUDA_CHECK(launch_fwd_gemm(xm, wmap, p, f->grid, f->smem_g, st));
+      if (only != 1) {
+        if (f->pair) {
+          CUDA_CHECK(launch_fwd_gemm_pair(xm, wmap, f->amap, p, f->grid, f->smem_g, st));
+        } else {
+          CUDA_CHECK(launch_fwd_gemm(xm, wmap, p, f->grid, f->smem_g, st));
+        }
+      }
       cur = nxt;
       xm = f->bmap[nxt];
     }

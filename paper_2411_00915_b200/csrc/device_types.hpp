@@ -198,7 +198,7 @@ struct FwdExt {
   int32_t lo, hi;          // tile-local rows [lo, hi) of the segment
   int32_t col;             // first TMEM / B-image column in its shrink item
   float scale;             // slot scale
-  int32_t pad;
+  int32_t umap;            // pair GEMM: index of the slot's up^T tensor map
 };
 struct FwdItem {           // one shrink work item: a tile's chunks [e_begin, e_end)
   int32_t tile, e_begin, e_end, ncols;
@@ -221,7 +221,16 @@ struct FwdParams {
   int32_t num_items;
   int32_t stages;
   int32_t sbytes;            // shrink: B bytes per stage (max item columns x 128)
-  int32_t pad;
+  int32_t pair;              // 1: fwd_gemm_pair_kernel (2-SM cta_group::2 tiles of 256 rows)
+  // pair mode: the union of the two row tiles' K-extension chunks, per pair:
+  // entries [pext_begin[pi], pext_begin[pi+1]) of pext = {ext index for rank 0,
+  // ext index for rank 1} (-1: that row tile has no rows in the chunk -> zero image)
+  const int32_t* pext;
+  const int32_t* pext_begin;
+  const uint8_t* zero_a;     // 16 KB of zeros
+  const CUtensorMap* umaps;  // pair GEMM: per-slot up^T maps {64, r_pad/8, L * d_out_pad/8}, box {64, 4, bn/16}
+  int32_t zero_img;          // pair GEMM: index of the zero A image (A images are 16 KB slots)
+  int32_t dbg;               // A/B switches (ATMM_FWD_DBG)
   uint64_t* trace;           // debug: per-CTA %globaltimer events (atmm_debug_set_trace)
 };
 

@@ -573,3 +573,239 @@ cudaError_t launch_fwd_gemm(const CUtensorMap& xmap, const CUtensorMap& wmap, co
 }
 
 }  // namespace atmm
+
+namespace atmm {
+using namespace ptx;
+
+// -------------------------------------------------------------------------
+// CTA-pair GEMM (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x bn tile (rank r owns row tile 2 pi + r); the leader issues
+// tcgen05.mma with M = 256, each SM stages its 128 rows of X and HALF of the
+// W columns, so per-SM operand traffic per MMA cycle halves against the
+// 1-SM kernel.  The pair runs the union of its two row tiles' K-extension
+// chunks (a row tile without rows in a chunk streams a zero A image).
+// smem per CTA: [stages x (A 16 KB | B bn/2 x 128 B)]
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    fwd_gemm_pair_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+                         const __grid_constant__ CUtensorMap amap, const FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = align1024(smem_raw);
+  __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2];
+  __shared__ uint32_t tslot;
+  const int S = p.stages, bn = p.bn, hb = p.bn / 2;
+  const uint32_t kStage = kFwdA + static_cast<uint32_t>(hb) * 128u;
+  const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  const int rank = static_cast<int>(cluster_ctarank());
+  const bool leader = rank == 0;
+  const int pair_id = static_cast<int>(blockIdx.x) / 2, npairs = static_cast<int>(gridDim.x) / 2;
+  const int row_tiles = static_cast<int>((p.n + kTileM - 1) / kTileM);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);   // the leader's expect_tx arrive; both CTAs' bytes count as tx
+      mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast to both)
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&xmap);
+    tma_prefetch_desc(&wmap);
+  }
+  if (warp == 1) tmem_alloc_cg2(&tslot, static_cast<uint32_t>(2 * bn));
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      bool waited = p.exts == nullptr;
+      if (waited) griddep_wait();
+      const uint32_t lead_full0 = map_cta(smem_u32(&full[0]), 0);
+      int i = 0;
+      for (int g = pair_id; g < p.num_tiles; g += npairs) {
+        const int pi = g / p.ntn;
+        const int t = 2 * pi + rank;
+        const int n0 = (g % p.ntn) * bn;
+        const int nh = n0 + rank * hb;  // this CTA's half of the N tile
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          const int s = i % S;
+          mbar_wait(&empty[s], (static_cast<uint32_t>(i / S) & 1u) ^ 1u);
+          uint8_t* a = sm + s * kStage;
+          uint8_t* b = a + kFwdA;
+          const uint32_t lf = lead_full0 + static_cast<uint32_t>(s) * 8u;
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * kStage);
+          tma_load_2d_cg2(a, &xmap, lf, kb * kBK, t * kTileM);
+          for (int c = 0; c < hb; c += 64) tma_load_3d_cg2(b + c * 128, &wmap, lf, nh + c, kb * kBK, p.layer);
+        }
+        if (p.exts == nullptr) continue;
+        for (int e = p.pext_begin[pi]; e < p.pext_begin[pi + 1]; ++e, ++i) {
+          if (!waited) {
+            griddep_wait();  // the A images are the shrink launch's output
+            waited = true;
+          }
+          // Both CTAs: their own A image (or the zero image) and their half of
+          // the up^T chunk, by TMA onto the leader's barrier.
+          const int mine = p.pext[2 * e + rank];
+          const FwdExt& x = p.exts[p.pext[2 * e] >= 0 ? p.pext[2 * e] : p.pext[2 * e + 1]];
+          const int s = i % S;
+          mbar_wait(&empty[s], (static_cast<uint32_t>(i / S) & 1u) ^ 1u);
+          uint8_t* a = sm + s * kStage;
+          uint8_t* b = a + kFwdA;
+          const uint32_t lf = lead_full0 + static_cast<uint32_t>(s) * 8u;
+          const uint32_t boxc = static_cast<uint32_t>(min(4, x.r_pad / 8));  // up^T core-matrix columns per row group
+          if (leader) mbar_arrive_expect_tx(&full[s], 2u * (kFwdA + static_cast<uint32_t>(hb / 8) * boxc * 128u));
+          const int img = mine >= 0 ? static_cast<int>(p.exts[mine].a_off >> 14) : p.zero_img;
+          tma_load_2d_cg2(a, &amap, lf, 0, img * kTileM);
+          const int g_pad = static_cast<int>(x.up_ls / x.r_pad / 8);
+          tma_load_3d_cg2(b, p.umaps + x.umap, lf, 0, 4 * x.kc, p.layer * g_pad + nh / 8);
+        }
+        (void)row_tiles;
+      }
+      griddep_launch_dependents();
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader && elect_one()) {
+      const uint32_t idesc_main = idesc_bf16(256, static_cast<uint32_t>(bn), 0, 1);
+      const uint32_t idesc_ext = idesc_bf16(256, static_cast<uint32_t>(bn));
+      int i = 0, it = 0;
+      for (int g = pair_id; g < p.num_tiles; g += npairs, ++it) {
+        const int pi = g / p.ntn;
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
+        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+          const int s = i % S;
+          if (p.dbg & 1) mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
+          else mbar_wait_cluster(&full[s], static_cast<uint32_t>(i / S) & 1u);
+          tc_fence_after();
+          const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            mma_bf16_cg2(d, smem_desc(a + k * 32, 16, 1024, kLayoutSW128), smem_desc(b + k * 2048, 8192, 1024, kLayoutSW128),
+                         idesc_main, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit_cg2(&empty[s], 3);
+        }
+        if (p.exts != nullptr) {
+          for (int e = p.pext_begin[pi]; e < p.pext_begin[pi + 1]; ++e, ++i) {
+            const int e0 = p.pext[2 * e] >= 0 ? p.pext[2 * e] : p.pext[2 * e + 1];
+            const int kk = p.exts[e0].kk;
+            const int s = i % S;
+            mbar_wait_cluster(&full[s], static_cast<uint32_t>(i / S) & 1u);
+            tc_fence_after();
+            const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
+            // A image: 2 kk columns [hi | lo] (SBO 2 kk x 16 B); up^T: 4 core-matrix columns per row group
+            const uint32_t sbo_a = static_cast<uint32_t>(kk) * 32u;
+            const uint32_t sbo_b = static_cast<uint32_t>(min(4, p.exts[e0].r_pad / 8)) * 128u;
+            for (int k = 0; k < kk / 16; ++k) {
+              const uint64_t bd = smem_desc(b + k * 256, 128, sbo_b, kLayoutNone);
+              mma_bf16_cg2(d, smem_desc(a + k * 256, 128, sbo_a, kLayoutNone), bd, idesc_ext, 1u);
+              mma_bf16_cg2(d, smem_desc(a + kk * 16 + k * 256, 128, sbo_a, kLayoutNone), bd, idesc_ext, 1u);
+            }
+            mma_commit_cg2(&empty[s], 3);
+          }
+        }
+        mma_commit_cg2(&tfull[acc], 3);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    int it = 0;
+    for (int g = pair_id; g < p.num_tiles; g += npairs, ++it) {
+      const int pi = g / p.ntn;
+      const int t = 2 * pi + rank;
+      const int n0 = (g % p.ntn) * bn;
+      const int acc = it & 1;
+      const int64_t srow = int64_t(t) * kTileM + q * 32 + lane;
+      const bool rv = srow < p.n;
+      const int64_t orow = rv && p.out_rows ? p.out_rows[srow] : srow;
+      uint16_t* dst = p.out + orow * p.ldo + n0;
+      mbar_wait_sleep(&tfull[acc], static_cast<uint32_t>(it >> 1) & 1u, 32);
+      tc_fence_after();
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * bn);
+      for (int c = 0; c < bn; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+        tmem_wait_ld();
+        uint32_t h[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) h[j] = pack_bf16x2(tanh_fast(__uint_as_float(v[2 * j])), tanh_fast(__uint_as_float(v[2 * j + 1])));
+        if (rv) {
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg) {
+            if (n0 + c + 8 * gg < p.d) st_global_v4(dst + c + 8 * gg, h[4 * gg], h[4 * gg + 1], h[4 * gg + 2], h[4 * gg + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) {
+          mbar_arrive(&tempty[acc]);
+        } else {
+          mbar_arrive_remote(&tempty[acc], 0, 1);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while its peer may still arrive / read its smem
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem, static_cast<uint32_t>(2 * bn));
+  }
+}
+
+cudaError_t launch_fwd_gemm_pair(const CUtensorMap& xmap, const CUtensorMap& wmap, const CUtensorMap& amap,
+                                 const FwdParams& p, int grid, size_t smem, cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(fwd_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kFwdThreads, 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = std::getenv("ATMM_NO_PDL") ? 1 : 2;
+  return cudaLaunchKernelEx(&cfg, fwd_gemm_pair_kernel, xmap, wmap, amap, p);
+}
+
+int fwd_gemm_pair_max_clusters(size_t smem) {
+  if (cudaFuncSetAttribute(fwd_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+      cudaSuccess)
+    return 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kFwdThreads, 1, 1);
+  cfg.gridDim = dim3(2, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fwd_gemm_pair_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+}  // namespace atmm
