@@ -329,8 +329,8 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
                      int64_t num_layers, const void* x, int64_t ldx, void* out, int64_t ldo,
                      void* stream);
 /* {n, d, bn, tiles, grid, ext blocks, shrink items, shrink K split, sorted,
- *  GEMM stages, shrink stages, GEMM cta_group (1 or 2)}: the first
- *  min(cap, 12) are written. */
+ *  GEMM stages, shrink stages, GEMM cta_group (1 or 2), GEMM split-K}: the
+ *  first min(cap, 13) are written. */
 int atmm_forward_stats(const atmm_forward* f, int64_t* out, int64_t cap);
 
 #ifdef __cplusplus

@@ -496,7 +496,7 @@ class LayerForward:
     the shape).  bf16 activations / weights, fp32 accumulation, bf16 out."""
 
     STATS = ("n", "d", "bn", "tiles", "grid", "ext_blocks", "shrink_items", "shrink_ks", "sorted", "gemm_stages",
-             "shrink_stages", "gemm_cta_group")
+             "shrink_stages", "gemm_cta_group", "gemm_split_k")
 
     def __init__(self, plan=None, n: Optional[int] = None, hidden_dim: Optional[int] = None, device: int = 0):
         if isinstance(plan, MixturePlan):

@@ -1690,6 +1690,7 @@ struct atmm_forward {
   int32_t row_tiles = 0, bn = 128, ntn = 0, num_tiles = 0, nkb = 0, ks = 1, num_items = 0, num_ext = 0;
   int32_t stages_g = 0, stages_s = 0, grid = 0, sbytes = 0;
   bool pair = false;  // GEMM as 2-SM CTA pairs (fwd_gemm_pair_kernel)
+  int32_t kz = 1;     // 1-SM GEMM split-K cluster
   int64_t zero_off = 0;
   CUtensorMap amap;            // pair GEMM: the A images, 16 KB slots
   DevBuf<CUtensorMap> umaps;   // pair GEMM: per-slot up^T maps
@@ -1791,7 +1792,17 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       if (clusters <= 0) clusters = sms / 2;
       f->grid = std::min(f->num_tiles, clusters) * 2;
     } else {
-      f->grid = std::min(f->num_tiles, sms);
+      // Split-K for small batches: clusters of kz CTAs per tile while every
+      // tile still gets its own cluster on the SMs and each rank >= 8 K blocks.
+      f->kz = 1;
+      if (f->bn == 128) {
+        while (f->kz < 8 && int64_t(f->num_tiles) * f->kz * 2 <= sms && f->nkb / (f->kz * 2) >= 8) f->kz *= 2;
+      }
+      if (const char* e = std::getenv("ATMM_FWD_KZ")) {
+        const int v = std::atoi(e);
+        f->kz = (v == 2 || v == 4 || v == 8) && f->bn == 128 && f->nkb / v >= 1 ? v : 1;
+      }
+      f->grid = f->kz > 1 ? f->num_tiles * f->kz : std::min(f->num_tiles, sms);
     }
 
     std::vector<int32_t> order;
@@ -1955,7 +1966,7 @@ int atmm_forward_stats(const atmm_forward* f, int64_t* out, int64_t cap) {
   return guarded([&] {
     if (!f || !out) fail(ATMM_ERR_CONFIG, "null forward or output");
     const int64_t v[] = {f->n, f->d, f->bn, f->num_tiles, f->grid, f->num_ext, f->num_items, f->ks, f->sorted ? 1 : 0,
-                         f->stages_g, f->stages_s, f->pair ? 2 : 1};
+                         f->stages_g, f->stages_s, f->pair ? 2 : 1, f->kz};
     const int64_t k = std::min<int64_t>(cap, static_cast<int64_t>(sizeof(v) / sizeof(v[0])));
     for (int64_t i = 0; i < k; ++i) out[i] = v[i];
   });
@@ -2013,6 +2024,7 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     p.sbytes = f->sbytes;
     p.pair = f->pair ? 1 : 0;
     p.dbg = std::getenv("ATMM_FWD_DBG") ? std::atoi(std::getenv("ATMM_FWD_DBG")) : 0;
+    p.kz = f->kz;
     p.pext = f->pext.p;
     p.pext_begin = f->pext_begin.p;
     p.zero_a = f->ext.p ? f->ext.p + f->zero_off : nullptr;

@@ -326,11 +326,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     const FwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2];
+  __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2], recv_bar;
   __shared__ uint32_t tslot;
   const int S = p.stages, bn = p.bn;
   const uint32_t kStage = kFwdA + static_cast<uint32_t>(bn) * 128u;
   const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
+  // Split-K (small batches): a cluster of kz CTAs shares one tile, rank z
+  // accumulates K blocks [kb0, kb1) and the last rank adds the K-extension
+  // blocks; partial rows meet their owner rank by bulk DSMEM pushes and are
+  // summed in rank order (deterministic), then tanh.  One tile per cluster.
+  const int kz = p.kz;
+  const int z = static_cast<int>(blockIdx.x) % kz;
+  const int cl = static_cast<int>(blockIdx.x) / kz, ncl = static_cast<int>(gridDim.x) / kz;
+  const int kb0 = p.nkb * z / kz, kb1 = p.nkb * (z + 1) / kz;
+  const bool do_ext = p.exts != nullptr && z == kz - 1;
+  const int rows_per = kTileM / kz;
+  const int pitch = bn + 4;  // fp32 words per staged row (16-byte skew)
+  const uint32_t slot_bytes = static_cast<uint32_t>(rows_per * pitch) * 4u;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -341,15 +353,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
+    mbar_init(&recv_bar, 1);
     fence_mbar_init();
     tma_prefetch_desc(&xmap);
     tma_prefetch_desc(&wmap);
+    if (kz > 1) mbar_arrive_expect_tx(&recv_bar, static_cast<uint32_t>(kz) * slot_bytes);
   }
   if (threadIdx.x == 0) FTRACE(4096, 0);
-  if (threadIdx.x == 0 && p.trace) p.trace[(4096 + blockIdx.x) * 16 + 14] = clock64();
   if (warp == 1) tmem_alloc(&tslot, static_cast<uint32_t>(2 * bn));
   tc_fence_before();
-  __syncthreads();
+  if (kz > 1) {
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem = tslot;
 
@@ -362,10 +379,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       bool waited = p.exts == nullptr;
       if (waited) griddep_wait();
       int i = 0;
-      for (int tile = static_cast<int>(blockIdx.x); tile < p.num_tiles; tile += static_cast<int>(gridDim.x)) {
+      for (int tile = cl; tile < p.num_tiles; tile += ncl) {
         const int t = tile / p.ntn;
         const int n0 = (tile % p.ntn) * bn;
-        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % S;
           const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);
@@ -375,7 +392,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tma_load_2d(a, &xmap, &full[s], kb * kBK, t * kTileM);
           for (int c = 0; c < bn; c += 64) tma_load_3d(b + c * 128, &wmap, &full[s], n0 + c, kb * kBK, p.layer);
         }
-        if (p.exts == nullptr) continue;
+        if (!do_ext) continue;
         for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
           if (!waited) {
             griddep_wait();  // the A images are the shrink launch's output
@@ -410,26 +427,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t idesc_main = idesc_bf16(128, static_cast<uint32_t>(bn), 0, 1);
       const uint32_t idesc_ext = idesc_bf16(128, static_cast<uint32_t>(bn));
       int i = 0, it = 0;
-      for (int tile = static_cast<int>(blockIdx.x); tile < p.num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+      for (int tile = cl; tile < p.num_tiles; tile += ncl, ++it) {
         const int t = tile / p.ntn;
         const int acc = it & 1;
         mbar_wait(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
-        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int s = i % S;
           mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
-          if (it == 0 && kb == 0) FTRACE(4096, 1);
+          if (it == 0 && kb == kb0) FTRACE(4096, 1);
           tc_fence_after();
           const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             mma_bf16(d, smem_desc(a + k * 32, 16, 1024, kLayoutSW128), smem_desc(b + k * 2048, 8192, 1024, kLayoutSW128),
-                     idesc_main, (kb > 0 || k > 0) ? 1u : 0u);
+                     idesc_main, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           mma_commit(&empty[s]);
         }
-        if (p.exts != nullptr) {
+        if (do_ext) {
           for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
             const int kk = p.exts[e].kk;
             const int s = i % S;
@@ -450,10 +467,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
     __syncwarp();
-  } else {
+  } else if (kz == 1) {
     const int q = warp & 3;
     int it = 0;
-    for (int tile = static_cast<int>(blockIdx.x); tile < p.num_tiles; tile += static_cast<int>(gridDim.x), ++it) {
+    for (int tile = cl; tile < p.num_tiles; tile += ncl, ++it) {
       const int t = tile / p.ntn;
       const int n0 = (tile % p.ntn) * bn;
       const int acc = it & 1;
@@ -484,11 +501,90 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (it == 0 && threadIdx.x == 64) FTRACE(4096, 5);
     }
+  } else {
+    // Split-K epilogue (one tile per cluster; the ring is idle once the
+    // accumulator is complete, so it holds the staged partial and the
+    // receive slots).
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int tile = cl;
+    const int t = tile / p.ntn;
+    const int n0 = (tile % p.ntn) * bn;
+    float* stage = reinterpret_cast<float*>(sm);                 // 128 x pitch
+    float* recv = stage + kTileM * pitch;                         // kz slots x rows_per x pitch
+    if (tile < p.num_tiles) {
+      mbar_wait_sleep(&tfull[0], 0, 32);
+      tc_fence_after();
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
+      for (int c = 0; c < bn; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + static_cast<uint32_t>(c), v);
+        tmem_wait_ld();
+        const uint32_t dst = smem_u32(stage + row * pitch + c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) st_shared_v4(dst + j * 16, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    }
+    fence_proxy_async_smem();
+  }
+  if (kz > 1) {
+    // every rank's MMAs are done (its ring is free for the receive slots) and
+    // its partial is staged before anything is pushed
+    cluster_sync();
+  }
+  if (warp >= 2 && kz > 1) {
+    const int tile = cl;
+    const int t = tile / p.ntn;
+    const int n0 = (tile % p.ntn) * bn;
+    float* stage = reinterpret_cast<float*>(sm);
+    float* recv = stage + kTileM * pitch;
+    if (threadIdx.x == 64) {
+      const uint32_t src0 = smem_u32(stage), dst0 = smem_u32(recv) + static_cast<uint32_t>(z) * slot_bytes;
+      for (int r2 = 0; r2 < kz; ++r2) {
+        bulk_s2cluster(map_cta(dst0, static_cast<uint32_t>(r2)), src0 + static_cast<uint32_t>(r2) * slot_bytes, slot_bytes,
+                       map_cta(smem_u32(&recv_bar), static_cast<uint32_t>(r2)));
+      }
+    }
+    mbar_wait_cluster(&recv_bar, 0);
+    if (tile < p.num_tiles) {
+      const int tid = static_cast<int>(threadIdx.x) - 64;
+      const int groups = bn / 8;
+      const uint32_t recv_base = smem_u32(recv);
+      for (int u = tid; u < rows_per * groups; u += 128) {
+        const int lr = u / groups;
+        const int c = (u % groups) * 8;
+        const int64_t srow = int64_t(t) * kTileM + z * rows_per + lr;
+        if (srow >= p.n || n0 + c >= p.d) continue;
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int r2 = 0; r2 < kz; ++r2) {  // rank order: deterministic
+          const uint32_t off = recv_base + static_cast<uint32_t>(r2) * slot_bytes + static_cast<uint32_t>(lr * pitch + c) * 4u;
+          const uint4 v0 = ld_shared_v4(off), v1 = ld_shared_v4(off + 16);
+          acc[0] += __uint_as_float(v0.x);
+          acc[1] += __uint_as_float(v0.y);
+          acc[2] += __uint_as_float(v0.z);
+          acc[3] += __uint_as_float(v0.w);
+          acc[4] += __uint_as_float(v1.x);
+          acc[5] += __uint_as_float(v1.y);
+          acc[6] += __uint_as_float(v1.z);
+          acc[7] += __uint_as_float(v1.w);
+        }
+        const int64_t orow = p.out_rows ? p.out_rows[srow] : srow;
+        st_global_v4(p.out + orow * p.ldo + n0 + c, pack_bf16x2(tanh_fast(acc[0]), tanh_fast(acc[1])),
+                     pack_bf16x2(tanh_fast(acc[2]), tanh_fast(acc[3])), pack_bf16x2(tanh_fast(acc[4]), tanh_fast(acc[5])),
+                     pack_bf16x2(tanh_fast(acc[6]), tanh_fast(acc[7])));
+      }
+    }
   }
   if (threadIdx.x == 64) FTRACE(4096, 6);
   if (threadIdx.x == 64 && p.trace) p.trace[(4096 + blockIdx.x) * 16 + 15] = clock64();
   tc_fence_before();
-  __syncthreads();
+  if (kz > 1) {
+    cluster_sync();  // every pushed partial has landed before any rank leaves
+  } else {
+    __syncthreads();
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, static_cast<uint32_t>(2 * bn));
@@ -559,16 +655,20 @@ cudaError_t launch_fwd_gemm(const CUtensorMap& xmap, const CUtensorMap& wmap, co
                             cudaStream_t stream) {
   cudaError_t e = set_smem(fwd_gemm_kernel, smem);
   if (e != cudaSuccess) return e;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // split-K cluster (1: plain)
+  attr[0].val.clusterDim.x = static_cast<unsigned>(p.kz);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kFwdThreads, 1, 1);
   cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cfg.attrs = attr;
-  cfg.numAttrs = fwd_pdl() ? 1 : 0;
+  cfg.numAttrs = fwd_pdl() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, fwd_gemm_kernel, xmap, wmap, p);
 }
 

@@ -140,15 +140,17 @@ def test_forward_random_shapes(gpu, atmm, oracle, monkeypatch, seed):
     a = _assignment(ranks, lens, seed)
     x = oracle.round_bf16(oracle.random_matrix(oracle.rng(seed), a.size, d))
     want = oracle.forward_f64(x, w, "unmerged", a, facs)
-    for bn, ks, pair in [("128", None, "1"), ("256", "1", "1"), ("256", "4", "0"), ("128", "2", "0")]:
+    for bn, ks, pair, kz in [("128", None, "1", "1"), ("256", "1", "1", "1"), ("256", "4", "0", "1"),
+                             ("128", "2", "0", "1"), ("128", "2", "0", "4"), ("128", None, "0", "2")]:
         monkeypatch.setenv("ATMM_FWD_BN", bn)
         monkeypatch.setenv("ATMM_FWD_PAIR", pair)
+        monkeypatch.setenv("ATMM_FWD_KZ", kz)
         if ks:
             monkeypatch.setenv("ATMM_FWD_KS", ks)
         else:
             monkeypatch.delenv("ATMM_FWD_KS", raising=False)
         got = atmm.LayerForward(atmm.BypassPlan(reg, a)).run(_dev(w), _dev(x)).float().cpu().numpy()
-        assert np.max(np.abs(got - want)) <= tol_for(want), (bn, ks, pair, d, L, ranks, lens)
+        assert np.max(np.abs(got - want)) <= tol_for(want), (bn, ks, pair, kz, d, L, ranks, lens)
 
 
 def test_forward_large_rows_subset(gpu, atmm, oracle):
