@@ -758,7 +758,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     mb->grid = P;
     mb->part.alloc(static_cast<size_t>(total_seg) * kTileM * g.r_pad_max);
     mb->mid.alloc(static_cast<size_t>(T) * kTileM * g.r_pad_max);
-    mb->counter.alloc(2);
+    mb->counter.alloc(2 + static_cast<size_t>(T));  // [grid barrier x2][per-tile mid readiness]
     mb->tables.alloc(tables.size());
     CUDA_CHECK(cudaMemset(mb->mid.p, 0, mb->mid.n * sizeof(uint16_t)));
     CUDA_CHECK(cudaMemset(mb->counter.p, 0, mb->counter.n * sizeof(int32_t)));

@@ -142,7 +142,7 @@ struct SplitParams {
   const int32_t* part_off;   // [tile]
   float* part;               // [sum nseg][128][r_pad_max]
   uint16_t* mid;             // [tile][128 x r_pad_max] bf16, interleave layout
-  int32_t* counter;          // [2] grid barrier (arrivals, sense flag)
+  int32_t* counter;          // [2] grid barrier (arrivals, sense flag), then [tile] reduced mid items
   const int32_t* red_off;    // [tile + 1] prefix of rows x r_pad / 4 reduction items
   const int32_t* red_tile0;  // [grid] tile holding the CTA's first reduction item
   uint64_t* trace;

@@ -1294,11 +1294,39 @@ __device__ __forceinline__ void loader_drain(int n, int D, int S, uint64_t* full
 // Fixed-order sum of the shrink's segment partials -> bf16 mid, a share of
 // the (tile, row, 4 columns) items per participating thread (rt of nthr per
 // CTA, all CTAs).  Summation order = slot order: deterministic.
-__device__ __forceinline__ void split_reduce_mid(const SplitParams& p, int rt, int nthr) {
+// Per-CTA cache of the reduction tables of the tiles its item range touches
+// (static plan data: staged in shared memory before griddepcontrol.wait, so
+// the reduction issues its partial loads without a chain of table lookups).
+constexpr int kRedCache = 8;
+struct RedCache {
+  int32_t t0, n;
+  int32_t off[kRedCache + 1];  // red_off[t0 + i]
+  int32_t r_pad[kRedCache];
+  int32_t nseg[kRedCache];
+  int32_t part_off[kRedCache];
+};
+__device__ __forceinline__ void red_cache_load(const SplitParams& p, RedCache& rc, int rt) {
+  const int T = p.num_tiles;
+  const int t0 = p.red_tile0[blockIdx.x];
+  const int n = min(kRedCache, T - t0);
+  if (rt == 0) {
+    rc.t0 = t0;
+    rc.n = n;
+  }
+  if (rt <= n) rc.off[rt] = p.red_off[t0 + rt];
+  if (rt < n) {
+    rc.r_pad[rt] = p.tiles[t0 + rt].r_pad;
+    rc.nseg[rt] = p.nseg[t0 + rt];
+    rc.part_off[rt] = p.part_off[t0 + rt];
+  }
+}
+
+__device__ __forceinline__ void split_reduce_mid(const SplitParams& p, const RedCache& rc, int rt, int nthr) {
   // CTA b owns the contiguous item range [b N / P, (b + 1) N / P); its
   // threads stride through it (consecutive threads -> consecutive 16-byte
   // chunks of a row: coalesced); the tile of an item is found by walking
-  // forward from the CTA's first tile (host table red_tile0).
+  // forward from the CTA's first tile (host table red_tile0), through the
+  // shared-memory cache of those tiles' tables.
   const int T = p.num_tiles;
   const int total = p.red_off[T];
   const int P = static_cast<int>(gridDim.x);
@@ -1306,8 +1334,7 @@ __device__ __forceinline__ void split_reduce_mid(const SplitParams& p, int rt, i
   const int i_lo = static_cast<int>((static_cast<int64_t>(total) * b) / P);
   const int i_hi = static_cast<int>((static_cast<int64_t>(total) * (b + 1)) / P);
   const int64_t seg_stride = static_cast<int64_t>(kTileM) * p.r_pad_max;
-  int t = p.red_tile0[b];
-  int t_next_off = p.red_off[t + 1];
+  int ti = 0;  // cache index of the current tile
   constexpr int kB = 2;
   for (int i0 = i_lo + rt; i0 < i_hi; i0 += nthr * kB) {
     float4 acc[kB];
@@ -1322,13 +1349,27 @@ __device__ __forceinline__ void split_reduce_mid(const SplitParams& p, int rt, i
       src[q] = p.part;
       dst[q] = nullptr;
       if (i < i_hi) {
-        while (i >= t_next_off && t < T - 1) t_next_off = p.red_off[++t + 1];
-        const int r_pad = p.tiles[t].r_pad;
-        const int local = i - p.red_off[t];
+        int t, r_pad, base, nsg, poff;
+        while (ti < rc.n - 1 && i >= rc.off[ti + 1]) ++ti;
+        if (i < rc.off[min(ti + 1, rc.n)] || ti < rc.n - 1) {
+          t = rc.t0 + ti;
+          r_pad = rc.r_pad[ti];
+          base = rc.off[ti];
+          nsg = rc.nseg[ti];
+          poff = rc.part_off[ti];
+        } else {  // beyond the cache (a CTA range over > kRedCache tiles): walk the global tables
+          t = rc.t0 + rc.n - 1;
+          while (t < T - 1 && i >= p.red_off[t + 1]) ++t;
+          r_pad = p.tiles[t].r_pad;
+          base = p.red_off[t];
+          nsg = p.nseg[t];
+          poff = p.part_off[t];
+        }
+        const int local = i - base;
         const int rr = local / (r_pad / 4);
         const int c4 = local - rr * (r_pad / 4);
-        ns[q] = p.nseg[t];
-        src[q] = p.part + static_cast<int64_t>(p.part_off[t]) * seg_stride + static_cast<int64_t>(rr) * p.r_pad_max + c4 * 4;
+        ns[q] = nsg;
+        src[q] = p.part + static_cast<int64_t>(poff) * seg_stride + static_cast<int64_t>(rr) * p.r_pad_max + c4 * 4;
         dst[q] = reinterpret_cast<uint8_t*>(p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max) +
                  interleave_off(static_cast<uint32_t>(rr), static_cast<uint32_t>(c4 * 4), static_cast<uint32_t>(r_pad));
       }
@@ -1385,6 +1426,18 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
   const int i_beg = p.s_begin[blockIdx.x];
   const int i_end = p.s_begin[blockIdx.x + 1];
   if (tid == 0) STRACE(0);
+  // Every thread waits for the previous grid, then releases the expand
+  // launch at once: its CTAs take the SMs of finished shrink CTAs and stage
+  // their prologue and first up^T / Y loads under this grid's tail (they read
+  // the partials only after their own griddepcontrol.wait).
+  griddep_wait();
+  griddep_launch_dependents();
+  // The expand launch that follows counts reduced mid items per tile: reset
+  // (after the wait: the previous expand, which polled them, is complete; the
+  // next expand reads them after its own wait, i.e. after this grid).
+  if (blockIdx.x == 0) {
+    for (int t = static_cast<int>(tid); t < p.num_tiles; t += static_cast<int>(blockDim.x)) p.counter[2 + t] = 0;
+  }
 
   if (warp == 0) {
     // full: the 8 loader warps + the down^T bulk copy's expect_tx arrival
@@ -1542,6 +1595,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
                                              ~static_cast<uintptr_t>(127));
   __shared__ uint64_t bars[2 * 4 + 4 + 1];  // ... + mid_ready
   __shared__ uint32_t tmem_slot;
+  __shared__ RedCache rcache;
   constexpr int kEsz = static_cast<int>(sizeof(YT));
   constexpr int kCols = kTileM * G;  // output columns per item
   const uint32_t tid = threadIdx.x;
@@ -1566,6 +1620,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   const int i_beg = p.e_begin[blockIdx.x];
   const int i_end = p.e_begin[blockIdx.x + 1];
   if (tid == 0) STRACE(8);
+  // The next launch may start as SMs free up: it waits for this grid itself.
+  griddep_launch_dependents();
   const int64_t ldy_b = p.ldy * kEsz;
   const int nsl = (p.d_out + kCols - 1) / kCols;
 
@@ -1584,6 +1640,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   if (warp < kSplitLoaderWarps) {
     // ===================== loaders =====================
     bool waited = false;
+    int ready_tile = -1;
     int j = 0;
     for (int item = i_beg; item < i_end; ++item, ++j) {
       const int t = item / nsl;
@@ -1622,14 +1679,26 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
         const int c = q - r * cpr;
         cp_async16(Yb + static_cast<uint32_t>(r) * ypitch + c * 16, yb + static_cast<int64_t>(static_cast<int32_t>(ld_shared_u32(Rb + r * 4))) * ldy_b + c * 16, 16u);
       }
-      if (!waited) {
-        mbar_wait(mid_ready, 0);  // mid is reduced by this launch's epilogue warps (grid barrier)
-        waited = true;
-        if (tid == 0) STRACE(12);
-      }
       const uint16_t* ms = p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max;
       const int rows16 = (rows + 15) & ~15;
       if (tid == 0) {  // mid is one contiguous bf16 run: one TMA bulk copy
+        // once this launch's reducers (any CTA) have published all of tile t
+        if (t != ready_tile) {
+          const int need = p.red_off[t + 1] - p.red_off[t];
+          const int32_t* ready = p.counter + 2 + t;
+          int32_t v;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
+            if (v >= need) break;
+            __nanosleep(32);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          ready_tile = t;
+        }
+        if (!waited) {
+          waited = true;
+          STRACE(12);
+        }
         mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows16 * r_pad * 2));
         bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes + up_bytes, ms, static_cast<uint32_t>(rows16 * r_pad * 2),
                  &full[st]);
@@ -1676,13 +1745,29 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
     // and Y (which do not depend on mid).
     {
       const int et = static_cast<int>(tid) - static_cast<int>(kSplitWarpEpi) * 32;
+      red_cache_load(p, rcache, et);
+      named_bar_sync(3, 256);
       griddep_wait();  // partials are produced by the shrink launch
-      split_reduce_mid(p, et, 256);
+      if (et == 0) STRACE(13);
+      split_reduce_mid(p, rcache, et, 256);
       __threadfence();
       named_bar_sync(3, 256);
       if (et == 0) {
-        grid_arrive_wait(p.counter, gridDim.x);
-        mbar_arrive(mid_ready);
+        STRACE(14);
+        // publish: items of each tile this CTA's range covered
+        const int total = p.red_off[p.num_tiles];
+        const int P = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+        const int i_lo = static_cast<int>((static_cast<int64_t>(total) * b) / P);
+        const int i_hi = static_cast<int>((static_cast<int64_t>(total) * (b + 1)) / P);
+        for (int t = rcache.t0; t < p.num_tiles && i_lo < i_hi; ++t) {
+          const int k = t - rcache.t0;
+          const int o0 = k < rcache.n ? rcache.off[k] : p.red_off[t];
+          const int o1 = k + 1 <= rcache.n ? rcache.off[k + 1] : p.red_off[t + 1];
+          const int lo = max(i_lo, o0), hi = min(i_hi, o1);
+          if (lo >= i_hi) break;
+          if (hi > lo) atomicAdd(p.counter + 2 + t, hi - lo);
+        }
+        STRACE(15);
       }
     }
     // Warp w: TMEM lane quadrant w % 4, row blocks of RB rows alternating

@@ -14,7 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 EV = {0: "shrink start", 4: "shrink mma item0 full", 5: "shrink mma item1 full",
       **{16 + j: f"shrink ld issued item{j}" for j in range(12)},
       1: "shrink loaders done", 2: "shrink epilogue done", 3: "shrink end",
-      8: "expand start", 12: "expand griddep released", 9: "expand loaders done", 10: "expand epilogue done",
+      8: "expand start", 13: "expand epi griddep returned", 14: "expand reduce done", 15: "expand grid barrier passed",
+      12: "expand loaders see mid ready", 9: "expand loaders done", 10: "expand epilogue done",
       11: "expand end"}
 
 
