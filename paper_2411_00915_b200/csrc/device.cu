@@ -548,7 +548,7 @@ static int expand_g_bf16() {
 // Fixed per-item costs (bytes-equivalent) of the split kernels' balancing
 // (ATMM_SCOST / ATMM_ECOST for A/B runs).
 static int64_t shrink_fixed_cost() {
-  static const int64_t v = std::getenv("ATMM_SCOST") ? std::atoll(std::getenv("ATMM_SCOST")) : 16384;
+  static const int64_t v = std::getenv("ATMM_SCOST") ? std::atoll(std::getenv("ATMM_SCOST")) : 32768;
   return v;
 }
 static int64_t expand_fixed_cost() {
