@@ -942,6 +942,10 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
   const uint32_t tmem_base = *tmem_slot;
   cluster_arrive_relaxed();  // phase 1: barrier inits (fenced above) visible to peers
   if (threadIdx.x == 0) TRACE(1);
+  // Release the next launch now (every thread): its CTAs take the free SM
+  // slots and run their prologue and weight prefetch under this launch; they
+  // read X / Y only after their own griddepcontrol.wait (this grid complete).
+  griddep_launch_dependents();
 
   const uint32_t ybuf_s = smem_u32(ybuf);
   const int ngroups = (rows + 3) / 4;
