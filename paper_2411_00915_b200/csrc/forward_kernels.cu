@@ -369,6 +369,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   tc_fence_after();
   const uint32_t tmem = tslot;
+  // Release the next launch at once (every thread): it waits for this grid
+  // itself before reading what this grid writes; its CTAs only get SMs as
+  // these exit, so this just removes the launch gap.
+  griddep_launch_dependents();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -719,6 +723,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  griddep_launch_dependents();  // as in fwd_gemm_kernel
 
   if (warp == 0) {
     if (elect_one()) {
