@@ -1873,9 +1873,15 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       // K split of the shrink: when the GEMM grid leaves room, keep shrink +
       // GEMM co-resident (the GEMM's main loop then hides the shrink, which
       // only gates its final K-extension blocks); otherwise fill the SMs.
+      // Otherwise the shrink's CTAs delay the GEMM CTAs that get their SMs
+      // last: size it to the CTAs that own one tile fewer (they start late at
+      // no cost), with K split 1 when even that does not fit.
       f->ks = 1;
       const int64_t room = sms - f->grid;
-      const int64_t cap = room >= f->num_items ? room : sms;
+      const int64_t units = f->pair ? f->grid / 2 : f->grid;
+      const int64_t per = units > 0 ? (f->num_tiles + units - 1) / units : 1;
+      const int64_t slack = (units * per - f->num_tiles) * (f->pair ? 2 : 1);
+      const int64_t cap = room >= f->num_items ? room : slack;
       while (f->ks < 8 && int64_t(f->num_items) * f->ks * 2 <= cap && f->ks * 2 <= f->nkb) f->ks *= 2;
       if (const char* e = std::getenv("ATMM_FWD_KS")) f->ks = std::clamp(std::atoi(e), 1, 8);
       while (f->ks > 1 && f->ks > f->nkb) f->ks /= 2;  // every K slice gets >= 1 K block
