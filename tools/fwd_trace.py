@@ -22,6 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--layers", type=int, default=2)
+    ap.add_argument("--graph", action="store_true", help="replay the traced step from a CUDA graph")
     args = ap.parse_args()
     import torch
 
@@ -50,7 +51,18 @@ def main():
         tr.zero_()
         torch.cuda.synchronize()
         lib.atmm_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
-        fw.run(W, x, out, num_layers=1)
+        if args.graph:  # launches from a CUDA graph: no host gaps between them
+            s = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                fw.run(W, x, out, num_layers=1)
+            lib.atmm_debug_set_trace(None)
+            tr.zero_()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s):
+                g.replay()
+        else:
+            fw.run(W, x, out, num_layers=1)
         torch.cuda.synchronize()
         lib.atmm_debug_set_trace(None)
         raw = tr.cpu().numpy().reshape(8192, 16).astype(np.float64)
