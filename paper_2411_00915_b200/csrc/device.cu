@@ -2029,7 +2029,6 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     p.num_items = f->num_items;
     p.sbytes = f->sbytes;
     p.pair = f->pair ? 1 : 0;
-    p.dbg = std::getenv("ATMM_FWD_DBG") ? std::atoi(std::getenv("ATMM_FWD_DBG")) : 0;
     p.kz = f->kz;
     p.pext = f->pext.p;
     p.pext_begin = f->pext_begin.p;

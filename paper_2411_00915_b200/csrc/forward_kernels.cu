@@ -786,8 +786,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
         for (int kb = 0; kb < p.nkb; ++kb, ++i) {
           const int s = i % S;
-          if (p.dbg & 1) mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
-          else mbar_wait_cluster(&full[s], static_cast<uint32_t>(i / S) & 1u);
+          mbar_wait_cluster(&full[s], static_cast<uint32_t>(i / S) & 1u);
           tc_fence_after();
           const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
 #pragma unroll
