@@ -486,7 +486,7 @@ static A2aLayout resolve_a2a(int64_t d_in, int64_t d_out, int32_t cluster, int32
 }
 
 // Split path: mid partials (fp32, per tile x K slice), bf16 mid per tile and
-// per-tile arrival counters of one launch group, allocated with the plan.
+// per-tile mid readiness counters of one launch group, allocated with the plan.
 struct SplitBufs {
   DevBuf<float> part;
   DevBuf<uint16_t> mid;
@@ -758,7 +758,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     mb->grid = P;
     mb->part.alloc(static_cast<size_t>(total_seg) * kTileM * g.r_pad_max);
     mb->mid.alloc(static_cast<size_t>(T) * kTileM * g.r_pad_max);
-    mb->counter.alloc(2 + static_cast<size_t>(T));  // [grid barrier x2][per-tile mid readiness]
+    mb->counter.alloc(2 + static_cast<size_t>(T));  // [2 reserved][per-tile mid readiness]
     mb->tables.alloc(tables.size());
     CUDA_CHECK(cudaMemset(mb->mid.p, 0, mb->mid.n * sizeof(uint16_t)));
     CUDA_CHECK(cudaMemset(mb->counter.p, 0, mb->counter.n * sizeof(int32_t)));

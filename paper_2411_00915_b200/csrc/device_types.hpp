@@ -109,10 +109,11 @@ struct GroupArgs {
 //   shrink items = (tile, 64-wide K block), tile-major.  CTA b runs items
 //     [s_begin[b], s_begin[b+1]); the run of one tile inside one CTA is a
 //     "segment" whose fp32 partial mid rows go to part[part_off[t] + slot]
-//     (slots numbered in CTA order).  After a grid-wide barrier every CTA
+//     (slots numbered in CTA order).  In the expand launch every CTA first
 //     sums a share of the (tile, row, 4 columns) items over the tile's nseg[t]
-//     partials in FIXED slot order and writes bf16 mid[t] in the expand's
-//     B-operand (interleave) layout.
+//     partials in FIXED slot order, writes bf16 mid[t] in the expand's
+//     B-operand (interleave) layout and adds its item count to the tile's
+//     readiness counter.
 //   expand items = (tile, 128 output columns), tile-major; CTA b runs items
 //     [e_begin[b], e_begin[b+1]): Y[rows, cols] += s * mid . up.
 // part / mid stay in L2 between the two launches.
@@ -142,7 +143,7 @@ struct SplitParams {
   const int32_t* part_off;   // [tile]
   float* part;               // [sum nseg][128][r_pad_max]
   uint16_t* mid;             // [tile][128 x r_pad_max] bf16, interleave layout
-  int32_t* counter;          // [2] grid barrier (arrivals, sense flag), then [tile] reduced mid items
+  int32_t* counter;          // [2] reserved, then [tile] reduced mid items (reset by the shrink launch)
   const int32_t* red_off;    // [tile + 1] prefix of rows x r_pad / 4 reduction items
   const int32_t* red_tile0;  // [grid] tile holding the CTA's first reduction item
   uint64_t* trace;

@@ -1239,42 +1239,6 @@ constexpr int kExpandThreads = (kSplitLoaderWarps + 1 + 8) * 32;  // 8 epilogue 
     if (p.trace) p.trace[static_cast<size_t>(blockIdx.x) * kTraceEvents + (ev)] = globaltimer(); \
   } while (0)
 
-// Grid-wide barrier for a persistent grid whose CTAs are all co-resident:
-// ctr[0] counts arrivals, ctr[1] is a sense flag flipped by the last arrival
-// (which also resets ctr[0] for the next launch).
-__device__ __forceinline__ void grid_barrier(int32_t* ctr, uint32_t nblocks) {
-  if (threadIdx.x == 0) {
-    volatile int32_t* flag = ctr + 1;
-    const int32_t sense = *flag;
-    __threadfence();
-    if (atomicAdd(ctr, 1) == static_cast<int32_t>(nblocks) - 1) {
-      ctr[0] = 0;
-      __threadfence();
-      atomicExch(ctr + 1, sense ^ 1);
-    } else {
-      while (*flag == sense) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// Single-thread form of grid_barrier (no __syncthreads; the caller publishes
-// completion to the rest of its CTA itself).
-__device__ __forceinline__ void grid_arrive_wait(int32_t* ctr, uint32_t nblocks) {
-  volatile int32_t* flag = ctr + 1;
-  const int32_t sense = *flag;
-  __threadfence();
-  if (atomicAdd(ctr, 1) == static_cast<int32_t>(nblocks) - 1) {
-    ctr[0] = 0;
-    __threadfence();
-    atomicExch(ctr + 1, sense ^ 1);
-  } else {
-    while (*flag == sense) __nanosleep(32);
-  }
-  __threadfence();
-}
-
 // Loader-side completion: after issuing item j (committed as one cp.async
 // group), the item D groups back has landed for every lane of the warp;
 // lane 0 publishes it (full barriers count one arrival per loader warp).
@@ -1597,7 +1561,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   // interleave (no-swizzle) operands only need 16-byte alignment: align to 128
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
                                              ~static_cast<uintptr_t>(127));
-  __shared__ uint64_t bars[2 * 4 + 4 + 1];  // ... + mid_ready
+  __shared__ uint64_t bars[2 * 4 + 4];
   __shared__ uint32_t tmem_slot;
   __shared__ RedCache rcache;
   constexpr int kEsz = static_cast<int>(sizeof(YT));
@@ -1611,7 +1575,6 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   uint64_t* empty = bars + 4;      // [S], 256 epilogue arrivals
   uint64_t* acc_full = bars + 8;   // [2], MMA commit
   uint64_t* acc_empty = bars + 10; // [2], 256 epilogue arrivals
-  uint64_t* mid_ready = bars + 12; // grid-wide mid reduction done (1 arrival)
   const int rows16_max = (p.rows_max + 15) & ~15;
   const uint32_t up_bytes = static_cast<uint32_t>(kCols * p.r_pad_max * 2);
   const uint32_t mid_bytes = static_cast<uint32_t>((rows16_max * p.r_pad_max * 2 + 127) & ~127);
@@ -1631,7 +1594,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
 
   if (warp == 0) {
     // full: the 8 loader warps + the mid bulk copy's expect_tx arrival
-    if (lane < 13) mbar_init(&bars[lane], lane < 4 ? kSplitLoaderWarps + 1u : ((lane < 8 || (lane >= 10 && lane < 12)) ? 256u : 1u));
+    if (lane < 12) mbar_init(&bars[lane], lane < 4 ? kSplitLoaderWarps + 1u : ((lane < 8 || lane >= 10) ? 256u : 1u));
     fence_mbar_init();
   }
   if (warp == kSplitWarpMMA) tmem_alloc(&tmem_slot, tcols);
@@ -1744,9 +1707,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
     }
   } else {
     // ===================== epilogue (8 warps) =====================
-    // First: the shrink launch's partials -> bf16 mid, a share per CTA, then a
-    // grid-wide barrier; meanwhile the loaders already stream item 0's up^T
-    // and Y (which do not depend on mid).
+    // First: the shrink launch's partials -> bf16 mid, a share per CTA,
+    // published per tile (the loaders of an item wait only for its tile);
+    // meanwhile the loaders already stream item 0's up^T and Y (which do not
+    // depend on mid).
     {
       const int et = static_cast<int>(tid) - static_cast<int>(kSplitWarpEpi) * 32;
       red_cache_load(p, rcache, et);
