@@ -1882,8 +1882,8 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       const int64_t per = units > 0 ? (f->num_tiles + units - 1) / units : 1;
       const int64_t slack = (units * per - f->num_tiles) * (f->pair ? 2 : 1);
       const int64_t cap = room >= f->num_items ? room : slack;
-      while (f->ks < 8 && int64_t(f->num_items) * f->ks * 2 <= cap && f->ks * 2 <= f->nkb) f->ks *= 2;
-      if (const char* e = std::getenv("ATMM_FWD_KS")) f->ks = std::clamp(std::atoi(e), 1, 8);
+      while (f->ks < 16 && int64_t(f->num_items) * f->ks * 2 <= cap && f->ks * 2 <= f->nkb) f->ks *= 2;
+      if (const char* e = std::getenv("ATMM_FWD_KS")) f->ks = std::clamp(std::atoi(e), 1, 16);
       while (f->ks > 1 && f->ks > f->nkb) f->ks /= 2;  // every K slice gets >= 1 K block
       int32_t max_cols = 16;
       for (const FwdItem& it : items) max_cols = std::max(max_cols, it.ncols);

@@ -277,14 +277,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int row = kr * rows_per + lr;
         const int c = (u % groups) * 4;
         const uint32_t off = recv_base + static_cast<uint32_t>(lr * pitch + c) * 4u;
-        uint4 v[8];
+        uint4 v[16];
 #pragma unroll
-        for (int q2 = 0; q2 < 8; ++q2)
+        for (int q2 = 0; q2 < 16; ++q2)
           if (q2 < ks) v[q2] = ld_shared_v4(off + static_cast<uint32_t>(q2) * slot_bytes);
         float4 acc = make_float4(__uint_as_float(v[0].x), __uint_as_float(v[0].y), __uint_as_float(v[0].z),
                                  __uint_as_float(v[0].w));
 #pragma unroll
-        for (int q2 = 1; q2 < 8; ++q2) {
+        for (int q2 = 1; q2 < 16; ++q2) {
           if (q2 < ks) {
             acc.x += __uint_as_float(v[q2].x);
             acc.y += __uint_as_float(v[q2].y);
@@ -638,6 +638,14 @@ cudaError_t launch_fwd_gather(const uint16_t* x, int64_t ldx, uint16_t* dst, int
 cudaError_t launch_fwd_shrink(const CUtensorMap& xmap, const FwdParams& p, size_t smem, cudaStream_t stream) {
   cudaError_t e = set_smem(fwd_shrink_kernel, smem);
   if (e != cudaSuccess) return e;
+  if (p.ks > 8) {  // 16-CTA clusters are non-portable
+    static bool done = false;
+    if (!done) {
+      e = cudaFuncSetAttribute(fwd_shrink_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      done = true;
+    }
+  }
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(p.ks);
