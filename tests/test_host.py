@@ -222,6 +222,8 @@ def test_compute_fails_loudly_without_device(atmm):
         atmm.AdapterRegistry(1, 64, 64)
     with pytest.raises(atmm.NoDeviceError):
         atmm.atmm_multiply(np.ones((2, 2)), np.ones((2, 2)), (16,) * 6)
+    with pytest.raises(atmm.NoDeviceError):  # the layer forward has no CPU fallback either
+        atmm.LayerForward(None, n=4, hidden_dim=64)
 
 
 # -------------------------------------------------------------- C++ shim --
