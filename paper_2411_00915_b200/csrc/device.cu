@@ -304,6 +304,8 @@ struct A2aLayout {
 struct SplitLayout {
   bool ok = false;
   int32_t stages = 0, estages[2] = {0, 0};
+  bool ok_dt[2] = {false, false};  // usable for bf16 / fp32 Y
+  int32_t g_bf16 = 2;              // bf16 expand item width: 128 g_bf16 columns
   size_t smem_s = 0, smem_e[2] = {0, 0};
 };
 
@@ -522,7 +524,7 @@ enum class BypassPath { kA2a, kSplit, kFused };
 static BypassPath choose_path(const LaunchGroup& g, int y_dtype, bool y_vec) {
   const int di = y_dtype == ATMM_BF16 ? 0 : 1;
   const bool a2a = g.a2a[di].ok && y_vec;
-  const bool split = g.split.ok && y_vec;
+  const bool split = g.split.ok_dt[di] && y_vec;
   if (const char* e = std::getenv("ATMM_PATH")) {
     const std::string f(e);
     if (f == "a2a" && a2a) return BypassPath::kA2a;
@@ -565,16 +567,21 @@ static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, 
   l.stages = static_cast<int32_t>(std::min<int64_t>(8, avail / stage));
   l.smem_s = size_t(1024 + l.stages * stage);
   const int64_t rows16 = round_up(rows_max, 16);
-  bool ok = l.stages >= 2;
   for (int di = 0; di < 2; ++di) {
     const int64_t esz = di == 0 ? 2 : 4;
-    const int64_t cols = int64_t(kTileM) * (di == 0 ? expand_g_bf16() : 1);  // expand item width (128 G columns)
-    const int64_t est = round_up(cols * r_pad * 2 + round_up(rows16 * r_pad * 2, 128) + int64_t(rows_max) * cols * esz + kTileM * 4, 128);
-    l.estages[di] = static_cast<int32_t>(std::min<int64_t>(4, (avail + 1024 - 128) / est));  // 128-byte aligned kernel
-    l.smem_e[di] = size_t(128 + l.estages[di] * est);
-    ok = ok && l.estages[di] >= 2;
+    // bf16 items are 256 columns wide unless two of them do not fit (large
+    // rank x rows): then 128 columns
+    for (int g : di == 0 ? std::vector<int>{expand_g_bf16(), 1} : std::vector<int>{1}) {
+      const int64_t cols = int64_t(kTileM) * g;  // expand item width (128 G columns)
+      const int64_t est = round_up(cols * r_pad * 2 + round_up(rows16 * r_pad * 2, 128) + int64_t(rows_max) * cols * esz + kTileM * 4, 128);
+      l.estages[di] = static_cast<int32_t>(std::min<int64_t>(4, (avail + 1024 - 128) / est));  // 128-byte aligned kernel
+      l.smem_e[di] = size_t(128 + l.estages[di] * est);
+      if (di == 0) l.g_bf16 = g;
+      if (l.estages[di] >= 2) break;
+    }
+    l.ok_dt[di] = l.stages >= 2 && l.estages[di] >= 2;
   }
-  l.ok = ok;
+  l.ok = l.ok_dt[0] || l.ok_dt[1];
   return l;
 }
 
@@ -711,7 +718,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
       // bytes moved + a fixed per-item cost (pipeline step: barriers, 4 MMAs)
       for (int k = 0; k < nkb; ++k) scost.push_back(int64_t(td.rows) * 128 + int64_t(td.r_pad) * 128 + shrink_fixed_cost());
       for (int di = 0; di < 2; ++di) {
-        const int64_t cols = int64_t(kTileM) * (di == 0 ? expand_g_bf16() : 1), esz = di == 0 ? 2 : 4;
+        const int64_t cols = int64_t(kTileM) * (di == 0 ? g.split.g_bf16 : 1), esz = di == 0 ? 2 : 4;
         const int nsl = static_cast<int>((reg->d_out + cols - 1) / cols);
         for (int k = 0; k < nsl; ++k) ecost[di].push_back(int64_t(td.rows) * cols * esz * 2 + cols * td.r_pad * 2 + expand_fixed_cost());
       }
@@ -845,7 +852,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.stages = g.split.stages;
       sp.y_dtype = y_dtype == ATMM_BF16 ? 0 : 1;
       sp.estages = g.split.estages[sp.y_dtype];
-      sp.expand_g = sp.y_dtype == 0 ? expand_g_bf16() : 1;
+      sp.expand_g = sp.y_dtype == 0 ? g.split.g_bf16 : 1;
       sp.rows_max = g.rows_max;
       sp.s_begin = sb.tables.p;
       sp.e_begin = sb.tables.p + (P + 1) * (sp.y_dtype == 0 ? 1 : 2);

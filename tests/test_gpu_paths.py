@@ -140,3 +140,40 @@ def test_random_shapes_all_paths(gpu, atmm, oracle, monkeypatch, seed):
             want = y0.astype(np.float64) + want_b
             got = yt.float().cpu().numpy()
             assert np.max(np.abs(got - want)) <= tol_for(want), (path, dt, d_in, d_out, ranks, lens)
+
+
+def test_large_batch_row_subset(gpu, atmm, oracle):
+    """Maximum-size case: d = 8192, 64 rank-128 adapters,
+    16384 ragged rows; rows are independent, so a row subset is checked
+    against the oracle (and the whole output for finiteness)."""
+    import torch
+
+    d, n_ad = 8192, 64
+    ranks = {a: 128 for a in range(n_ad)}
+    rng = np.random.default_rng(77)
+    lens = (rng.zipf(1.3, n_ad) % 900 + 1).astype(int)
+    lens = (lens * (16384 / lens.sum())).astype(int) + 1
+    reg = atmm.AdapterRegistry(1, d, d)
+    orng = oracle.rng(5)
+    facs = {}
+    for a, r in ranks.items():
+        s = 1.0 / np.sqrt(np.float32(r))
+        facs[a] = (oracle.round_bf16(oracle.random_matrix(orng, d, r, -s, s)),
+                   oracle.round_bf16(oracle.random_matrix(orng, r, d, -s, s)))
+        reg.put(a, *facs[a])
+    assignment = np.concatenate([np.full(int(m), a, np.int32) for a, m in zip(sorted(ranks), lens)])
+    assignment = assignment[np.random.default_rng(3).permutation(assignment.size)]
+    n = assignment.size
+    x = torch.empty(n, d, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+    y0 = torch.empty(n, d, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1)
+    y = y0.clone()
+    plan = atmm.BypassPlan(reg, assignment)
+    assert {g["path_bf16"] for g in plan.describe()} <= {"split", "a2a", "fused"}
+    plan.apply(x, y)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y.float()).all()
+    pick = np.random.default_rng(1).choice(n, 24, replace=False)
+    xs = x[pick].float().cpu().numpy()
+    want = y0[pick].float().cpu().numpy().astype(np.float64) + oracle.bypass_rows_f64(xs, assignment[pick], facs)
+    got = y[pick].float().cpu().numpy()
+    assert np.max(np.abs(got - want)) <= tol_for(want)
