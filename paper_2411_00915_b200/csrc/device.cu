@@ -243,6 +243,7 @@ struct Slot {
   uint16_t* down_t = nullptr;
   uint16_t* up_t = nullptr;
   bool live = false;
+  bool async_owned = false;  // buffers from cudaMallocAsync (put_async): freed stream-ordered
 };
 
 }  // namespace atmm
@@ -255,6 +256,7 @@ struct atmm_registry {
   std::map<int32_t, int> slot_of;
   std::vector<Slot> slots;
   DevBuf<SlotDesc> d_slots;
+  DevBuf<float> stage;  // put_async fp32 staging, grow-only
   uint64_t generation = 0;
 
   ~atmm_registry() {
@@ -1197,20 +1199,42 @@ int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, 
     s.r_pad = r_pad;
     s.scale = scale;
     s.live = true;
-    float* stage = nullptr;
-    CUDA_CHECK(cudaMallocAsync(&s.down_t, dn * 2, st));
-    CUDA_CHECK(cudaMallocAsync(&s.up_t, un * 2, st));
-    CUDA_CHECK(cudaMallocAsync(&stage, (fd + fu) * 4, st));
+    // A swap of the same shape overwrites the slot's buffers in place (stream
+    // order: after every earlier use on this stream); the fp32 staging buffer
+    // is the registry's, grow-only -- no allocation on the swap path.
+    auto it = r->slot_of.find(adapter_id);
+    Slot* same = nullptr;
+    if (it != r->slot_of.end() && r->slots[static_cast<size_t>(it->second)].r_pad == r_pad &&
+        r->slots[static_cast<size_t>(it->second)].async_owned) {
+      same = &r->slots[static_cast<size_t>(it->second)];
+      s.down_t = same->down_t;
+      s.up_t = same->up_t;
+    } else {
+      CUDA_CHECK(cudaMallocAsync(&s.down_t, dn * 2, st));
+      CUDA_CHECK(cudaMallocAsync(&s.up_t, un * 2, st));
+    }
+    s.async_owned = true;
+    if (r->stage.n < fd + fu) {
+      CUDA_CHECK(cudaStreamSynchronize(st));  // the old staging buffer may still be read on this stream
+      r->stage.alloc(fd + fu);
+    }
+    float* stage = r->stage.p;
     CUDA_CHECK(cudaMemcpyAsync(stage, down, fd * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(stage + fd, up, fu * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(launch_pack_factors(stage, stage + fd, r->L, r->d_in, r->d_out, rank, r->d_in_pad, r->d_out_pad, r_pad,
                                    s.down_t, s.up_t, st));
-    CUDA_CHECK(cudaFreeAsync(stage, st));
-    auto it = r->slot_of.find(adapter_id);
-    if (it != r->slot_of.end()) {
+    if (same) {
+      *same = s;
+    } else if (it != r->slot_of.end()) {
       Slot& old = r->slots[static_cast<size_t>(it->second)];
-      CUDA_CHECK(cudaFreeAsync(old.down_t, st));  // stream order: after every earlier use on this stream
-      CUDA_CHECK(cudaFreeAsync(old.up_t, st));
+      if (old.async_owned) {
+        CUDA_CHECK(cudaFreeAsync(old.down_t, st));  // stream order: after every earlier use on this stream
+        CUDA_CHECK(cudaFreeAsync(old.up_t, st));
+      } else {
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaFree(old.down_t);
+        cudaFree(old.up_t);
+      }
       old = s;
     } else {
       int idx = -1;
