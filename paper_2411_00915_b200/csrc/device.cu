@@ -161,6 +161,35 @@ CUtensorMap make_y_map(const void* y, int64_t n, int64_t d_out, int64_t ldy, int
   return m;
 }
 
+// Small per-thread cache of encoded X / Y maps (kind 0: X, 1 + y_dtype: Y).
+CUtensorMap cached_map(int kind, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+  struct Entry {
+    const void* base;
+    int64_t rows, cols, ld;
+    int kind;
+    CUtensorMap map;
+  };
+  thread_local Entry cache[8];
+  thread_local int next = 0;
+  thread_local bool init = false;
+  if (!init) {
+    for (auto& e : cache) e.base = nullptr;
+    init = true;
+  }
+  for (const auto& e : cache) {
+    if (e.base == base && e.rows == rows && e.cols == cols && e.ld == ld && e.kind == kind) return e.map;
+  }
+  Entry& e = cache[next];
+  next = (next + 1) % 8;
+  e.map = kind == 0 ? make_x_map(base, rows, cols, ld) : make_y_map(base, rows, cols, ld, kind - 1);
+  e.base = base;
+  e.rows = rows;
+  e.cols = cols;
+  e.ld = ld;
+  e.kind = kind;
+  return e.map;
+}
+
 // W (m x n, bf16 or fp32, row stride ldw) for the TMA-staged merge: box =
 // 128 rows x one 128-byte column slab, 128-byte swizzle (loads and stores).
 // 3-D over layers: (n, m, L) with layer stride w_ls elements (L = 1: one matrix).
@@ -820,8 +849,24 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       return;
     }
   }
-  const CUtensorMap tmap_x = make_x_map(x, p->n, reg->d_in, ldx);
-  const CUtensorMap tmap_y = y_vec ? make_y_map(y, p->n, reg->d_out, ldy, y_dtype) : tmap_x;
+  // Tensor maps are encoded on first use only (the split path needs none) and
+  // cached per thread by (base, shape, stride): serving loops reuse buffers.
+  CUtensorMap tmap_x_v, tmap_y_v;
+  bool have_x = false, have_y = false;
+  auto tmap_x_get = [&]() -> const CUtensorMap& {
+    if (!have_x) {
+      tmap_x_v = cached_map(0, x, p->n, reg->d_in, ldx);
+      have_x = true;
+    }
+    return tmap_x_v;
+  };
+  auto tmap_y_get = [&]() -> const CUtensorMap& {
+    if (!have_y) {
+      tmap_y_v = y_vec ? cached_map(1 + y_dtype, y, p->n, reg->d_out, ldy) : tmap_x_get();
+      have_y = true;
+    }
+    return tmap_y_v;
+  };
 
   bool merged_ok = p->merged_first >= 0;
   for (size_t gi = merged_ok ? static_cast<size_t>(p->merged_first) : 0; merged_ok && gi < p->groups.size(); ++gi) {
@@ -923,7 +968,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       ga.count = count > 1 ? count : 1;
       for (int c = 0; c < ga.count; ++c) {
         const void* xc = count > 1 ? xs[c] : x;
-        ga.x_map[c] = count > 1 ? make_x_map(xc, p->n, reg->d_in, ldx) : tmap_x;
+        ga.x_map[c] = count > 1 ? cached_map(0, xc, p->n, reg->d_in, ldx) : tmap_x_get();
         ga.x[c] = xc;
         ga.y[c] = count > 1 ? ys[c] : y;
         ga.layer[c] = static_cast<int32_t>(count > 1 ? layers[c] : layer);
@@ -932,7 +977,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
       continue;
     }
-    const cudaError_t e = launch_bypass(y_dtype, tmap_x, tmap_y, bp, g.cluster, static_cast<int>(g.num_tiles), g.smem, stream);
+    const cudaError_t e = launch_bypass(y_dtype, tmap_x_get(), tmap_y_get(), bp, g.cluster, static_cast<int>(g.num_tiles), g.smem, stream);
     if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
   }
 }
@@ -1520,7 +1565,7 @@ int atmm_run_bypass_host_bf16_pipelined(const atmm_plan* p, const int64_t* layer
     };
     // Three independent batches in flight: one H2D, one on the SMs, one D2H
     // (the copy engines run both directions at once).
-    constexpr size_t kSlots = 4;
+    static const size_t kSlots = std::getenv("ATMM_E2E_SLOTS") ? std::max(2, std::atoi(std::getenv("ATMM_E2E_SLOTS"))) : 4;
     thread_local std::vector<std::unique_ptr<Slot>> slots;
     thread_local int slots_dev = -1;
     if (slots_dev != r->device) slots.clear();
