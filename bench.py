@@ -473,7 +473,7 @@ def impl_ours_bypass(args, w):
                "d2h_bytes_per_step": int(w.tokens * w.d_out * 2),
                "us_per_batch": e2e_s / e2e_steps * 1e6, "steps": e2e_steps,
                "path": "atmm_run_bypass_host_bf16_pipelined = run_bypass (batch.hpp:48) on pinned bf16 host "
-                       "buffers: H2D X, fused kernel into a fresh output, D2H; 3 streams"}
+                       "buffers: H2D X, fused kernel into a fresh output, D2H; 4 streams"}
         r_s = timed(lambda a, b, c: atmm.residual_host_bf16_pipelined(plan, a, b, c))
         e2e_res = {"value": world * flops_step * e2e_steps / r_s / 1e12, "unit": "TFLOP/s",
                    "h2d_bytes_per_step": int(w.tokens * (w.d_in + w.d_out) * 2),
