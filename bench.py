@@ -247,7 +247,49 @@ def impl_reference(args, w):
 
 
 # -------------------------------------------------------- ours (GPU) ------
-def measure_forward(atmm, plan, w, x, stream, reps=10, num_layers=2):
+def reference_forward_rate(w, seconds: float):
+    """The reference's forward_unmerged (model.hpp:216-246, fp32, its tiled
+    ATMM) on a bounded row sample of this workload, one layer, one sample per
+    host thread in parallel: TFLOP/s of 2 n d^2 + bypass FLOPs."""
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    d, rows = w.d_in, 16
+    threads = cpu_threads()
+    rng = np.random.default_rng(9)
+    W = rng.uniform(-1 / np.sqrt(d), 1 / np.sqrt(d), (1, d, d)).astype(np.float32)
+    ads = {}
+    for a, r in w.ranks.items():
+        s = 1.0 / np.sqrt(r)
+        ads[a] = (rng.uniform(-s, s, (1, d, r)).astype(np.float32), rng.uniform(-s, s, (1, r, d)).astype(np.float32))
+    asg = np.ascontiguousarray(w.assignment[:rows], np.int32)
+    x = rng.uniform(-1, 1, (rows, d)).astype(np.float32)
+    sub = {a: ads[a] for a in set(asg.tolist())}
+    flops = 2 * rows * d * d + sum(4 * d * w.ranks[int(a)] for a in asg)
+    ref.forward(x, W, "unmerged", asg, sub)  # warm-up
+    counts = [0] * threads
+    stop = threading.Event()
+
+    def worker(i):
+        while not stop.is_set():
+            ref.forward(x, W, "unmerged", asg, sub)
+            counts[i] += 1
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    time.sleep(seconds)
+    stop.set()
+    for t in ths:
+        t.join()
+    el = time.perf_counter() - t0
+    return {"tflops": flops * sum(counts) / el / 1e12, "cores": threads, "kind": "reference",
+            "sample": f"{sum(counts)} calls of forward_unmerged on {rows} rows x 1 layer (d {d}) in {el:.1f} s, "
+                      f"one per host thread, oracle/_ref built from the reference headers"}
+
+
+def measure_forward(atmm, plan, w, x, stream, reps=10, num_layers=2, cpu_sample_s=0.0):
     """Side measurement (not the headline): the model's layer forward
     tanh(x W_l + bypass_l(x)) (model.hpp:216-246) on this batch through
     LayerForward (bypass fused into the base GEMM as extra K blocks), beside
@@ -303,12 +345,18 @@ def measure_forward(atmm, plan, w, x, stream, reps=10, num_layers=2):
 
     t_f, t_u, t_c = per_layer_us(fused), per_layer_us(unfused), per_layer_us(cublas)
     flops = 2 * w.tokens * d * d + w.flops()
+    cpu_ref = None
+    if cpu_sample_s > 0:
+        try:
+            cpu_ref = reference_forward_rate(w, cpu_sample_s)
+        except FileNotFoundError as e:
+            cpu_ref = {"unavailable": str(e)}
     peak = measured_bf16_peak()
     st = fw.stats()
     return {"us_per_layer": t_f, "tflops": flops / (t_f * 1e-6) / 1e12,
             "roofline": {"bound": "tensor", "peak": peak, "unit": "TFLOP/s",
                          "frac": flops / (t_f * 1e-6) / 1e12 / peak if peak else None},
-            "unfused_us_per_layer": t_u, "cublas_mm_only_us_per_layer": t_c,
+            "unfused_us_per_layer": t_u, "cublas_mm_only_us_per_layer": t_c, "cpu_reference": cpu_ref,
             "layers": num_layers, "launches_per_layer": 2, "gemm_tile_n": st["bn"], "shrink_k_split": st["shrink_ks"],
             "note": "side measurement: tanh(x W + bypass) per layer, fused forward (fwd_shrink + fwd_gemm) vs "
                     "cuBLAS x@W + bypass kernel + tanh; W bf16 random, not the headline"}
@@ -423,7 +471,8 @@ def impl_ours_bypass(args, w):
 
     layer_fwd = None
     if not args.no_forward and w.d_in == w.d_out:
-        layer_fwd = measure_forward(atmm, plan, w, xs[0], stream, reps=10)
+        layer_fwd = measure_forward(atmm, plan, w, xs[0], stream, reps=10,
+                                    cpu_sample_s=0.0 if (args.no_cpu_baseline or world > 1 or rank != 0) else 3.0)
 
     flops_step = w.flops()
     value = world * flops_step * args.steps / (ms * 1e-3) / 1e12
