@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tma_prefetch_desc(&xmap);
     tma_prefetch_desc(&wmap);
   }
+  if (threadIdx.x == 0) FTRACE(4096, 0);
   if (warp == 1) tmem_alloc_cg2(&tslot, static_cast<uint32_t>(2 * bn));
   tc_fence_before();
   cluster_sync();
@@ -867,6 +868,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   }
+  if (threadIdx.x == 64) FTRACE(4096, 6);
   tc_fence_before();
   cluster_sync();  // no CTA leaves while its peer may still arrive / read its smem
   if (warp == 1) {
