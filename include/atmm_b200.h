@@ -333,6 +333,16 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
  *  first min(cap, 13) are written. */
 int atmm_forward_stats(const atmm_forward* f, int64_t* out, int64_t cap);
 
+/* Plain device GEMM C = A . B, the base-model product of every layer
+ * (atmm_multiply_into, atmm.hpp:111-154, with a dense right operand as in
+ * model.hpp:238): A m x k bf16 row-major (row stride lda), B k x n bf16
+ * row-major (ldb), C m x n (ldc) in c_dtype ATMM_BF16 or ATMM_F32, fp32
+ * accumulation on the tensor cores, C overwritten.  n a multiple of 8;
+ * lda / ldb multiples of 8, ldc 16-byte aligned rows; 16-byte aligned bases.
+ * The device is the current one; stream-ordered on `stream`.  k = 0 zeroes C. */
+int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int c_dtype,
+              int64_t m, int64_t k, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

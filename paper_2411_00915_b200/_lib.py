@@ -74,6 +74,8 @@ _SIGS = {
     "atmm_forward_run": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,
                                  c_void_p]),
     "atmm_forward_stats": (c_int, [c_void_p, i64p, c_int64]),
+    "atmm_gemm": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int, c_int64, c_int64, c_int64,
+                          c_void_p]),
     "atmm_plan_routing": (c_int, [c_void_p, i32p, i64p, i64p, i64p]),
     "atmm_plan_stats": (c_int, [c_void_p, i64p, i64p, i64p]),
     "atmm_plan_describe": (c_int, [c_void_p, ctypes.c_char_p, c_size_t]),

@@ -560,6 +560,32 @@ def forward_merged(w, x, device: Optional[int] = None):
     return LayerForward(None, n=x.shape[0], hidden_dim=x.shape[1], device=dev or 0).run(w, x)
 
 
+def gemm(a, b, out=None, out_dtype=None):
+    """Plain device GEMM out = a @ b (atmm_multiply_into, atmm.hpp:111-154,
+    with a dense right operand; the base GEMM of model.hpp:238): bf16 CUDA
+    tensors a [m, k], b [k, n] (unit inner stride), fp32 accumulation, out
+    bf16 or fp32 [m, n] (overwritten)."""
+    import torch
+
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[0]:
+        raise ShapeError(f"gemm shapes {tuple(a.shape)} x {tuple(b.shape)} do not chain")
+    if a.dtype != torch.bfloat16 or b.dtype != torch.bfloat16 or not (a.is_cuda and b.is_cuda):
+        raise ShapeError("a and b must be bf16 CUDA tensors")
+    if a.stride(1) != 1 or b.stride(1) != 1:
+        raise ShapeError("a and b need unit inner stride")
+    m, k = a.shape
+    n = b.shape[1]
+    if out is None:
+        out = torch.empty(m, n, device=a.device, dtype=out_dtype or torch.bfloat16)
+    if out.dtype not in (torch.bfloat16, torch.float32) or tuple(out.shape) != (m, n) or out.stride(1) != 1:
+        raise ShapeError("out must be a bf16 or fp32 [m, n] tensor with unit inner stride")
+    with torch.cuda.device(a.device):
+        _check(lib.atmm_gemm(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0),
+                             F32 if out.dtype == torch.float32 else BF16, m, k, n,
+                             torch.cuda.current_stream(a.device).cuda_stream))
+    return out
+
+
 def run_bypass_host_bf16_pipelined(plan: "BypassPlan", xs, outs, layers) -> None:
     """run_bypass (batch.hpp:48) end to end from bf16 host buffers (uint16
     numpy views, pinned for overlap): outs[i] = bypass(xs[i]) at layers[i],

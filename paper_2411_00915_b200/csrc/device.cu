@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -78,12 +79,16 @@ void require_device(int device) {
     fail(ATMM_ERR_NO_DEVICE, "no CUDA device visible: the ATMM operator has no CPU fallback");
   }
   if (device < 0 || device >= count) fail(ATMM_ERR_NO_DEVICE, "device ordinal out of range");
+  // cudaGetDeviceProperties costs milliseconds: check each device once
+  static std::atomic<uint8_t> checked[64] = {};
+  if (device < 64 && checked[device].load(std::memory_order_relaxed)) return;
   cudaDeviceProp prop;
   CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) {
     fail(ATMM_ERR_NO_DEVICE, std::string("device ") + prop.name +
                                  " is not sm_100 (Blackwell B200); kernels are built for sm_100a only");
   }
+  if (device < 64) checked[device].store(1, std::memory_order_relaxed);
 }
 
 struct DeviceGuard {
@@ -1795,12 +1800,12 @@ CUtensorMap make_act_map(const void* x, int64_t rows, int64_t d, int64_t ld) {
   if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(activations) failed: " + std::to_string(r));
   return m;
 }
-// Layer weights W_l (d x d bf16, [k][n], row stride ldw, layer stride w_ls):
+// Layer weights W_l (k x n bf16, [k][n], row stride ldw, layer stride w_ls):
 // box = 64 K rows x 64 N columns, 128-byte swizzle = the MN-major B operand.
-CUtensorMap make_layer_w_map(const void* w, int64_t d, int64_t ldw, int64_t L, int64_t w_ls) {
+CUtensorMap make_layer_w_map(const void* w, int64_t k, int64_t n, int64_t ldw, int64_t L, int64_t w_ls) {
   CUtensorMap m;
-  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(L)};
-  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldw) * 2, static_cast<cuuint64_t>(L > 1 ? w_ls : ldw * d) * 2};
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(L)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldw) * 2, static_cast<cuuint64_t>(L > 1 ? w_ls : ldw * k) * 2};
   const cuuint32_t box[3] = {kBK, kBK, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides, box, estr,
@@ -1811,6 +1816,44 @@ CUtensorMap make_layer_w_map(const void* w, int64_t d, int64_t ldw, int64_t L, i
 }
 void require_aligned16(const void* p, const char* what) {
   if (reinterpret_cast<uintptr_t>(p) % 16 != 0) fail(ATMM_ERR_SHAPE, std::string(what) + " must be 16-byte aligned");
+}
+
+// Tile shape of the base GEMM (m rows x n columns, nkb K blocks) on `sms` SMs
+// given the 1-SM / 2-SM choice: N tile width, persistent grid, ring depth and
+// the 1-SM split-K cluster size.
+struct GemmTiling {
+  int32_t bn = 128, ntn = 1, num_tiles = 1, stages = 1, grid = 1, kz = 1;
+  size_t smem = 0;
+};
+GemmTiling gemm_tiling(int64_t m, int64_t n, int32_t nkb, int sms, bool pair) {
+  GemmTiling t;
+  const int64_t row_tiles = (m + kTileM - 1) / kTileM;
+  const int64_t mtiles = pair ? (row_tiles + 1) / 2 : row_tiles;
+  const int64_t units = pair ? sms / 2 : sms;
+  t.bn = mtiles * ((n + 255) / 256) >= units ? 256 : 128;
+  if (const char* e = std::getenv("ATMM_FWD_BN")) t.bn = std::atoi(e) == 256 ? 256 : 128;
+  t.ntn = static_cast<int32_t>((n + t.bn - 1) / t.bn);
+  t.num_tiles = static_cast<int32_t>(mtiles) * t.ntn;
+  const size_t gstage = 16384 + static_cast<size_t>(pair ? t.bn / 2 : t.bn) * 128;
+  t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage));
+  t.smem = 1024 + t.stages * gstage;
+  if (pair) {
+    int clusters = fwd_gemm_pair_max_clusters(t.smem);
+    if (clusters <= 0) clusters = sms / 2;
+    t.grid = std::min(t.num_tiles, clusters) * 2;
+  } else {
+    // Split-K for small batches: clusters of kz CTAs per tile while every
+    // tile still gets its own cluster on the SMs and each rank >= 8 K blocks.
+    if (t.bn == 128) {
+      while (t.kz < 8 && int64_t(t.num_tiles) * t.kz * 2 <= sms && nkb / (t.kz * 2) >= 8) t.kz *= 2;
+    }
+    if (const char* e = std::getenv("ATMM_FWD_KZ")) {
+      const int v = std::atoi(e);
+      t.kz = (v == 2 || v == 4 || v == 8) && t.bn == 128 && nkb / v >= 1 ? v : 1;
+    }
+    t.grid = t.kz > 1 ? t.num_tiles * t.kz : std::min(t.num_tiles, sms);
+  }
+  return t;
 }
 }  // namespace
 }  // namespace atmm
@@ -1854,32 +1897,14 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
     const int64_t pair_tiles = int64_t((f->row_tiles + 1) / 2) * ((d + 255) / 256);
     f->pair = f->row_tiles >= 2 && (!bypass_plan || pair_tiles >= 2 * sms);
     if (const char* e = std::getenv("ATMM_FWD_PAIR")) f->pair = f->row_tiles >= 2 && std::atoi(e) != 0;
-    const int64_t mtiles = f->pair ? (f->row_tiles + 1) / 2 : f->row_tiles;
-    const int64_t units = f->pair ? sms / 2 : sms;
-    f->bn = mtiles * ((d + 255) / 256) >= units ? 256 : 128;
-    if (const char* e = std::getenv("ATMM_FWD_BN")) f->bn = std::atoi(e) == 256 ? 256 : 128;
-    f->ntn = static_cast<int32_t>((d + f->bn - 1) / f->bn);
-    f->num_tiles = static_cast<int32_t>(mtiles) * f->ntn;
-    const size_t gstage = 16384 + static_cast<size_t>(f->pair ? f->bn / 2 : f->bn) * 128;
-    f->stages_g = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage));
-    f->smem_g = 1024 + f->stages_g * gstage;
-    if (f->pair) {
-      int clusters = fwd_gemm_pair_max_clusters(f->smem_g);
-      if (clusters <= 0) clusters = sms / 2;
-      f->grid = std::min(f->num_tiles, clusters) * 2;
-    } else {
-      // Split-K for small batches: clusters of kz CTAs per tile while every
-      // tile still gets its own cluster on the SMs and each rank >= 8 K blocks.
-      f->kz = 1;
-      if (f->bn == 128) {
-        while (f->kz < 8 && int64_t(f->num_tiles) * f->kz * 2 <= sms && f->nkb / (f->kz * 2) >= 8) f->kz *= 2;
-      }
-      if (const char* e = std::getenv("ATMM_FWD_KZ")) {
-        const int v = std::atoi(e);
-        f->kz = (v == 2 || v == 4 || v == 8) && f->bn == 128 && f->nkb / v >= 1 ? v : 1;
-      }
-      f->grid = f->kz > 1 ? f->num_tiles * f->kz : std::min(f->num_tiles, sms);
-    }
+    const GemmTiling gt = gemm_tiling(n_, d, f->nkb, sms, f->pair);
+    f->bn = gt.bn;
+    f->ntn = gt.ntn;
+    f->num_tiles = gt.num_tiles;
+    f->stages_g = gt.stages;
+    f->smem_g = gt.smem;
+    f->grid = gt.grid;
+    f->kz = gt.kz;
 
     std::vector<int32_t> order;
     std::vector<FwdExt> exts;
@@ -2079,7 +2104,7 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
       CUDA_CHECK(cudaMemcpy2DAsync(out, ldo * 2, x, ldx * 2, d * 2, n, cudaMemcpyDeviceToDevice, st));
       return;
     }
-    const CUtensorMap wmap = make_layer_w_map(w, d, ldw, num_layers, w_layer_stride);
+    const CUtensorMap wmap = make_layer_w_map(w, d, d, ldw, num_layers, w_layer_stride);
     CUtensorMap xm;
     int cur = -1;  // -1: the caller's X
     if (f->sorted) {
@@ -2134,6 +2159,68 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
       }
       cur = nxt;
       xm = f->bmap[nxt];
+    }
+  });
+}
+
+// Plain device GEMM C = A . B (atmm.hpp:111-154 atmm_multiply_into with a
+// dense right operand; the base GEMM of model.hpp:238): the layer-forward
+// GEMM kernels without the bypass extension and with an identity epilogue.
+int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int c_dtype, int64_t m,
+              int64_t k, int64_t n, void* stream) {
+  return guarded([&] {
+    if (m < 0 || k < 0 || n < 0) fail(ATMM_ERR_SHAPE, "negative GEMM shape");
+    if (c_dtype != ATMM_BF16 && c_dtype != ATMM_F32) fail(ATMM_ERR_CONFIG, "c_dtype must be ATMM_BF16 or ATMM_F32");
+    if (n % 8 != 0) fail(ATMM_ERR_SHAPE, "n must be a multiple of 8 (16-byte output rows)");
+    if (m == 0 || n == 0) return;
+    if (!c || (k > 0 && (!a || !b))) fail(ATMM_ERR_CONFIG, "null A, B or C");
+    if (k > 0 && (lda < k || lda % 8 != 0)) fail(ATMM_ERR_SHAPE, "A row stride must be >= k and a multiple of 8");
+    if (k > 0 && (ldb < n || ldb % 8 != 0)) fail(ATMM_ERR_SHAPE, "B row stride must be >= n and a multiple of 8");
+    if (ldc < n || ldc % (c_dtype == ATMM_F32 ? 4 : 8) != 0) fail(ATMM_ERR_SHAPE, "C row stride must be >= n and 16-byte aligned");
+    if (m > std::numeric_limits<int32_t>::max() / 2 || n > (int64_t(1) << 31) || k > (int64_t(1) << 31)) {
+      fail(ATMM_ERR_SHAPE, "GEMM too large");
+    }
+    require_aligned16(a, "A");
+    require_aligned16(b, "B");
+    require_aligned16(c, "C");
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    require_device(dev);
+    const auto st = static_cast<cudaStream_t>(stream);
+    const size_t esz = c_dtype == ATMM_F32 ? 4 : 2;
+    if (k == 0) {
+      CUDA_CHECK(cudaMemset2DAsync(c, ldc * esz, 0, n * esz, m, st));
+      return;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int32_t nkb = static_cast<int32_t>((k + kBK - 1) / kBK);
+    const int64_t row_tiles = (m + kTileM - 1) / kTileM;
+    bool pair = row_tiles >= 2;
+    if (const char* e = std::getenv("ATMM_FWD_PAIR")) pair = row_tiles >= 2 && std::atoi(e) != 0;
+    const GemmTiling gt = gemm_tiling(m, n, nkb, sms, pair);
+    const CUtensorMap amap = make_act_map(a, m, k, lda);
+    const CUtensorMap bmap = make_layer_w_map(b, k, n, ldb, 1, 0);
+    FwdParams p{};
+    p.out = static_cast<uint16_t*>(c);
+    p.ldo = ldc;
+    p.n = m;
+    p.d = n;
+    p.bn = gt.bn;
+    p.ntn = gt.ntn;
+    p.num_tiles = gt.num_tiles;
+    p.nkb = nkb;
+    p.ks = 1;
+    p.stages = gt.stages;
+    p.pair = pair ? 1 : 0;
+    p.kz = gt.kz;
+    p.act_none = 1;
+    p.out_f32 = c_dtype == ATMM_F32 ? 1 : 0;
+    p.trace = g_trace;
+    if (pair) {
+      CUDA_CHECK(launch_fwd_gemm_pair(amap, bmap, amap, p, gt.grid, gt.smem, st));
+    } else {
+      CUDA_CHECK(launch_fwd_gemm(amap, bmap, p, gt.grid, gt.smem, st));
     }
   });
 }

@@ -232,6 +232,8 @@ struct FwdParams {
   const CUtensorMap* umaps;  // pair GEMM: per-slot up^T maps {64, r_pad/8, L * d_out_pad/8}, box {64, 4, bn/16}
   int32_t zero_img;          // pair GEMM: index of the zero A image (A images are 16 KB slots)
   int32_t kz;                // 1-SM GEMM split-K cluster size (1: none; > 1: one tile per cluster)
+  int32_t act_none;          // 1: plain GEMM epilogue (no tanh)
+  int32_t out_f32;           // plain GEMM: fp32 output (with act_none)
   uint64_t* trace;           // debug: per-CTA %globaltimer events (atmm_debug_set_trace)
 };
 

@@ -24,6 +24,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 
 #include "device_types.hpp"
@@ -70,6 +72,25 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(addr));
   return v;
+}
+
+// Epilogue store of 8 accumulator columns [c, c + 8) of one output row:
+// tanh (layer forward) or identity (plain GEMM), bf16 or fp32 out.
+__device__ __forceinline__ void store8(const FwdParams& p, int64_t orow, int col, const float (&a)[8]) {
+  if (p.act_none) {
+    if (p.out_f32) {
+      float* o = reinterpret_cast<float*>(p.out) + orow * p.ldo + col;
+      st_global_v4(o, __float_as_uint(a[0]), __float_as_uint(a[1]), __float_as_uint(a[2]), __float_as_uint(a[3]));
+      st_global_v4(o + 4, __float_as_uint(a[4]), __float_as_uint(a[5]), __float_as_uint(a[6]), __float_as_uint(a[7]));
+    } else {
+      st_global_v4(p.out + orow * p.ldo + col, pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]), pack_bf16x2(a[4], a[5]),
+                   pack_bf16x2(a[6], a[7]));
+    }
+    return;
+  }
+  st_global_v4(p.out + orow * p.ldo + col, pack_bf16x2(tanh_fast(a[0]), tanh_fast(a[1])),
+               pack_bf16x2(tanh_fast(a[2]), tanh_fast(a[3])), pack_bf16x2(tanh_fast(a[4]), tanh_fast(a[5])),
+               pack_bf16x2(tanh_fast(a[6]), tanh_fast(a[7])));
 }
 
 // Element offset of (row, col) in a K-extension A image: 128 x kk bf16 in
@@ -481,7 +502,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int64_t srow = int64_t(t) * kTileM + q * 32 + lane;
       const bool rv = srow < p.n;
       const int64_t orow = rv && p.out_rows ? p.out_rows[srow] : srow;
-      uint16_t* dst = p.out + orow * p.ldo + n0;
       mbar_wait_sleep(&tfull[acc], static_cast<uint32_t>(it >> 1) & 1u, 32);
       if (it == 0 && threadIdx.x == 64) FTRACE(4096, 4);
       tc_fence_after();
@@ -490,13 +510,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         uint32_t v[32];
         tmem_ld32(tbase + static_cast<uint32_t>(c), v);
         tmem_wait_ld();
-        uint32_t h[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) h[j] = pack_bf16x2(tanh_fast(__uint_as_float(v[2 * j])), tanh_fast(__uint_as_float(v[2 * j + 1])));
         if (rv) {
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
-            if (n0 + c + 8 * g < p.d) st_global_v4(dst + c + 8 * g, h[4 * g], h[4 * g + 1], h[4 * g + 2], h[4 * g + 3]);
+            float a8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a8[j] = __uint_as_float(v[8 * g + j]);
+            if (n0 + c + 8 * g < p.d) store8(p, orow, n0 + c + 8 * g, a8);
           }
         }
       }
@@ -575,9 +595,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           acc[7] += __uint_as_float(v1.w);
         }
         const int64_t orow = p.out_rows ? p.out_rows[srow] : srow;
-        st_global_v4(p.out + orow * p.ldo + n0 + c, pack_bf16x2(tanh_fast(acc[0]), tanh_fast(acc[1])),
-                     pack_bf16x2(tanh_fast(acc[2]), tanh_fast(acc[3])), pack_bf16x2(tanh_fast(acc[4]), tanh_fast(acc[5])),
-                     pack_bf16x2(tanh_fast(acc[6]), tanh_fast(acc[7])));
+        store8(p, orow, n0 + c, acc);
       }
     }
   }
@@ -839,7 +857,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int64_t srow = int64_t(t) * kTileM + q * 32 + lane;
       const bool rv = srow < p.n;
       const int64_t orow = rv && p.out_rows ? p.out_rows[srow] : srow;
-      uint16_t* dst = p.out + orow * p.ldo + n0;
       mbar_wait_sleep(&tfull[acc], static_cast<uint32_t>(it >> 1) & 1u, 32);
       tc_fence_after();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * bn);
@@ -847,13 +864,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         uint32_t v[32];
         tmem_ld32(tbase + static_cast<uint32_t>(c), v);
         tmem_wait_ld();
-        uint32_t h[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) h[j] = pack_bf16x2(tanh_fast(__uint_as_float(v[2 * j])), tanh_fast(__uint_as_float(v[2 * j + 1])));
         if (rv) {
 #pragma unroll
           for (int gg = 0; gg < 4; ++gg) {
-            if (n0 + c + 8 * gg < p.d) st_global_v4(dst + c + 8 * gg, h[4 * gg], h[4 * gg + 1], h[4 * gg + 2], h[4 * gg + 3]);
+            float a8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a8[j] = __uint_as_float(v[8 * gg + j]);
+            if (n0 + c + 8 * gg < p.d) store8(p, orow, n0 + c + 8 * gg, a8);
           }
         }
       }
@@ -900,6 +917,16 @@ cudaError_t launch_fwd_gemm_pair(const CUtensorMap& xmap, const CUtensorMap& wma
 }
 
 int fwd_gemm_pair_max_clusters(size_t smem) {
+  // the occupancy query is slow: cache it per (device, smem)
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, smem});
+    if (it != cache.end()) return it->second;
+  }
   if (cudaFuncSetAttribute(fwd_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
       cudaSuccess)
     return 0;
@@ -919,6 +946,8 @@ int fwd_gemm_pair_max_clusters(size_t smem) {
     cudaGetLastError();
     return 0;
   }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[{dev, smem}] = n;
   return n;
 }
 

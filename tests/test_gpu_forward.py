@@ -189,3 +189,59 @@ def test_forward_errors_and_edges(gpu, atmm, oracle):
     with pytest.raises(atmm.ShapeError):
         atmm.LayerForward(None, n=4, hidden_dim=100)
     torch.cuda.synchronize()
+
+
+GEMM_CASES = [(1, 64, 8), (7, 104, 136), (130, 256, 512), (300, 1000, 264), (257, 72, 1024), (512, 4096, 4096)]
+
+
+@pytest.mark.parametrize("m,k,n", GEMM_CASES)
+@pytest.mark.parametrize("out", ["bf16", "f32"])
+def test_gemm_parity(gpu, atmm, oracle, monkeypatch, m, k, n, out):
+    """atmm_gemm (the base GEMM of model.hpp:238, atmm_multiply_into with a
+    dense operand) against an fp64 product of the same bf16 inputs, over the
+    1-SM, split-K and 2-SM tile paths; reruns bit-identical."""
+    import torch
+
+    rng = np.random.default_rng(m * 7 + k + n)
+    a = oracle.round_bf16(rng.uniform(-1, 1, (m, k)))
+    b = oracle.round_bf16(rng.uniform(-1, 1, (k, n)) / np.sqrt(k))
+    want = a @ b
+    dt = torch.float32 if out == "f32" else torch.bfloat16
+    for pair, kz in [("1", "1"), ("0", "1"), ("0", "2"), ("0", "4")]:
+        monkeypatch.setenv("ATMM_FWD_PAIR", pair)
+        monkeypatch.setenv("ATMM_FWD_KZ", kz)
+        at, bt = _dev(a), _dev(b)
+        got = atmm.gemm(at, bt, out_dtype=dt)
+        again = atmm.gemm(at, bt, out_dtype=dt)
+        torch.cuda.synchronize()
+        g = got.float().cpu().numpy()
+        assert np.max(np.abs(g - want)) <= tol_for(want), (pair, kz)
+        assert torch.equal(got, again)
+
+
+def test_gemm_strides_and_edges(gpu, atmm, oracle):
+    import torch
+
+    rng = np.random.default_rng(1)
+    a = oracle.round_bf16(rng.uniform(-1, 1, (70, 96)))
+    b = oracle.round_bf16(rng.uniform(-1, 1, (96, 40)))
+    abig = torch.zeros(70, 128, device="cuda", dtype=torch.bfloat16)
+    abig[:, :96] = _dev(a)
+    bbig = torch.zeros(96, 64, device="cuda", dtype=torch.bfloat16)
+    bbig[:, :40] = _dev(b)
+    cbig = torch.full((70, 48), 7.0, device="cuda")
+    atmm.gemm(abig[:, :96], bbig[:, :40], out=cbig[:, :40])
+    got = cbig.cpu().numpy()
+    assert np.max(np.abs(got[:, :40] - a @ b)) <= tol_for(a @ b)
+    assert np.all(got[:, 40:] == 7.0), "columns past n must not be written"
+    # k = 0 zeroes C; m = 0 is a no-op
+    c = torch.full((5, 8), 3.0, device="cuda")
+    atmm.gemm(torch.empty(5, 0, device="cuda", dtype=torch.bfloat16),
+              torch.empty(0, 8, device="cuda", dtype=torch.bfloat16), out=c)
+    assert torch.count_nonzero(c) == 0
+    atmm.gemm(torch.empty(0, 16, device="cuda", dtype=torch.bfloat16), _dev(b[:16, :8]))
+    with pytest.raises(atmm.ShapeError):
+        atmm.gemm(_dev(a), _dev(b[:, :36]))          # n not a multiple of 8
+    with pytest.raises(atmm.ShapeError):
+        atmm.gemm(_dev(a), _dev(b[:64]))             # shapes do not chain
+    torch.cuda.synchronize()
