@@ -51,6 +51,7 @@ cudaError_t launch_fwd_gemm(const CUtensorMap& xmap, const CUtensorMap& wmap, co
 cudaError_t launch_fwd_gemm_pair(const CUtensorMap& xmap, const CUtensorMap& wmap, const CUtensorMap& amap,
                                  const FwdParams& p, int grid, size_t smem, cudaStream_t stream);
 int fwd_gemm_pair_max_clusters(size_t smem);
+int fwd_gemm_max_clusters(size_t smem, int csize);
 cudaError_t launch_pack_factors(const float* down, const float* up, int64_t L, int64_t d_in, int64_t d_out,
                                 int64_t r, int64_t d_in_pad, int64_t d_out_pad, int64_t r_pad, uint16_t* down_t,
                                 uint16_t* up_t, cudaStream_t stream);
@@ -1788,11 +1789,11 @@ struct atmm_forward {
 namespace atmm {
 namespace {
 // Activations (rows x d bf16, row stride ld): box = 128 rows x one 64-wide K block, 128-byte swizzle.
-CUtensorMap make_act_map(const void* x, int64_t rows, int64_t d, int64_t ld) {
+CUtensorMap make_act_map(const void* x, int64_t rows, int64_t d, int64_t ld, int box_rows = kTileM) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-  const cuuint32_t box[2] = {kBK, kTileM};
+  const cuuint32_t box[2] = {kBK, static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1822,15 +1823,19 @@ void require_aligned16(const void* p, const char* what) {
 // given the 1-SM / 2-SM choice: N tile width, persistent grid, ring depth and
 // the 1-SM split-K cluster size.
 struct GemmTiling {
-  int32_t bn = 128, ntn = 1, num_tiles = 1, stages = 1, grid = 1, kz = 1;
+  int32_t bn = 128, ntn = 1, num_tiles = 1, stages = 1, grid = 1, kz = 1, mc = 1;
   size_t smem = 0;
 };
-GemmTiling gemm_tiling(int64_t m, int64_t n, int32_t nkb, int sms, bool pair) {
+int gemm_krot() { return std::getenv("ATMM_GEMM_NOROT") ? 0 : 1; }
+GemmTiling gemm_tiling(int64_t m, int64_t n, int32_t nkb, int sms, bool pair, bool allow_mc = false) {
   GemmTiling t;
   const int64_t row_tiles = (m + kTileM - 1) / kTileM;
   const int64_t mtiles = pair ? (row_tiles + 1) / 2 : row_tiles;
   const int64_t units = pair ? sms / 2 : sms;
-  t.bn = mtiles * ((n + 255) / 256) >= units ? 256 : 128;
+  // 256-wide N tiles once they alone fill the SMs, or when 128-wide ones
+  // would need more waves (measured: m = 1024, n = 4096 pair tiles 41 -> 26 us)
+  const int64_t t128 = mtiles * ((n + 127) / 128), t256 = mtiles * ((n + 255) / 256);
+  t.bn = t256 >= units || (t128 + units - 1) / units > (t256 + units - 1) / units ? 256 : 128;
   if (const char* e = std::getenv("ATMM_FWD_BN")) t.bn = std::atoi(e) == 256 ? 256 : 128;
   t.ntn = static_cast<int32_t>((n + t.bn - 1) / t.bn);
   t.num_tiles = static_cast<int32_t>(mtiles) * t.ntn;
@@ -1852,6 +1857,19 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int32_t nkb, int sms, bool pair) {
       t.kz = (v == 2 || v == 4 || v == 8) && t.bn == 128 && nkb / v >= 1 ? v : 1;
     }
     t.grid = t.kz > 1 ? t.num_tiles * t.kz : std::min(t.num_tiles, sms);
+    // A multicast across mc adjacent N tiles (plain GEMM; replaces split-K)
+    if (allow_mc) {
+      if (const char* e = std::getenv("ATMM_GEMM_MC")) {
+        const int v = std::atoi(e);
+        if ((v == 2 || v == 4) && t.ntn % v == 0) t.mc = v;
+      }
+      if (t.mc > 1) {
+        t.kz = 1;
+        int clusters = fwd_gemm_max_clusters(t.smem, t.mc);
+        if (clusters <= 0) clusters = sms / t.mc;
+        t.grid = std::min(t.num_tiles / t.mc, clusters) * t.mc;
+      }
+    }
   }
   return t;
 }
@@ -2137,6 +2155,8 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     p.umaps = f->umaps.p;
     p.zero_img = static_cast<int32_t>(f->zero_off / 16384);
     p.trace = g_trace;
+    p.krot = gemm_krot();
+    p.mc = 1;
     for (int64_t l = 0; l < num_layers; ++l) {
       const bool last = l + 1 == num_layers;
       const int nxt = cur == 0 ? 1 : 0;
@@ -2198,8 +2218,8 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     const int64_t row_tiles = (m + kTileM - 1) / kTileM;
     bool pair = row_tiles >= 2;
     if (const char* e = std::getenv("ATMM_FWD_PAIR")) pair = row_tiles >= 2 && std::atoi(e) != 0;
-    const GemmTiling gt = gemm_tiling(m, n, nkb, sms, pair);
-    const CUtensorMap amap = make_act_map(a, m, k, lda);
+    const GemmTiling gt = gemm_tiling(m, n, nkb, sms, pair, true);
+    const CUtensorMap amap = make_act_map(a, m, k, lda, kTileM / gt.mc);
     const CUtensorMap bmap = make_layer_w_map(b, k, n, ldb, 1, 0);
     FwdParams p{};
     p.out = static_cast<uint16_t*>(c);
@@ -2215,6 +2235,8 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     p.pair = pair ? 1 : 0;
     p.kz = gt.kz;
     p.act_none = 1;
+    p.krot = gemm_krot();
+    p.mc = gt.mc;
     p.out_f32 = c_dtype == ATMM_F32 ? 1 : 0;
     p.trace = g_trace;
     if (pair) {

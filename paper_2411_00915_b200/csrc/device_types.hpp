@@ -234,6 +234,8 @@ struct FwdParams {
   int32_t kz;                // 1-SM GEMM split-K cluster size (1: none; > 1: one tile per cluster)
   int32_t act_none;          // 1: plain GEMM epilogue (no tanh)
   int32_t out_f32;           // plain GEMM: fp32 output (with act_none)
+  int32_t mc;                // 1-SM GEMM A-multicast cluster size (1: none; exclusive with kz > 1)
+  int32_t krot;              // 1: rotate each tile's K order by its N tile index (spreads A reads over L2)
   uint64_t* trace;           // debug: per-CTA %globaltimer events (atmm_debug_set_trace)
 };
 

@@ -356,9 +356,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   // accumulates K blocks [kb0, kb1) and the last rank adds the K-extension
   // blocks; partial rows meet their owner rank by bulk DSMEM pushes and are
   // summed in rank order (deterministic), then tanh.  One tile per cluster.
-  const int kz = p.kz;
-  const int z = static_cast<int>(blockIdx.x) % kz;
-  const int cl = static_cast<int>(blockIdx.x) / kz, ncl = static_cast<int>(gridDim.x) / kz;
+  // A multicast (mc > 1, small batches, no split-K): a cluster of mc CTAs
+  // runs mc adjacent N tiles of one row tile in lockstep; each CTA loads
+  // 128 / mc rows of every A block and multicasts them to all, so the A
+  // traffic per SM drops mc-fold.  A stage is refilled once every CTA of the
+  // cluster has consumed it (empty count mc, commits multicast).
+  const int kz = p.kz, mc = p.mc;
+  const int csize = kz * mc;
+  const int crank = static_cast<int>(blockIdx.x) % csize;
+  const int z = kz > 1 ? crank : 0;
+  const int mr = mc > 1 ? crank : 0;
+  const uint16_t mc_mask = static_cast<uint16_t>((1u << mc) - 1u);
+  const int cl = static_cast<int>(blockIdx.x) / csize, ncl = static_cast<int>(gridDim.x) / csize;
+  // work units: tiles (mc == 1) or groups of mc N tiles (tile of this CTA: tile_of)
+  const int gpr = p.ntn / mc, ngroups = p.num_tiles / mc;
+  auto tile_of = [&](int g) { return mc == 1 ? g : (g / gpr) * p.ntn + (g % gpr) * mc + mr; };
   const int kb0 = p.nkb * z / kz, kb1 = p.nkb * (z + 1) / kz;
   const bool do_ext = p.exts != nullptr && z == kz - 1;
   const int rows_per = kTileM / kz;
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], static_cast<uint32_t>(mc));
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -383,8 +395,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (threadIdx.x == 0) FTRACE(4096, 0);
   if (warp == 1) tmem_alloc(&tslot, static_cast<uint32_t>(2 * bn));
   tc_fence_before();
-  if (kz > 1) {
-    cluster_sync();
+  if (csize > 1) {
+    cluster_sync();  // (mc: every CTA's barriers exist before any multicast lands)
   } else {
     __syncthreads();
   }
@@ -403,18 +415,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // griddep_wait, so cur is complete; the A images are waited for below.
       bool waited = p.exts == nullptr;
       if (waited) griddep_wait();
+      FTRACE(4096, 7);
       int i = 0;
-      for (int tile = cl; tile < p.num_tiles; tile += ncl) {
+      for (int g = cl; g < ngroups; g += ncl) {
+        const int tile = tile_of(g);
         const int t = tile / p.ntn;
         const int n0 = (tile % p.ntn) * bn;
-        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+        // K order rotated per tile (per group under mc: the cluster's A
+        // blocks must match) so concurrent CTAs spread over the L2 lines
+        const int nk = kb1 - kb0, rot = p.krot ? (g % max(gpr, 1)) % max(nk, 1) : 0;
+        for (int j = 0; j < nk; ++j, ++i) {
+          const int kb = kb0 + (j + rot < nk ? j + rot : j + rot - nk);
           const int s = i % S;
           const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);
           uint8_t* a = sm + s * kStage;
           uint8_t* b = a + kFwdA;
           mbar_arrive_expect_tx(&full[s], kStage);
-          tma_load_2d(a, &xmap, &full[s], kb * kBK, t * kTileM);
+          if (mc > 1) {
+            const int rows = kTileM / mc;
+            tma_load_2d_mc(a + mr * rows * 128, &xmap, &full[s], kb * kBK, t * kTileM + mr * rows, mc_mask);
+          } else {
+            tma_load_2d(a, &xmap, &full[s], kb * kBK, t * kTileM);
+          }
           for (int c = 0; c < bn; c += 64) tma_load_3d(b + c * 128, &wmap, &full[s], n0 + c, kb * kBK, p.layer);
         }
         if (!do_ext) continue;
@@ -440,9 +463,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (x.kk == x.r_pad) {
             bulk_g2s(b, ub, g_bytes * static_cast<uint32_t>(g_n), &full[s]);
           } else {
-            for (int g = 0; g < g_n; ++g) bulk_g2s(b + g * g_bytes, ub + int64_t(g) * x.r_pad * 8, g_bytes, &full[s]);
+            for (int gg = 0; gg < g_n; ++gg) bulk_g2s(b + gg * g_bytes, ub + int64_t(gg) * x.r_pad * 8, g_bytes, &full[s]);
           }
         }
+      }
+      if (mc > 1) {  // every CTA's commits to this CTA's empty barriers have landed
+        for (int j = 0; j < S; ++j, ++i) mbar_wait(&empty[i % S], (static_cast<uint32_t>(i / S) & 1u) ^ 1u);
       }
       griddep_launch_dependents();
     }
@@ -452,13 +478,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const uint32_t idesc_main = idesc_bf16(128, static_cast<uint32_t>(bn), 0, 1);
       const uint32_t idesc_ext = idesc_bf16(128, static_cast<uint32_t>(bn));
       int i = 0, it = 0;
-      for (int tile = cl; tile < p.num_tiles; tile += ncl, ++it) {
-        const int t = tile / p.ntn;
+      for (int g = cl; g < ngroups; g += ncl, ++it) {
+        const int t = tile_of(g) / p.ntn;
         const int acc = it & 1;
         mbar_wait(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
-        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {  // (the producer's rotated K order: the sum is order-free here)
           const int s = i % S;
           mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
           if (it == 0 && kb == kb0) FTRACE(4096, 1);
@@ -469,7 +495,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             mma_bf16(d, smem_desc(a + k * 32, 16, 1024, kLayoutSW128), smem_desc(b + k * 2048, 8192, 1024, kLayoutSW128),
                      idesc_main, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);
+          if (mc > 1) {
+            mma_commit_mc(&empty[s], mc_mask);
+          } else {
+            mma_commit(&empty[s]);
+          }
         }
         if (do_ext) {
           for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
@@ -484,7 +514,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               mma_bf16(d, smem_desc(a + k * 256, 128, sbo_a, kLayoutNone), bd, idesc_ext, 1u);
               mma_bf16(d, smem_desc(a + kk * 16 + k * 256, 128, sbo_a, kLayoutNone), bd, idesc_ext, 1u);
             }
-            mma_commit(&empty[s]);
+            if (mc > 1) {
+              mma_commit_mc(&empty[s], mc_mask);
+            } else {
+              mma_commit(&empty[s]);
+            }
           }
         }
         if (it == 0) FTRACE(4096, 2);
@@ -495,7 +529,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   } else if (kz == 1) {
     const int q = warp & 3;
     int it = 0;
-    for (int tile = cl; tile < p.num_tiles; tile += ncl, ++it) {
+    for (int g = cl; g < ngroups; g += ncl, ++it) {
+      const int tile = tile_of(g);
       const int t = tile / p.ntn;
       const int n0 = (tile % p.ntn) * bn;
       const int acc = it & 1;
@@ -602,8 +637,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (threadIdx.x == 64) FTRACE(4096, 6);
   if (threadIdx.x == 64 && p.trace) p.trace[(4096 + blockIdx.x) * 16 + 15] = clock64();
   tc_fence_before();
-  if (kz > 1) {
-    cluster_sync();  // every pushed partial has landed before any rank leaves
+  if (csize > 1) {
+    cluster_sync();  // every pushed partial / multicast block has landed before any rank leaves
   } else {
     __syncthreads();
   }
@@ -687,7 +722,7 @@ cudaError_t launch_fwd_gemm(const CUtensorMap& xmap, const CUtensorMap& wmap, co
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;  // split-K cluster (1: plain)
-  attr[0].val.clusterDim.x = static_cast<unsigned>(p.kz);
+  attr[0].val.clusterDim.x = static_cast<unsigned>(p.kz * p.mc);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -763,7 +798,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int t = 2 * pi + rank;
         const int n0 = (g % p.ntn) * bn;
         const int nh = n0 + rank * hb;  // this CTA's half of the N tile
-        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+        // K order rotated per N tile: the CTAs that share a row tile then read
+        // different A blocks at any moment instead of all hitting the same L2 lines
+        const int rot = p.krot ? (g % p.ntn) % p.nkb : 0;
+        for (int j = 0; j < p.nkb; ++j, ++i) {
+          const int kb = j + rot < p.nkb ? j + rot : j + rot - p.nkb;
           const int s = i % S;
           mbar_wait(&empty[s], (static_cast<uint32_t>(i / S) & 1u) ^ 1u);
           uint8_t* a = sm + s * kStage;
@@ -914,6 +953,40 @@ cudaError_t launch_fwd_gemm_pair(const CUtensorMap& xmap, const CUtensorMap& wma
   cfg.attrs = attr;
   cfg.numAttrs = std::getenv("ATMM_NO_PDL") ? 1 : 2;
   return cudaLaunchKernelEx(&cfg, fwd_gemm_pair_kernel, xmap, wmap, amap, p);
+}
+
+int fwd_gemm_max_clusters(size_t smem, int csize) {
+  static std::mutex mu;
+  static std::map<std::pair<int, std::pair<size_t, int>>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, {smem, csize}});
+    if (it != cache.end()) return it->second;
+  }
+  if (cudaFuncSetAttribute(fwd_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+      cudaSuccess)
+    return 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(csize);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kFwdThreads, 1, 1);
+  cfg.gridDim = dim3(static_cast<unsigned>(csize), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fwd_gemm_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache[{dev, {smem, csize}}] = n;
+  return n;
 }
 
 int fwd_gemm_pair_max_clusters(size_t smem) {

@@ -245,3 +245,24 @@ def test_gemm_strides_and_edges(gpu, atmm, oracle):
     with pytest.raises(atmm.ShapeError):
         atmm.gemm(_dev(a), _dev(b[:64]))             # shapes do not chain
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("mc", ["2", "4"])
+@pytest.mark.parametrize("m,k,n", [(1, 64, 512), (130, 1000, 1024), (300, 4096, 2048)])
+def test_gemm_a_multicast(gpu, atmm, oracle, monkeypatch, mc, m, k, n):
+    """The 1-SM GEMM with A multicast over clusters of mc N tiles."""
+    import torch
+
+    monkeypatch.setenv("ATMM_FWD_PAIR", "0")
+    monkeypatch.setenv("ATMM_FWD_BN", "128")
+    monkeypatch.setenv("ATMM_GEMM_MC", mc)
+    rng = np.random.default_rng(m + k + n)
+    a = oracle.round_bf16(rng.uniform(-1, 1, (m, k)))
+    b = oracle.round_bf16(rng.uniform(-1, 1, (k, n)) / np.sqrt(k))
+    want = a @ b
+    at, bt = _dev(a), _dev(b)
+    got = atmm.gemm(at, bt, out_dtype=torch.float32)
+    again = atmm.gemm(at, bt, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(got.cpu().numpy() - want)) <= tol_for(want)
+    assert torch.equal(got, again)
