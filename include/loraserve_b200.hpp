@@ -236,6 +236,15 @@ inline void merge_layers_into(const AdapterRegistry& reg, int adapter_id, std::s
                                 static_cast<int64_t>(w_layer_stride), w_dtype, sign, stream));
 }
 
+// atmm_multiply_into (atmm.hpp:111-142) on device buffers with a dense right
+// operand, the base GEMM of every layer (model.hpp:238): C = A . B, bf16 A/B
+// row-major, C bf16 or fp32 (c_dtype ATMM_BF16 / ATMM_F32), overwritten.
+inline void gemm(const void* a, std::size_t lda, const void* b, std::size_t ldb, void* c, std::size_t ldc, int c_dtype,
+                 std::size_t m, std::size_t k, std::size_t n, void* stream = nullptr) {
+  check(atmm_gemm(a, static_cast<int64_t>(lda), b, static_cast<int64_t>(ldb), c, static_cast<int64_t>(ldc), c_dtype,
+                  static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(n), stream));
+}
+
 // forward_mixture's per-layer bypass (model.hpp:252-328) on device buffers:
 // guest rows (adapter != merged_id) get (x.down_a).up_a - (x.down_m).up_m in
 // ONE launch through combined slots (ids combined_base - k); merged rows are

@@ -56,6 +56,8 @@ static void host_checks() {
   CHECK(p3.segments.size() == 3);
   for (const Segment& s : p3.segments) CHECK(s.rows.size() == 1);
   CHECK_THROWS_AS(plan_batch({}), ConfigError);
+  // device GEMM shape checks run before any device access
+  CHECK_THROWS_AS(gemm(nullptr, 8, nullptr, 40, nullptr, 40, ATMM_F32, 4, 8, 36), ShapeError);
 
   // test_tiling.cpp:55-87 -- validity, bucketing, lookup rules
   CHECK((TilingConfig{64, 32, 32, 32, 32, 32}.structurally_valid()));
@@ -223,6 +225,28 @@ static void gpu_checks() {
     }
     CHECK(fworst <= 2e-2);  // bf16 output + bf16-rounded mid in run_bypass
     CHECK_THROWS_AS(fw.run(wd, d, d * d, 2, xd, d, od, d), ShapeError);  // the adapters carry one layer
+  }
+  // gemm (atmm.hpp:111-142 with a dense operand): X . I == X exactly, fp32 out
+  {
+    std::vector<uint16_t> eye(d * d, 0);
+    for (std::size_t i = 0; i < d; ++i) eye[i * d + i] = 0x3F80;  // bf16 1.0
+    void* cd = nullptr;
+    CHECK(cudaMemcpy(wd, eye.data(), d * d * 2, cudaMemcpyHostToDevice) == cudaSuccess);
+    CHECK(cudaMalloc(&cd, n * d * 4) == cudaSuccess);
+    gemm(xd, d, wd, d, cd, d, ATMM_F32, n, d, d);
+    std::vector<float> cg(n * d);
+    std::vector<uint16_t> xdev(n * d);
+    CHECK(cudaMemcpy(cg.data(), cd, n * d * 4, cudaMemcpyDeviceToHost) == cudaSuccess);
+    CHECK(cudaMemcpy(xdev.data(), xd, n * d * 2, cudaMemcpyDeviceToHost) == cudaSuccess);
+    bool same = true;
+    for (std::size_t i = 0; i < n * d; ++i) {
+      const uint32_t bits = static_cast<uint32_t>(xdev[i]) << 16;
+      float want;
+      std::memcpy(&want, &bits, 4);
+      same = same && cg[i] == want;
+    }
+    CHECK(same);
+    cudaFree(cd);
   }
   cudaFree(wd);
   cudaFree(od);
