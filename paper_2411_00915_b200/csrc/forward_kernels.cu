@@ -573,6 +573,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float* recv = stage + kTileM * pitch;                         // kz slots x rows_per x pitch
     if (tile < p.num_tiles) {
       mbar_wait_sleep(&tfull[0], 0, 32);
+      if (threadIdx.x == 64) FTRACE(4096, 4);
       tc_fence_after();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
       for (int c = 0; c < bn; c += 32) {
@@ -585,11 +586,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
     fence_proxy_async_smem();
+    if (threadIdx.x == 64) FTRACE(4096, 5);
   }
   if (kz > 1) {
     // every rank's MMAs are done (its ring is free for the receive slots) and
     // its partial is staged before anything is pushed
     cluster_sync();
+    if (threadIdx.x == 64) FTRACE(4096, 8);
   }
   if (warp >= 2 && kz > 1) {
     const int tile = cl;
@@ -605,6 +608,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
     mbar_wait_cluster(&recv_bar, 0);
+    if (threadIdx.x == 64) FTRACE(4096, 9);
     if (tile < p.num_tiles) {
       const int tid = static_cast<int>(threadIdx.x) - 64;
       const int groups = bn / 8;
