@@ -15,7 +15,7 @@ import paper_2411_00915_b200 as atmm  # noqa: E402
 from paper_2411_00915_b200._lib import lib  # noqa: E402
 
 EV = {0: "start", 7: "griddep released", 1: "first full", 2: "tile0 mma issued", 4: "tile0 tfull",
-      5: "tile0 epi/staged", 8: "kz cluster sync", 9: "kz partials in", 6: "end"}
+      5: "tile0 epi done", 6: "end"}
 
 
 def main():
