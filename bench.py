@@ -441,6 +441,21 @@ def impl_ours_bypass(args, w):
     ms_local = e0.elapsed_time(e1)
     ms = max_over_ranks(ms_local, world)
 
+    # ---- single-launch latency: one eager call bracketed by
+    # events on an idle GPU, median of 20 (includes the launch itself) ----
+    single = []
+    with torch.cuda.stream(stream):
+        for i in range(20):
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a0.record(stream)
+            step(i, stream)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            single.append(a0.elapsed_time(a1) * 1e3)
+    single_launch_us = float(np.median(single))
+
     # ---- grouped launches: G consecutive independent steps (e.g. the q/k/v
     # projections of one decoder layer) as ONE launch (atmm_bypass_apply_group) ----
     grouped = None
@@ -550,6 +565,7 @@ def impl_ours_bypass(args, w):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "us_per_batch": ms_per_step * 1e3,
+            "single_launch_us": single_launch_us,
             "config": {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens,
                        "adapters": len(w.ranks), "ranks": sorted(set(w.ranks.values())),
                        "segment_rows": sorted(set(w.lengths.values()))[:4],

@@ -2155,7 +2155,7 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     p.umaps = f->umaps.p;
     p.zero_img = static_cast<int32_t>(f->zero_off / 16384);
     p.trace = g_trace;
-    p.krot = gemm_krot();
+    p.krot = f->pair ? gemm_krot() : 0;  // measured: helps pairs, costs 1-SM 256-wide tiles
     p.mc = 1;
     for (int64_t l = 0; l < num_layers; ++l) {
       const bool last = l + 1 == num_layers;
@@ -2235,7 +2235,7 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     p.pair = pair ? 1 : 0;
     p.kz = gt.kz;
     p.act_none = 1;
-    p.krot = gemm_krot();
+    p.krot = pair ? gemm_krot() : 0;
     p.mc = gt.mc;
     p.out_f32 = c_dtype == ATMM_F32 ? 1 : 0;
     p.trace = g_trace;
