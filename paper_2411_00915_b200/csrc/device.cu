@@ -2155,7 +2155,9 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     p.umaps = f->umaps.p;
     p.zero_img = static_cast<int32_t>(f->zero_off / 16384);
     p.trace = g_trace;
-    p.krot = f->pair ? gemm_krot() : 0;  // measured: helps pairs, costs 1-SM 256-wide tiles
+    // natural K order: forward_mixture's host rows stay bit-identical to
+    // forward_merged across the 1-SM / pair kernels (rotation was neutral here)
+    p.krot = 0;
     p.mc = 1;
     for (int64_t l = 0; l < num_layers; ++l) {
       const bool last = l + 1 == num_layers;
@@ -2235,7 +2237,7 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     p.pair = pair ? 1 : 0;
     p.kz = gt.kz;
     p.act_none = 1;
-    p.krot = pair ? gemm_krot() : 0;
+    p.krot = pair ? gemm_krot() : 0;  // measured: helps pairs (m = 256: 32 -> 23 us), costs 1-SM 256-wide tiles
     p.mc = gt.mc;
     p.out_f32 = c_dtype == ATMM_F32 ? 1 : 0;
     p.trace = g_trace;
