@@ -1841,6 +1841,7 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int32_t nkb, int sms, bool pair, bo
   t.num_tiles = static_cast<int32_t>(mtiles) * t.ntn;
   const size_t gstage = 16384 + static_cast<size_t>(pair ? t.bn / 2 : t.bn) * 128;
   t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage));
+  if (const char* e = std::getenv("ATMM_GEMM_STAGES")) t.stages = std::clamp(std::atoi(e), 2, t.stages);  // A/B
   t.smem = 1024 + t.stages * gstage;
   if (pair) {
     int clusters = fwd_gemm_pair_max_clusters(t.smem);
