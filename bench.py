@@ -441,6 +441,34 @@ def impl_ours_bypass(args, w):
     ms_local = e0.elapsed_time(e1)
     ms = max_over_ranks(ms_local, world)
 
+    # ---- ATMM_PLAN_X_READY: the same K steps with X gathered before
+    # griddepcontrol.wait (X is never written here; a bypass that follows the
+    # base GEMM Y = X W may promise the same).  Side measurement ----
+    x_ready = None
+    plan.set_x_ready(True)
+    gx = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gx, stream=stream, capture_error_mode="thread_local"):
+        for i in range(args.steps):
+            step(i, stream)
+    plan.set_x_ready(False)
+    gx.replay()
+    torch.cuda.synchronize()
+    x0 = torch.cuda.Event(enable_timing=True)
+    x1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        x0.record(stream)
+        gx.replay()
+        x1.record(stream)
+    torch.cuda.synchronize()
+    xms = max_over_ranks(x0.elapsed_time(x1), world)
+    x_ready = {"us_per_batch": xms * 1e3 / args.steps,
+               "value": world * w.flops() * args.steps / (xms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "roofline_frac": step_bytes / (xms * 1e-3 / args.steps) / 1e9 / measured_peaks()[0],
+               "note": "same steps with atmm_plan_set_flags(ATMM_PLAN_X_READY): X gathered under the previous "
+                       "launch's tail; not the headline"}
+
     # ---- single-launch latency: one eager call bracketed by
     # events on an idle GPU, median of 20 (includes the launch itself) ----
     single = []
@@ -566,6 +594,7 @@ def impl_ours_bypass(args, w):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "us_per_batch": ms_per_step * 1e3,
             "single_launch_us": single_launch_us,
+            "x_ready": x_ready,
             "config": {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens,
                        "adapters": len(w.ranks), "ranks": sorted(set(w.ranks.values())),
                        "segment_rows": sorted(set(w.lengths.values()))[:4],

@@ -189,6 +189,15 @@ int atmm_plan_create(atmm_registry* r, const int32_t* assignment, int64_t n,
 int atmm_plan_create_mapped(atmm_registry* r, const int32_t* assignment, const int32_t* rows, int64_t n,
                             int64_t n_rows, const atmm_table* table, atmm_plan** out);
 void atmm_plan_destroy(atmm_plan* p);
+/* Plan flags (no reference counterpart: a launch-ordering promise).
+ * ATMM_PLAN_X_READY: the X handed to every apply of this plan is complete
+ * before the launch preceding the apply on its stream starts (e.g. the
+ * bypass follows the base GEMM Y = X.W, which reads X and writes Y).  The
+ * fused kernels then gather X before griddepcontrol.wait, under the tail of
+ * that launch; Y is still read only after it completes.  Results are
+ * unchanged; breaking the promise races on X. */
+#define ATMM_PLAN_X_READY 1u
+int atmm_plan_set_flags(atmm_plan* p, uint32_t flags);
 /* Routing tables actually uploaded (for bit-exact routing checks):
  * seg_adapter[S], seg_offsets[S+1], row_index[n]. */
 int atmm_plan_routing(const atmm_plan* p, int32_t* seg_adapter, int64_t* seg_offsets,

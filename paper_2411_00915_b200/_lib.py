@@ -69,6 +69,7 @@ _SIGS = {
     "atmm_merge_apply_layers": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_int64, c_int64, c_int,
                                         c_float, c_void_p]),
     "atmm_plan_destroy": (None, [c_void_p]),
+    "atmm_plan_set_flags": (c_int, [c_void_p, ctypes.c_uint32]),
     "atmm_forward_create": (c_int, [c_void_p, c_int, c_int64, c_int64, POINTER(c_void_p)]),
     "atmm_forward_destroy": (None, [c_void_p]),
     "atmm_forward_run": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,

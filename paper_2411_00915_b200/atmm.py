@@ -384,6 +384,13 @@ class BypassPlan:
     def handle(self):
         return self._h
 
+    def set_x_ready(self, ready: bool = True) -> None:
+        """ATMM_PLAN_X_READY: promise that the X of every apply is complete
+        before the launch preceding the apply on its stream starts (e.g. the
+        bypass follows the base GEMM Y = X W); X is then gathered under that
+        launch's tail.  Results are unchanged."""
+        _check(lib.atmm_plan_set_flags(self._h, 1 if ready else 0))
+
     def routing(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
         seg = np.zeros(self.n_routed, np.int32)
         off = np.zeros(self.n_routed + 1, np.int64)

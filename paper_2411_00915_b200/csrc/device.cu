@@ -550,6 +550,7 @@ struct atmm_plan {
   std::vector<int32_t> rows_host;  // routed entry (plan order) -> X / Y row
   DevBuf<TileDesc> d_tiles;
   int64_t total_ctas = 0;
+  uint32_t flags = 0;  // ATMM_PLAN_*
 };
 
 namespace atmm {
@@ -943,6 +944,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
     bp.ny = g.ny;
     bp.ycols = y_dtype == ATMM_BF16 ? 64 : 32;
     bp.ybuf_bytes = g.ybuf_bytes;
+    bp.x_ready = (p->flags & ATMM_PLAN_X_READY) ? 1 : 0;
     bp.red_rows = g.red_rows;
     bp.r_pad_max = g.r_pad_max;
     bp.off_up = g.off_up;
@@ -1389,6 +1391,14 @@ int atmm_plan_create_mapped(atmm_registry* r, const int32_t* assignment, const i
     if (n_rows < n) fail(ATMM_ERR_SHAPE, "n_rows must be >= the number of routed rows");
     const TilingTable* t = table ? &table->t : nullptr;
     *out = build_plan(r, assignment, n, t, nullptr, rows, n_rows).release();
+  });
+}
+
+int atmm_plan_set_flags(atmm_plan* p, uint32_t flags) {
+  return guarded([&] {
+    if (!p) fail(ATMM_ERR_CONFIG, "null plan");
+    if (flags & ~ATMM_PLAN_X_READY) fail(ATMM_ERR_CONFIG, "unknown plan flag");
+    p->flags = flags;
   });
 }
 

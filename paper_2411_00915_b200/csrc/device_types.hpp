@@ -85,6 +85,7 @@ struct BypassParams {
   // the buffer, off_up the whole up^T slice of the CTA.
   int32_t ypitch;
   int32_t gcols;        // output columns owned per epilogue thread (= expand MMAs per CTA: 1, 2, 4, 8)
+  int32_t x_ready;      // 1: X is not written by the preceding launch (gathered before griddepcontrol.wait)
 };
 
 constexpr int kTraceEvents = 32;

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     const uint32_t b_bytes = static_cast<uint32_t>(r_pad) * kBK * 2u;
     const uint32_t a_bytes = static_cast<uint32_t>(ngroups) * 512u;
     // X may be produced by the previous kernel (programmatic dependent launch).
-    griddep_wait();
+    if (!p.x_ready) griddep_wait();
     int stage = 0;
     uint32_t phase = 0;
     for (int kb = kb_lo; kb < kb_hi; ++kb) {
@@ -974,7 +974,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
 #pragma unroll
       for (int q = 0; q < 4; ++q) gr[q] = rows_s[min(g * 4 + q, rows - 1)];
     }
-    griddep_wait();  // X may be produced by the previous kernel
+    if (!p.x_ready) griddep_wait();  // X may be produced by the previous kernel
     int stage = 0;
     uint32_t phase = 0;
     for (int kb = kb_lo; kb < kb_hi; ++kb) {

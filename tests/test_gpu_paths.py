@@ -177,3 +177,40 @@ def test_large_batch_row_subset(gpu, atmm, oracle):
     want = y0[pick].float().cpu().numpy().astype(np.float64) + oracle.bypass_rows_f64(xs, assignment[pick], facs)
     got = y[pick].float().cpu().numpy()
     assert np.max(np.abs(got - want)) <= tol_for(want)
+
+
+@pytest.mark.parametrize("path", ["a2a", "fused", "split"])
+def test_x_ready_flag_same_results(gpu, atmm, oracle, monkeypatch, path):
+    """ATMM_PLAN_X_READY (X gathered before griddepcontrol.wait): K
+    back-to-back applies on one stream over distinct (X, Y) buffers give the
+    same bits as without the flag, and match the oracle."""
+    import torch
+
+    monkeypatch.setenv("ATMM_PATH", path)
+    d_in, d_out, ranks, lens = CASES[2]
+    facs, assignment, x, y0 = _inputs(oracle, d_in, d_out, ranks, lens, seed=5)
+    reg = atmm.AdapterRegistry(1, d_in, d_out)
+    for a, (down, up) in facs.items():
+        reg.put(a, down, up)
+    plan = atmm.BypassPlan(reg, assignment)
+    K = 6
+    rng = np.random.default_rng(3)
+    xs = [torch.from_numpy(oracle.round_bf16(x * rng.uniform(0.5, 1.5))).to("cuda", torch.bfloat16) for _ in range(K)]
+    ys0 = [torch.from_numpy(y0).to("cuda", torch.bfloat16) for _ in range(K)]
+    runs = []
+    for ready in (False, True):
+        plan.set_x_ready(ready)
+        ys = [y.clone() for y in ys0]
+        torch.cuda.synchronize()
+        for k in range(K):
+            plan.apply(xs[k], ys[k], layer=0)
+        torch.cuda.synchronize()
+        runs.append([y.float().cpu().numpy() for y in ys])
+    for k in range(K):
+        assert np.array_equal(runs[0][k], runs[1][k]), k
+    want = y0.astype(np.float64) + oracle.bypass_rows_f64(xs[K - 1].float().cpu().numpy(), assignment, facs)
+    assert np.max(np.abs(runs[1][K - 1] - want)) <= tol_for(want)
+    from paper_2411_00915_b200 import atmm as mod
+
+    with pytest.raises(atmm.ConfigError):  # unknown flag bits
+        mod._check(mod.lib.atmm_plan_set_flags(plan.handle, 8))
