@@ -1783,6 +1783,7 @@ struct atmm_forward {
   int32_t stages_g = 0, stages_s = 0, grid = 0, sbytes = 0;
   bool pair = false;  // GEMM as 2-SM CTA pairs (fwd_gemm_pair_kernel)
   int32_t kz = 1;     // 1-SM GEMM split-K cluster
+  bool bk2 = false;   // 1-SM GEMM with 128-deep K stages (A as 64-wide atoms)
   int64_t zero_off = 0;
   CUtensorMap amap;            // pair GEMM: the A images, 16 KB slots
   DevBuf<CUtensorMap> umaps;   // pair GEMM: per-slot up^T maps
@@ -1794,6 +1795,7 @@ struct atmm_forward {
   DevBuf<int32_t> ext_begin, order;
   DevBuf<FwdItem> items;
   CUtensorMap bmap[2];
+  CUtensorMap bmap2[2];  // bk2: the same buffers as 64-wide K atoms (GEMM A operand)
 };
 
 namespace atmm {
@@ -1813,16 +1815,31 @@ CUtensorMap make_act_map(const void* x, int64_t rows, int64_t d, int64_t ld, int
 }
 // Layer weights W_l (k x n bf16, [k][n], row stride ldw, layer stride w_ls):
 // box = 64 K rows x 64 N columns, 128-byte swizzle = the MN-major B operand.
-CUtensorMap make_layer_w_map(const void* w, int64_t k, int64_t n, int64_t ldw, int64_t L, int64_t w_ls) {
+CUtensorMap make_layer_w_map(const void* w, int64_t k, int64_t n, int64_t ldw, int64_t L, int64_t w_ls,
+                             int box_k = kBK) {
   CUtensorMap m;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(L)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldw) * 2, static_cast<cuuint64_t>(L > 1 ? w_ls : ldw * k) * 2};
-  const cuuint32_t box[3] = {kBK, kBK, 1};
+  const cuuint32_t box[3] = {kBK, static_cast<cuuint32_t>(box_k), 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(layer W) failed: " + std::to_string(r));
+  return m;
+}
+// Activations as 64-wide K atoms (K % 64 == 0): dims {64, rows, K / 64},
+// box {64, 128 rows, 2 atoms} = two 128-byte-swizzled K-major blocks.
+CUtensorMap make_act_map_atoms(const void* x, int64_t rows, int64_t k, int64_t ld) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kBK), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(k / kBK)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(kBK) * 2};
+  const cuuint32_t box[3] = {kBK, kTileM, 2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(activation atoms) failed: " + std::to_string(r));
   return m;
 }
 void require_aligned16(const void* p, const char* what) {
@@ -1834,10 +1851,25 @@ void require_aligned16(const void* p, const char* what) {
 // the 1-SM split-K cluster size.
 struct GemmTiling {
   int32_t bn = 128, ntn = 1, num_tiles = 1, stages = 1, grid = 1, kz = 1, mc = 1;
+  bool bk2 = false;  // 128-deep K stages (1-SM, bn 128, no split-K / multicast, K % 64 == 0)
   size_t smem = 0;
 };
 int gemm_krot() { return std::getenv("ATMM_GEMM_NOROT") ? 0 : 1; }
-GemmTiling gemm_tiling(int64_t m, int64_t n, int32_t nkb, int sms, bool pair, bool allow_mc = false) {
+bool bk2_enabled() {
+  static const bool on = !std::getenv("ATMM_GEMM_BK2") || std::atoi(std::getenv("ATMM_GEMM_BK2")) != 0;
+  return on;
+}
+// Without a bypass: 2-SM pairs unless one wave of 1-SM 128 x 128 tiles with
+// 128-deep K stages covers the GEMM (measured m = 512, n = k = 4096: 19.1 us
+// vs 22.9 us for pairs; m = 1024 needs two waves and pairs win, 26 vs 34 us).
+bool pair_without_bypass(int64_t m, int64_t n, int64_t k, int sms) {
+  const int64_t row_tiles = (m + kTileM - 1) / kTileM;
+  if (row_tiles < 2) return false;
+  if (const char* e = std::getenv("ATMM_FWD_PAIR")) return std::atoi(e) != 0;
+  return !(bk2_enabled() && k % kBK == 0 && row_tiles * ((n + 127) / 128) <= sms);
+}
+GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool allow_mc = false) {
+  const int32_t nkb = static_cast<int32_t>((k + kBK - 1) / kBK);
   GemmTiling t;
   const int64_t row_tiles = (m + kTileM - 1) / kTileM;
   const int64_t mtiles = pair ? (row_tiles + 1) / 2 : row_tiles;
@@ -1880,6 +1912,19 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int32_t nkb, int sms, bool pair, bo
         if (clusters <= 0) clusters = sms / t.mc;
         t.grid = std::min(t.num_tiles / t.mc, clusters) * t.mc;
       }
+    }
+    // 128-deep K stages: half the TMA instructions and barrier round trips
+    // (measured m = 512, n = k = 4096: 25.2 -> 19.1 us; 256-wide tiles lose,
+    // two stages only).  ATMM_GEMM_BK2=0 disables (A/B).
+    if (bk2_enabled() && t.kz == 2 && t.mc == 1 && k % kBK == 0 && !std::getenv("ATMM_FWD_KZ")) {
+      t.kz = 1;  // measured m = 256: 128-deep stages 18.4 us beat split-K 2 at 20.4 us (split-K 4 still wins)
+      t.grid = std::min(t.num_tiles, sms);
+    }
+    if (bk2_enabled() && t.kz == 1 && t.mc == 1 && t.bn == 128 && k % kBK == 0) {
+      t.bk2 = true;
+      const size_t gstage2 = 2 * 16384 + static_cast<size_t>(t.bn) * 256;
+      t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage2));
+      t.smem = 1024 + t.stages * gstage2;
     }
   }
   return t;
@@ -1924,9 +1969,10 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
     // (measured: cfg5-sized batches win, cfg2/cfg3-sized ones lose).
     const bool bypass_plan = plan && !plan->bp.seg_adapter.empty();
     const int64_t pair_tiles = int64_t((f->row_tiles + 1) / 2) * ((d + 255) / 256);
-    f->pair = f->row_tiles >= 2 && (!bypass_plan || pair_tiles >= 2 * sms);
+    f->pair = bypass_plan ? f->row_tiles >= 2 && pair_tiles >= 2 * sms : pair_without_bypass(n_, d, d, sms);
     if (const char* e = std::getenv("ATMM_FWD_PAIR")) f->pair = f->row_tiles >= 2 && std::atoi(e) != 0;
-    const GemmTiling gt = gemm_tiling(n_, d, f->nkb, sms, f->pair);
+    const GemmTiling gt = gemm_tiling(n_, d, d, sms, f->pair);
+    f->bk2 = gt.bk2;
     f->bn = gt.bn;
     f->ntn = gt.ntn;
     f->num_tiles = gt.num_tiles;
@@ -2087,6 +2133,7 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
     for (int b = 0; b < 2; ++b) {
       f->buf[b].alloc(static_cast<size_t>(n_ * d));
       f->bmap[b] = make_act_map(f->buf[b].p, n_, d, d);
+      if (f->bk2) f->bmap2[b] = make_act_map_atoms(f->buf[b].p, n_, d, d);
     }
     *out = f.release();
   });
@@ -2133,15 +2180,17 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
       CUDA_CHECK(cudaMemcpy2DAsync(out, ldo * 2, x, ldx * 2, d * 2, n, cudaMemcpyDeviceToDevice, st));
       return;
     }
-    const CUtensorMap wmap = make_layer_w_map(w, d, d, ldw, num_layers, w_layer_stride);
-    CUtensorMap xm;
+    const CUtensorMap wmap = make_layer_w_map(w, d, d, ldw, num_layers, w_layer_stride, f->bk2 ? 2 * kBK : kBK);
+    CUtensorMap xm, xg;  // activations for the shrink / for the GEMM (64-wide K atoms under bk2)
     int cur = -1;  // -1: the caller's X
     if (f->sorted) {
       CUDA_CHECK(launch_fwd_gather(static_cast<const uint16_t*>(x), ldx, f->buf[0].p, d, f->order.p, n, d, st));
       cur = 0;
       xm = f->bmap[0];
+      xg = f->bk2 ? f->bmap2[0] : xm;
     } else {
       xm = make_act_map(x, n, d, ldx);
+      xg = f->bk2 ? make_act_map_atoms(x, n, d, ldx) : xm;
     }
     FwdParams p{};
     const bool bypass = f->num_ext > 0;
@@ -2170,6 +2219,7 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     // forward_merged across the 1-SM / pair kernels (rotation was neutral here)
     p.krot = 0;
     p.mc = 1;
+    p.bk2 = f->bk2 ? 1 : 0;
     for (int64_t l = 0; l < num_layers; ++l) {
       const bool last = l + 1 == num_layers;
       const int nxt = cur == 0 ? 1 : 0;
@@ -2187,11 +2237,12 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
         if (f->pair) {
           CUDA_CHECK(launch_fwd_gemm_pair(xm, wmap, f->amap, p, f->grid, f->smem_g, st));
         } else {
-          CUDA_CHECK(launch_fwd_gemm(xm, wmap, p, f->grid, f->smem_g, st));
+          CUDA_CHECK(launch_fwd_gemm(xg, wmap, p, f->grid, f->smem_g, st));
         }
       }
       cur = nxt;
       xm = f->bmap[nxt];
+      xg = f->bk2 ? f->bmap2[nxt] : xm;
     }
   });
 }
@@ -2228,12 +2279,11 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int32_t nkb = static_cast<int32_t>((k + kBK - 1) / kBK);
-    const int64_t row_tiles = (m + kTileM - 1) / kTileM;
-    bool pair = row_tiles >= 2;
-    if (const char* e = std::getenv("ATMM_FWD_PAIR")) pair = row_tiles >= 2 && std::atoi(e) != 0;
-    const GemmTiling gt = gemm_tiling(m, n, nkb, sms, pair, true);
-    const CUtensorMap amap = make_act_map(a, m, k, lda, kTileM / gt.mc);
-    const CUtensorMap bmap = make_layer_w_map(b, k, n, ldb, 1, 0);
+    const bool pair = pair_without_bypass(m, n, k, sms);
+    const GemmTiling gt = gemm_tiling(m, n, k, sms, pair, true);
+    const bool bk2 = gt.bk2;
+    const CUtensorMap amap = bk2 ? make_act_map_atoms(a, m, k, lda) : make_act_map(a, m, k, lda, kTileM / gt.mc);
+    const CUtensorMap bmap = make_layer_w_map(b, k, n, ldb, 1, 0, bk2 ? 2 * kBK : kBK);
     FwdParams p{};
     p.out = static_cast<uint16_t*>(c);
     p.ldo = ldc;
@@ -2250,6 +2300,7 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     p.act_none = 1;
     p.krot = pair ? gemm_krot() : 0;  // measured: helps pairs (m = 256: 32 -> 23 us), costs 1-SM 256-wide tiles
     p.mc = gt.mc;
+    p.bk2 = bk2 ? 1 : 0;
     p.out_f32 = c_dtype == ATMM_F32 ? 1 : 0;
     p.trace = g_trace;
     if (pair) {

@@ -237,6 +237,7 @@ struct FwdParams {
   int32_t out_f32;           // plain GEMM: fp32 output (with act_none)
   int32_t mc;                // 1-SM GEMM A-multicast cluster size (1: none; exclusive with kz > 1)
   int32_t krot;              // 1: rotate each tile's K order by its N tile index (spreads A reads over L2)
+  int32_t bk2;               // plain GEMM: 128-deep K stages (xmap 3-D {64, rows, K / 64}, wmap box 128 K rows)
   uint64_t* trace;           // debug: per-CTA %globaltimer events (atmm_debug_set_trace)
 };
 

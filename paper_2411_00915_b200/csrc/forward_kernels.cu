@@ -350,7 +350,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2], recv_bar;
   __shared__ uint32_t tslot;
   const int S = p.stages, bn = p.bn;
-  const uint32_t kStage = kFwdA + static_cast<uint32_t>(bn) * 128u;
+  // bk2 (plain GEMM, K % 64 == 0): 128-deep K stages, A as two 64-wide atoms
+  // in one 3-D TMA box, W as 128-row boxes: half the TMA instructions and
+  // barrier round trips per K
+  const bool bk2 = p.bk2 != 0;
+  const uint32_t kA = bk2 ? 2u * kFwdA : kFwdA;
+  const uint32_t kStage = kA + static_cast<uint32_t>(bn) * (bk2 ? 256u : 128u);
   const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   // Split-K (small batches): a cluster of kz CTAs shares one tile, rank z
   // accumulates K blocks [kb0, kb1) and the last rank adds the K-extension
@@ -421,24 +426,36 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int tile = tile_of(g);
         const int t = tile / p.ntn;
         const int n0 = (tile % p.ntn) * bn;
-        // K order rotated per tile (per group under mc: the cluster's A
-        // blocks must match) so concurrent CTAs spread over the L2 lines
-        const int nk = kb1 - kb0, rot = p.krot ? (g % max(gpr, 1)) % max(nk, 1) : 0;
-        for (int j = 0; j < nk; ++j, ++i) {
-          const int kb = kb0 + (j + rot < nk ? j + rot : j + rot - nk);
-          const int s = i % S;
-          const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);
-          uint8_t* a = sm + s * kStage;
-          uint8_t* b = a + kFwdA;
-          mbar_arrive_expect_tx(&full[s], kStage);
-          if (mc > 1) {
-            const int rows = kTileM / mc;
-            tma_load_2d_mc(a + mr * rows * 128, &xmap, &full[s], kb * kBK, t * kTileM + mr * rows, mc_mask);
-          } else {
-            tma_load_2d(a, &xmap, &full[s], kb * kBK, t * kTileM);
+        if (bk2) {
+          for (int j = 0; j < (p.nkb + 1) / 2; ++j, ++i) {
+            const int s = i % S;
+            mbar_wait(&empty[s], (static_cast<uint32_t>(i / S) & 1u) ^ 1u);
+            uint8_t* a = sm + s * kStage;
+            uint8_t* b = a + kA;
+            mbar_arrive_expect_tx(&full[s], kStage);
+            tma_load_3d(a, &xmap, &full[s], 0, t * kTileM, 2 * j);
+            for (int c = 0; c < bn; c += 64) tma_load_3d(b + c * 256, &wmap, &full[s], n0 + c, j * 2 * kBK, p.layer);
           }
-          for (int c = 0; c < bn; c += 64) tma_load_3d(b + c * 128, &wmap, &full[s], n0 + c, kb * kBK, p.layer);
+        } else {
+          // K order rotated per tile (per group under mc: the cluster's A
+          // blocks must match) so concurrent CTAs spread over the L2 lines
+          const int nk = kb1 - kb0, rot = p.krot ? (g % max(gpr, 1)) % max(nk, 1) : 0;
+          for (int j = 0; j < nk; ++j, ++i) {
+            const int kb = kb0 + (j + rot < nk ? j + rot : j + rot - nk);
+            const int s = i % S;
+            const uint32_t ph = static_cast<uint32_t>(i / S) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            uint8_t* a = sm + s * kStage;
+            uint8_t* b = a + kFwdA;
+            mbar_arrive_expect_tx(&full[s], kStage);
+            if (mc > 1) {
+              const int rows = kTileM / mc;
+              tma_load_2d_mc(a + mr * rows * 128, &xmap, &full[s], kb * kBK, t * kTileM + mr * rows, mc_mask);
+            } else {
+              tma_load_2d(a, &xmap, &full[s], kb * kBK, t * kTileM);
+            }
+            for (int c = 0; c < bn; c += 64) tma_load_3d(b + c * 128, &wmap, &full[s], n0 + c, kb * kBK, p.layer);
+          }
         }
         if (!do_ext) continue;
         for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
@@ -484,21 +501,36 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
-        for (int kb = kb0; kb < kb1; ++kb, ++i) {  // (the producer's rotated K order: the sum is order-free here)
-          const int s = i % S;
-          mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
-          if (it == 0 && kb == kb0) FTRACE(4096, 1);
-          tc_fence_after();
-          const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
+        if (bk2) {
+          for (int j = 0; j < (p.nkb + 1) / 2; ++j, ++i) {
+            const int s = i % S;
+            mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
+            tc_fence_after();
+            const uint32_t a = smem_u32(sm + s * kStage), b = a + kA;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            mma_bf16(d, smem_desc(a + k * 32, 16, 1024, kLayoutSW128), smem_desc(b + k * 2048, 8192, 1024, kLayoutSW128),
-                     idesc_main, (kb > kb0 || k > 0) ? 1u : 0u);
-          }
-          if (mc > 1) {
-            mma_commit_mc(&empty[s], mc_mask);
-          } else {
+            for (int k = 0; k < 8; ++k) {
+              mma_bf16(d, smem_desc(a + (k >> 2) * kFwdA + (k & 3) * 32, 16, 1024, kLayoutSW128),
+                       smem_desc(b + k * 2048, 16384, 1024, kLayoutSW128), idesc_main, (j > 0 || k > 0) ? 1u : 0u);
+            }
             mma_commit(&empty[s]);
+          }
+        } else {
+          for (int kb = kb0; kb < kb1; ++kb, ++i) {  // (the producer's rotated K order: the sum is order-free here)
+            const int s = i % S;
+            mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
+            if (it == 0 && kb == kb0) FTRACE(4096, 1);
+            tc_fence_after();
+            const uint32_t a = smem_u32(sm + s * kStage), b = a + kFwdA;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              mma_bf16(d, smem_desc(a + k * 32, 16, 1024, kLayoutSW128), smem_desc(b + k * 2048, 8192, 1024, kLayoutSW128),
+                       idesc_main, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            if (mc > 1) {
+              mma_commit_mc(&empty[s], mc_mask);
+            } else {
+              mma_commit(&empty[s]);
+            }
           }
         }
         if (do_ext) {
