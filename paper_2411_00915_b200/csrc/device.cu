@@ -1916,11 +1916,7 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool
     // 128-deep K stages: half the TMA instructions and barrier round trips
     // (measured m = 512, n = k = 4096: 25.2 -> 19.1 us; 256-wide tiles lose,
     // two stages only).  ATMM_GEMM_BK2=0 disables (A/B).
-    if (bk2_enabled() && t.kz == 2 && t.mc == 1 && k % kBK == 0 && !std::getenv("ATMM_FWD_KZ")) {
-      t.kz = 1;  // measured m = 256: 128-deep stages 18.4 us beat split-K 2 at 20.4 us (split-K 4 still wins)
-      t.grid = std::min(t.num_tiles, sms);
-    }
-    if (bk2_enabled() && t.kz == 1 && t.mc == 1 && t.bn == 128 && k % kBK == 0) {
+    if (bk2_enabled() && t.mc == 1 && t.bn == 128 && k % kBK == 0 && (k / kBK + 1) / 2 >= t.kz) {
       t.bk2 = true;
       const size_t gstage2 = 2 * 16384 + static_cast<size_t>(t.bn) * 256;
       t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage2));

@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int gpr = p.ntn / mc, ngroups = p.num_tiles / mc;
   auto tile_of = [&](int g) { return mc == 1 ? g : (g / gpr) * p.ntn + (g % gpr) * mc + mr; };
   const int kb0 = p.nkb * z / kz, kb1 = p.nkb * (z + 1) / kz;
+  const int nk2 = (p.nkb + 1) / 2, j0 = nk2 * z / kz, j1 = nk2 * (z + 1) / kz;  // bk2: 128-deep K blocks
   const bool do_ext = p.exts != nullptr && z == kz - 1;
   const int rows_per = kTileM / kz;
   const int pitch = bn + 4;  // fp32 words per staged row (16-byte skew)
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int t = tile / p.ntn;
         const int n0 = (tile % p.ntn) * bn;
         if (bk2) {
-          for (int j = 0; j < (p.nkb + 1) / 2; ++j, ++i) {
+          for (int j = j0; j < j1; ++j, ++i) {
             const int s = i % S;
             mbar_wait(&empty[s], (static_cast<uint32_t>(i / S) & 1u) ^ 1u);
             uint8_t* a = sm + s * kStage;
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
         if (bk2) {
-          for (int j = 0; j < (p.nkb + 1) / 2; ++j, ++i) {
+          for (int j = j0; j < j1; ++j, ++i) {
             const int s = i % S;
             mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
             tc_fence_after();
@@ -510,7 +511,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               mma_bf16(d, smem_desc(a + (k >> 2) * kFwdA + (k & 3) * 32, 16, 1024, kLayoutSW128),
-                       smem_desc(b + k * 2048, 16384, 1024, kLayoutSW128), idesc_main, (j > 0 || k > 0) ? 1u : 0u);
+                       smem_desc(b + k * 2048, 16384, 1024, kLayoutSW128), idesc_main, (j > j0 || k > 0) ? 1u : 0u);
             }
             mma_commit(&empty[s]);
           }
