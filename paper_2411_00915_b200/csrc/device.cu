@@ -1855,6 +1855,10 @@ struct GemmTiling {
   size_t smem = 0;
 };
 int gemm_krot() { return std::getenv("ATMM_GEMM_NOROT") ? 0 : 1; }
+bool pair_bk2_enabled() {
+  static const bool on = !std::getenv("ATMM_PAIR_BK2") || std::atoi(std::getenv("ATMM_PAIR_BK2")) != 0;  // A/B
+  return on;
+}
 bool bk2_enabled() {
   static const bool on = !std::getenv("ATMM_GEMM_BK2") || std::atoi(std::getenv("ATMM_GEMM_BK2")) != 0;
   return on;
@@ -1886,6 +1890,12 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool
   if (const char* e = std::getenv("ATMM_GEMM_STAGES")) t.stages = std::clamp(std::atoi(e), 2, t.stages);  // A/B
   t.smem = 1024 + t.stages * gstage;
   if (pair) {
+    if (bk2_enabled() && k % kBK == 0 && pair_bk2_enabled()) {  // 128-deep K stages
+      t.bk2 = true;
+      const size_t gstage2 = 2 * 16384 + static_cast<size_t>(t.bn / 2) * 256;
+      t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage2));
+      t.smem = 1024 + t.stages * gstage2;
+    }
     int clusters = fwd_gemm_pair_max_clusters(t.smem);
     if (clusters <= 0) clusters = sms / 2;
     t.grid = std::min(t.num_tiles, clusters) * 2;
@@ -2231,7 +2241,7 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
       static const int only = std::getenv("ATMM_FWD_ONLY") ? std::atoi(std::getenv("ATMM_FWD_ONLY")) : 0;  // A/B: 1 = shrink only
       if (only != 1) {
         if (f->pair) {
-          CUDA_CHECK(launch_fwd_gemm_pair(xm, wmap, f->amap, p, f->grid, f->smem_g, st));
+          CUDA_CHECK(launch_fwd_gemm_pair(xg, wmap, f->amap, p, f->grid, f->smem_g, st));
         } else {
           CUDA_CHECK(launch_fwd_gemm(xg, wmap, p, f->grid, f->smem_g, st));
         }

@@ -796,7 +796,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __shared__ uint64_t full[8], empty[8], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
   const int S = p.stages, bn = p.bn, hb = p.bn / 2;
-  const uint32_t kStage = kFwdA + static_cast<uint32_t>(hb) * 128u;
+  const bool bk2 = p.bk2 != 0;  // 128-deep K stages, as in fwd_gemm_kernel
+  const uint32_t kA = bk2 ? 2u * kFwdA : kFwdA;
+  const uint32_t kStage = kA + static_cast<uint32_t>(hb) * (bk2 ? 256u : 128u);
   const int warp = static_cast<int>(threadIdx.x >> 5), lane = static_cast<int>(threadIdx.x & 31);
   const int rank = static_cast<int>(cluster_ctarank());
   const bool leader = rank == 0;
@@ -837,6 +839,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int nh = n0 + rank * hb;  // this CTA's half of the N tile
         // K order rotated per N tile: the CTAs that share a row tile then read
         // different A blocks at any moment instead of all hitting the same L2 lines
+        if (bk2) {
+          for (int j = 0; j < (p.nkb + 1) / 2; ++j, ++i) {
+            const int s = i % S;
+            mbar_wait(&empty[s], (static_cast<uint32_t>(i / S) & 1u) ^ 1u);
+            uint8_t* a = sm + s * kStage;
+            uint8_t* b = a + kA;
+            const uint32_t lf = lead_full0 + static_cast<uint32_t>(s) * 8u;
+            if (leader) mbar_arrive_expect_tx(&full[s], 2u * kStage);
+            tma_load_3d_cg2(a, &xmap, lf, 0, t * kTileM, 2 * j);
+            for (int c = 0; c < hb; c += 64) tma_load_3d_cg2(b + c * 256, &wmap, lf, nh + c, j * 2 * kBK, p.layer);
+          }
+        } else {
         const int rot = p.krot ? (g % p.ntn) % p.nkb : 0;
         for (int j = 0; j < p.nkb; ++j, ++i) {
           const int kb = j + rot < p.nkb ? j + rot : j + rot - p.nkb;
@@ -848,6 +862,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (leader) mbar_arrive_expect_tx(&full[s], 2u * kStage);
           tma_load_2d_cg2(a, &xmap, lf, kb * kBK, t * kTileM);
           for (int c = 0; c < hb; c += 64) tma_load_3d_cg2(b + c * 128, &wmap, lf, nh + c, kb * kBK, p.layer);
+        }
         }
         if (p.exts == nullptr) continue;
         for (int e = p.pext_begin[pi]; e < p.pext_begin[pi + 1]; ++e, ++i) {
@@ -887,7 +902,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&tempty[acc], (static_cast<uint32_t>(it >> 1) & 1u) ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * bn);
-        for (int kb = 0; kb < p.nkb; ++kb, ++i) {
+        if (bk2) {
+          for (int j = 0; j < (p.nkb + 1) / 2; ++j, ++i) {
+            const int s = i % S;
+            mbar_wait_cluster(&full[s], static_cast<uint32_t>(i / S) & 1u);
+            tc_fence_after();
+            const uint32_t a = smem_u32(sm + s * kStage), b = a + kA;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              mma_bf16_cg2(d, smem_desc(a + (k >> 2) * kFwdA + (k & 3) * 32, 16, 1024, kLayoutSW128),
+                           smem_desc(b + k * 2048, 16384, 1024, kLayoutSW128), idesc_main, (j > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit_cg2(&empty[s], 3);
+          }
+        }
+        for (int kb = 0; kb < (bk2 ? 0 : p.nkb); ++kb, ++i) {
           const int s = i % S;
           mbar_wait_cluster(&full[s], static_cast<uint32_t>(i / S) & 1u);
           tc_fence_after();
