@@ -514,7 +514,7 @@ def impl_ours_bypass(args, w):
 
     layer_fwd = None
     if not args.no_forward and w.d_in == w.d_out:
-        layer_fwd = measure_forward(atmm, plan, w, xs[0], stream, reps=10,
+        layer_fwd = measure_forward(atmm, plan, w, xs[0], stream, reps=20, num_layers=min(4, layers),
                                     cpu_sample_s=0.0 if (args.no_cpu_baseline or world > 1 or rank != 0) else 3.0)
 
     flops_step = w.flops()
