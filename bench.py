@@ -64,14 +64,25 @@ def measured_peaks():
     return FALLBACK_HBM, "fallback"
 
 
-def committed_traffic(config: str):
-    """dram bytes per launch of the bypass kernel from the committed ncu capture."""
+def committed_ncu(config: str) -> dict:
+    """The committed ncu capture of this config's kernel(s) (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_bypass_summary.json")
     if os.path.exists(p):
         with open(p) as f:
-            d = json.load(f)
-        return d.get(config, {}).get("dram_bytes_per_launch")
-    return None
+            return json.load(f).get(config, {})
+    return {}
+
+
+def committed_traffic(config: str):
+    """dram bytes per launch of the bypass kernel from the committed ncu capture."""
+    return committed_ncu(config).get("dram_bytes_per_launch")
+
+
+def isolated_frac(config: str, step_bytes: int, peak: float):
+    """Roofline fraction of ONE isolated launch (ncu: cold cache, serialised,
+    no overlap with the neighbouring steps) beside the pipelined `frac`."""
+    us = committed_ncu(config).get("duration_us")
+    return (step_bytes / (us * 1e-6) / 1e9 / peak, us) if us else (None, None)
 
 
 # ------------------------------------------------------------ clocks ------
@@ -221,6 +232,61 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def bench_config(w, world: int) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens, "adapters": len(w.ranks),
+            "ranks": sorted(set(w.ranks.values())), "segment_rows": sorted(set(w.lengths.values()))[:4],
+            "parallelism": f"request-sharded x{world} (no collective)"}
+
+
+def merge_config(mw, world: int) -> dict:
+    return {"workload": "cfg4", "d_in": mw.d_in, "d_out": mw.d_out, "rank": mw.rank, "layers": mw.layers,
+            "w_dtype": "bf16", "parallelism": f"layer-sharded x{world} (no collective)"}
+
+
+def reference_one_thread_rate(w, seconds: float = 2.0) -> float:
+    """The reference's run_bypass on ONE host thread (LORASERVE_THREADS=1,
+    its default), TFLOP/s over a bounded sample."""
+    os.environ["LORASERVE_THREADS"] = "1"
+    el, batches = run_reference_parallel(w, 1, seconds=seconds)
+    return w.flops() * batches / el / 1e12
+
+
+def reference_merge_rate(mw, threads: int, layers: int = 1):
+    """The reference's merge of ONE cfg4 layer: delta_w_into (its tiled ATMM,
+    model.hpp:120-125) + add_inplace (model.hpp:157-158) through
+    oracle/_ref's ref_merge_rect, LORASERVE_THREADS=threads (atmm.hpp:126-141
+    splits the 4096 output rows over that many jthreads).  Returns
+    (seconds per layer, TFLOP/s)."""
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    os.environ["LORASERVE_THREADS"] = str(threads)
+    rng = np.random.default_rng(21)
+    s = 1.0 / np.sqrt(mw.rank)
+    down = rng.uniform(-s, s, (mw.d_in, mw.rank)).astype(np.float32)
+    up = rng.uniform(-s, s, (mw.rank, mw.d_out)).astype(np.float32)
+    W = rng.uniform(-1 / np.sqrt(mw.d_in), 1 / np.sqrt(mw.d_in), (mw.d_in, mw.d_out)).astype(np.float32)
+    ref.merge_rect(W, down, up, 1)  # warm-up (page faults, allocator)
+    t0 = time.perf_counter()
+    for i in range(layers):
+        ref.merge_rect(W, down, up, -1 if i % 2 else 1)
+    el = (time.perf_counter() - t0) / layers
+    per_layer_flops = 2 * mw.d_in * mw.d_out * mw.rank + mw.d_in * mw.d_out
+    return el, per_layer_flops / el / 1e12
+
+
 def impl_reference(args, w):
     rank, world, _ = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), 0
     if rank != 0:
@@ -231,17 +297,48 @@ def impl_reference(args, w):
     elapsed, batches = run_reference_parallel(w, threads, steps=args.steps)
     flops = w.flops() * batches
     value = flops / elapsed / 1e12
-    cfg = {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens, "adapters": len(w.ranks),
-           "ranks": sorted(set(w.ranks.values())), "dtype_ref": "f32"}
+    cfg = bench_config(w, world)
     sample = (f"{args.steps} steps x {threads} concurrent {w.name} batches (one per host thread) through the "
-              f"reference's run_bypass (batch.hpp:48), fp32")
+              f"reference's run_bypass (batch.hpp:48), fp32, oracle/_ref built from the reference headers")
+    one = reference_one_thread_rate(w)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": cfg,
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference", "sample": sample,
+                         "cpu_model": cpu_model(), "value_1thread": one},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def impl_reference_merge(args):
+    """cfg4 reference arm: the reference's merge (delta_w_into + add_inplace)
+    of one 4096 x 11008 rank-64 layer per step, all host threads; the rate
+    is comparable with the GPU arm's all-32-layer TFLOP/s."""
+    from paper_2411_00915_b200.workloads import MergeWorkload
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    mw = MergeWorkload()
+    threads = cpu_threads()
+    for _ in range(max(args.warmup, 1)):
+        reference_merge_rate(mw, threads, 1)
+    el, rate = reference_merge_rate(mw, threads, args.steps)
+    _, one = reference_merge_rate(mw, 1, 1)
+    sample = (f"{args.steps} steps, each ONE cfg4 layer (4096 x 11008, r64, fp32) through the reference's "
+              f"delta_w_into + add_inplace (model.hpp:120-125,157-158) with LORASERVE_THREADS={threads}; "
+              f"ms_per_step projects the 32-layer merge")
+    line = {
+        "impl": "reference", "metric": "ATMM merge/unmerge W +- s.down.up, all 32 layers (mode switch) TFLOP/s",
+        "value": rate, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el * mw.layers * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": merge_config(mw, world),
+        "cpu_baseline": {"value": rate, "unit": "TFLOP/s", "cores": threads, "kind": "reference", "sample": sample,
+                         "cpu_model": cpu_model(), "value_1thread": one},
+        "e2e": {"value": rate, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -530,6 +627,7 @@ def impl_ours_bypass(args, w):
     kernel_us = ms_local * 1e3 / args.steps
     hbm_peak, peak_kind = measured_peaks()
     achieved_gbs = step_bytes / (kernel_us * 1e-6) / 1e9
+    frac_iso, iso_us = isolated_frac(w.name, step_bytes, hbm_peak)
 
     # ---- end to end through the C ABI with pinned host buffers ----
     # run_bypass (batch.hpp:48) semantics, the reference's own call: every
@@ -540,7 +638,9 @@ def impl_ours_bypass(args, w):
     e2e = None
     e2e_res = None
     if not args.no_e2e:
-        e2e_steps = max(3, min(args.steps, 64))
+        # enough batches that pipeline fill / drain (3 slots) is amortised;
+        # independent of --steps (the e2e leg is a few ms of PCIe traffic)
+        e2e_steps = 128
         nbuf = 6
         xh = [torch.empty(w.tokens, w.d_in, dtype=torch.bfloat16).uniform_(-1, 1).pin_memory() for _ in range(nbuf)]
         yh = [torch.zeros(w.tokens, w.d_out, dtype=torch.bfloat16).pin_memory() for _ in range(nbuf)]
@@ -583,7 +683,8 @@ def impl_ours_bypass(args, w):
                    "kind": "reference",
                    "sample": f"{batches} {w.name} batches in {el:.1f} s, {threads} concurrent batches "
                              f"(one per host thread) through the reference run_bypass (batch.hpp:48, fp32), "
-                             f"oracle/_ref built from the reference headers"}
+                             f"oracle/_ref built from the reference headers",
+                   "cpu_model": cpu_model(), "value_1thread": reference_one_thread_rate(w)}
         except FileNotFoundError as e:
             cpu = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
@@ -595,18 +696,19 @@ def impl_ours_bypass(args, w):
             "us_per_batch": ms_per_step * 1e3,
             "single_launch_us": single_launch_us,
             "x_ready": x_ready,
-            "config": {"workload": w.name, "d_in": w.d_in, "d_out": w.d_out, "tokens": w.tokens,
-                       "adapters": len(w.ranks), "ranks": sorted(set(w.ranks.values())),
-                       "segment_rows": sorted(set(w.lengths.values()))[:4],
-                       "parallelism": f"request-sharded x{world} (no collective)",
-                       "l2": f"inputs rotate over {layers} layer buffer sets ({layers * step_bytes / 2**20:.0f} MiB "
-                             f"> 2x L2); K steps in one CUDA graph",
-                       "launches_per_step": launches_per_step, "tiles": tiles, "ctas": ctas,
-                       "launch_groups": plan.describe()},
+            "config": bench_config(w, world),
+            "timing": {"l2": f"inputs rotate over {layers} layer buffer sets ({layers * step_bytes / 2**20:.0f} MiB "
+                             f"> 2x L2); K steps in one CUDA graph, CUDA events on the launch stream"},
+            "plan": {"launches_per_step": launches_per_step, "tiles": tiles, "ctas": ctas,
+                     "launch_groups": plan.describe()},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": committed_traffic(w.name),
+                         "frac_isolated": frac_iso, "isolated_launch_us": iso_us,
+                         "isolated_source": "profiles/ncu_bypass_summary.json (ncu gpu__time_duration, cold L2, "
+                                            "one launch alone)",
                          "peak_kind": peak_kind, "kernel": " + ".join(kernel_names[p] for p in paths),
-                         "scope": f"one step = {launches_per_step} launch(es); bytes and time of the whole step",
+                         "scope": f"one step = {launches_per_step} launch(es); bytes and time of the whole step "
+                                  f"(pipelined: consecutive steps overlap their prologues through PDL)",
                          "step_us": kernel_us, "algorithmic_bytes_per_step": step_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -699,14 +801,27 @@ def impl_ours_merge(args):
                    "h2d_bytes": int(dn.numel() + upf.numel()) * 4,
                    "note": "put_async (pinned fp32 factors, 32 layers, r64) + one-launch merge of all layers"}
     achieved = bytes_step / (per_step_ms * 1e-3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = cpu_threads()
+            el, rate = reference_merge_rate(mw, threads, 2)
+            _, one = reference_merge_rate(mw, 1, 1)
+            cpu = {"value": rate, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+                   "sample": f"2 cfg4 layers (4096 x 11008, r64, fp32) through the reference's delta_w_into + "
+                             f"add_inplace, LORASERVE_THREADS={threads}: {el * 1e3:.0f} ms per layer",
+                   "cpu_model": cpu_model(), "value_1thread": one}
+        except FileNotFoundError as e:
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
     if rank == 0:
         print(json.dumps({
             "metric": "ATMM merge/unmerge W +- s.down.up, all 32 layers (mode switch) TFLOP/s", "value":
                 world * mw.flops() / (per_step_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "cfg4", "d_in": mw.d_in, "d_out": mw.d_out, "rank": mw.rank, "layers": mw.layers,
-                       "w_dtype": "bf16", "l2": "W of 32 layers = 2.9 GB >> L2"},
+            "config": merge_config(mw, world),
+            "timing": {"l2": "W of 32 layers = 2.9 GB >> L2; K steps in one CUDA graph"},
+            "cpu_baseline": cpu,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
                          "kernel": "atmm_merge_tma_kernel"},
@@ -720,7 +835,7 @@ def main():
 
     if args.config == "cfg4":
         if args.impl == "reference":
-            print(json.dumps({"impl": "reference", "unavailable": "cfg4 reference arm: use tests/ or profiles/"}))
+            impl_reference_merge(args)
             return
         impl_ours_merge(args)
         return

@@ -56,6 +56,20 @@ int atmm_abi_version(void);
 /* Number of sm_100 devices visible (0 on a CPU-only host; never fails). */
 int atmm_device_count(void);
 
+/* Algorithmic FLOP accounting (flops.hpp:10-24): a thread-local counter of
+ * the FLOPs (2 per multiply-add) the reference's GEMMs would count for the
+ * same calls -- padding-free, heterogeneous ranks at their own rank.  Every
+ * compute entry point below adds to it on success (atmm_bypass_apply: the
+ * plan's sum_seg 2 ns r (d_in + d_out); merge: 2 d_in d_out r per layer; GEMM:
+ * 2 m n k; forward: per layer 2 n d^2 + the bypass). */
+uint64_t atmm_flops_read(void);
+void atmm_flops_reset(void);
+/* Host-only: the bypass FLOPs of one batch, sum over plan_batch segments of
+ * 2 ns r_a (d_in + d_out) (test_batch.cpp:96-128).  UnknownAdapter if a
+ * segment's id is not in adapter_ids. */
+int atmm_bypass_flops(const int32_t* assignment, int64_t n, const int32_t* adapter_ids, const int64_t* adapter_ranks,
+                      int64_t num_adapters, int64_t d_in, int64_t d_out, uint64_t* flops);
+
 /* ===================================================================== */
 /* Planner                                                                */
 /* ===================================================================== */
@@ -271,6 +285,30 @@ int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* 
 int atmm_merge_apply_layers(atmm_registry* r, int32_t adapter_id, int64_t layer0, int64_t num_layers, void* w,
                             int64_t ldw, int64_t w_layer_stride, int w_dtype, float sign, void* stream);
 int atmm_delta_w_host(atmm_registry* r, int32_t adapter_id, int64_t layer, float* out);
+
+/* ModelState (model.hpp:104-112) + merge / unmerge / mode_switch on device
+ * weights.  A state binds the registry to the model's weights W (all
+ * num_layers of the registry, layer l at w + l * w_layer_stride elements,
+ * w_dtype ATMM_BF16 or ATMM_F32) and enforces the reference's mode contract:
+ *   merge    (model.hpp:144-165) requires Unmerged, else ATMM_ERR_MODE;
+ *   unmerge  (model.hpp:167-188) requires Merged/Mixture of that adapter;
+ *   mode_switch (serving.hpp:38-74) issues the minimal sequence of one-shot
+ *            (all-layer, one-launch) un/merges; Merged <-> Mixture of the same
+ *            adapter touches no weights.  `launches` = weight rewrites issued.
+ * Stream-ordered; W must stay allocated (address-stable) while bound. */
+enum { ATMM_MODE_UNMERGED = 0, ATMM_MODE_MERGED = 1, ATMM_MODE_MIXTURE = 2 };
+typedef struct atmm_model_state atmm_model_state;
+int atmm_state_create(atmm_registry* r, void* w, int64_t ldw, int64_t w_layer_stride, int w_dtype,
+                      atmm_model_state** out);
+void atmm_state_destroy(atmm_model_state* st);
+int atmm_state_get(const atmm_model_state* st, int* mode, int32_t* merged_adapter, int64_t* weight_writes);
+int atmm_state_merge(atmm_model_state* st, int32_t adapter_id, void* stream);
+int atmm_state_unmerge(atmm_model_state* st, int32_t adapter_id, void* stream);
+/* init_delora (serving.hpp:24-33) + state.mode = Mixture (acceptance.cpp:131-132):
+ * requires the adapter to be the merged one. */
+int atmm_state_set_mixture(atmm_model_state* st, int32_t adapter_id);
+int atmm_state_mode_switch(atmm_model_state* st, int to_mode, int32_t target_adapter, void* stream,
+                           int64_t* launches);
 
 /* ===================================================================== */
 /* Plain ATMM GEMM (atmm.hpp:111-154)                                    */

@@ -2,48 +2,33 @@
 
 Public API mirrors the reference loraserve operator interface; see
 ``paper_2411_00915_b200.atmm`` and include/atmm_b200.h.
+
+The operator names are resolved lazily: ``import paper_2411_00915_b200`` and
+its pure-Python submodules (``workloads``) do not load libatmm_b200.so; the
+first access to an operator name imports ``.atmm``, which loads the library
+and fails loudly if it is missing (there is no CPU fallback).
 """
-from .atmm import (  # noqa: F401
-    BF16,
-    F32,
-    AdapterRegistry,
-    BatchPlan,
-    BypassPlan,
-    ConfigError,
-    CudaError,
-    Error,
-    IoError,
-    LayerForward,
-    MixturePlan,
-    ModeError,
-    NoDeviceError,
-    ParseError,
-    Segment,
-    ShapeError,
-    TilingConfig,
-    TilingTable,
-    UnknownAdapterError,
-    atmm_multiply,
-    bench_launches,
-    candidate_configs,
-    default_candidates,
-    delta_w,
-    device_count,
-    fixture_info,
-    forward_merged,
-    forward_mixture,
-    forward_unmerged,
-    gemm,
-    load_matrix,
-    heuristic_launch,
-    m_bucket_of,
-    merge_into,
-    merge_layers_into,
-    plan_batch,
-    plan_batch_csr,
-    residual_host_bf16_pipelined,
-    run_bypass,
-    run_bypass_host_bf16_pipelined,
-    save_matrix,
-    shard_rows,
+from __future__ import annotations
+
+import importlib
+
+_ATMM_NAMES = (
+    "BF16", "F32", "AdapterRegistry", "BatchPlan", "BypassPlan", "ConfigError", "CudaError", "Error", "IoError",
+    "LayerForward", "MixturePlan", "ModeError", "ModelState", "NoDeviceError", "ParseError", "Segment", "ShapeError",
+    "TilingConfig", "TilingTable", "UnknownAdapterError", "atmm_multiply", "bench_launches", "candidate_configs",
+    "default_candidates", "delta_w", "device_count", "fixture_info", "forward_merged", "forward_mixture",
+    "forward_unmerged", "gemm", "load_matrix", "heuristic_launch", "m_bucket_of", "merge_into", "merge_layers_into",
+    "plan_batch", "plan_batch_csr", "residual_host_bf16_pipelined", "run_bypass", "run_bypass_host_bf16_pipelined",
+    "save_matrix", "shard_rows", "flops_read", "flops_reset", "FlopScope", "bypass_flops",
 )
+
+__all__ = list(_ATMM_NAMES)
+
+
+def __getattr__(name):
+    if name in _ATMM_NAMES:
+        mod = importlib.import_module(".atmm", __name__)
+        val = getattr(mod, name)
+        globals()[name] = val
+        return val
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -12,10 +12,6 @@ from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libatmm_b200.so")
-# Development A/B runs only: load another in-tree build of the same library
-# (e.g. tools/ab/libatmm_b200_<tag>.so).  Must live inside the repository.
-if os.environ.get("ATMM_LIB_VARIANT"):
-    LIB_PATH = os.path.join(os.path.dirname(_HERE), "tools", "ab", f"libatmm_b200_{os.environ['ATMM_LIB_VARIANT']}.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -34,6 +30,16 @@ _SIGS = {
     "atmm_last_error": (c_char_p, []),
     "atmm_abi_version": (c_int, []),
     "atmm_device_count": (c_int, []),
+    "atmm_flops_read": (ctypes.c_uint64, []),
+    "atmm_flops_reset": (None, []),
+    "atmm_bypass_flops": (c_int, [i32p, c_int64, i32p, i64p, c_int64, c_int64, c_int64, POINTER(ctypes.c_uint64)]),
+    "atmm_state_create": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, POINTER(c_void_p)]),
+    "atmm_state_destroy": (None, [c_void_p]),
+    "atmm_state_get": (c_int, [c_void_p, POINTER(c_int), i32p, i64p]),
+    "atmm_state_merge": (c_int, [c_void_p, c_int32, c_void_p]),
+    "atmm_state_unmerge": (c_int, [c_void_p, c_int32, c_void_p]),
+    "atmm_state_set_mixture": (c_int, [c_void_p, c_int32]),
+    "atmm_state_mode_switch": (c_int, [c_void_p, c_int, c_int32, c_void_p, i64p]),
     "atmm_plan_batch": (c_int, [i32p, c_int64, i32p, i64p, i64p, i64p]),
     "atmm_config_valid": (c_int, [i32p]),
     "atmm_m_bucket_of": (c_int, [c_int64]),

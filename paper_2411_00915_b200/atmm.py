@@ -89,6 +89,40 @@ def device_count() -> int:
     return int(lib.atmm_device_count())
 
 
+# ---------------------------------------------------------------- flops ---
+
+
+def flops_read() -> int:
+    """flops.hpp:15: this thread's algorithmic FLOP counter."""
+    return int(lib.atmm_flops_read())
+
+
+def flops_reset() -> None:
+    lib.atmm_flops_reset()
+
+
+class FlopScope:
+    """flops::Scope (flops.hpp:18-24): FLOPs counted since construction."""
+
+    def __init__(self):
+        self.start = flops_read()
+
+    def elapsed(self) -> int:
+        return flops_read() - self.start
+
+
+def bypass_flops(assignment: Sequence[int], adapter_ranks: dict, d_in: int, d_out: Optional[int] = None) -> int:
+    """Algorithmic FLOPs of one bypass pass (batch.hpp:45-47 via atmm.hpp:123):
+    sum over plan_batch segments of 2 ns r (d_in + d_out).  Host only."""
+    a = _i32(assignment).reshape(-1)
+    ids = _i32(sorted(adapter_ranks))
+    ranks = np.ascontiguousarray(np.asarray([adapter_ranks[i] for i in sorted(adapter_ranks)], np.int64))
+    out = ctypes.c_uint64(0)
+    _check(lib.atmm_bypass_flops(_p(a, i32p), a.size, _p(ids, i32p), _p(ranks, i64p), ids.size, int(d_in),
+                                 int(d_in if d_out is None else d_out), ctypes.byref(out)))
+    return int(out.value)
+
+
 # -------------------------------------------------------------- planner ---
 
 
@@ -303,9 +337,23 @@ class AdapterRegistry:
         L, di, r = dshape
         if L != self.num_layers or di != self.d_in or tuple(ushape) != (L, r, self.d_out):
             raise ShapeError(f"adapter factor shapes {dshape} / {ushape} do not match registry")
-        _check(lib.atmm_registry_put_async(self._h, adapter_id, r, dptr, uptr, float(scale), _stream_ptr(stream)))
+        sp = _stream_ptr(stream)
+        _check(lib.atmm_registry_put_async(self._h, adapter_id, r, dptr, uptr, float(scale), sp))
         self._drop_combined(adapter_id)
-        self.__dict__.setdefault("_async_keep", []).append((dkeep, ukeep))
+        # The host factors must outlive the stream-ordered H2D copy: keep them
+        # until an event recorded after the swap has completed, and drop every
+        # kept pair whose swap is done (bounded: nothing outlives its copy).
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(sp, device=torch.device("cuda", self.device)))
+        keep = [k for k in self.__dict__.get("_async_keep", []) if not k[0].query()]
+        keep.append((ev, dkeep, ukeep))
+        self._async_keep = keep
+
+    def pending_swaps(self) -> int:
+        """put_async swaps whose host buffers are still held (copy not yet done)."""
+        return sum(1 for k in self.__dict__.get("_async_keep", []) if not k[0].query())
 
     def load_fixture(self, directory: str) -> int:
         """Every adapter of a reference fixture directory (manifest.json +
@@ -672,6 +720,73 @@ def merge_layers_into(registry: AdapterRegistry, adapter_id: int, w, sign: float
     _check(lib.atmm_merge_apply_layers(registry.handle, adapter_id, layer0, w.shape[0], w.data_ptr(), w.stride(1),
                                        w.stride(0), F32 if w.dtype == torch.float32 else BF16, float(sign),
                                        _stream_ptr(stream)))
+
+
+UNMERGED, MERGED, MIXTURE = 0, 1, 2
+_MODE_NAMES = {UNMERGED: "unmerged", MERGED: "merged", MIXTURE: "mixture"}
+
+
+class ModelState:
+    """ModelState (model.hpp:104-112) bound to a model's device weights
+    ``w`` ([L, d_in, d_out] CUDA tensor, fp32 or bf16, address-stable): merge
+    / unmerge enforce the reference's mode contract (ModeError on a double
+    merge or an unmerge of the wrong adapter, model.hpp:147,170,173), every
+    weight rewrite is ONE all-layer launch, and mode_switch issues the minimal
+    sequence (serving.hpp:38-74)."""
+
+    def __init__(self, registry: AdapterRegistry, w):
+        import torch
+
+        if w.dim() != 3 or w.stride(2) != 1 or not w.is_cuda or w.dtype not in (torch.float32, torch.bfloat16):
+            raise ShapeError("w must be a [L, d_in, d_out] CUDA float32/bfloat16 tensor with contiguous rows")
+        if tuple(w.shape) != (registry.num_layers, registry.d_in, registry.d_out):
+            raise ShapeError(f"w shape {tuple(w.shape)} != ({registry.num_layers}, {registry.d_in}, {registry.d_out})")
+        h = ctypes.c_void_p()
+        _check(lib.atmm_state_create(registry.handle, w.data_ptr(), w.stride(1), w.stride(0),
+                                     F32 if w.dtype == torch.float32 else BF16, ctypes.byref(h)))
+        self._h = h
+        self.registry = registry
+        self.w = w  # keeps the bound weights alive
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.atmm_state_destroy(h)
+            self._h = None
+
+    def _get(self):
+        m, a, n = ctypes.c_int(0), ctypes.c_int32(0), ctypes.c_int64(0)
+        _check(lib.atmm_state_get(self._h, ctypes.byref(m), ctypes.byref(a), ctypes.byref(n)))
+        return m.value, a.value, n.value
+
+    @property
+    def mode(self) -> str:
+        return _MODE_NAMES[self._get()[0]]
+
+    @property
+    def merged_adapter(self) -> int:
+        return self._get()[1]
+
+    @property
+    def weight_writes(self) -> int:
+        return self._get()[2]
+
+    def merge(self, adapter_id: int, stream=None) -> None:
+        _check(lib.atmm_state_merge(self._h, int(adapter_id), _stream_ptr(stream)))
+
+    def unmerge(self, adapter_id: int, stream=None) -> None:
+        _check(lib.atmm_state_unmerge(self._h, int(adapter_id), _stream_ptr(stream)))
+
+    def set_mixture(self, adapter_id: int) -> None:
+        _check(lib.atmm_state_set_mixture(self._h, int(adapter_id)))
+
+    def mode_switch(self, to_mode: str, target_adapter: int = -1, stream=None) -> int:
+        """Returns the number of all-layer weight rewrites issued (0 for
+        merged <-> mixture of the same adapter)."""
+        m = {v: k for k, v in _MODE_NAMES.items()}[to_mode]
+        n = ctypes.c_int64(0)
+        _check(lib.atmm_state_mode_switch(self._h, m, int(target_adapter), _stream_ptr(stream), ctypes.byref(n)))
+        return n.value
 
 
 def save_matrix(path: str, m) -> None:

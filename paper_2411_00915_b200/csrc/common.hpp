@@ -25,6 +25,11 @@ struct Failure : std::runtime_error {
 
 void set_last_error(const std::string& msg);
 
+// flops.hpp:10-24: thread-local algorithmic FLOP counter (one multiply-add =
+// 2 FLOPs, padding never counted).  Every compute entry point adds what the
+// reference's GEMMs would have counted for the same call.
+void flops_add(uint64_t n);
+
 // Runs f, mapping exceptions to ATMM status codes.
 template <typename F>
 int guarded(F&& f) noexcept {

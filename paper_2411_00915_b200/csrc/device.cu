@@ -274,6 +274,7 @@ struct DevBuf {
 struct Slot {
   int32_t id = -1;
   int64_t rank = 0, r_pad = 0;
+  int64_t alg_rank = 0;  // FLOP accounting rank: the true rank (a combined slot: the sum of its parts')
   float scale = 1.0f;
   uint16_t* down_t = nullptr;
   uint16_t* up_t = nullptr;
@@ -291,7 +292,16 @@ struct atmm_registry {
   std::map<int32_t, int> slot_of;
   std::vector<Slot> slots;
   DevBuf<SlotDesc> d_slots;
-  DevBuf<float> stage;  // put_async fp32 staging, grow-only
+  // put_async fp32 staging, one grow-only buffer per stream: a swap on
+  // stream B never overwrites the buffer a pack kernel on stream A still reads.
+  std::vector<std::pair<cudaStream_t, std::unique_ptr<DevBuf<float>>>> stage;
+  DevBuf<float>& stage_for(cudaStream_t st) {
+    for (auto& [s, b] : stage) {
+      if (s == st) return *b;
+    }
+    stage.emplace_back(st, std::make_unique<DevBuf<float>>());
+    return *stage.back().second;
+  }
   uint64_t generation = 0;
 
   ~atmm_registry() {
@@ -524,14 +534,63 @@ static A2aLayout resolve_a2a(int64_t d_in, int64_t d_out, int32_t cluster, int32
   return l;
 }
 
-// Split path: mid partials (fp32, per tile x K slice), bf16 mid per tile and
-// per-tile mid readiness counters of one launch group, allocated with the plan.
-struct SplitBufs {
+// Split path scratch written by the shrink and read by the expand: mid
+// partials (fp32, per tile x K slice), bf16 mid per tile and per-tile mid
+// readiness counters.  One set per CUDA stream that applies the plan, so
+// applies of one plan on different streams never share scratch (the shrink
+// resets the counters its own stream's previous expand polled).
+struct SplitScratch {
   DevBuf<float> part;
   DevBuf<uint16_t> mid;
   DevBuf<int32_t> counter;
+};
+
+// Split path of one plan: the read-only balancing tables (shared by every
+// stream) and the per-stream scratch sets, created on a stream's first apply.
+struct SplitBufs {
   DevBuf<int32_t> tables;  // [s_begin | e_begin bf16 | e_begin fp32 (P+1 each) | seg_slot0 (P) | nseg | part_off (T) | red_off (T+1) | red_tile0 (P)]
   int32_t grid = 0;
+  size_t part_elems = 0, mid_elems = 0, counter_elems = 0;
+  std::mutex mu;
+  std::vector<std::pair<cudaStream_t, std::unique_ptr<SplitScratch>>> scratch;
+  static constexpr size_t kMaxStreams = 32;
+
+  // The scratch set of `stream`.  A new stream's set is allocated and zeroed
+  // outside the caller's stream (relaxed capture mode for this thread, a
+  // private non-blocking stream for the zero fill), so the first apply on a
+  // stream may happen inside a CUDA graph capture.
+  SplitScratch& for_stream(cudaStream_t stream) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& [s, sc] : scratch) {
+      if (s == stream) return *sc;
+    }
+    if (scratch.size() >= kMaxStreams) {
+      fail(ATMM_ERR_CONFIG, "split-path plan applied on more than 32 distinct streams");
+    }
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    auto sc = std::make_unique<SplitScratch>();
+    cudaError_t err = cudaSuccess;
+    cudaStream_t init = nullptr;
+    try {
+      sc->part.alloc(part_elems);
+      sc->mid.alloc(mid_elems);
+      sc->counter.alloc(counter_elems);
+      err = cudaStreamCreateWithFlags(&init, cudaStreamNonBlocking);
+      if (err == cudaSuccess) err = cudaMemsetAsync(sc->mid.p, 0, mid_elems * sizeof(uint16_t), init);
+      if (err == cudaSuccess) err = cudaMemsetAsync(sc->counter.p, 0, counter_elems * sizeof(int32_t), init);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(init);
+    } catch (...) {
+      if (init) cudaStreamDestroy(init);
+      cudaThreadExchangeStreamCaptureMode(&mode);
+      throw;
+    }
+    if (init) cudaStreamDestroy(init);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (err != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("split scratch init failed: ") + cudaGetErrorString(err));
+    scratch.emplace_back(stream, std::move(sc));
+    return *scratch.back().second;
+  }
 };
 
 struct atmm_plan {
@@ -550,6 +609,7 @@ struct atmm_plan {
   std::vector<int32_t> rows_host;  // routed entry (plan order) -> X / Y row
   DevBuf<TileDesc> d_tiles;
   int64_t total_ctas = 0;
+  uint64_t flops = 0;  // algorithmic FLOPs of one apply (flops.hpp accounting)
   uint32_t flags = 0;  // ATMM_PLAN_*
 };
 
@@ -671,6 +731,8 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     const Slot& sl = reg->slots[static_cast<size_t>(it->second)];
     const int64_t b = plan->bp.seg_offsets[s], e = plan->bp.seg_offsets[s + 1];
     const int64_t ns = e - b;
+    plan->flops += 2ull * static_cast<uint64_t>(ns) * static_cast<uint64_t>(sl.alg_rank) *
+                   static_cast<uint64_t>(reg->d_in + reg->d_out);
     LaunchCfg lc = forced ? *forced
                           : (table ? table->resolve_launch(ns, reg->d_in, sl.rank, reg->d_out)
                                    : heuristic_launch(ns, reg->d_in, sl.rank, reg->d_out));
@@ -801,12 +863,10 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     auto& mb = plan->merged_bufs;
     mb = std::make_unique<SplitBufs>();
     mb->grid = P;
-    mb->part.alloc(static_cast<size_t>(total_seg) * kTileM * g.r_pad_max);
-    mb->mid.alloc(static_cast<size_t>(T) * kTileM * g.r_pad_max);
-    mb->counter.alloc(2 + static_cast<size_t>(T));  // [2 reserved][per-tile mid readiness]
+    mb->part_elems = static_cast<size_t>(total_seg) * kTileM * g.r_pad_max;
+    mb->mid_elems = static_cast<size_t>(T) * kTileM * g.r_pad_max;
+    mb->counter_elems = 2 + static_cast<size_t>(T);  // [2 reserved][per-tile mid readiness]
     mb->tables.alloc(tables.size());
-    CUDA_CHECK(cudaMemset(mb->mid.p, 0, mb->mid.n * sizeof(uint16_t)));
-    CUDA_CHECK(cudaMemset(mb->counter.p, 0, mb->counter.n * sizeof(int32_t)));
     CUDA_CHECK(cudaMemcpy(mb->tables.p, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice));
   }
   plan->d_rows.alloc(rows32.size());
@@ -886,7 +946,8 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
     BypassPath path = as_merged ? BypassPath::kSplit : choose_path(g, y_dtype, y_vec != 0);
     if (path == BypassPath::kSplit && !as_merged) path = BypassPath::kFused;  // split runs only as the merged range
     if (path == BypassPath::kSplit) {
-      const SplitBufs& sb = *p->merged_bufs;
+      SplitBufs& sb = *p->merged_bufs;
+      SplitScratch& sc = sb.for_stream(stream);
       const int P = sb.grid;
       const int T = static_cast<int>(g.num_tiles);
       SplitParams sp{};
@@ -915,9 +976,9 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.part_off = sp.nseg + T;
       sp.red_off = sp.part_off + T;
       sp.red_tile0 = sp.red_off + T + 1;
-      sp.part = sb.part.p;
-      sp.mid = sb.mid.p;
-      sp.counter = sb.counter.p;
+      sp.part = sc.part.p;
+      sp.mid = sc.mid.p;
+      sp.counter = sc.counter.p;
       sp.trace = g_trace;
       const cudaError_t e = launch_split(sp.y_dtype, sp, P, g.split.smem_s, g.split.smem_e[sp.y_dtype], stream);
       if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
@@ -1133,6 +1194,7 @@ int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const 
     s.id = adapter_id;
     s.rank = rank;
     s.r_pad = r_pad;
+    s.alg_rank = rank;
     s.scale = scale;
     s.live = true;
     CUDA_CHECK(cudaMalloc(&s.down_t, hd.size() * 2));
@@ -1170,10 +1232,11 @@ int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts
   return guarded([&] {
     if (!r || !part_ids || !part_signs || n_parts < 1) fail(ATMM_ERR_CONFIG, "null registry or empty part list");
     std::vector<Slot> parts;
-    int64_t r_c = 0;
+    int64_t r_c = 0, alg = 0;
     for (int64_t i = 0; i < n_parts; ++i) {
       parts.push_back(r->at(part_ids[i]));
       r_c += parts.back().r_pad;
+      alg += parts.back().alg_rank;
     }
     if (r_c > kMaxRank) fail(ATMM_ERR_CONFIG, "combined rank " + std::to_string(r_c) + " exceeds 128");
     DeviceGuard g(r->device);
@@ -1181,6 +1244,7 @@ int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts
     s.id = new_id;
     s.rank = r_c;
     s.r_pad = r_c;
+    s.alg_rank = alg;
     s.scale = 1.0f;
     s.live = true;
     const size_t dn = static_cast<size_t>(r->d_in_pad * r_c), un = static_cast<size_t>(r->d_out_pad * r_c);
@@ -1250,6 +1314,7 @@ int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, 
     s.id = adapter_id;
     s.rank = rank;
     s.r_pad = r_pad;
+    s.alg_rank = rank;
     s.scale = scale;
     s.live = true;
     // A swap of the same shape overwrites the slot's buffers in place (stream
@@ -1267,11 +1332,12 @@ int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, 
       CUDA_CHECK(cudaMallocAsync(&s.up_t, un * 2, st));
     }
     s.async_owned = true;
-    if (r->stage.n < fd + fu) {
+    DevBuf<float>& stage_buf = r->stage_for(st);
+    if (stage_buf.n < fd + fu) {
       CUDA_CHECK(cudaStreamSynchronize(st));  // the old staging buffer may still be read on this stream
-      r->stage.alloc(fd + fu);
+      stage_buf.alloc(fd + fu);
     }
-    float* stage = r->stage.p;
+    float* stage = stage_buf.p;
     CUDA_CHECK(cudaMemcpyAsync(stage, down, fd * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(stage + fd, up, fu * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(launch_pack_factors(stage, stage + fd, r->L, r->d_in, r->d_out, rank, r->d_in_pad, r->d_out_pad, r_pad,
@@ -1473,6 +1539,7 @@ int atmm_bypass_apply(const atmm_plan* p, int64_t layer, const void* x, int64_t 
     if (!p) fail(ATMM_ERR_CONFIG, "null plan");
     DeviceGuard g(p->reg->device);
     apply_plan(p, layer, x, ldx, y, ldy, y_dtype, scale, static_cast<cudaStream_t>(stream));
+    flops_add(p->flops);
   });
 }
 
@@ -1484,6 +1551,7 @@ int atmm_bypass_apply_group(const atmm_plan* p, int64_t count, const int64_t* la
     DeviceGuard g(p->reg->device);
     apply_plan(p, layers[0], xs[0], ldx, ys[0], ldy, y_dtype, scale, static_cast<cudaStream_t>(stream),
                static_cast<int>(count), layers, xs, ys);
+    flops_add(p->flops * static_cast<uint64_t>(count));
   });
 }
 
@@ -1504,6 +1572,7 @@ int atmm_run_bypass_host(atmm_registry* r, const float* x, int64_t n, const int3
     CUDA_CHECK(launch_f32_to_bf16(xf.p, xb.p, n, r->d_in, r->d_in, ldx, nullptr));
     apply_plan(plan.get(), layer, xb.p, ldx, y.p, ldy, ATMM_F32, 1.0f, nullptr);
     CUDA_CHECK(cudaMemcpy2D(out, r->d_out * 4, y.p, ldy * 4, r->d_out * 4, n, cudaMemcpyDeviceToHost));
+    flops_add(plan->flops);
   });
 }
 
@@ -1527,6 +1596,7 @@ int atmm_bypass_residual_host_bf16(const atmm_plan* p, int64_t layer, const uint
     apply_plan(p, layer, xs.p, ldx, ys.p, ldy, ATMM_BF16, scale, s);
     CUDA_CHECK(cudaMemcpy2DAsync(y_host, r->d_out * 2, ys.p, ldy * 2, r->d_out * 2, p->n, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
+    flops_add(p->flops);
   });
 }
 
@@ -1564,6 +1634,7 @@ int atmm_bypass_residual_host_bf16_pipelined(const atmm_plan* p, const int64_t* 
       CUDA_CHECK(cudaMemcpy2DAsync(y_hosts[i], r->d_out * 2, s.y.p, ldy * 2, r->d_out * 2, p->n, cudaMemcpyDeviceToHost, s.s));
     }
     for (auto& s : slots) CUDA_CHECK(cudaStreamSynchronize(s->s));
+    flops_add(p->flops * static_cast<uint64_t>(count));
   });
 }
 
@@ -1611,6 +1682,7 @@ int atmm_run_bypass_host_bf16_pipelined(const atmm_plan* p, const int64_t* layer
       }
     }
     for (auto& s : slots) CUDA_CHECK(cudaStreamSynchronize(s->s));
+    flops_add(p->flops * static_cast<uint64_t>(count));
   });
 }
 
@@ -1629,6 +1701,7 @@ int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* 
     DeviceGuard g(r->device);
     run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
               r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream));
+    flops_add(2ull * static_cast<uint64_t>(r->d_in * r->d_out * s.alg_rank));  // delta_w_into (model.hpp:124)
   });
 }
 
@@ -1650,6 +1723,142 @@ int atmm_merge_apply_layers(atmm_registry* r, int32_t adapter_id, int64_t layer0
     run_merge(s.down_t + layer0 * r->d_in_pad * s.r_pad, s.up_t + layer0 * r->d_out_pad * s.r_pad, r->d_in,
               r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream), num_layers,
               r->d_in_pad * s.r_pad, r->d_out_pad * s.r_pad, w_layer_stride);
+    flops_add(2ull * static_cast<uint64_t>(num_layers * r->d_in * r->d_out * s.alg_rank));
+  });
+}
+
+}  // extern "C"
+
+// ModelState (model.hpp:104-112) bound to the device weights of one model:
+// which adapter is folded into W, the inference mode, and the weight binding
+// (every layer of W is rewritten in ONE merge launch).
+struct atmm_model_state {
+  atmm_registry* reg = nullptr;
+  void* w = nullptr;
+  int64_t ldw = 0, w_layer_stride = 0;
+  int w_dtype = ATMM_BF16;
+  int mode = ATMM_MODE_UNMERGED;
+  int32_t merged_adapter = -1;
+  int64_t weight_writes = 0;  // merge/unmerge launches issued so far
+};
+
+namespace atmm {
+namespace {
+const char* mode_name(int m) {
+  return m == ATMM_MODE_UNMERGED ? "unmerged" : (m == ATMM_MODE_MERGED ? "merged" : "mixture");
+}
+// One-shot all-layer W +-= s.down.up for the state's weights.
+void state_merge_launch(atmm_model_state* st, int32_t adapter_id, float sign, cudaStream_t stream) {
+  const int rc = atmm_merge_apply_layers(st->reg, adapter_id, 0, st->reg->L, st->w, st->ldw, st->w_layer_stride,
+                                         st->w_dtype, sign, stream);
+  if (rc != ATMM_OK) fail(rc, atmm_last_error());
+  ++st->weight_writes;
+}
+// merge (model.hpp:144-165): requires the unmerged state.
+void state_merge(atmm_model_state* st, int32_t adapter_id, cudaStream_t stream) {
+  if (st->mode != ATMM_MODE_UNMERGED) {
+    fail(ATMM_ERR_MODE, std::string("merge requires unmerged state (currently ") + mode_name(st->mode) + ")");
+  }
+  state_merge_launch(st, adapter_id, +1.0f, stream);
+  st->mode = ATMM_MODE_MERGED;
+  st->merged_adapter = adapter_id;
+}
+// unmerge (model.hpp:167-188): requires merged / mixture state of this adapter.
+void state_unmerge(atmm_model_state* st, int32_t adapter_id, cudaStream_t stream) {
+  if (st->mode == ATMM_MODE_UNMERGED) fail(ATMM_ERR_MODE, "unmerge requires merged or mixture state");
+  if (st->merged_adapter != adapter_id) {
+    fail(ATMM_ERR_MODE, "unmerge of adapter " + std::to_string(adapter_id) + " but adapter " +
+                            std::to_string(st->merged_adapter) + " is merged");
+  }
+  state_merge_launch(st, adapter_id, -1.0f, stream);
+  st->mode = ATMM_MODE_UNMERGED;
+  st->merged_adapter = -1;
+}
+}  // namespace
+}  // namespace atmm
+
+extern "C" {
+
+int atmm_state_create(atmm_registry* r, void* w, int64_t ldw, int64_t w_layer_stride, int w_dtype,
+                      atmm_model_state** out) {
+  return guarded([&] {
+    if (!r || !w || !out) fail(ATMM_ERR_CONFIG, "null registry, W or output");
+    if (w_dtype != ATMM_BF16 && w_dtype != ATMM_F32) fail(ATMM_ERR_CONFIG, "w_dtype must be ATMM_BF16 or ATMM_F32");
+    if (ldw < r->d_out) fail(ATMM_ERR_SHAPE, "W row stride ldw must be >= d_out");
+    if (r->L > 1 && w_layer_stride < ldw * r->d_in) fail(ATMM_ERR_SHAPE, "W layer stride must be >= ldw * d_in");
+    auto st = std::make_unique<atmm_model_state>();
+    st->reg = r;
+    st->w = w;
+    st->ldw = ldw;
+    st->w_layer_stride = r->L > 1 ? w_layer_stride : ldw * r->d_in;
+    st->w_dtype = w_dtype;
+    *out = st.release();
+  });
+}
+
+void atmm_state_destroy(atmm_model_state* st) { delete st; }
+
+int atmm_state_get(const atmm_model_state* st, int* mode, int32_t* merged_adapter, int64_t* weight_writes) {
+  return guarded([&] {
+    if (!st) fail(ATMM_ERR_CONFIG, "null state");
+    if (mode) *mode = st->mode;
+    if (merged_adapter) *merged_adapter = st->merged_adapter;
+    if (weight_writes) *weight_writes = st->weight_writes;
+  });
+}
+
+int atmm_state_merge(atmm_model_state* st, int32_t adapter_id, void* stream) {
+  return guarded([&] {
+    if (!st) fail(ATMM_ERR_CONFIG, "null state");
+    state_merge(st, adapter_id, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atmm_state_unmerge(atmm_model_state* st, int32_t adapter_id, void* stream) {
+  return guarded([&] {
+    if (!st) fail(ATMM_ERR_CONFIG, "null state");
+    state_unmerge(st, adapter_id, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int atmm_state_set_mixture(atmm_model_state* st, int32_t adapter_id) {
+  return guarded([&] {
+    if (!st) fail(ATMM_ERR_CONFIG, "null state");
+    // init_delora (serving.hpp:24-33): the subtraction branch is the merged adapter
+    if (st->mode == ATMM_MODE_UNMERGED) fail(ATMM_ERR_MODE, "mixture requires a merged adapter");
+    if (st->merged_adapter != adapter_id) {
+      fail(ATMM_ERR_MODE, "delora branch must be the merged adapter " + std::to_string(st->merged_adapter));
+    }
+    if (!atmm_registry_contains(st->reg, adapter_id)) {
+      fail(ATMM_ERR_MODE, "mixture integrity: subtraction branch missing");
+    }
+    st->mode = ATMM_MODE_MIXTURE;
+  });
+}
+
+int atmm_state_mode_switch(atmm_model_state* st, int to_mode, int32_t target_adapter, void* stream,
+                           int64_t* launches) {
+  return guarded([&] {
+    if (!st) fail(ATMM_ERR_CONFIG, "null state");
+    if (to_mode != ATMM_MODE_UNMERGED && to_mode != ATMM_MODE_MERGED && to_mode != ATMM_MODE_MIXTURE) {
+      fail(ATMM_ERR_CONFIG, "unknown inference mode");
+    }
+    const auto s = static_cast<cudaStream_t>(stream);
+    const int64_t before = st->weight_writes;
+    if (to_mode == ATMM_MODE_UNMERGED) {
+      if (st->mode != ATMM_MODE_UNMERGED) state_unmerge(st, st->merged_adapter, s);
+    } else {
+      if (target_adapter < 0) fail(ATMM_ERR_MODE, "merged/mixture transition needs a target adapter");
+      if (!atmm_registry_contains(st->reg, target_adapter)) {
+        fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(target_adapter));
+      }
+      if (st->mode != ATMM_MODE_UNMERGED && st->merged_adapter != target_adapter) {
+        state_unmerge(st, st->merged_adapter, s);
+      }
+      if (st->mode == ATMM_MODE_UNMERGED) state_merge(st, target_adapter, s);
+      st->mode = to_mode;  // merged <-> mixture of the same adapter touches no weights
+    }
+    if (launches) *launches = st->weight_writes - before;
   });
 }
 
@@ -1666,6 +1875,7 @@ int atmm_delta_w_host(atmm_registry* r, int32_t adapter_id, int64_t layer, float
     run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
               r->d_out, s.r_pad, w.p, ldw, ATMM_F32, s.scale, 0.0f, nullptr);
     CUDA_CHECK(cudaMemcpy2D(out, r->d_out * 4, w.p, ldw * 4, r->d_out * 4, r->d_in, cudaMemcpyDeviceToHost));
+    flops_add(2ull * static_cast<uint64_t>(r->d_in * r->d_out * s.alg_rank));
   });
 }
 
@@ -1701,6 +1911,7 @@ int atmm_multiply_host(const float* a, int64_t m, int64_t k, const float* b, int
       CUDA_CHECK(cudaDeviceSynchronize());
     }
     CUDA_CHECK(cudaMemcpy2D(c, n * 4, cd.p, ldc * 4, n * 4, m, cudaMemcpyDeviceToHost));
+    flops_add(2ull * static_cast<uint64_t>(m * n * k));  // atmm.hpp:123
   });
 }
 
@@ -1776,6 +1987,7 @@ int atmm_bench_launches(int device, int64_t m, int64_t d_in, int64_t rank, int64
 struct atmm_forward {
   atmm_registry* reg = nullptr;  // null: forward_merged (no bypass)
   uint64_t generation = 0;
+  uint64_t bypass_flops = 0;     // algorithmic FLOPs of one layer's bypass (the plan's)
   int device = 0;
   int64_t n = 0, d = 0;
   bool sorted = false;  // rows run in plan order (gathered in, scattered out)
@@ -1950,6 +2162,7 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       if (n > 0 && n != plan->n) fail(ATMM_ERR_SHAPE, "row count does not match the plan");
       f->reg = reg;
       f->generation = reg->generation;
+      f->bypass_flops = plan->flops;
       f->device = reg->device;
       f->n = plan->n;
       f->d = reg->d_in;
@@ -2250,6 +2463,8 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
       xm = f->bmap[nxt];
       xg = f->bk2 ? f->bmap2[nxt] : xm;
     }
+    // model.hpp:238 (2 n d^2 per layer) + run_bypass per layer (batch.hpp:70-73)
+    flops_add(static_cast<uint64_t>(num_layers) * (2ull * static_cast<uint64_t>(n * d * d) + f->bypass_flops));
   });
 }
 
@@ -2314,5 +2529,6 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     } else {
       CUDA_CHECK(launch_fwd_gemm(amap, bmap, p, gt.grid, gt.smem, st));
     }
+    flops_add(2ull * static_cast<uint64_t>(m * n * k));  // atmm.hpp:123
   });
 }

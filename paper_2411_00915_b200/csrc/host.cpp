@@ -25,8 +25,10 @@ namespace atmm {
 
 namespace {
 thread_local std::string g_last_error;
+thread_local uint64_t g_flops = 0;
 }
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+void flops_add(uint64_t n) { g_flops += n; }
 
 // ------------------------------------------------------------- tiling ---
 
@@ -553,6 +555,28 @@ int atmm_matrix_load(const char* path, int64_t* rows, int64_t* cols, float* out,
 }
 
 const char* atmm_last_error(void) { return g_last_error.c_str(); }
+uint64_t atmm_flops_read(void) { return g_flops; }
+void atmm_flops_reset(void) { g_flops = 0; }
+
+int atmm_bypass_flops(const int32_t* assignment, int64_t n, const int32_t* adapter_ids, const int64_t* adapter_ranks,
+                      int64_t num_adapters, int64_t d_in, int64_t d_out, uint64_t* flops) {
+  return guarded([&] {
+    if (!flops || (num_adapters > 0 && (!adapter_ids || !adapter_ranks))) fail(ATMM_ERR_CONFIG, "null argument");
+    if (d_in < 1 || d_out < 1) fail(ATMM_ERR_SHAPE, "dimensions must be >= 1");
+    std::map<int32_t, int64_t> rank_of;
+    for (int64_t i = 0; i < num_adapters; ++i) rank_of[adapter_ids[i]] = adapter_ranks[i];
+    const BatchPlan bp = plan_batch(assignment, n);
+    uint64_t f = 0;
+    for (size_t s = 0; s < bp.seg_adapter.size(); ++s) {
+      auto it = rank_of.find(bp.seg_adapter[s]);
+      if (it == rank_of.end()) fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(bp.seg_adapter[s]));
+      const uint64_t ns = static_cast<uint64_t>(bp.seg_offsets[s + 1] - bp.seg_offsets[s]);
+      // shrink 2*ns*d_in*r + expand 2*ns*r*d_out (batch.hpp:70-73 via atmm.hpp:123)
+      f += 2ull * ns * static_cast<uint64_t>(it->second) * static_cast<uint64_t>(d_in + d_out);
+    }
+    *flops = f;
+  });
+}
 int atmm_abi_version(void) { return ATMM_ABI_VERSION; }
 
 int atmm_plan_batch(const int32_t* assignment, int64_t n, int32_t* seg_adapter,

@@ -252,3 +252,71 @@ def test_grouped_apply_matches_single_calls(gpu, atmm, oracle):
         want = y0[c].float().cpu().numpy().astype(np.float64) + 0.5 * oracle.bypass_rows_f64(
             xs[c].float().cpu().numpy(), assignment, {a: (f[0][layers[c]], f[1][layers[c]]) for a, f in facs.items()})
         assert np.max(np.abs(ya[c].float().cpu().numpy() - want)) <= tol_for(want)
+
+
+def _split_path_case(atmm, oracle, L=2):
+    """A plan whose bf16-Y groups take the split shrink + expand pair (tiles
+    of > 32 rows), i.e. the path with per-stream scratch."""
+    d, n = 1024, 640
+    ranks = {1: 16, 2: 64, 3: 32}
+    reg, facs = _setup(atmm, oracle, d, d, ranks, L=L)
+    assignment = np.asarray([(1, 1, 2, 3, 2)[i % 5] for i in range(n)], np.int32)
+    plan = atmm.BypassPlan(reg, assignment)
+    assert "split" in {g["path_bf16"] for g in plan.describe()}
+    return reg, facs, plan, assignment, d, n
+
+
+def test_pipelined_host_split_path(gpu, atmm, oracle):
+    """the pipelined host paths run applies of one plan on
+    2-4 streams concurrently; split-path plans need per-stream scratch."""
+    import torch
+
+    reg, facs, plan, assignment, d, n = _split_path_case(atmm, oracle)
+    xs, ys, outs, wants, wants_fresh, layers = [], [], [], [], [], []
+    for i in range(8):
+        x = oracle.round_bf16(oracle.random_matrix(oracle.rng(300 + i), n, d))
+        y0 = oracle.round_bf16(oracle.random_matrix(oracle.rng(400 + i), n, d))
+        layer = i % 2
+        byp = oracle.bypass_rows_f64(x, assignment, {a: (f[0][layer], f[1][layer]) for a, f in facs.items()})
+        xt = torch.from_numpy(x).to(torch.bfloat16).pin_memory()
+        yt = torch.from_numpy(y0).to(torch.bfloat16).pin_memory()
+        ot = torch.zeros(n, d, dtype=torch.bfloat16).pin_memory()
+        xs.append(xt.view(torch.int16).numpy().view(np.uint16))
+        ys.append(yt.view(torch.int16).numpy().view(np.uint16))
+        outs.append(ot.view(torch.int16).numpy().view(np.uint16))
+        wants.append((y0.astype(np.float64) + byp, yt))
+        wants_fresh.append((byp, ot))
+        layers.append(layer)
+    atmm.residual_host_bf16_pipelined(plan, xs, ys, layers)
+    for want, yt in wants:
+        assert np.max(np.abs(yt.float().numpy() - want)) <= tol_for(want)
+    atmm.run_bypass_host_bf16_pipelined(plan, xs, outs, layers)
+    for want, ot in wants_fresh:
+        assert np.max(np.abs(ot.float().numpy() - want)) <= tol_for(want)
+
+
+def test_split_plan_concurrent_streams_bit_identical(gpu, atmm, oracle):
+    """Applies of one split-path plan on several streams at once give the
+    same bits as the serialized applies."""
+    import torch
+
+    reg, facs, plan, assignment, d, n = _split_path_case(atmm, oracle)
+    S = 4
+    xs = [torch.from_numpy(_x(oracle, n, d, seed=60 + c)).to("cuda", torch.bfloat16) for c in range(S)]
+    y0 = [torch.from_numpy(_x(oracle, n, d, seed=70 + c)).to("cuda", torch.bfloat16) for c in range(S)]
+    K = 3  # each stream accumulates K applies into its own Y
+    ser = [y.clone() for y in y0]
+    for c in range(S):
+        for _ in range(K):
+            plan.apply(xs[c], ser[c], layer=c % 2)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    for rep in range(3):
+        par = [y.clone() for y in y0]
+        torch.cuda.synchronize()
+        for _ in range(K):  # interleaved issue: every stream has work in flight
+            for c in range(S):
+                plan.apply(xs[c], par[c], layer=c % 2, stream=streams[c])
+        torch.cuda.synchronize()
+        for c in range(S):
+            assert torch.equal(par[c], ser[c]), (rep, c)
