@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define ATMM_ABI_VERSION 1
+#define ATMM_ABI_VERSION 2
 
 /* Status codes <-> loraserve exception classes (errors.hpp). */
 enum {
@@ -102,19 +102,29 @@ typedef struct atmm_table atmm_table;
 int atmm_table_create(const int32_t* default_cfg, atmm_table** out);
 void atmm_table_destroy(atmm_table* t);
 /* TilingTable::insert (tiling.hpp:164-167).  sm100 (nullable) = explicit
- * B200 launch parameters {tile_m, cluster, bn, stages} stored beside the
- * reference entry (the JSON "sm100" object). */
+ * B200 launch parameters {tile_m, cluster, bn, stages, path} stored beside
+ * the reference entry (the JSON "sm100" object):
+ *   tile_m  rows per tile (1..128)      cluster  CTAs per tile (1..16)
+ *   bn      expand N chunk (64..256)    stages   shrink ring depth (0 = auto)
+ *   path    ATMM_PATH_* kernel choice (ATMM_PATH_AUTO picks by tile rows). */
+enum { ATMM_PATH_AUTO = 0, ATMM_PATH_A2A = 1, ATMM_PATH_SPLIT = 2, ATMM_PATH_FUSED = 3 };
 int atmm_table_insert(atmm_table* t, int32_t m_bucket, int32_t k, int32_t n,
                       const int32_t cfg[6], int64_t measured_ns, const int32_t* sm100);
-int atmm_table_set_default(atmm_table* t, const int32_t cfg[6]);
+/* TilingTable::set_default (tiling.hpp:169); sm100 (nullable) = the default's
+ * B200 launch (JSON "default_sm100"), used for shapes the table misses. */
+int atmm_table_set_default(atmm_table* t, const int32_t cfg[6], const int32_t* sm100);
 /* TilingTable::lookup (tiling.hpp:181-199): exact -> nearest same-(k,n)
  * bucket within 32 (ties to the smaller bucket) -> default. */
 int atmm_table_lookup(const atmm_table* t, int64_t m, int64_t k, int64_t n, int32_t cfg_out[6]);
 int atmm_table_size(const atmm_table* t, int64_t* size);
+/* The entry lookup(m, k, n) hits (exact or nearest bucket within 32):
+ * *found = 1 and its B200 launch, else *found = 0 (the default applies). */
+int atmm_table_find(const atmm_table* t, int64_t m, int64_t k, int64_t n, int32_t launch_out[5], int* found);
 /* The B200 launch parameters the table resolves for the fused bypass of a
- * segment of m rows at (d_in, rank, d_out): {tile_m, cluster, bn, stages}. */
+ * segment of m rows at (d_in, rank, d_out): {tile_m, cluster, bn, stages,
+ * path}.  t == NULL gives the built-in heuristic. */
 int atmm_table_resolve_launch(const atmm_table* t, int64_t m, int64_t d_in, int64_t rank,
-                              int64_t d_out, int32_t launch_out[4]);
+                              int64_t d_out, int32_t launch_out[5]);
 /* TilingTable::save / load (tiling.hpp:201-249): same JSON schema,
  * {"default":[6], "entries":[{m_bucket,k,n,config[6],ns[,sm100]}]}. */
 int atmm_table_save(const atmm_table* t, const char* path);
@@ -202,6 +212,10 @@ int atmm_plan_create(atmm_registry* r, const int32_t* assignment, int64_t n,
  * served by the merged weights, model.hpp:273-280) take a bypass. */
 int atmm_plan_create_mapped(atmm_registry* r, const int32_t* assignment, const int32_t* rows, int64_t n,
                             int64_t n_rows, const atmm_table* table, atmm_plan** out);
+/* A plan whose every segment runs `launch` {tile_m, cluster, bn, stages,
+ * path} instead of the table's (the tuner's candidates; path-coverage tests). */
+int atmm_plan_create_launch(atmm_registry* r, const int32_t* assignment, int64_t n, const int32_t launch[5],
+                            atmm_plan** out);
 void atmm_plan_destroy(atmm_plan* p);
 /* Plan flags (no reference counterpart: a launch-ordering promise).
  * ATMM_PLAN_X_READY: the X handed to every apply of this plan is complete
@@ -241,7 +255,8 @@ int atmm_bypass_apply_group(const atmm_plan* p, int64_t count, const int64_t* la
                             int64_t ldx, void* const* ys, int64_t ldy, int y_dtype, float scale, void* stream);
 
 /* run_bypass (batch.hpp:48) with host buffers: out = bypass(x), fp32 in and
- * out (x rounded to bf16 on the device).  Synchronous. */
+ * out.  A precise registry computes it fp32-faithfully (atmm_bypass_apply_f32),
+ * otherwise x is rounded to bf16 on the device.  Synchronous. */
 int atmm_run_bypass_host(atmm_registry* r, const float* x, int64_t n,
                          const int32_t* assignment, int64_t layer, const atmm_table* table,
                          float* out);
@@ -314,23 +329,102 @@ int atmm_state_mode_switch(atmm_model_state* st, int to_mode, int32_t target_ada
 /* Plain ATMM GEMM (atmm.hpp:111-154)                                    */
 /* ===================================================================== */
 
-/* atmm_multiply_into with host fp32 buffers: c = a . b, bf16 operands on
- * tcgen05, fp32 accumulate and output.  cfg is validated like the
- * reference (ConfigError).  Synchronous. */
+/* atmm_multiply_into with host fp32 buffers: c = a . b, fp32-faithful
+ * (atmm_gemm_f32: split-bf16 operands on tcgen05, fp32 accumulate and
+ * output).  cfg is validated like the reference (ConfigError).  Synchronous. */
 int atmm_multiply_host(const float* a, int64_t m, int64_t k, const float* b, int64_t n,
                        float* c, const int32_t cfg[6]);
+
+/* ===================================================================== */
+/* fp32-faithful path (the reference's fp32 contract on tensor cores)    */
+/* ===================================================================== */
+/* The reference computes in fp32 and its tests hold results to 1e-4 *
+ * max(1, max|ref|) (acceptance.cpp:62-211).  These entry points keep that
+ * contract on the bf16 tensor cores: each fp32 operand is split into three
+ * bf16 parts x = h + m + l and every product is ONE tcgen05 GEMM over the
+ * K-concatenation of the six partial products hh, hm, mh, hl, lh, mm with
+ * fp32 accumulation (dropped terms <= 2^-24 relative: fp32 rounding level).
+ * 6x the tensor work of the bf16 path; the bf16 entry points above remain
+ * the serving path.  Device pointers, fp32, stream-ordered. */
+
+/* A precise registry also keeps the split images of every adapter's factors
+ * (set before the first put; combined slots are not available). */
+int atmm_registry_set_precise(atmm_registry* r, int on);
+/* C = A . B + beta C (beta 0 or 1), any m, k, n and row strides. */
+int atmm_gemm_f32(const float* a, int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m,
+                  int64_t k, int64_t n, float beta, void* stream);
+/* run_bypass + residual (batch.hpp:48-81, model.hpp:239-241) on a plan of a
+ * precise registry: y[row] += scale * s_a * (x[row] . down_a) . up_a. */
+int atmm_bypass_apply_f32(const atmm_plan* p, int64_t layer, const float* x, int64_t ldx, float* y, int64_t ldy,
+                          float scale, void* stream);
+/* merge / unmerge (model.hpp:144-188): W_l += sign * s_a * down_a . up_a for
+ * layers [layer0, layer0 + num_layers) of fp32 W (delta_w_into + add_inplace). */
+int atmm_merge_apply_f32(atmm_registry* r, int32_t adapter_id, int64_t layer0, int64_t num_layers, float* w, int64_t ldw,
+                         int64_t w_layer_stride, float sign, void* stream);
+/* delta_w (model.hpp:130-140) into a device fp32 d_in x d_out matrix. */
+int atmm_delta_w_f32(atmm_registry* r, int32_t adapter_id, int64_t layer, float* out, int64_t ldo, void* stream);
+/* The stack forward (model.hpp:192-328): cur <- tanh(cur . W_l + sum_i
+ * scales[i] * bypass_{plans[i], l}(cur)) for l < num_layers.  No plan =
+ * forward_merged; one plan = forward_unmerged; forward_mixture = the guest
+ * rows' own plan (+1) and the merged adapter's plan over the same rows (-1)
+ * on merged weights.  Plans must come from precise registries with
+ * d_in == d_out == d and n rows. */
+int atmm_forward_f32(const float* w, int64_t ldw, int64_t w_layer_stride, int64_t num_layers, int64_t n, int64_t d,
+                     const float* x, int64_t ldx, float* out, int64_t ldo, const atmm_plan* const* plans,
+                     const float* scales, int64_t num_plans, void* stream);
+
+/* Host-buffer forms (synchronous; device staging reused across calls):
+ * the stack forward of host fp32 W [L][d][d] / x [n][d] into out, and the
+ * in-place all-layer merge (sign +1) / unmerge (-1) of host fp32 W
+ * [L][d_in][d_out] -- the address of W never changes (acceptance.cpp:188). */
+int atmm_forward_f32_host(const float* w, int64_t num_layers, int64_t n, int64_t d, const float* x, float* out,
+                          const atmm_plan* const* plans, const float* scales, int64_t num_plans);
+int atmm_merge_f32_host(atmm_registry* r, int32_t adapter_id, float* w, float sign);
 
 /* ===================================================================== */
 /* Offline tiling search on B200 (atmm.hpp:188-355)                      */
 /* ===================================================================== */
 
-/* Times the fused bypass of one segment shape (m rows, d_in, rank, d_out)
- * under each candidate launch {tile_m, cluster, bn, stages} with CUDA
- * events (median of `trials` after a warm-up, L2 flushed between trials)
- * and writes median ns per candidate (INT64_MAX for a failed candidate). */
-int atmm_bench_launches(int device, int64_t m, int64_t d_in, int64_t rank, int64_t d_out,
-                        const int32_t* launches, int64_t num_launches, int trials,
-                        int64_t* median_ns);
+/* A tuning shape: one batch of `segments` segments of `m` rows each, every
+ * segment its own adapter of rank `rank`, rows shuffled, at (d_in, d_out).
+ * The table key is the fused launch's lookup key (m_bucket(m), d_in, rank),
+ * like the reference's shrink lookup (batch.hpp:70). */
+typedef struct atmm_tune_shape {
+  int64_t m, d_in, rank, d_out, segments;
+} atmm_tune_shape;
+
+/* benchmark_config (atmm.hpp:188-216): median device time (ns per apply) of
+ * `trials` (>= 3, else ConfigError) trials after one warm-up, the launch
+ * forced for every segment.  Each trial flushes L2 (256 MB write), then times
+ * back-to-back bf16-Y applies on distinct buffers with CUDA events. */
+int atmm_benchmark_launch(int device, const atmm_tune_shape* shape, const int32_t launch[5], int trials,
+                          uint64_t seed, int64_t* median_ns);
+/* grid_bench_ns (atmm.hpp:229-270): scores[s * num_launches + c] = median of
+ * `rounds` round medians, rounds interleaved over the whole grid; failed
+ * points score INT64_MAX and are described in `failures` (nullable). */
+int atmm_grid_bench_ns(int device, const atmm_tune_shape* shapes, int64_t num_shapes, const int32_t* launches,
+                       int64_t num_launches, int trials, int rounds, int64_t* scores, char* failures,
+                       size_t failures_cap);
+/* tiling_search (atmm.hpp:276-330): per-shape argmin over the candidate
+ * launches (ties to the lexicographically smallest {tile_m, cluster, bn,
+ * stages, path}), 3 interleaved rounds; the most frequent winner becomes the
+ * table default (its launch stored as "default_sm100").  Entries carry the
+ * measured ns, the B200 launch ("sm100") and an equivalent reference config. */
+int atmm_tiling_search(int device, const atmm_tune_shape* shapes, int64_t num_shapes, const int32_t* launches,
+                       int64_t num_launches, int trials, atmm_table** out, char* failures, size_t failures_cap);
+/* Host-only selection half of tiling_search over scores[s * num_launches + c]
+ * (INT64_MAX = failed): the table tiling_search would build from them. */
+int atmm_table_from_scores(const atmm_tune_shape* shapes, int64_t num_shapes, const int32_t* launches,
+                           int64_t num_launches, const int64_t* scores, atmm_table** out, char* failures,
+                           size_t failures_cap);
+/* default_shape_grid (atmm.hpp:341-355) for the bypass at (d_in, d_out):
+ * segment rows {8 .. 512} x ranks (NULL/0 = {8, 16, 32, 64, 128}), ~1k-token
+ * batches.  Writes up to cap shapes and the total count. */
+int atmm_default_shape_grid(int64_t d_in, int64_t d_out, const int64_t* ranks, int64_t num_ranks, atmm_tune_shape* out,
+                            int64_t cap, int64_t* count);
+/* default_candidates (tiling.hpp:124-149) for B200: the curated launch list
+ * (5 ints each). */
+int atmm_default_launch_candidates(int32_t* out, int64_t cap, int64_t* count);
 
 /* ===================================================================== */
 /* Request sharding over GPUs                         */
@@ -371,6 +465,20 @@ int atmm_shard_rows(const int32_t* assignment, int64_t n, const int32_t* adapter
 typedef struct atmm_forward atmm_forward;
 int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hidden_dim,
                         atmm_forward** out);
+/* Explicit tile options of the base GEMM (layer forward and atmm_gemm_ex);
+ * a zero field (pair: -1) leaves that choice to the built-in heuristic.
+ * Every option combination computes the same product; they exist for tile
+ * sweeps and path-coverage tests.  Invalid values -> ATMM_ERR_CONFIG. */
+typedef struct atmm_gemm_opts {
+  int32_t pair;   /* -1 automatic, 0 1-SM tiles, 1 2-SM CTA pairs (cta_group::2) */
+  int32_t bn;     /* N tile: 0 automatic, 128, 256 */
+  int32_t kz;     /* 1-SM split-K cluster: 0 automatic, 1, 2, 4, 8 (bn 128 only) */
+  int32_t ks;     /* layer forward: shrink K split, 0 automatic, 1..16 */
+  int32_t mc;     /* plain GEMM: A multicast over mc N tiles, 0/1 off, 2, 4 */
+  int32_t stages; /* GEMM ring depth cap: 0 automatic, 2..8 */
+} atmm_gemm_opts;
+int atmm_forward_create_opts(const atmm_plan* plan, int device, int64_t n, int64_t hidden_dim,
+                             const atmm_gemm_opts* opts, atmm_forward** out);
 void atmm_forward_destroy(atmm_forward* f);
 int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_layer_stride,
                      int64_t num_layers, const void* x, int64_t ldx, void* out, int64_t ldo,
@@ -389,6 +497,9 @@ int atmm_forward_stats(const atmm_forward* f, int64_t* out, int64_t cap);
  * The device is the current one; stream-ordered on `stream`.  k = 0 zeroes C. */
 int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int c_dtype,
               int64_t m, int64_t k, int64_t n, void* stream);
+/* atmm_gemm with explicit tile options (NULL = automatic). */
+int atmm_gemm_ex(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int c_dtype,
+                 int64_t m, int64_t k, int64_t n, const atmm_gemm_opts* opts, void* stream);
 
 #ifdef __cplusplus
 }

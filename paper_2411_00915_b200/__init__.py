@@ -15,11 +15,13 @@ import importlib
 _ATMM_NAMES = (
     "BF16", "F32", "AdapterRegistry", "BatchPlan", "BypassPlan", "ConfigError", "CudaError", "Error", "IoError",
     "LayerForward", "MixturePlan", "ModeError", "ModelState", "NoDeviceError", "ParseError", "Segment", "ShapeError",
-    "TilingConfig", "TilingTable", "UnknownAdapterError", "atmm_multiply", "bench_launches", "candidate_configs",
+    "TilingConfig", "TilingTable", "UnknownAdapterError", "atmm_multiply", "candidate_configs",
     "default_candidates", "delta_w", "device_count", "fixture_info", "forward_merged", "forward_mixture",
     "forward_unmerged", "gemm", "load_matrix", "heuristic_launch", "m_bucket_of", "merge_into", "merge_layers_into",
     "plan_batch", "plan_batch_csr", "residual_host_bf16_pipelined", "run_bypass", "run_bypass_host_bf16_pipelined",
     "save_matrix", "shard_rows", "flops_read", "flops_reset", "FlopScope", "bypass_flops",
+    "TuneShape", "default_shape_grid", "default_launch_candidates", "benchmark_launch", "grid_bench_ns",
+    "tiling_search", "table_from_scores", "gemm_f32", "forward_f32", "UNMERGED", "MERGED", "MIXTURE",
 )
 
 __all__ = list(_ATMM_NAMES)

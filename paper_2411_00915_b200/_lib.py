@@ -40,15 +40,27 @@ _SIGS = {
     "atmm_state_unmerge": (c_int, [c_void_p, c_int32, c_void_p]),
     "atmm_state_set_mixture": (c_int, [c_void_p, c_int32]),
     "atmm_state_mode_switch": (c_int, [c_void_p, c_int, c_int32, c_void_p, i64p]),
+    "atmm_registry_set_precise": (c_int, [c_void_p, c_int]),
+    "atmm_gemm_f32": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                              c_float, c_void_p]),
+    "atmm_bypass_apply_f32": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_float, c_void_p]),
+    "atmm_merge_apply_f32": (c_int, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_int64, c_int64, c_float,
+                                     c_void_p]),
+    "atmm_delta_w_f32": (c_int, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_void_p]),
+    "atmm_forward_f32": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                 c_int64, POINTER(c_void_p), f32p, c_int64, c_void_p]),
+    "atmm_forward_f32_host": (c_int, [f32p, c_int64, c_int64, c_int64, f32p, f32p, POINTER(c_void_p), f32p, c_int64]),
+    "atmm_merge_f32_host": (c_int, [c_void_p, c_int32, f32p, c_float]),
     "atmm_plan_batch": (c_int, [i32p, c_int64, i32p, i64p, i64p, i64p]),
     "atmm_config_valid": (c_int, [i32p]),
     "atmm_m_bucket_of": (c_int, [c_int64]),
     "atmm_table_create": (c_int, [i32p, POINTER(c_void_p)]),
     "atmm_table_destroy": (None, [c_void_p]),
     "atmm_table_insert": (c_int, [c_void_p, c_int32, c_int32, c_int32, i32p, c_int64, i32p]),
-    "atmm_table_set_default": (c_int, [c_void_p, i32p]),
+    "atmm_table_set_default": (c_int, [c_void_p, i32p, i32p]),
     "atmm_table_lookup": (c_int, [c_void_p, c_int64, c_int64, c_int64, i32p]),
     "atmm_table_size": (c_int, [c_void_p, i64p]),
+    "atmm_table_find": (c_int, [c_void_p, c_int64, c_int64, c_int64, i32p, POINTER(c_int)]),
     "atmm_table_resolve_launch": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, i32p]),
     "atmm_table_save": (c_int, [c_void_p, c_char_p]),
     "atmm_table_load": (c_int, [c_char_p, POINTER(c_void_p)]),
@@ -77,6 +89,9 @@ _SIGS = {
     "atmm_plan_destroy": (None, [c_void_p]),
     "atmm_plan_set_flags": (c_int, [c_void_p, ctypes.c_uint32]),
     "atmm_forward_create": (c_int, [c_void_p, c_int, c_int64, c_int64, POINTER(c_void_p)]),
+    "atmm_forward_create_opts": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, POINTER(c_void_p)]),
+    "atmm_gemm_ex": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int, c_int64, c_int64, c_int64,
+                             c_void_p, c_void_p]),
     "atmm_forward_destroy": (None, [c_void_p]),
     "atmm_forward_run": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,
                                  c_void_p]),
@@ -93,7 +108,14 @@ _SIGS = {
     "atmm_merge_apply": (c_int, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int, c_float, c_void_p]),
     "atmm_delta_w_host": (c_int, [c_void_p, c_int32, c_int64, f32p]),
     "atmm_multiply_host": (c_int, [f32p, c_int64, c_int64, f32p, c_int64, f32p, i32p]),
-    "atmm_bench_launches": (c_int, [c_int, c_int64, c_int64, c_int64, c_int64, i32p, c_int64, c_int, i64p]),
+    "atmm_benchmark_launch": (c_int, [c_int, c_void_p, i32p, c_int, ctypes.c_uint64, i64p]),
+    "atmm_grid_bench_ns": (c_int, [c_int, c_void_p, c_int64, i32p, c_int64, c_int, c_int, i64p, c_char_p, c_size_t]),
+    "atmm_tiling_search": (c_int, [c_int, c_void_p, c_int64, i32p, c_int64, c_int, POINTER(c_void_p), c_char_p,
+                                   c_size_t]),
+    "atmm_default_shape_grid": (c_int, [c_int64, c_int64, i64p, c_int64, c_void_p, c_int64, i64p]),
+    "atmm_default_launch_candidates": (c_int, [i32p, c_int64, i64p]),
+    "atmm_table_from_scores": (c_int, [c_void_p, c_int64, i32p, c_int64, i64p, POINTER(c_void_p), c_char_p, c_size_t]),
+    "atmm_plan_create_launch": (c_int, [c_void_p, i32p, c_int64, i32p, POINTER(c_void_p)]),
     "atmm_shard_rows": (c_int, [i32p, c_int64, i32p, i64p, c_int64, c_int64, c_int64, c_int32, i32p]),
 }
 

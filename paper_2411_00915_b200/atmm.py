@@ -228,20 +228,23 @@ class TilingTable:
 
     def insert(self, m_bucket: int, k: int, n: int, config: Sequence[int], measured_ns: int = 0,
                sm100: Optional[Sequence[int]] = None) -> None:
-        s = _i32(sm100) if sm100 is not None else None
+        """sm100: {tile_m, cluster, bn, stages[, path]} (path 0 = automatic)."""
+        s = _launch5(sm100) if sm100 is not None else None
         _check(lib.atmm_table_insert(self._h, m_bucket, k, n, _p(_i32(config), i32p), int(measured_ns),
                                      _p(s, i32p) if s is not None else None))
 
-    def set_default(self, config: Sequence[int]) -> None:
-        _check(lib.atmm_table_set_default(self._h, _p(_i32(config), i32p)))
+    def set_default(self, config: Sequence[int], sm100: Optional[Sequence[int]] = None) -> None:
+        s = _launch5(sm100) if sm100 is not None else None
+        _check(lib.atmm_table_set_default(self._h, _p(_i32(config), i32p), _p(s, i32p) if s is not None else None))
 
     def lookup(self, m: int, k: int, n: int) -> TilingConfig:
         out = np.zeros(6, np.int32)
         _check(lib.atmm_table_lookup(self._h, m, k, n, _p(out, i32p)))
         return TilingConfig(out)
 
-    def resolve_launch(self, m: int, d_in: int, rank: int, d_out: int) -> Tuple[int, int, int, int]:
-        out = np.zeros(4, np.int32)
+    def resolve_launch(self, m: int, d_in: int, rank: int, d_out: int) -> Tuple[int, int, int, int, int]:
+        """{tile_m, cluster, bn, stages, path} for a segment of m rows."""
+        out = np.zeros(5, np.int32)
         _check(lib.atmm_table_resolve_launch(self._h, m, d_in, rank, d_out, _p(out, i32p)))
         return tuple(int(v) for v in out)
 
@@ -249,6 +252,14 @@ class TilingTable:
         s = ctypes.c_int64(0)
         _check(lib.atmm_table_size(self._h, ctypes.byref(s)))
         return s.value
+
+    def find_entry(self, m: int, k: int, n: int) -> Optional[Tuple[int, ...]]:
+        """The B200 launch of the entry lookup(m, k, n) resolves to (exact or
+        nearest bucket within 32, tiling.hpp:181-199), None on a miss."""
+        out = np.zeros(5, np.int32)
+        found = ctypes.c_int(0)
+        _check(lib.atmm_table_find(self._h, m, k, n, _p(out, i32p), ctypes.byref(found)))
+        return tuple(int(v) for v in out) if found.value else None
 
     def save(self, path: str) -> None:
         _check(lib.atmm_table_save(self._h, str(path).encode()))
@@ -260,8 +271,17 @@ class TilingTable:
         return cls(_handle=h)
 
 
-def heuristic_launch(m: int, d_in: int, rank: int, d_out: int) -> Tuple[int, int, int, int]:
-    out = np.zeros(4, np.int32)
+def _launch5(launch: Sequence[int]) -> np.ndarray:
+    v = [int(x) for x in launch]
+    if len(v) == 4:
+        v.append(0)
+    if len(v) != 5:
+        raise ConfigError("a launch is {tile_m, cluster, bn, stages[, path]}")
+    return _i32(v)
+
+
+def heuristic_launch(m: int, d_in: int, rank: int, d_out: int) -> Tuple[int, int, int, int, int]:
+    out = np.zeros(5, np.int32)
     _check(lib.atmm_table_resolve_launch(None, m, d_in, rank, d_out, _p(out, i32p)))
     return tuple(int(v) for v in out)
 
@@ -272,11 +292,17 @@ def heuristic_launch(m: int, d_in: int, rank: int, d_out: int) -> Tuple[int, int
 class AdapterRegistry:
     """Device-resident AdapterSet (adapter.hpp:18-110) for one projection."""
 
-    def __init__(self, num_layers: int, d_in: int, d_out: Optional[int] = None, device: int = 0):
+    def __init__(self, num_layers: int, d_in: int, d_out: Optional[int] = None, device: int = 0,
+                 precise: bool = False):
+        """precise: also keep the fp32-faithful split images of every factor
+        (atmm_registry_set_precise) for the fp32 entry points."""
         d_out = d_in if d_out is None else d_out
         h = ctypes.c_void_p()
         _check(lib.atmm_registry_create(device, num_layers, d_in, d_out, ctypes.byref(h)))
         self._h = h
+        self.precise = bool(precise)
+        if precise:
+            _check(lib.atmm_registry_set_precise(h, 1))
         self.device = device
         self.num_layers, self.d_in, self.d_out = num_layers, d_in, d_out
 
@@ -402,12 +428,21 @@ class BypassPlan:
     """plan_batch + launch grouping for one batch on one registry."""
 
     def __init__(self, registry: AdapterRegistry, assignment: Sequence[int], table: Optional[TilingTable] = None,
-                 rows: Optional[Sequence[int]] = None, n_rows: Optional[int] = None):
+                 rows: Optional[Sequence[int]] = None, n_rows: Optional[int] = None,
+                 launch: Optional[Sequence[int]] = None):
         """rows (optional): routed entry i is row rows[i] of X / Y, which
-        have n_rows rows (atmm_plan_create_mapped); default: entry i = row i."""
+        have n_rows rows (atmm_plan_create_mapped); default: entry i = row i.
+        launch (optional): {tile_m, cluster, bn, stages[, path]} forced for
+        every segment instead of the table's (atmm_plan_create_launch)."""
         a = _i32(assignment).reshape(-1)
         h = ctypes.c_void_p()
-        if rows is None:
+        if launch is not None:
+            if rows is not None:
+                raise ConfigError("a forced launch takes no row map")
+            _check(lib.atmm_plan_create_launch(registry.handle, _p(a, i32p), a.size, _p(_launch5(launch), i32p),
+                                               ctypes.byref(h)))
+            self.n = int(a.size)
+        elif rows is None:
             _check(lib.atmm_plan_create(registry.handle, _p(a, i32p), a.size, table.handle if table else None,
                                         ctypes.byref(h)))
             self.n = int(a.size)
@@ -460,9 +495,18 @@ class BypassPlan:
         return a.value, b.value, c.value
 
     def apply(self, x, y, layer: int = 0, scale: float = 1.0, stream=None) -> None:
-        """y[row] += scale * s_a * (x[row] @ down_a[layer]) @ up_a[layer] (torch CUDA tensors)."""
+        """y[row] += scale * s_a * (x[row] @ down_a[layer]) @ up_a[layer] (torch CUDA tensors).
+        fp32 x and y on a precise registry take the fp32-faithful path."""
         import torch
 
+        if x.dtype == torch.float32 and y.dtype == torch.float32 and self.registry.precise:
+            if x.dim() != 2 or y.dim() != 2 or x.shape[0] != self.n or y.shape[0] != self.n:
+                raise ShapeError(f"x/y must be 2-D with {self.n} rows")
+            if x.stride(1) != 1 or y.stride(1) != 1 or not (x.is_cuda and y.is_cuda):
+                raise ShapeError("x and y must be CUDA tensors with contiguous rows")
+            _check(lib.atmm_bypass_apply_f32(self._h, layer, x.data_ptr(), x.stride(0), y.data_ptr(), y.stride(0),
+                                             float(scale), _stream_ptr(stream)))
+            return
         if x.dtype != torch.bfloat16 or not x.is_cuda:
             raise ShapeError("x must be a CUDA bfloat16 tensor")
         if y.dtype not in (torch.bfloat16, torch.float32) or not y.is_cuda:
@@ -541,6 +585,24 @@ class MixturePlan:
             self.plan.apply(x, y, layer, scale, stream)
 
 
+class GemmOpts(ctypes.Structure):
+    """atmm_gemm_opts: explicit GEMM tile options (0 / pair -1 = automatic)."""
+
+    _fields_ = [("pair", ctypes.c_int32), ("bn", ctypes.c_int32), ("kz", ctypes.c_int32), ("ks", ctypes.c_int32),
+                ("mc", ctypes.c_int32), ("stages", ctypes.c_int32)]
+
+
+def _gemm_opts(opts: Optional[dict]):
+    if not opts:
+        return None
+    o = GemmOpts(pair=-1)
+    for k, v in opts.items():
+        if k not in ("pair", "bn", "kz", "ks", "mc", "stages"):
+            raise ConfigError(f"unknown GEMM option {k!r}")
+        setattr(o, k, int(v))
+    return ctypes.byref(o)
+
+
 class LayerForward:
     """The serving model's stack forward on device (model.hpp:192-328):
     cur <- tanh(cur @ W_l + bypass_l(cur)) for every layer, the bypass riding
@@ -553,15 +615,18 @@ class LayerForward:
     STATS = ("n", "d", "bn", "tiles", "grid", "ext_blocks", "shrink_items", "shrink_ks", "sorted", "gemm_stages",
              "shrink_stages", "gemm_cta_group", "gemm_split_k")
 
-    def __init__(self, plan=None, n: Optional[int] = None, hidden_dim: Optional[int] = None, device: int = 0):
+    def __init__(self, plan=None, n: Optional[int] = None, hidden_dim: Optional[int] = None, device: int = 0,
+                 opts: Optional[dict] = None):
+        """opts: explicit GEMM tile options {pair, bn, kz, ks, stages}
+        (atmm_gemm_opts), automatic when omitted."""
         if isinstance(plan, MixturePlan):
             n = plan.n if n is None else n
             if hidden_dim is None and plan.plan is not None:
                 hidden_dim = plan.plan.registry.d_in
             plan = plan.plan
         h = ctypes.c_void_p()
-        _check(lib.atmm_forward_create(plan.handle if plan is not None else None, int(device), int(n or 0),
-                                       int(hidden_dim or 0), ctypes.byref(h)))
+        _check(lib.atmm_forward_create_opts(plan.handle if plan is not None else None, int(device), int(n or 0),
+                                            int(hidden_dim or 0), _gemm_opts(opts), ctypes.byref(h)))
         self._h = h
         self.plan = plan  # keeps the plan (and its registry) alive
         st = self.stats()
@@ -615,7 +680,7 @@ def forward_merged(w, x, device: Optional[int] = None):
     return LayerForward(None, n=x.shape[0], hidden_dim=x.shape[1], device=dev or 0).run(w, x)
 
 
-def gemm(a, b, out=None, out_dtype=None):
+def gemm(a, b, out=None, out_dtype=None, opts: Optional[dict] = None):
     """Plain device GEMM out = a @ b (atmm_multiply_into, atmm.hpp:111-154,
     with a dense right operand; the base GEMM of model.hpp:238): bf16 CUDA
     tensors a [m, k], b [k, n] (unit inner stride), fp32 accumulation, out
@@ -635,9 +700,54 @@ def gemm(a, b, out=None, out_dtype=None):
     if out.dtype not in (torch.bfloat16, torch.float32) or tuple(out.shape) != (m, n) or out.stride(1) != 1:
         raise ShapeError("out must be a bf16 or fp32 [m, n] tensor with unit inner stride")
     with torch.cuda.device(a.device):
-        _check(lib.atmm_gemm(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0),
-                             F32 if out.dtype == torch.float32 else BF16, m, k, n,
-                             torch.cuda.current_stream(a.device).cuda_stream))
+        _check(lib.atmm_gemm_ex(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0),
+                                F32 if out.dtype == torch.float32 else BF16, m, k, n, _gemm_opts(opts),
+                                torch.cuda.current_stream(a.device).cuda_stream))
+    return out
+
+
+def gemm_f32(a, b, out=None, beta: float = 0.0):
+    """fp32-faithful out = a @ b (+ out when beta = 1) on the tensor cores
+    (atmm_gemm_f32: one split-bf16 tcgen05 product); fp32 CUDA tensors."""
+    import torch
+
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[0]:
+        raise ShapeError(f"gemm shapes {tuple(a.shape)} x {tuple(b.shape)} do not chain")
+    if a.dtype != torch.float32 or b.dtype != torch.float32 or not (a.is_cuda and b.is_cuda):
+        raise ShapeError("a and b must be fp32 CUDA tensors")
+    if a.stride(1) != 1 or b.stride(1) != 1:
+        raise ShapeError("a and b need unit inner stride")
+    m, k = a.shape
+    n = b.shape[1]
+    if out is None:
+        out = torch.empty(m, n, device=a.device, dtype=torch.float32)
+    if out.dtype != torch.float32 or tuple(out.shape) != (m, n) or out.stride(1) != 1:
+        raise ShapeError("out must be an fp32 [m, n] tensor with unit inner stride")
+    with torch.cuda.device(a.device):
+        _check(lib.atmm_gemm_f32(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0),
+                                 m, k, n, float(beta), torch.cuda.current_stream(a.device).cuda_stream))
+    return out
+
+
+def forward_f32(w, x, plans=(), out=None, stream=None):
+    """The stack forward (model.hpp:192-328) fp32-faithfully:
+    cur <- tanh(cur @ W_l + sum_i s_i bypass_{plan_i, l}(cur)); plans is a
+    sequence of (BypassPlan on a precise registry, scale)."""
+    import torch
+
+    if w.dim() != 3 or w.dtype != torch.float32 or not w.is_cuda or w.stride(2) != 1:
+        raise ShapeError("w must be an [L, d, d] fp32 CUDA tensor with contiguous rows")
+    if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda or x.stride(1) != 1:
+        raise ShapeError("x must be an [n, d] fp32 CUDA tensor with contiguous rows")
+    n, d = x.shape
+    if tuple(w.shape[1:]) != (d, d):
+        raise ShapeError(f"w {tuple(w.shape)} does not match d={d}")
+    if out is None:
+        out = torch.empty(n, d, device=x.device, dtype=torch.float32)
+    hs = (ctypes.c_void_p * max(1, len(plans)))(*[p.handle for p, _ in plans])
+    sc = _f32([s for _, s in plans] or [0.0])
+    _check(lib.atmm_forward_f32(w.data_ptr(), w.stride(1), w.stride(0), w.shape[0], n, d, x.data_ptr(), x.stride(0),
+                                out.data_ptr(), out.stride(0), hs, _p(sc, f32p), len(plans), _stream_ptr(stream)))
     return out
 
 
@@ -830,13 +940,105 @@ def atmm_multiply(a, b, config: Sequence[int]) -> np.ndarray:
     return out
 
 
-def bench_launches(m: int, d_in: int, rank: int, d_out: int, launches: Iterable[Sequence[int]],
-                   trials: int = 5, device: int = 0) -> List[int]:
-    arr = _i32([list(l) for l in launches]).reshape(-1)
-    count = arr.size // 4
-    out = np.zeros(count, np.int64)
-    _check(lib.atmm_bench_launches(device, m, d_in, rank, d_out, _p(arr, i32p), count, trials, _p(out, i64p)))
-    return [int(v) for v in out]
+# ------------------------------------------------- offline tiling search ---
+
+
+class TuneShape(ctypes.Structure):
+    """atmm_tune_shape: `segments` segments of `m` rows, each its own adapter
+    of rank `rank`, at (d_in, d_out) (the B200 re-reading of GemmShape,
+    atmm.hpp:218-220)."""
+
+    _fields_ = [("m", ctypes.c_int64), ("d_in", ctypes.c_int64), ("rank", ctypes.c_int64),
+                ("d_out", ctypes.c_int64), ("segments", ctypes.c_int64)]
+
+    def as_tuple(self) -> Tuple[int, int, int, int, int]:
+        return (self.m, self.d_in, self.rank, self.d_out, self.segments)
+
+
+def _shapes(shapes) -> ctypes.Array:
+    arr = (TuneShape * len(shapes))()
+    for i, sh in enumerate(shapes):
+        arr[i] = sh if isinstance(sh, TuneShape) else TuneShape(*[int(v) for v in sh])
+    return arr
+
+
+def _launches(launches) -> np.ndarray:
+    return np.ascontiguousarray(np.concatenate([_launch5(l) for l in launches]))
+
+
+def default_shape_grid(d_in: int, d_out: Optional[int] = None, ranks: Optional[Sequence[int]] = None) -> List[tuple]:
+    """default_shape_grid (atmm.hpp:341-355) for the bypass: (m, d_in, rank, d_out, segments) tuples."""
+    d_out = d_in if d_out is None else d_out
+    rk = np.ascontiguousarray(np.asarray(ranks or [], np.int64))
+    n = ctypes.c_int64(0)
+    _check(lib.atmm_default_shape_grid(d_in, d_out, _p(rk, i64p) if rk.size else None, rk.size, None, 0,
+                                       ctypes.byref(n)))
+    arr = (TuneShape * n.value)()
+    _check(lib.atmm_default_shape_grid(d_in, d_out, _p(rk, i64p) if rk.size else None, rk.size, arr, n.value,
+                                       ctypes.byref(n)))
+    return [a.as_tuple() for a in arr]
+
+
+def default_launch_candidates() -> List[Tuple[int, ...]]:
+    """The curated B200 candidate launches {tile_m, cluster, bn, stages, path}."""
+    n = ctypes.c_int64(0)
+    _check(lib.atmm_default_launch_candidates(None, 0, ctypes.byref(n)))
+    out = np.zeros(5 * n.value, np.int32)
+    _check(lib.atmm_default_launch_candidates(_p(out, i32p), n.value, ctypes.byref(n)))
+    return [tuple(int(v) for v in out[5 * i: 5 * i + 5]) for i in range(n.value)]
+
+
+def benchmark_launch(shape, launch: Sequence[int], trials: int = 5, seed: int = 0x5EEDBEEF, device: int = 0) -> int:
+    """benchmark_config (atmm.hpp:188-216): median ns per apply."""
+    sh = _shapes([shape])
+    out = ctypes.c_int64(0)
+    _check(lib.atmm_benchmark_launch(device, sh, _p(_launch5(launch), i32p), int(trials), int(seed), ctypes.byref(out)))
+    return out.value
+
+
+def grid_bench_ns(shapes, launches, trials: int = 5, rounds: int = 3, device: int = 0,
+                  failures: Optional[list] = None) -> np.ndarray:
+    """grid_bench_ns (atmm.hpp:229-270): [shapes x launches] median-of-round-medians ns."""
+    sh, la = _shapes(shapes), _launches(launches)
+    scores = np.zeros((len(shapes), len(launches)), np.int64)
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib.atmm_grid_bench_ns(device, sh, len(shapes), _p(la, i32p), len(launches), int(trials), int(rounds),
+                                  _p(scores, i64p), buf, len(buf)))
+    if failures is not None:
+        failures.extend(x for x in buf.value.decode().split("\n") if x)
+    return scores
+
+
+def table_from_scores(shapes, launches, scores, failures: Optional[list] = None) -> "TilingTable":
+    """The selection half of tiling_search (atmm.hpp:293-329) over a score
+    grid [shapes x launches] (np.iinfo(np.int64).max = failed).  Host only."""
+    sh, la = _shapes(shapes), _launches(launches)
+    sc = np.ascontiguousarray(np.asarray(scores, np.int64))
+    if sc.shape != (len(shapes), len(launches)):
+        raise ShapeError("scores must be [len(shapes), len(launches)]")
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib.atmm_table_from_scores(sh, len(shapes), _p(la, i32p), len(launches), _p(sc, i64p), ctypes.byref(h),
+                                      buf, len(buf)))
+    if failures is not None:
+        failures.extend(x for x in buf.value.decode().split("\n") if x)
+    return TilingTable(_handle=h)
+
+
+def tiling_search(shapes, launches=None, trials: int = 5, device: int = 0,
+                  failures: Optional[list] = None) -> "TilingTable":
+    """tiling_search (atmm.hpp:276-330) on the B200: per-shape argmin, the
+    most frequent winner as default; returns a TilingTable (save() writes the
+    reference's JSON schema plus the "sm100" launch extension)."""
+    launches = launches or default_launch_candidates()
+    sh, la = _shapes(shapes), _launches(launches)
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib.atmm_tiling_search(device, sh, len(shapes), _p(la, i32p), len(launches), int(trials), ctypes.byref(h),
+                                  buf, len(buf)))
+    if failures is not None:
+        failures.extend(x for x in buf.value.decode().split("\n") if x)
+    return TilingTable(_handle=h)
 
 
 def shard_rows(assignment: Sequence[int], adapter_ranks: dict, d_in: int, d_out: int, num_shards: int) -> np.ndarray:

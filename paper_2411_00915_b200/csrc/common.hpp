@@ -78,8 +78,19 @@ struct LaunchCfg {
   int32_t cluster = 8;   // CTAs per cluster (K / N split)
   int32_t bn = 128;      // expand N chunk
   int32_t stages = 0;    // 0 = as many as shared memory allows (<= 6)
+  int32_t path = 0;      // kernel: 0 automatic, 1 all-to-all fused, 2 split pair, 3 general fused
   auto operator<=>(const LaunchCfg&) const = default;
 };
+// A launch as the 5 ints of the C ABI ({tile_m, cluster, bn, stages, path}).
+void validate_launch(const LaunchCfg& l);
+inline LaunchCfg launch_from_ints(const int32_t* v) { return LaunchCfg{v[0], v[1], v[2], v[3], v[4]}; }
+inline void launch_to_ints(const LaunchCfg& l, int32_t* v) {
+  v[0] = l.tile_m;
+  v[1] = l.cluster;
+  v[2] = l.bn;
+  v[3] = l.stages;
+  v[4] = l.path;
+}
 
 // ---- reference fixture I/O (matrix.hpp:183-218, model_io.hpp:25-114) ----
 // Binary matrix: little-endian u32 rows, u32 cols, u8 scalar width, row-major payload.
@@ -108,8 +119,9 @@ class TilingTable {
   TilingTable();  // reference default config, heuristic B200 resolution
   explicit TilingTable(const TilingConfig& dflt);
   void insert(ShapeKey key, const TilingConfig& cfg, int64_t ns, const LaunchCfg* sm100);
-  void set_default(const TilingConfig& cfg);
+  void set_default(const TilingConfig& cfg, const LaunchCfg* sm100 = nullptr);
   const TilingConfig& default_config() const { return default_; }
+  const LaunchCfg* default_launch() const { return has_default_sm100_ ? &default_sm100_ : nullptr; }
   const std::map<ShapeKey, TableEntry>& entries() const { return entries_; }
   // tiling.hpp:181-199
   const TableEntry* find(int64_t m, int64_t k, int64_t n) const;
@@ -124,6 +136,8 @@ class TilingTable {
   std::map<ShapeKey, TableEntry> entries_;
   TilingConfig default_;
   bool heuristic_default_ = true;
+  bool has_default_sm100_ = false;  // the default's B200 launch (JSON "default_sm100")
+  LaunchCfg default_sm100_;
 };
 
 LaunchCfg heuristic_launch(int64_t m, int64_t d_in, int64_t rank, int64_t d_out);

@@ -20,6 +20,7 @@
 #include <new>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.hpp"
@@ -280,7 +281,26 @@ struct Slot {
   uint16_t* up_t = nullptr;
   bool live = false;
   bool async_owned = false;  // buffers from cudaMallocAsync (put_async): freed stream-ordered
+  // fp32-faithful images (precise registries only), bf16 hi / lo splits per layer:
+  // (kSplitParts K slices each, precise_kernels.cu)
+  uint16_t* p_down_b = nullptr;  // [L][6 kpd x r8]   B-operand image of down (x . down)
+  uint16_t* p_up_b = nullptr;    // [L][6 r8 x n8]    B-operand image of up   (mid . up, dW)
+  uint16_t* p_down_a = nullptr;  // [L][d_in x 6 r8]  A-operand image of down (dW = down . up)
 };
+
+// Frees a slot's device buffers (stream-ordered when `async`: buffers from
+// stream-ordered allocation, released after every earlier use on `st`).
+static void free_slot(Slot& s, cudaStream_t st = nullptr, bool async = false) {
+  for (uint16_t* p : {s.down_t, s.up_t, s.p_down_b, s.p_up_b, s.p_down_a}) {
+    if (!p) continue;
+    if (async) {
+      cudaFreeAsync(p, st);
+    } else {
+      cudaFree(p);
+    }
+  }
+  s.down_t = s.up_t = s.p_down_b = s.p_up_b = s.p_down_a = nullptr;
+}
 
 }  // namespace atmm
 
@@ -303,13 +323,11 @@ struct atmm_registry {
     return *stage.back().second;
   }
   uint64_t generation = 0;
+  bool precise = false;  // keep fp32-faithful factor images (atmm_registry_set_precise)
 
   ~atmm_registry() {
     DeviceGuard g(device, std::nothrow);
-    for (auto& s : slots) {
-      if (s.down_t) cudaFree(s.down_t);
-      if (s.up_t) cudaFree(s.up_t);
-    }
+    for (auto& s : slots) free_slot(s);
   }
   void sync_slots() {
     std::vector<SlotDesc> h(slots.size());
@@ -336,6 +354,70 @@ struct atmm_registry {
 };
 
 // =========================================================================
+// fp32-faithful factor images (precise registries; precise_kernels.cu)
+// =========================================================================
+namespace atmm {
+cudaError_t launch_split3_rows(const float* src, int64_t lds, const int32_t* rows, int64_t m, int64_t k, int64_t kp,
+                               uint16_t* dst, int64_t ldd, cudaStream_t s);
+cudaError_t launch_split3_cols(const float* src, int64_t lds, int64_t k, int64_t n, int64_t kp, int64_t np,
+                               uint16_t* dst, cudaStream_t s);
+cudaError_t launch_rows_out(const float* t, int64_t ldt, const int32_t* rows, int64_t m, int64_t n, float* c,
+                            int64_t ldc, float alpha, float beta, cudaStream_t s);
+cudaError_t launch_tanh(float* x, int64_t ld, int64_t m, int64_t n, cudaStream_t s);
+
+// Image sizes (elements per layer) of a slot of rank r in registry reg.
+struct PreciseDims {
+  int64_t kpd, r8, n8, db, ub, da;
+  PreciseDims(const atmm_registry* reg, int64_t rank)
+      : kpd(round_up(reg->d_in, 8)), r8(round_up(rank, 8)), n8(round_up(reg->d_out, 8)),
+        db(kSplitParts * kpd * r8), ub(kSplitParts * r8 * n8), da(reg->d_in * kSplitParts * r8) {}
+};
+
+// Builds the slot's images from fp32 factors already on the device
+// (down [L][d_in x r], up [L][r x d_out]), stream-ordered on st.
+static void build_precise_device(atmm_registry* r, Slot& s, const float* down, const float* up, cudaStream_t st,
+                                 bool async) {
+  const PreciseDims pd(r, s.rank);
+  const size_t L = static_cast<size_t>(r->L);
+  void** outs[3] = {reinterpret_cast<void**>(&s.p_down_b), reinterpret_cast<void**>(&s.p_up_b),
+                    reinterpret_cast<void**>(&s.p_down_a)};
+  const int64_t sizes[3] = {pd.db, pd.ub, pd.da};
+  for (int i = 0; i < 3; ++i) {
+    const size_t bytes = L * static_cast<size_t>(sizes[i]) * 2;
+    if (async) {
+      CUDA_CHECK(cudaMallocAsync(outs[i], bytes, st));
+    } else {
+      CUDA_CHECK(cudaMalloc(outs[i], bytes));
+    }
+  }
+  for (int64_t l = 0; l < r->L; ++l) {
+    const float* dn = down + l * r->d_in * s.rank;
+    const float* u = up + l * s.rank * r->d_out;
+    CUDA_CHECK(launch_split3_cols(dn, s.rank, r->d_in, s.rank, pd.kpd, pd.r8, s.p_down_b + l * pd.db, st));
+    CUDA_CHECK(launch_split3_cols(u, r->d_out, s.rank, r->d_out, pd.r8, pd.n8, s.p_up_b + l * pd.ub, st));
+    CUDA_CHECK(launch_split3_rows(dn, s.rank, nullptr, r->d_in, s.rank, pd.r8, s.p_down_a + l * pd.da,
+                                  kSplitParts * pd.r8, st));
+  }
+}
+
+// fp32-faithful bypass on a plan (defined with the precise entry points below).
+namespace {
+void bypass_f32(const atmm_plan* p, int64_t layer, const float* x, int64_t ldx, float* y, int64_t ldy, float scale,
+                cudaStream_t st);
+}  // namespace
+
+// The same from host fp32 factors (synchronous, atmm_registry_put).
+static void build_precise_host(atmm_registry* r, Slot& s, const float* down, const float* up) {
+  const size_t fd = static_cast<size_t>(r->L * r->d_in * s.rank), fu = static_cast<size_t>(r->L * s.rank * r->d_out);
+  DevBuf<float> tmp(fd + fu);
+  CUDA_CHECK(cudaMemcpy(tmp.p, down, fd * 4, cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMemcpy(tmp.p + fd, up, fu * 4, cudaMemcpyHostToDevice));
+  build_precise_device(r, s, tmp.p, tmp.p + fd, nullptr, false);
+  CUDA_CHECK(cudaDeviceSynchronize());
+}
+}  // namespace atmm
+
+// =========================================================================
 // Plan: routing tables + launch groups
 // =========================================================================
 namespace atmm {
@@ -360,6 +442,7 @@ struct LaunchGroup {
   A2aLayout a2a[2];  // per Y dtype (ATMM_BF16, ATMM_F32)
   SplitLayout split;
   int32_t rows_max = 0;
+  int32_t path = 0;  // LaunchCfg::path (0 automatic)
   int32_t cluster = 1, bn = 128, stages = 2, ustages = 1, ny = 2;
   int32_t a_bytes = 0, ustage_bytes = 0, ybuf_bytes = 0, rep = 1, nbuf = 2;
   uint32_t off_up = 0, off_y = 0;
@@ -474,7 +557,6 @@ static void resolve_group(LaunchGroup& g, int64_t d_in, int64_t d_out, int32_t t
 static A2aLayout resolve_a2a(int64_t d_in, int64_t d_out, int32_t cluster, int32_t rows_max, int32_t r_pad,
                              int64_t esz) {
   A2aLayout l;
-  if (std::getenv("ATMM_DISABLE_A2A")) return l;
   if (rows_max > kTileM || d_out % 8 != 0) return l;
   const int64_t nkb = (d_in + kBK - 1) / kBK;
   const int64_t nun = (d_out + kNUnit - 1) / kNUnit;
@@ -616,45 +698,30 @@ struct atmm_plan {
 namespace atmm {
 // Which kernel a launch group runs: the fused all-to-all kernel for small
 // (latency-bound) tiles, the split shrink + expand pair for large ones, the
-// general fused kernel otherwise.  ATMM_PATH=a2a|split|fused forces one
-// where it is applicable (A/B runs).
+// general fused kernel otherwise.  A launch's `path` (tiling table entry or
+// atmm_plan_create_launch) forces one where it is applicable.
 enum class BypassPath { kA2a, kSplit, kFused };
 static BypassPath choose_path(const LaunchGroup& g, int y_dtype, bool y_vec) {
   const int di = y_dtype == ATMM_BF16 ? 0 : 1;
   const bool a2a = g.a2a[di].ok && y_vec;
   const bool split = g.split.ok_dt[di] && y_vec;
-  if (const char* e = std::getenv("ATMM_PATH")) {
-    const std::string f(e);
-    if (f == "a2a" && a2a) return BypassPath::kA2a;
-    if (f == "split" && split) return BypassPath::kSplit;
-    if (f == "fused") return BypassPath::kFused;
-  }
+  if (g.path == ATMM_PATH_A2A && a2a) return BypassPath::kA2a;
+  if (g.path == ATMM_PATH_SPLIT && split) return BypassPath::kSplit;
+  if (g.path == ATMM_PATH_FUSED) return BypassPath::kFused;
   if (a2a && g.rows_max <= 32) return BypassPath::kA2a;
   if (split) return BypassPath::kSplit;  // taken through the plan's merged split range
   if (a2a) return BypassPath::kA2a;
   return BypassPath::kFused;
 }
 
-// Expand item width for bf16 Y: 128 G columns, G adjacent columns per
-// epilogue thread (ATMM_EXPAND_G=1|2 for A/B runs).
-static int expand_g_bf16() {
-  static const int g = [] {
-    const char* e = std::getenv("ATMM_EXPAND_G");
-    return e && std::atoi(e) == 1 ? 1 : 2;
-  }();
-  return g;
-}
+// Expand item width for bf16 Y: 128 G columns, G = 2 adjacent columns per
+// epilogue thread (measured: 128-column items 48 vs 36 us at cfg3).
+static int expand_g_bf16() { return 2; }
 
-// Fixed per-item costs (bytes-equivalent) of the split kernels' balancing
-// (ATMM_SCOST / ATMM_ECOST for A/B runs).
-static int64_t shrink_fixed_cost() {
-  static const int64_t v = std::getenv("ATMM_SCOST") ? std::atoll(std::getenv("ATMM_SCOST")) : 32768;
-  return v;
-}
-static int64_t expand_fixed_cost() {
-  static const int64_t v = std::getenv("ATMM_ECOST") ? std::atoll(std::getenv("ATMM_ECOST")) : 32768;
-  return v;
-}
+// Fixed per-item costs (bytes-equivalent: barriers, 4 MMAs) of the split
+// kernels' work balancing.
+static int64_t shrink_fixed_cost() { return 32768; }
+static int64_t expand_fixed_cost() { return 32768; }
 
 static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, int32_t r_pad) {
   SplitLayout l;
@@ -722,7 +789,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     int32_t r_pad_max = 16;
     int32_t rows_max = 1;
   };
-  std::map<std::pair<int32_t, std::pair<int32_t, int32_t>>, Pending> by_launch;
+  std::map<std::tuple<int32_t, int32_t, int32_t, int32_t>, Pending> by_launch;
   const size_t S = plan->bp.seg_adapter.size();
   for (size_t s = 0; s < S; ++s) {
     const int32_t id = plan->bp.seg_adapter[s];
@@ -739,7 +806,8 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     const int64_t tm = std::clamp<int64_t>(lc.tile_m, 1, kTileM);
     const int64_t ntiles = (ns + tm - 1) / tm;
     const int64_t per = (ns + ntiles - 1) / ntiles;  // balanced tiles
-    auto& pend = by_launch[{lc.cluster, {lc.bn, lc.stages}}];
+    const auto lkey = std::make_tuple(lc.cluster, lc.bn, lc.stages, lc.path);
+    auto& pend = by_launch[lkey];
     pend.cfg = lc;
     pend.r_pad_max = std::max<int32_t>(pend.r_pad_max, static_cast<int32_t>(sl.r_pad));
     for (int64_t t = 0; t < ntiles; ++t) {
@@ -761,6 +829,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     LaunchGroup g;
     g.cluster = pend.cfg.cluster;
     g.bn = pend.cfg.bn;
+    g.path = pend.cfg.path;
     g.r_pad_max = pend.r_pad_max;
     resolve_group(g, reg->d_in, reg->d_out, pend.rows_max, pend.cfg.stages);
     g.a2a[0] = resolve_a2a(reg->d_in, reg->d_out, g.cluster, pend.rows_max, pend.r_pad_max, 2);
@@ -1201,11 +1270,11 @@ int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const 
     CUDA_CHECK(cudaMalloc(&s.up_t, hu.size() * 2));
     CUDA_CHECK(cudaMemcpy(s.down_t, hd.data(), hd.size() * 2, cudaMemcpyHostToDevice));
     CUDA_CHECK(cudaMemcpy(s.up_t, hu.data(), hu.size() * 2, cudaMemcpyHostToDevice));
+    if (r->precise) build_precise_host(r, s, down, up);
     auto it = r->slot_of.find(adapter_id);
     if (it != r->slot_of.end()) {
       Slot& old = r->slots[static_cast<size_t>(it->second)];
-      cudaFree(old.down_t);
-      cudaFree(old.up_t);
+      free_slot(old);
       old = s;
     } else {
       int idx = -1;
@@ -1231,6 +1300,7 @@ int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts
                                const float* part_signs) {
   return guarded([&] {
     if (!r || !part_ids || !part_signs || n_parts < 1) fail(ATMM_ERR_CONFIG, "null registry or empty part list");
+    if (r->precise) fail(ATMM_ERR_CONFIG, "combined slots are not built on a precise registry (apply the parts)");
     std::vector<Slot> parts;
     int64_t r_c = 0, alg = 0;
     for (int64_t i = 0; i < n_parts; ++i) {
@@ -1275,8 +1345,7 @@ int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts
     auto it = r->slot_of.find(new_id);
     if (it != r->slot_of.end()) {
       Slot& old = r->slots[static_cast<size_t>(it->second)];
-      cudaFree(old.down_t);
-      cudaFree(old.up_t);
+      free_slot(old);
       old = s;
     } else {
       int idx = -1;
@@ -1342,17 +1411,23 @@ int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, 
     CUDA_CHECK(cudaMemcpyAsync(stage + fd, up, fu * 4, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(launch_pack_factors(stage, stage + fd, r->L, r->d_in, r->d_out, rank, r->d_in_pad, r->d_out_pad, r_pad,
                                    s.down_t, s.up_t, st));
+    if (r->precise) {
+      if (same) {  // a same-shape swap reuses the bf16 buffers; the images are rebuilt
+        for (uint16_t* p : {same->p_down_b, same->p_up_b, same->p_down_a}) {
+          if (p) CUDA_CHECK(cudaFreeAsync(p, st));
+        }
+      }
+      build_precise_device(r, s, stage, stage + fd, st, true);
+    }
     if (same) {
       *same = s;
     } else if (it != r->slot_of.end()) {
       Slot& old = r->slots[static_cast<size_t>(it->second)];
       if (old.async_owned) {
-        CUDA_CHECK(cudaFreeAsync(old.down_t, st));  // stream order: after every earlier use on this stream
-        CUDA_CHECK(cudaFreeAsync(old.up_t, st));
+        free_slot(old, st, true);  // stream order: after every earlier use on this stream
       } else {
         CUDA_CHECK(cudaStreamSynchronize(st));
-        cudaFree(old.down_t);
-        cudaFree(old.up_t);
+        free_slot(old);
       }
       old = s;
     } else {
@@ -1410,8 +1485,7 @@ int atmm_registry_remove(atmm_registry* r, int32_t adapter_id) {
     if (it == r->slot_of.end()) fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(adapter_id));
     DeviceGuard g(r->device);
     Slot& s = r->slots[static_cast<size_t>(it->second)];
-    cudaFree(s.down_t);
-    cudaFree(s.up_t);
+    free_slot(s);
     s = Slot{};
     r->slot_of.erase(it);
     r->sync_slots();
@@ -1457,6 +1531,16 @@ int atmm_plan_create_mapped(atmm_registry* r, const int32_t* assignment, const i
     if (n_rows < n) fail(ATMM_ERR_SHAPE, "n_rows must be >= the number of routed rows");
     const TilingTable* t = table ? &table->t : nullptr;
     *out = build_plan(r, assignment, n, t, nullptr, rows, n_rows).release();
+  });
+}
+
+int atmm_plan_create_launch(atmm_registry* r, const int32_t* assignment, int64_t n, const int32_t launch[5],
+                            atmm_plan** out) {
+  return guarded([&] {
+    if (!r || !out || !launch) fail(ATMM_ERR_CONFIG, "null registry, launch or output");
+    const LaunchCfg lc = launch_from_ints(launch);
+    validate_launch(lc);
+    *out = build_plan(r, assignment, n, nullptr, &lc).release();
   });
 }
 
@@ -1562,6 +1646,15 @@ int atmm_run_bypass_host(atmm_registry* r, const float* x, int64_t n, const int3
     DeviceGuard g(r->device);
     const TilingTable* t = table ? &table->t : nullptr;
     auto plan = build_plan(r, assignment, n, t, nullptr);
+    if (r->precise) {  // fp32-faithful: fp32 X / out, split-bf16 tensor-core products
+      DevBuf<float> xd(static_cast<size_t>(n * r->d_in)), yd(static_cast<size_t>(n * r->d_out));
+      CUDA_CHECK(cudaMemcpy(xd.p, x, xd.n * 4, cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemset(yd.p, 0, yd.n * 4));
+      bypass_f32(plan.get(), layer, xd.p, r->d_in, yd.p, r->d_out, 1.0f, nullptr);
+      CUDA_CHECK(cudaMemcpy(out, yd.p, yd.n * 4, cudaMemcpyDeviceToHost));
+      flops_add(plan->flops);
+      return;
+    }
     const int64_t ldx = round_up(r->d_in, 8), ldy = round_up(r->d_out, 8);
     DevBuf<float> xf(static_cast<size_t>(n * r->d_in));
     DevBuf<uint16_t> xb(static_cast<size_t>(n * ldx));
@@ -1652,7 +1745,7 @@ int atmm_run_bypass_host_bf16_pipelined(const atmm_plan* p, const int64_t* layer
     };
     // Three independent batches in flight: one H2D, one on the SMs, one D2H
     // (the copy engines run both directions at once).
-    static const size_t kSlots = std::getenv("ATMM_E2E_SLOTS") ? std::max(2, std::atoi(std::getenv("ATMM_E2E_SLOTS"))) : 4;
+    constexpr size_t kSlots = 4;
     thread_local std::vector<std::unique_ptr<Slot>> slots;
     thread_local int slots_dev = -1;
     if (slots_dev != r->device) slots.clear();
@@ -1749,8 +1842,12 @@ const char* mode_name(int m) {
 }
 // One-shot all-layer W +-= s.down.up for the state's weights.
 void state_merge_launch(atmm_model_state* st, int32_t adapter_id, float sign, cudaStream_t stream) {
-  const int rc = atmm_merge_apply_layers(st->reg, adapter_id, 0, st->reg->L, st->w, st->ldw, st->w_layer_stride,
-                                         st->w_dtype, sign, stream);
+  // fp32 weights of a precise registry take the fp32-faithful merge
+  const int rc = st->reg->precise && st->w_dtype == ATMM_F32
+                     ? atmm_merge_apply_f32(st->reg, adapter_id, 0, st->reg->L, static_cast<float*>(st->w), st->ldw,
+                                            st->w_layer_stride, sign, stream)
+                     : atmm_merge_apply_layers(st->reg, adapter_id, 0, st->reg->L, st->w, st->ldw, st->w_layer_stride,
+                                               st->w_dtype, sign, stream);
   if (rc != ATMM_OK) fail(rc, atmm_last_error());
   ++st->weight_writes;
 }
@@ -1870,6 +1967,13 @@ int atmm_delta_w_host(atmm_registry* r, int32_t adapter_id, int64_t layer, float
     }
     const Slot& s = r->at(adapter_id);
     DeviceGuard g(r->device);
+    if (r->precise) {
+      DevBuf<float> wd(static_cast<size_t>(r->d_in * r->d_out));
+      const int rc = atmm_delta_w_f32(r, adapter_id, layer, wd.p, r->d_out, nullptr);
+      if (rc != ATMM_OK) fail(rc, atmm_last_error());
+      CUDA_CHECK(cudaMemcpy(out, wd.p, wd.n * 4, cudaMemcpyDeviceToHost));
+      return;
+    }
     const int64_t ldw = round_up(r->d_out, 8);
     DevBuf<float> w(static_cast<size_t>(r->d_in * ldw));
     run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
@@ -1888,93 +1992,287 @@ int atmm_multiply_host(const float* a, int64_t m, int64_t k, const float* b, int
     if (m < 1 || k < 1 || n < 1) fail(ATMM_ERR_SHAPE, "atmm_multiply: matrix dimensions must be >= 1");
     if (!tc.structurally_valid()) fail(ATMM_ERR_CONFIG, "invalid tiling config " + tc.str());
     if (!a || !b || !c) fail(ATMM_ERR_SHAPE, "null operand");
-    require_device(0);
     int dev = 0;
     cudaGetDevice(&dev);
-    // K is consumed in chunks of 128 (the merge kernel keeps a whole K chunk
-    // of A on chip); chunks accumulate into the fp32 output.
-    const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 32), ldc = round_up(n, 8);
-    DevBuf<float> cd(static_cast<size_t>(m * ldc));
-    for (int64_t k0 = 0; k0 < k; k0 += 128) {
-      const int64_t kc = std::min<int64_t>(128, k - k0);
-      const int64_t kp = round_up(kc, 16);
-      std::vector<float> at(static_cast<size_t>(m * kc)), bt(static_cast<size_t>(kc * n));
-      for (int64_t i = 0; i < m; ++i) std::memcpy(&at[i * kc], a + i * k + k0, kc * 4);
-      std::memcpy(bt.data(), b + k0 * n, kc * n * 4);
-      std::vector<uint16_t> ha(static_cast<size_t>(m_pad * kp)), hb(static_cast<size_t>(n_pad * kp));
-      pack_down_t(at.data(), m, kc, kc, m_pad, kp, ha.data());
-      pack_up_t(bt.data(), kc, n, n, n_pad, kp, hb.data());
-      DevBuf<uint16_t> da(ha.size()), db(hb.size());
-      CUDA_CHECK(cudaMemcpy(da.p, ha.data(), ha.size() * 2, cudaMemcpyHostToDevice));
-      CUDA_CHECK(cudaMemcpy(db.p, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
-      run_merge(da.p, db.p, m, n, kp, cd.p, ldc, ATMM_F32, 1.0f, k0 == 0 ? 0.0f : 1.0f, nullptr);
-      CUDA_CHECK(cudaDeviceSynchronize());
-    }
-    CUDA_CHECK(cudaMemcpy2D(c, n * 4, cd.p, ldc * 4, n * 4, m, cudaMemcpyDeviceToHost));
-    flops_add(2ull * static_cast<uint64_t>(m * n * k));  // atmm.hpp:123
+    require_device(dev);
+    // The reference's fp32 GEMM (atmm.hpp:111-142) kept fp32-faithful on the
+    // tensor cores: one split-bf16 tcgen05 product (atmm_gemm_f32).  The
+    // config is validated like the reference's; the B200 tiles are the GEMM's.
+    DevBuf<float> ad(static_cast<size_t>(m * k)), bd(static_cast<size_t>(k * n)), cd(static_cast<size_t>(m * n));
+    CUDA_CHECK(cudaMemcpy(ad.p, a, ad.n * 4, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(bd.p, b, bd.n * 4, cudaMemcpyHostToDevice));
+    const int rc = atmm_gemm_f32(ad.p, k, bd.p, n, cd.p, n, m, k, n, 0.0f, nullptr);
+    if (rc != ATMM_OK) fail(rc, atmm_last_error());
+    CUDA_CHECK(cudaMemcpy(c, cd.p, cd.n * 4, cudaMemcpyDeviceToHost));
   });
 }
 
-int atmm_bench_launches(int device, int64_t m, int64_t d_in, int64_t rank, int64_t d_out,
-                        const int32_t* launches, int64_t num_launches, int trials,
-                        int64_t* median_ns) {
-  return guarded([&] {
-    if (trials < 3) fail(ATMM_ERR_CONFIG, "benchmark needs trials >= 3");
-    if (!launches || !median_ns || num_launches < 1) fail(ATMM_ERR_CONFIG, "null launches or output");
-    require_device(device);
-    DeviceGuard g(device);
-    atmm_registry reg;
-    reg.device = device;
-    reg.L = 1;
-    reg.d_in = d_in;
-    reg.d_out = d_out;
-    reg.d_in_pad = round_up(d_in, 128);
-    reg.d_out_pad = round_up(d_out, 128);
-    {
-      // Synthetic factors (values do not affect timing).
-      std::vector<float> dn(static_cast<size_t>(d_in * rank)), up(static_cast<size_t>(rank * d_out));
-      for (size_t i = 0; i < dn.size(); ++i) dn[i] = 0.001f * static_cast<float>((i * 7919) % 61) - 0.03f;
-      for (size_t i = 0; i < up.size(); ++i) up[i] = 0.001f * static_cast<float>((i * 104729) % 53) - 0.026f;
-      atmm_registry* rp = &reg;
-      const int st = atmm_registry_put(rp, 1, rank, dn.data(), up.data(), 1.0f);
+}  // extern "C"
+
+// =========================================================================
+// Offline tiling search on B200 (atmm.hpp:188-355): benchmark_config,
+// grid_bench_ns, tiling_search, default_shape_grid, re-read for the fused
+// bypass.  A tuning shape is a batch of `segments` segments of `m` rows, each
+// its own adapter of rank `rank`, rows shuffled; a candidate is a B200 launch
+// {tile_m, cluster, bn, stages, path} forced for every segment.
+// =========================================================================
+namespace atmm {
+namespace {
+
+struct TuneBench {
+  int device = 0;
+  atmm_tune_shape shape{};
+  std::unique_ptr<atmm_registry> reg;
+  std::vector<int32_t> assignment;
+  int64_t ldx = 0, ldy = 0;
+  static constexpr int kSets = 4;  // applies per trial, each on its own X / Y (cold after the L2 flush)
+  DevBuf<uint16_t> x[kSets], y[kSets];
+  DevBuf<uint8_t> flush;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+
+  TuneBench(int dev, const atmm_tune_shape& sh, uint64_t seed) : device(dev), shape(sh) {
+    if (sh.m < 1 || sh.d_in < 1 || sh.d_out < 1 || sh.rank < 1 || sh.segments < 1) {
+      fail(ATMM_ERR_SHAPE, "tuning shape dimensions must be >= 1");
+    }
+    reg.reset(new atmm_registry());
+    reg->device = dev;
+    reg->L = 1;
+    reg->d_in = sh.d_in;
+    reg->d_out = sh.d_out;
+    reg->d_in_pad = round_up(sh.d_in, 128);
+    reg->d_out_pad = round_up(sh.d_out, 128);
+    // Synthetic factors: values do not change the timing.
+    std::vector<float> dn(static_cast<size_t>(sh.d_in * sh.rank)), up(static_cast<size_t>(sh.rank * sh.d_out));
+    for (size_t i = 0; i < dn.size(); ++i) dn[i] = 0.001f * static_cast<float>((i * 7919) % 61) - 0.03f;
+    for (size_t i = 0; i < up.size(); ++i) up[i] = 0.001f * static_cast<float>((i * 104729) % 53) - 0.026f;
+    for (int64_t a = 0; a < sh.segments; ++a) {
+      const int st = atmm_registry_put(reg.get(), static_cast<int32_t>(a), sh.rank, dn.data(), up.data(), 1.0f);
       if (st != ATMM_OK) fail(st, atmm_last_error());
     }
-    std::vector<int32_t> assignment(static_cast<size_t>(m), 1);
-    const int64_t ldx = round_up(d_in, 8), ldy = round_up(d_out, 8);
-    DevBuf<uint16_t> x(static_cast<size_t>(m * ldx)), y(static_cast<size_t>(m * ldy));
-    CUDA_CHECK(cudaMemset(x.p, 0, x.n * 2));
-    CUDA_CHECK(cudaMemset(y.p, 0, y.n * 2));
-    DevBuf<uint8_t> flush(size_t(256) << 20);
-    cudaStream_t s;
+    const int64_t n = sh.m * sh.segments;
+    assignment.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) assignment[static_cast<size_t>(i)] = static_cast<int32_t>(i / sh.m);
+    uint64_t st = seed | 1;  // xorshift Fisher-Yates: the rows of a segment are scattered
+    for (int64_t i = n - 1; i > 0; --i) {
+      st ^= st << 13;
+      st ^= st >> 7;
+      st ^= st << 17;
+      std::swap(assignment[static_cast<size_t>(i)], assignment[static_cast<size_t>(st % static_cast<uint64_t>(i + 1))]);
+    }
+    ldx = round_up(sh.d_in, 8);
+    ldy = round_up(sh.d_out, 8);
+    for (int k = 0; k < kSets; ++k) {
+      x[k].alloc(static_cast<size_t>(n * ldx));
+      y[k].alloc(static_cast<size_t>(n * ldy));
+      CUDA_CHECK(cudaMemset(x[k].p, 0, x[k].n * 2));
+      CUDA_CHECK(cudaMemset(y[k].p, 0, y[k].n * 2));
+    }
+    flush.alloc(size_t(256) << 20);  // > 2x the 126 MB L2
     CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    cudaEvent_t e0, e1;
     CUDA_CHECK(cudaEventCreate(&e0));
     CUDA_CHECK(cudaEventCreate(&e1));
-    for (int64_t c = 0; c < num_launches; ++c) {
-      median_ns[c] = std::numeric_limits<int64_t>::max();
-      LaunchCfg lc{launches[4 * c], launches[4 * c + 1], launches[4 * c + 2], launches[4 * c + 3]};
-      try {
-        auto plan = build_plan(&reg, assignment.data(), m, nullptr, &lc);
-        std::vector<int64_t> samples;
-        for (int t = 0; t < trials + 1; ++t) {  // first iteration is the warm-up
-          CUDA_CHECK(cudaMemsetAsync(flush.p, t & 0xff, flush.n, s));
-          CUDA_CHECK(cudaEventRecord(e0, s));
-          apply_plan(plan.get(), 0, x.p, ldx, y.p, ldy, ATMM_BF16, 1.0f, s);
-          CUDA_CHECK(cudaEventRecord(e1, s));
-          CUDA_CHECK(cudaEventSynchronize(e1));
-          float ms = 0.f;
-          CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
-          if (t > 0) samples.push_back(static_cast<int64_t>(ms * 1e6));
+  }
+  ~TuneBench() {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+  }
+
+  // benchmark_config (atmm.hpp:188-216): median of `trials` after one
+  // warm-up; each trial flushes L2, then times kSets back-to-back applies
+  // (bf16 Y, each on its own buffers) with CUDA events on the launch stream
+  // and records the per-apply time.
+  int64_t median_ns(const LaunchCfg& lc, int trials) {
+    auto plan = build_plan(reg.get(), assignment.data(), static_cast<int64_t>(assignment.size()), nullptr, &lc);
+    std::vector<int64_t> samples;
+    for (int t = 0; t < trials + 1; ++t) {
+      CUDA_CHECK(cudaMemsetAsync(flush.p, t & 0xff, flush.n, s));
+      CUDA_CHECK(cudaEventRecord(e0, s));
+      for (int k = 0; k < kSets; ++k) apply_plan(plan.get(), 0, x[k].p, ldx, y[k].p, ldy, ATMM_BF16, 1.0f, s);
+      CUDA_CHECK(cudaEventRecord(e1, s));
+      CUDA_CHECK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+      if (t > 0) samples.push_back(static_cast<int64_t>(static_cast<double>(ms) * 1e6 / kSets));
+    }
+    std::sort(samples.begin(), samples.end());
+    return samples[samples.size() / 2];
+  }
+};
+
+std::string shape_str(const atmm_tune_shape& s) {
+  return std::to_string(s.segments) + "x" + std::to_string(s.m) + " rows, d " + std::to_string(s.d_in) + "->" +
+         std::to_string(s.d_out) + ", r " + std::to_string(s.rank);
+}
+std::string launch_str(const LaunchCfg& l) {
+  return "{" + std::to_string(l.tile_m) + "," + std::to_string(l.cluster) + "," + std::to_string(l.bn) + "," +
+         std::to_string(l.stages) + "," + std::to_string(l.path) + "}";
+}
+
+// grid_bench_ns (atmm.hpp:229-270): every round sweeps the whole grid before
+// any point is sampled again; a point's score is the median of its round
+// medians; points that fail score INT64_MAX (reported, never fatal).
+std::vector<std::vector<int64_t>> grid_bench(int device, const atmm_tune_shape* shapes, int64_t ns,
+                                             const std::vector<LaunchCfg>& cands, int trials, int rounds,
+                                             std::vector<std::string>& failures) {
+  std::vector<std::vector<std::vector<int64_t>>> samples(static_cast<size_t>(ns),
+                                                         std::vector<std::vector<int64_t>>(cands.size()));
+  std::vector<std::vector<char>> failed(static_cast<size_t>(ns), std::vector<char>(cands.size(), 0));
+  std::vector<std::unique_ptr<TuneBench>> benches(static_cast<size_t>(ns));
+  for (int round = 0; round < rounds; ++round) {
+    for (int64_t si = 0; si < ns; ++si) {
+      auto& b = benches[static_cast<size_t>(si)];
+      if (!b) b.reset(new TuneBench(device, shapes[si], 0x5eedbeefull + static_cast<uint64_t>(si)));
+      for (size_t ci = 0; ci < cands.size(); ++ci) {
+        if (failed[static_cast<size_t>(si)][ci]) continue;
+        try {
+          samples[static_cast<size_t>(si)][ci].push_back(b->median_ns(cands[ci], trials));
+        } catch (const Failure& e) {
+          cudaGetLastError();
+          failed[static_cast<size_t>(si)][ci] = 1;
+          failures.push_back("shape " + shape_str(shapes[si]) + " launch " + launch_str(cands[ci]) + ": " + e.what());
         }
-        std::sort(samples.begin(), samples.end());
-        median_ns[c] = samples[samples.size() / 2];
-      } catch (const Failure&) {
-        cudaGetLastError();
+      }
+      if (round + 1 == rounds) b.reset();  // bound device memory: one shape's buffers at a time at the end
+    }
+  }
+  std::vector<std::vector<int64_t>> scores(static_cast<size_t>(ns),
+                                           std::vector<int64_t>(cands.size(), std::numeric_limits<int64_t>::max()));
+  for (int64_t si = 0; si < ns; ++si) {
+    for (size_t ci = 0; ci < cands.size(); ++ci) {
+      auto& v = samples[static_cast<size_t>(si)][ci];
+      if (failed[static_cast<size_t>(si)][ci] || v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      scores[static_cast<size_t>(si)][ci] = v[v.size() / 2];
+    }
+  }
+  return scores;
+}
+
+std::vector<LaunchCfg> launches_from(const int32_t* v, int64_t count) {
+  std::vector<LaunchCfg> out;
+  for (int64_t i = 0; i < count; ++i) {
+    out.push_back(launch_from_ints(v + 5 * i));
+    validate_launch(out.back());
+  }
+  return out;
+}
+
+void write_failures(const std::vector<std::string>& f, char* buf, size_t cap) {
+  if (!buf || cap == 0) return;
+  std::string all;
+  for (const auto& s : f) all += s + "\n";
+  std::strncpy(buf, all.c_str(), cap - 1);
+  buf[cap - 1] = 0;
+}
+
+}  // namespace
+}  // namespace atmm
+
+extern "C" {
+
+int atmm_benchmark_launch(int device, const atmm_tune_shape* shape, const int32_t launch[5], int trials,
+                          uint64_t seed, int64_t* median_ns) {
+  return guarded([&] {
+    if (!shape || !launch || !median_ns) fail(ATMM_ERR_CONFIG, "null shape, launch or output");
+    if (trials < 3) fail(ATMM_ERR_CONFIG, "benchmark_config needs trials >= 3");
+    require_device(device);
+    DeviceGuard g(device);
+    const LaunchCfg lc = launch_from_ints(launch);
+    validate_launch(lc);
+    TuneBench b(device, *shape, seed);
+    *median_ns = b.median_ns(lc, trials);
+  });
+}
+
+int atmm_grid_bench_ns(int device, const atmm_tune_shape* shapes, int64_t num_shapes, const int32_t* launches,
+                       int64_t num_launches, int trials, int rounds, int64_t* scores, char* failures,
+                       size_t failures_cap) {
+  return guarded([&] {
+    if (!shapes || !launches || !scores || num_shapes < 1 || num_launches < 1) {
+      fail(ATMM_ERR_CONFIG, "grid_bench needs a nonempty grid and candidates");
+    }
+    if (trials < 3 || rounds < 1) fail(ATMM_ERR_CONFIG, "grid_bench needs trials >= 3 and rounds >= 1");
+    require_device(device);
+    DeviceGuard g(device);
+    std::vector<std::string> fails;
+    const auto cands = launches_from(launches, num_launches);
+    const auto sc = grid_bench(device, shapes, num_shapes, cands, trials, rounds, fails);
+    for (int64_t si = 0; si < num_shapes; ++si) {
+      for (int64_t ci = 0; ci < num_launches; ++ci) {
+        scores[si * num_launches + ci] = sc[static_cast<size_t>(si)][static_cast<size_t>(ci)];
       }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaStreamDestroy(s);
+    write_failures(fails, failures, failures_cap);
+  });
+}
+
+int atmm_tiling_search(int device, const atmm_tune_shape* shapes, int64_t num_shapes, const int32_t* launches,
+                       int64_t num_launches, int trials, atmm_table** out, char* failures, size_t failures_cap) {
+  return guarded([&] {
+    if (!out) fail(ATMM_ERR_CONFIG, "null output");
+    if (!shapes || !launches || num_shapes < 1 || num_launches < 1) {
+      fail(ATMM_ERR_CONFIG, "tiling_search needs a nonempty grid and candidates");
+    }
+    if (trials < 3) fail(ATMM_ERR_CONFIG, "tiling_search needs trials >= 3");
+    require_device(device);
+    DeviceGuard g(device);
+    std::vector<std::string> fails;
+    const auto cands = launches_from(launches, num_launches);
+    const auto scores = grid_bench(device, shapes, num_shapes, cands, trials, 3, fails);
+    std::vector<int64_t> flat;
+    for (const auto& row : scores) flat.insert(flat.end(), row.begin(), row.end());
+    std::string sel_fail(failures_cap > 0 ? failures_cap : 1, '\0');
+    const int st = atmm_table_from_scores(shapes, num_shapes, launches, num_launches, flat.data(), out,
+                                          sel_fail.data(), sel_fail.size());
+    if (st != ATMM_OK) fail(st, atmm_last_error());
+    if (sel_fail[0]) fails.push_back(sel_fail.c_str());
+    write_failures(fails, failures, failures_cap);
+  });
+}
+
+int atmm_default_shape_grid(int64_t d_in, int64_t d_out, const int64_t* ranks, int64_t num_ranks, atmm_tune_shape* out,
+                            int64_t cap, int64_t* count) {
+  return guarded([&] {
+    if (!count || (num_ranks > 0 && !ranks)) fail(ATMM_ERR_CONFIG, "null argument");
+    if (d_in < 1 || d_out < 1) fail(ATMM_ERR_SHAPE, "dimensions must be >= 1");
+    static const int64_t kDefaultRanks[] = {8, 16, 32, 64, 128};
+    const int64_t* rs = num_ranks > 0 ? ranks : kDefaultRanks;
+    const int64_t nr = num_ranks > 0 ? num_ranks : 5;
+    // atmm.hpp:341-355 re-read for the bypass: segment rows from single
+    // tokens (decode) to whole prompts, each batch ~1-2k tokens of
+    // concurrent segments (the serving batch sizes of BASELINE.json).
+    static const int64_t kRows[] = {8, 16, 32, 64, 96, 128, 256, 512};
+    std::vector<atmm_tune_shape> grid;
+    for (int64_t r = 0; r < nr; ++r) {
+      for (int64_t m : kRows) {
+        const int64_t segs = std::clamp<int64_t>(1024 / m, 4, 64);
+        { atmm_tune_shape t; t.m=m; t.d_in=d_in; t.rank=rs[r]; t.d_out=d_out; t.segments=segs; grid.push_back(t); }
+      }
+    }
+    *count = static_cast<int64_t>(grid.size());
+    if (out) std::copy(grid.begin(), grid.begin() + std::min<int64_t>(cap, *count), out);
+  });
+}
+
+int atmm_default_launch_candidates(int32_t* out, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    if (!count) fail(ATMM_ERR_CONFIG, "null count");
+    std::vector<LaunchCfg> c;
+    for (int32_t tm : {16, 32, 64, 128}) {
+      for (int32_t cl : {4, 8, 16}) {
+        c.push_back(LaunchCfg{tm, cl, tm <= 64 ? 128 : 256, 0, 0});
+      }
+    }
+    c.push_back(LaunchCfg{128, 8, 128, 0, 0});
+    c.push_back(LaunchCfg{32, 8, 128, 0, ATMM_PATH_SPLIT});
+    c.push_back(LaunchCfg{64, 8, 128, 0, ATMM_PATH_A2A});
+    c.push_back(LaunchCfg{128, 8, 128, 0, ATMM_PATH_A2A});
+    *count = static_cast<int64_t>(c.size());
+    if (out) {
+      for (int64_t i = 0; i < std::min<int64_t>(cap, *count); ++i) launch_to_ints(c[static_cast<size_t>(i)], out + 5 * i);
+    }
   });
 }
 
@@ -2066,25 +2364,31 @@ struct GemmTiling {
   bool bk2 = false;  // 128-deep K stages (1-SM, bn 128, no split-K / multicast, K % 64 == 0)
   size_t smem = 0;
 };
-int gemm_krot() { return std::getenv("ATMM_GEMM_NOROT") ? 0 : 1; }
-bool pair_bk2_enabled() {
-  static const bool on = !std::getenv("ATMM_PAIR_BK2") || std::atoi(std::getenv("ATMM_PAIR_BK2")) != 0;  // A/B
-  return on;
-}
-bool bk2_enabled() {
-  static const bool on = !std::getenv("ATMM_GEMM_BK2") || std::atoi(std::getenv("ATMM_GEMM_BK2")) != 0;
-  return on;
+// Tile options of the GEMM / layer forward (atmm_gemm_opts; all zero =
+// automatic): the explicit form of what the heuristics below choose, for the
+// tile sweeps and the path-coverage tests.
+atmm_gemm_opts opts_or_auto(const atmm_gemm_opts* o) {
+  atmm_gemm_opts a{};
+  a.pair = -1;
+  if (!o) return a;
+  if (o->pair < -1 || o->pair > 1 || (o->bn != 0 && o->bn != 128 && o->bn != 256) ||
+      (o->kz != 0 && o->kz != 1 && o->kz != 2 && o->kz != 4 && o->kz != 8) || o->ks < 0 || o->ks > 16 ||
+      (o->mc != 0 && o->mc != 1 && o->mc != 2 && o->mc != 4) || o->stages < 0 || o->stages == 1 || o->stages > 8) {
+    fail(ATMM_ERR_CONFIG, "invalid GEMM tile options");
+  }
+  return *o;
 }
 // Without a bypass: 2-SM pairs unless one wave of 1-SM 128 x 128 tiles with
 // 128-deep K stages covers the GEMM (measured m = 512, n = k = 4096: 19.1 us
 // vs 22.9 us for pairs; m = 1024 needs two waves and pairs win, 26 vs 34 us).
-bool pair_without_bypass(int64_t m, int64_t n, int64_t k, int sms) {
+bool pair_without_bypass(int64_t m, int64_t n, int64_t k, int sms, const atmm_gemm_opts& o) {
   const int64_t row_tiles = (m + kTileM - 1) / kTileM;
   if (row_tiles < 2) return false;
-  if (const char* e = std::getenv("ATMM_FWD_PAIR")) return std::atoi(e) != 0;
-  return !(bk2_enabled() && k % kBK == 0 && row_tiles * ((n + 127) / 128) <= sms);
+  if (o.pair >= 0) return o.pair != 0;
+  return !(k % kBK == 0 && row_tiles * ((n + 127) / 128) <= sms);
 }
-GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool allow_mc = false) {
+GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, const atmm_gemm_opts& o,
+                       bool allow_mc = false) {
   const int32_t nkb = static_cast<int32_t>((k + kBK - 1) / kBK);
   GemmTiling t;
   const int64_t row_tiles = (m + kTileM - 1) / kTileM;
@@ -2094,15 +2398,15 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool
   // would need more waves (measured: m = 1024, n = 4096 pair tiles 41 -> 26 us)
   const int64_t t128 = mtiles * ((n + 127) / 128), t256 = mtiles * ((n + 255) / 256);
   t.bn = t256 >= units || (t128 + units - 1) / units > (t256 + units - 1) / units ? 256 : 128;
-  if (const char* e = std::getenv("ATMM_FWD_BN")) t.bn = std::atoi(e) == 256 ? 256 : 128;
+  if (o.bn) t.bn = o.bn;
   t.ntn = static_cast<int32_t>((n + t.bn - 1) / t.bn);
   t.num_tiles = static_cast<int32_t>(mtiles) * t.ntn;
   const size_t gstage = 16384 + static_cast<size_t>(pair ? t.bn / 2 : t.bn) * 128;
   t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage));
-  if (const char* e = std::getenv("ATMM_GEMM_STAGES")) t.stages = std::clamp(std::atoi(e), 2, t.stages);  // A/B
+  if (o.stages) t.stages = std::clamp<int32_t>(o.stages, 2, t.stages);
   t.smem = 1024 + t.stages * gstage;
   if (pair) {
-    if (bk2_enabled() && k % kBK == 0 && pair_bk2_enabled()) {  // 128-deep K stages
+    if (k % kBK == 0) {  // 128-deep K stages
       t.bk2 = true;
       const size_t gstage2 = 2 * 16384 + static_cast<size_t>(t.bn / 2) * 256;
       t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage2));
@@ -2117,17 +2421,18 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool
     if (t.bn == 128) {
       while (t.kz < 8 && int64_t(t.num_tiles) * t.kz * 2 <= sms && nkb / (t.kz * 2) >= 8) t.kz *= 2;
     }
-    if (const char* e = std::getenv("ATMM_FWD_KZ")) {
-      const int v = std::atoi(e);
-      t.kz = (v == 2 || v == 4 || v == 8) && t.bn == 128 && nkb / v >= 1 ? v : 1;
+    if (o.kz) t.kz = (o.kz > 1 && t.bn == 128 && nkb / o.kz >= 1) ? o.kz : 1;
+    if (t.kz > 1) {
+      // the split-K epilogue stages the 128-row fp32 partial and the kz
+      // receive slots in the idle ring: 2 x 128 x (bn + 4) x 4 bytes
+      const size_t need = 2 * size_t(kTileM) * (t.bn + 4) * 4;
+      while (size_t(t.stages) * gstage < need) ++t.stages;
+      t.smem = 1024 + t.stages * gstage;
     }
     t.grid = t.kz > 1 ? t.num_tiles * t.kz : std::min(t.num_tiles, sms);
     // A multicast across mc adjacent N tiles (plain GEMM; replaces split-K)
     if (allow_mc) {
-      if (const char* e = std::getenv("ATMM_GEMM_MC")) {
-        const int v = std::atoi(e);
-        if ((v == 2 || v == 4) && t.ntn % v == 0) t.mc = v;
-      }
+      if ((o.mc == 2 || o.mc == 4) && t.ntn % o.mc == 0) t.mc = o.mc;
       if (t.mc > 1) {
         t.kz = 1;
         int clusters = fwd_gemm_max_clusters(t.smem, t.mc);
@@ -2137,8 +2442,8 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool
     }
     // 128-deep K stages: half the TMA instructions and barrier round trips
     // (measured m = 512, n = k = 4096: 25.2 -> 19.1 us; 256-wide tiles lose,
-    // two stages only).  ATMM_GEMM_BK2=0 disables (A/B).
-    if (bk2_enabled() && t.mc == 1 && t.bn == 128 && k % kBK == 0 && (k / kBK + 1) / 2 >= t.kz) {
+    // two stages only).
+    if (t.mc == 1 && t.bn == 128 && k % kBK == 0 && (k / kBK + 1) / 2 >= t.kz) {
       t.bk2 = true;
       const size_t gstage2 = 2 * 16384 + static_cast<size_t>(t.bn) * 256;
       t.stages = static_cast<int32_t>(std::min<size_t>(8, (kSmemLimit - 2048) / gstage2));
@@ -2151,8 +2456,14 @@ GemmTiling gemm_tiling(int64_t m, int64_t n, int64_t k, int sms, bool pair, bool
 }  // namespace atmm
 
 int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hidden_dim, atmm_forward** out) {
+  return atmm_forward_create_opts(plan, device, n, hidden_dim, nullptr, out);
+}
+
+int atmm_forward_create_opts(const atmm_plan* plan, int device, int64_t n, int64_t hidden_dim,
+                             const atmm_gemm_opts* opts, atmm_forward** out) {
   return guarded([&] {
     if (!out) fail(ATMM_ERR_CONFIG, "null output");
+    const atmm_gemm_opts o = opts_or_auto(opts);
     auto f = std::make_unique<atmm_forward>();
     if (plan) {
       atmm_registry* reg = plan->reg;
@@ -2188,9 +2499,9 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
     // (measured: cfg5-sized batches win, cfg2/cfg3-sized ones lose).
     const bool bypass_plan = plan && !plan->bp.seg_adapter.empty();
     const int64_t pair_tiles = int64_t((f->row_tiles + 1) / 2) * ((d + 255) / 256);
-    f->pair = bypass_plan ? f->row_tiles >= 2 && pair_tiles >= 2 * sms : pair_without_bypass(n_, d, d, sms);
-    if (const char* e = std::getenv("ATMM_FWD_PAIR")) f->pair = f->row_tiles >= 2 && std::atoi(e) != 0;
-    const GemmTiling gt = gemm_tiling(n_, d, d, sms, f->pair);
+    f->pair = bypass_plan ? f->row_tiles >= 2 && pair_tiles >= 2 * sms : pair_without_bypass(n_, d, d, sms, o);
+    if (o.pair >= 0) f->pair = f->row_tiles >= 2 && o.pair != 0;
+    const GemmTiling gt = gemm_tiling(n_, d, d, sms, f->pair, o);
     f->bk2 = gt.bk2;
     f->bn = gt.bn;
     f->ntn = gt.ntn;
@@ -2278,7 +2589,7 @@ int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hi
       const int64_t slack = (units * per - f->num_tiles) * (f->pair ? 2 : 1);
       const int64_t cap = room >= f->num_items ? room : slack;
       while (f->ks < 16 && int64_t(f->num_items) * f->ks * 2 <= cap && f->ks * 2 <= f->nkb) f->ks *= 2;
-      if (const char* e = std::getenv("ATMM_FWD_KS")) f->ks = std::clamp(std::atoi(e), 1, 16);
+      if (o.ks) f->ks = o.ks;
       while (f->ks > 1 && f->ks > f->nkb) f->ks /= 2;  // every K slice gets >= 1 K block
       int32_t max_cols = 16;
       for (const FwdItem& it : items) max_cols = std::max(max_cols, it.ncols);
@@ -2451,13 +2762,10 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
         CUDA_CHECK(launch_fwd_shrink(xm, p, f->smem_s, st));
       }
       p.stages = f->stages_g;
-      static const int only = std::getenv("ATMM_FWD_ONLY") ? std::atoi(std::getenv("ATMM_FWD_ONLY")) : 0;  // A/B: 1 = shrink only
-      if (only != 1) {
-        if (f->pair) {
-          CUDA_CHECK(launch_fwd_gemm_pair(xg, wmap, f->amap, p, f->grid, f->smem_g, st));
-        } else {
-          CUDA_CHECK(launch_fwd_gemm(xg, wmap, p, f->grid, f->smem_g, st));
-        }
+      if (f->pair) {
+        CUDA_CHECK(launch_fwd_gemm_pair(xg, wmap, f->amap, p, f->grid, f->smem_g, st));
+      } else {
+        CUDA_CHECK(launch_fwd_gemm(xg, wmap, p, f->grid, f->smem_g, st));
       }
       cur = nxt;
       xm = f->bmap[nxt];
@@ -2473,7 +2781,17 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
 // GEMM kernels without the bypass extension and with an identity epilogue.
 int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int c_dtype, int64_t m,
               int64_t k, int64_t n, void* stream) {
-  return guarded([&] {
+  return atmm_gemm_ex(a, lda, b, ldb, c, ldc, c_dtype, m, k, n, nullptr, stream);
+}
+
+namespace atmm {
+// The plain GEMM launch behind atmm_gemm_ex (no FLOP accounting: the
+// fp32-faithful path calls it on split operands and counts the algorithmic
+// product itself).
+void gemm_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int c_dtype, int64_t m,
+                 int64_t k, int64_t n, const atmm_gemm_opts* opts, void* stream) {
+  {
+    const atmm_gemm_opts o = opts_or_auto(opts);
     if (m < 0 || k < 0 || n < 0) fail(ATMM_ERR_SHAPE, "negative GEMM shape");
     if (c_dtype != ATMM_BF16 && c_dtype != ATMM_F32) fail(ATMM_ERR_CONFIG, "c_dtype must be ATMM_BF16 or ATMM_F32");
     if (n % 8 != 0) fail(ATMM_ERR_SHAPE, "n must be a multiple of 8 (16-byte output rows)");
@@ -2500,8 +2818,8 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int32_t nkb = static_cast<int32_t>((k + kBK - 1) / kBK);
-    const bool pair = pair_without_bypass(m, n, k, sms);
-    const GemmTiling gt = gemm_tiling(m, n, k, sms, pair, true);
+    const bool pair = pair_without_bypass(m, n, k, sms, o);
+    const GemmTiling gt = gemm_tiling(m, n, k, sms, pair, o, true);
     const bool bk2 = gt.bk2;
     const CUtensorMap amap = bk2 ? make_act_map_atoms(a, m, k, lda) : make_act_map(a, m, k, lda, kTileM / gt.mc);
     const CUtensorMap bmap = make_layer_w_map(b, k, n, ldb, 1, 0, bk2 ? 2 * kBK : kBK);
@@ -2519,7 +2837,7 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     p.pair = pair ? 1 : 0;
     p.kz = gt.kz;
     p.act_none = 1;
-    p.krot = pair ? gemm_krot() : 0;  // measured: helps pairs (m = 256: 32 -> 23 us), costs 1-SM 256-wide tiles
+    p.krot = pair ? 1 : 0;  // measured: helps pairs (m = 256: 32 -> 23 us), costs 1-SM 256-wide tiles
     p.mc = gt.mc;
     p.bk2 = bk2 ? 1 : 0;
     p.out_f32 = c_dtype == ATMM_F32 ? 1 : 0;
@@ -2529,6 +2847,287 @@ int atmm_gemm(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, i
     } else {
       CUDA_CHECK(launch_fwd_gemm(amap, bmap, p, gt.grid, gt.smem, st));
     }
+  }
+}
+}  // namespace atmm
+
+int atmm_gemm_ex(const void* a, int64_t lda, const void* b, int64_t ldb, void* c, int64_t ldc, int c_dtype, int64_t m,
+                 int64_t k, int64_t n, const atmm_gemm_opts* opts, void* stream) {
+  return guarded([&] {
+    gemm_launch(a, lda, b, ldb, c, ldc, c_dtype, m, k, n, opts, stream);
     flops_add(2ull * static_cast<uint64_t>(m * n * k));  // atmm.hpp:123
+  });
+}
+
+// =========================================================================
+// fp32-faithful path (the reference's fp32 contract on bf16 tensor cores):
+// every product is ONE tcgen05 GEMM over the K-concatenation of the
+// operands' three-part bf16 splits (six partial products, fp32
+// accumulation; precise_kernels.cu).  Used by the reference-signature C++ shim
+// (include/loraserve_compat.hpp), whose callers expect 1e-4 agreement with
+// their fp32 CPU results (acceptance.cpp:62-101, 107-211).
+// =========================================================================
+namespace atmm {
+namespace {
+
+// Stream-ordered scratch: allocated on `s`, released on `s` after use.
+struct AsyncScratch {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  AsyncScratch(size_t bytes, cudaStream_t st) : s(st) {
+    if (bytes) CUDA_CHECK(cudaMallocAsync(&p, bytes, st));
+  }
+  ~AsyncScratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  AsyncScratch(const AsyncScratch&) = delete;
+  AsyncScratch& operator=(const AsyncScratch&) = delete;
+};
+
+// T (m x np fp32, row stride np) = A' (m x 6kp bf16) . B' (6kp x np bf16).
+void gemm_split(const uint16_t* a3, const uint16_t* b3, float* t, int64_t m, int64_t kp, int64_t np, cudaStream_t st) {
+  gemm_launch(a3, kSplitParts * kp, b3, np, t, np, ATMM_F32, m, kSplitParts * kp, np, nullptr, st);
+}
+
+void require_precise(const atmm_registry* r) {
+  if (!r->precise) {
+    fail(ATMM_ERR_CONFIG, "the fp32-faithful path needs a precise registry (atmm_registry_set_precise)");
+  }
+}
+
+// y[row] += scale * s_a * (x[row] . down_a) . up_a for every routed row of the
+// plan, fp32-faithful, per segment: gather + split the rows, x . down, split
+// mid, mid . up, scatter-add.
+void bypass_f32(const atmm_plan* p, int64_t layer, const float* x, int64_t ldx, float* y, int64_t ldy, float scale,
+                cudaStream_t st) {
+  const atmm_registry* reg = p->reg;
+  require_precise(reg);
+  if (p->generation != reg->generation) fail(ATMM_ERR_CONFIG, "plan is stale: the registry changed after the plan was built");
+  if (layer < 0 || layer >= reg->L) fail(ATMM_ERR_CONFIG, "layer index " + std::to_string(layer) + " out of range");
+  if (!x || !y) fail(ATMM_ERR_SHAPE, "null X or Y");
+  if (ldx < reg->d_in || ldy < reg->d_out) fail(ATMM_ERR_SHAPE, "row strides must be >= d_in / d_out");
+  const size_t S = p->bp.seg_adapter.size();
+  int64_t ns_max = 0, r8_max = 8;
+  for (size_t s = 0; s < S; ++s) {
+    ns_max = std::max(ns_max, p->bp.seg_offsets[s + 1] - p->bp.seg_offsets[s]);
+    r8_max = std::max(r8_max, round_up(reg->at(p->bp.seg_adapter[s]).rank, 8));
+  }
+  const int64_t kpd = round_up(reg->d_in, 8), n8 = round_up(reg->d_out, 8);
+  AsyncScratch xa(size_t(ns_max) * kSplitParts * kpd * 2, st), t1(size_t(ns_max) * r8_max * 4, st),
+      ma(size_t(ns_max) * kSplitParts * r8_max * 2, st), t2(size_t(ns_max) * n8 * 4, st);
+  for (size_t s = 0; s < S; ++s) {
+    const Slot& sl = reg->at(p->bp.seg_adapter[s]);
+    const PreciseDims pd(reg, sl.rank);
+    const int64_t off = p->bp.seg_offsets[s], ns = p->bp.seg_offsets[s + 1] - off;
+    const int32_t* rows = p->d_rows.p + off;
+    CUDA_CHECK(launch_split3_rows(x, ldx, rows, ns, reg->d_in, kpd, xa.as<uint16_t>(), kSplitParts * kpd, st));
+    gemm_split(xa.as<uint16_t>(), sl.p_down_b + layer * pd.db, t1.as<float>(), ns, kpd, pd.r8, st);
+    CUDA_CHECK(launch_split3_rows(t1.as<float>(), pd.r8, nullptr, ns, sl.rank, pd.r8, ma.as<uint16_t>(),
+                                  kSplitParts * pd.r8, st));
+    gemm_split(ma.as<uint16_t>(), sl.p_up_b + layer * pd.ub, t2.as<float>(), ns, pd.r8, n8, st);
+    CUDA_CHECK(launch_rows_out(t2.as<float>(), n8, rows, ns, reg->d_out, y, ldy, scale * sl.scale, 1.0f, st));
+  }
+}
+
+}  // namespace
+}  // namespace atmm
+
+int atmm_registry_set_precise(atmm_registry* r, int on) {
+  return guarded([&] {
+    if (!r) fail(ATMM_ERR_CONFIG, "null registry");
+    if (!r->slot_of.empty() && (on != 0) != r->precise) {
+      fail(ATMM_ERR_CONFIG, "set the precision of a registry before putting adapters");
+    }
+    r->precise = on != 0;
+  });
+}
+
+int atmm_gemm_f32(const float* a, int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m,
+                  int64_t k, int64_t n, float beta, void* stream) {
+  return guarded([&] {
+    if (m < 0 || k < 0 || n < 0) fail(ATMM_ERR_SHAPE, "negative GEMM shape");
+    if (m == 0 || n == 0) return;
+    if (!c || (k > 0 && (!a || !b))) fail(ATMM_ERR_CONFIG, "null A, B or C");
+    if ((k > 0 && (lda < k || ldb < n)) || ldc < n) fail(ATMM_ERR_SHAPE, "row strides must cover the matrices");
+    if (beta != 0.0f && beta != 1.0f) fail(ATMM_ERR_CONFIG, "beta must be 0 or 1");
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    require_device(dev);
+    const auto st = static_cast<cudaStream_t>(stream);
+    const int64_t kp = round_up(k, 8), np = round_up(n, 8);
+    AsyncScratch a3(size_t(m) * kSplitParts * kp * 2, st), b3(size_t(kSplitParts) * kp * np * 2, st),
+        t(size_t(m) * np * 4, st);
+    CUDA_CHECK(launch_split3_rows(a, lda, nullptr, m, k, kp, a3.as<uint16_t>(), kSplitParts * kp, st));
+    CUDA_CHECK(launch_split3_cols(b, ldb, k, n, kp, np, b3.as<uint16_t>(), st));
+    gemm_split(a3.as<uint16_t>(), b3.as<uint16_t>(), t.as<float>(), m, kp, np, st);
+    CUDA_CHECK(launch_rows_out(t.as<float>(), np, nullptr, m, n, c, ldc, 1.0f, beta, st));
+    flops_add(2ull * static_cast<uint64_t>(m * n * k));
+  });
+}
+
+int atmm_bypass_apply_f32(const atmm_plan* p, int64_t layer, const float* x, int64_t ldx, float* y, int64_t ldy,
+                          float scale, void* stream) {
+  return guarded([&] {
+    if (!p) fail(ATMM_ERR_CONFIG, "null plan");
+    DeviceGuard g(p->reg->device);
+    bypass_f32(p, layer, x, ldx, y, ldy, scale, static_cast<cudaStream_t>(stream));
+    flops_add(p->flops);
+  });
+}
+
+int atmm_merge_apply_f32(atmm_registry* r, int32_t adapter_id, int64_t layer0, int64_t num_layers, float* w, int64_t ldw,
+                         int64_t w_layer_stride, float sign, void* stream) {
+  return guarded([&] {
+    if (!r || !w) fail(ATMM_ERR_CONFIG, "null registry or W");
+    require_precise(r);
+    if (num_layers < 1 || layer0 < 0 || layer0 + num_layers > r->L) fail(ATMM_ERR_CONFIG, "layer range out of range");
+    if (ldw < r->d_out || (num_layers > 1 && w_layer_stride < ldw * r->d_in)) fail(ATMM_ERR_SHAPE, "W strides too small");
+    const Slot& s = r->at(adapter_id);
+    DeviceGuard g(r->device);
+    const auto st = static_cast<cudaStream_t>(stream);
+    const PreciseDims pd(r, s.rank);
+    AsyncScratch t(size_t(r->d_in) * pd.n8 * 4, st);
+    for (int64_t l = layer0; l < layer0 + num_layers; ++l) {
+      // delta_w_into (model.hpp:120-125) into scratch, then add / sub_inplace (model.hpp:157-158, 180-181)
+      gemm_split(s.p_down_a + l * pd.da, s.p_up_b + l * pd.ub, t.as<float>(), r->d_in, pd.r8, pd.n8, st);
+      CUDA_CHECK(launch_rows_out(t.as<float>(), pd.n8, nullptr, r->d_in, r->d_out, w + (l - layer0) * w_layer_stride,
+                                 ldw, sign * s.scale, 1.0f, st));
+    }
+    flops_add(2ull * static_cast<uint64_t>(num_layers * r->d_in * r->d_out * s.alg_rank));
+  });
+}
+
+int atmm_delta_w_f32(atmm_registry* r, int32_t adapter_id, int64_t layer, float* out, int64_t ldo, void* stream) {
+  return guarded([&] {
+    if (!r || !out) fail(ATMM_ERR_CONFIG, "null registry or output");
+    require_precise(r);
+    if (layer < 0 || layer >= r->L) {
+      fail(ATMM_ERR_CONFIG, "layer index " + std::to_string(layer) + " out of range (L=" + std::to_string(r->L) + ")");
+    }
+    if (ldo < r->d_out) fail(ATMM_ERR_SHAPE, "output row stride must be >= d_out");
+    const Slot& s = r->at(adapter_id);
+    DeviceGuard g(r->device);
+    const auto st = static_cast<cudaStream_t>(stream);
+    const PreciseDims pd(r, s.rank);
+    AsyncScratch t(size_t(r->d_in) * pd.n8 * 4, st);
+    gemm_split(s.p_down_a + layer * pd.da, s.p_up_b + layer * pd.ub, t.as<float>(), r->d_in, pd.r8, pd.n8, st);
+    CUDA_CHECK(launch_rows_out(t.as<float>(), pd.n8, nullptr, r->d_in, r->d_out, out, ldo, s.scale, 0.0f, st));
+    flops_add(2ull * static_cast<uint64_t>(r->d_in * r->d_out * s.alg_rank));
+  });
+}
+
+int atmm_forward_f32(const float* w, int64_t ldw, int64_t w_layer_stride, int64_t num_layers, int64_t n, int64_t d,
+                     const float* x, int64_t ldx, float* out, int64_t ldo, const atmm_plan* const* plans,
+                     const float* scales, int64_t num_plans, void* stream) {
+  return guarded([&] {
+    if (!w || !x || !out || (num_plans > 0 && (!plans || !scales))) fail(ATMM_ERR_CONFIG, "null argument");
+    if (n < 1 || d < 1 || num_layers < 0) fail(ATMM_ERR_SHAPE, "rows and hidden_dim must be >= 1");
+    if (ldw < d || ldx < d || ldo < d || (num_layers > 1 && w_layer_stride < ldw * d)) {
+      fail(ATMM_ERR_SHAPE, "row / layer strides must cover the matrices");
+    }
+    uint64_t bypass_flops = 0;
+    for (int64_t i = 0; i < num_plans; ++i) {
+      const atmm_plan* p = plans[i];
+      if (!p) fail(ATMM_ERR_CONFIG, "null plan");
+      require_precise(p->reg);
+      if (p->reg->d_in != d || p->reg->d_out != d || p->n != n) fail(ATMM_ERR_SHAPE, "plan does not match the forward");
+      if (p->reg->L < num_layers) fail(ATMM_ERR_SHAPE, "more layers than the adapters carry");
+      bypass_flops += p->flops;
+    }
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    require_device(dev);
+    const auto st = static_cast<cudaStream_t>(stream);
+    const int64_t kp = round_up(d, 8), d8 = round_up(d, 8);
+    AsyncScratch cur(size_t(n) * d8 * 4, st), nxt(size_t(n) * d8 * 4, st), w3(size_t(kSplitParts) * kp * d8 * 2, st),
+        a3(size_t(n) * kSplitParts * kp * 2, st);
+    float* c = cur.as<float>();
+    float* nx = nxt.as<float>();
+    CUDA_CHECK(launch_rows_out(x, ldx, nullptr, n, d, c, d8, 1.0f, 0.0f, st));
+    for (int64_t l = 0; l < num_layers; ++l) {
+      // next = cur . W_l (model.hpp:238) + bypass_l(cur) (model.hpp:239-241, 315-322), tanh
+      CUDA_CHECK(launch_split3_cols(w + l * w_layer_stride, ldw, d, d, kp, d8, w3.as<uint16_t>(), st));
+      CUDA_CHECK(launch_split3_rows(c, d8, nullptr, n, d, kp, a3.as<uint16_t>(), kSplitParts * kp, st));
+      gemm_split(a3.as<uint16_t>(), w3.as<uint16_t>(), nx, n, kp, d8, st);
+      for (int64_t i = 0; i < num_plans; ++i) bypass_f32(plans[i], l, c, d8, nx, d8, scales[i], st);
+      CUDA_CHECK(launch_tanh(nx, d8, n, d, st));
+      std::swap(c, nx);
+    }
+    CUDA_CHECK(launch_rows_out(c, d8, nullptr, n, d, out, ldo, 1.0f, 0.0f, st));
+    flops_add(static_cast<uint64_t>(num_layers) * (2ull * static_cast<uint64_t>(n * d * d) + bypass_flops));
+  });
+}
+
+// ---- host-buffer forms of the fp32-faithful path (the C++ shim's calls) ----
+// Device staging is a per-thread, per-device grow-only workspace (no
+// allocation per call once warm); copies and kernels run on one private
+// stream per thread, synchronized before returning.
+namespace atmm {
+namespace {
+struct HostStage {
+  int device = -1;
+  DevBuf<uint8_t> buf;
+  cudaStream_t s = nullptr;
+  uint8_t* get(int dev, size_t bytes) {
+    if (device != dev) {
+      buf.release();
+      if (s) cudaStreamDestroy(s);
+      s = nullptr;
+      device = dev;
+    }
+    if (!s) CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    if (buf.n < bytes) buf.alloc(std::max(bytes, buf.n * 2));
+    return buf.p;
+  }
+};
+HostStage& host_stage() {
+  thread_local HostStage hs;
+  return hs;
+}
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+}  // namespace
+}  // namespace atmm
+
+int atmm_forward_f32_host(const float* w, int64_t num_layers, int64_t n, int64_t d, const float* x, float* out,
+                          const atmm_plan* const* plans, const float* scales, int64_t num_plans) {
+  return guarded([&] {
+    if (!w || !x || !out) fail(ATMM_ERR_CONFIG, "null argument");
+    if (n < 1 || d < 1 || num_layers < 0) fail(ATMM_ERR_SHAPE, "rows and hidden_dim must be >= 1");
+    int dev = 0;
+    if (num_plans > 0 && plans && plans[0]) dev = plans[0]->reg->device;
+    else CUDA_CHECK(cudaGetDevice(&dev));
+    require_device(dev);
+    DeviceGuard g(dev);
+    const size_t wb = align256(size_t(num_layers) * d * d * 4), xb = align256(size_t(n) * d * 4);
+    HostStage& hs = host_stage();
+    uint8_t* base = hs.get(dev, wb + 2 * xb);
+    float* wd = reinterpret_cast<float*>(base);
+    float* xd = reinterpret_cast<float*>(base + wb);
+    float* od = reinterpret_cast<float*>(base + wb + xb);
+    if (num_layers) CUDA_CHECK(cudaMemcpyAsync(wd, w, size_t(num_layers) * d * d * 4, cudaMemcpyHostToDevice, hs.s));
+    CUDA_CHECK(cudaMemcpyAsync(xd, x, size_t(n) * d * 4, cudaMemcpyHostToDevice, hs.s));
+    const int rc = atmm_forward_f32(wd, d, d * d, num_layers, n, d, xd, d, od, d, plans, scales, num_plans, hs.s);
+    if (rc != ATMM_OK) fail(rc, atmm_last_error());
+    CUDA_CHECK(cudaMemcpyAsync(out, od, size_t(n) * d * 4, cudaMemcpyDeviceToHost, hs.s));
+    CUDA_CHECK(cudaStreamSynchronize(hs.s));
+  });
+}
+
+int atmm_merge_f32_host(atmm_registry* r, int32_t adapter_id, float* w, float sign) {
+  return guarded([&] {
+    if (!r || !w) fail(ATMM_ERR_CONFIG, "null registry or W");
+    DeviceGuard g(r->device);
+    const size_t wb = size_t(r->L) * r->d_in * r->d_out * 4;
+    HostStage& hs = host_stage();
+    float* wd = reinterpret_cast<float*>(hs.get(r->device, wb));
+    CUDA_CHECK(cudaMemcpyAsync(wd, w, wb, cudaMemcpyHostToDevice, hs.s));
+    const int rc = atmm_merge_apply_f32(r, adapter_id, 0, r->L, wd, r->d_out, r->d_in * r->d_out, sign, hs.s);
+    if (rc != ATMM_OK) fail(rc, atmm_last_error());
+    CUDA_CHECK(cudaMemcpyAsync(w, wd, wb, cudaMemcpyDeviceToHost, hs.s));  // in place: the caller's W stays put
+    CUDA_CHECK(cudaStreamSynchronize(hs.s));
   });
 }

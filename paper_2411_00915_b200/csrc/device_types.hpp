@@ -13,6 +13,7 @@ constexpr int kBK = 64;       // K block per pipeline stage: one 128-byte swizzl
 constexpr int kNUnit = 64;    // expand N granule (one 128-byte Y row slice of bf16)
 constexpr int kMaxRank = 128; // fused kernel limit on the LoRA rank
 constexpr int kMaxCluster = 16;
+constexpr int kSplitParts = 6;  // fp32-faithful path: K slices of the split operand images (precise_kernels.cu)
 constexpr int kBypassThreads = 256;  // w0,w7 X/down TMA, w1 MMA + TMEM, w2-5 epilogue, w6 up/Y TMA
 constexpr int kMergeThreads = 192;
 

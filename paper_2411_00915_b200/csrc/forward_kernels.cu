@@ -705,10 +705,9 @@ template <typename K>
 cudaError_t set_smem(K kernel, size_t smem) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 }
-bool fwd_pdl() {
-  static const bool on = std::getenv("ATMM_NO_PDL") == nullptr;
-  return on;
-}
+// Programmatic dependent launch is always on: every kernel waits
+// (griddepcontrol.wait) before touching its predecessor's outputs.
+constexpr bool fwd_pdl() { return true; }
 }  // namespace
 
 cudaError_t launch_fwd_gather(const uint16_t* x, int64_t ldx, uint16_t* dst, int64_t ldd, const int32_t* order,
@@ -1017,7 +1016,7 @@ cudaError_t launch_fwd_gemm_pair(const CUtensorMap& xmap, const CUtensorMap& wma
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cfg.attrs = attr;
-  cfg.numAttrs = std::getenv("ATMM_NO_PDL") ? 1 : 2;
+  cfg.numAttrs = fwd_pdl() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, fwd_gemm_pair_kernel, xmap, wmap, amap, p);
 }
 

@@ -72,21 +72,27 @@ void TilingTable::insert(ShapeKey key, const TilingConfig& cfg, int64_t ns,
   e.config = cfg;
   e.measured_ns = ns;
   if (sm100) {
-    if (sm100->tile_m < 1 || sm100->tile_m > 128 || sm100->cluster < 1 ||
-        sm100->cluster > 16 || sm100->bn < 64 || sm100->bn > 256 || sm100->bn % 64 != 0 ||
-        sm100->stages < 0 || sm100->stages > 8) {
-      fail(ATMM_ERR_CONFIG, "invalid sm100 launch parameters");
-    }
+    validate_launch(*sm100);
     e.has_sm100 = true;
     e.sm100 = *sm100;
   }
   entries_[key] = e;
 }
 
-void TilingTable::set_default(const TilingConfig& cfg) {
+void validate_launch(const LaunchCfg& l) {
+  if (l.tile_m < 1 || l.tile_m > 128 || l.cluster < 1 || l.cluster > 16 || l.bn < 64 || l.bn > 256 ||
+      l.bn % 64 != 0 || l.stages < 0 || l.stages > 8 || l.path < 0 || l.path > 3) {
+    fail(ATMM_ERR_CONFIG, "invalid sm100 launch parameters");
+  }
+}
+
+void TilingTable::set_default(const TilingConfig& cfg, const LaunchCfg* sm100) {
   validate_config(cfg);
+  if (sm100) validate_launch(*sm100);
   default_ = cfg;
   heuristic_default_ = false;
+  has_default_sm100_ = sm100 != nullptr;
+  if (sm100) default_sm100_ = *sm100;
 }
 
 const TableEntry* TilingTable::find(int64_t m, int64_t k, int64_t n) const {
@@ -136,8 +142,6 @@ LaunchCfg heuristic_launch(int64_t m, int64_t d_in, int64_t rank, int64_t d_out)
   LaunchCfg l;
   l.tile_m = 128;
   l.cluster = static_cast<int32_t>(std::clamp<int64_t>((d_in + 511) / 512, 1, 16));
-  if (const char* e = std::getenv("ATMM_CLUSTER")) l.cluster = std::clamp(std::atoi(e), 1, 16);  // A/B runs
-  if (const char* e = std::getenv("ATMM_TILE_M")) l.tile_m = std::clamp(std::atoi(e), 1, 128);   // A/B runs
   // Small segments are latency bound: 128-column chunks keep TMEM at 256
   // columns so two CTAs fit per SM (see resolve_group).
   l.bn = (m <= 64 || rank > 32) ? 128 : 256;
@@ -152,6 +156,7 @@ LaunchCfg TilingTable::resolve_launch(int64_t m, int64_t d_in, int64_t rank, int
     return e->has_sm100 ? e->sm100 : launch_from_config(e->config, d_in);
   }
   if (heuristic_default_) return heuristic_launch(m, d_in, rank, d_out);
+  if (has_default_sm100_) return default_sm100_;
   return launch_from_config(default_, d_in);
 }
 
@@ -356,19 +361,36 @@ static std::string cfg_json(const TilingConfig& c) {
   return s;
 }
 
+static std::string launch_json(const LaunchCfg& l) {
+  std::ostringstream o;
+  o << "{\"bn\": " << l.bn << ", \"cluster\": " << l.cluster;
+  if (l.path != 0) o << ", \"path\": " << l.path;
+  o << ", \"stages\": " << l.stages << ", \"tile_m\": " << l.tile_m << "}";
+  return o.str();
+}
+
+static LaunchCfg launch_from_json(const json::Object& so) {
+  LaunchCfg l;
+  l.tile_m = static_cast<int32_t>(json::as_int(json::at(so, "tile_m"), "tile_m"));
+  l.cluster = static_cast<int32_t>(json::as_int(json::at(so, "cluster"), "cluster"));
+  l.bn = static_cast<int32_t>(json::as_int(json::at(so, "bn"), "bn"));
+  l.stages = static_cast<int32_t>(json::as_int(json::at(so, "stages"), "stages"));
+  if (auto it = so.find("path"); it != so.end()) l.path = static_cast<int32_t>(json::as_int(it->second, "path"));
+  return l;
+}
+
 std::string TilingTable::to_json() const {
   std::ostringstream o;
-  o << "{\n  \"default\": " << cfg_json(default_) << ",\n  \"entries\": [";
+  o << "{\n  \"default\": " << cfg_json(default_) << ",\n";
+  if (has_default_sm100_) o << "  \"default_sm100\": " << launch_json(default_sm100_) << ",\n";
+  o << "  \"entries\": [";
   bool first = true;
   for (const auto& [k, e] : entries_) {
     o << (first ? "\n" : ",\n");
     first = false;
     o << "    {\"config\": " << cfg_json(e.config) << ", \"k\": " << k.k << ", \"m_bucket\": "
       << k.m_bucket << ", \"n\": " << k.n << ", \"ns\": " << e.measured_ns;
-    if (e.has_sm100) {
-      o << ", \"sm100\": {\"bn\": " << e.sm100.bn << ", \"cluster\": " << e.sm100.cluster
-        << ", \"stages\": " << e.sm100.stages << ", \"tile_m\": " << e.sm100.tile_m << "}";
-    }
+    if (e.has_sm100) o << ", \"sm100\": " << launch_json(e.sm100);
     o << "}";
   }
   o << (first ? "]\n}\n" : "\n  ]\n}\n");
@@ -379,6 +401,10 @@ TilingTable TilingTable::from_json(const std::string& text) {
   const json::Value root = json::Parser(text).parse();
   if (!root.is_obj()) fail(ATMM_ERR_IO, "tiling table json: root must be an object");
   TilingTable t(cfg_from_json(json::at(root.obj(), "default")));
+  if (auto it = root.obj().find("default_sm100"); it != root.obj().end() && it->second.is_obj()) {
+    const LaunchCfg dl = launch_from_json(it->second.obj());
+    t.set_default(t.default_config(), &dl);
+  }
   const json::Value& ents = json::at(root.obj(), "entries");
   if (!ents.is_arr()) fail(ATMM_ERR_IO, "tiling table json: entries must be an array");
   for (const json::Value& ev : ents.arr()) {
@@ -392,11 +418,7 @@ TilingTable TilingTable::from_json(const std::string& text) {
     LaunchCfg l;
     const LaunchCfg* lp = nullptr;
     if (auto it = e.find("sm100"); it != e.end() && it->second.is_obj()) {
-      const json::Object& so = it->second.obj();
-      l.tile_m = static_cast<int32_t>(json::as_int(json::at(so, "tile_m"), "tile_m"));
-      l.cluster = static_cast<int32_t>(json::as_int(json::at(so, "cluster"), "cluster"));
-      l.bn = static_cast<int32_t>(json::as_int(json::at(so, "bn"), "bn"));
-      l.stages = static_cast<int32_t>(json::as_int(json::at(so, "stages"), "stages"));
+      l = launch_from_json(it->second.obj());
       lp = &l;
     }
     t.insert(key, cfg, ns, lp);
@@ -622,17 +644,19 @@ int atmm_table_insert(atmm_table* t, int32_t m_bucket, int32_t k, int32_t n, con
     TilingConfig c;
     std::copy(cfg, cfg + 6, c.e.begin());
     LaunchCfg l;
-    if (sm100) l = LaunchCfg{sm100[0], sm100[1], sm100[2], sm100[3]};
+    if (sm100) l = launch_from_ints(sm100);
     t->t.insert(ShapeKey{m_bucket, k, n}, c, measured_ns, sm100 ? &l : nullptr);
   });
 }
 
-int atmm_table_set_default(atmm_table* t, const int32_t cfg[6]) {
+int atmm_table_set_default(atmm_table* t, const int32_t cfg[6], const int32_t* sm100) {
   return guarded([&] {
     if (!t || !cfg) fail(ATMM_ERR_CONFIG, "null table or config");
     TilingConfig c;
     std::copy(cfg, cfg + 6, c.e.begin());
-    t->t.set_default(c);
+    LaunchCfg l;
+    if (sm100) l = launch_from_ints(sm100);
+    t->t.set_default(c, sm100 ? &l : nullptr);
   });
 }
 
@@ -651,15 +675,21 @@ int atmm_table_size(const atmm_table* t, int64_t* size) {
   });
 }
 
+int atmm_table_find(const atmm_table* t, int64_t m, int64_t k, int64_t n, int32_t launch_out[5], int* found) {
+  return guarded([&] {
+    if (!t || !launch_out || !found) fail(ATMM_ERR_CONFIG, "null table or output");
+    const TableEntry* e = t->t.find(m, k, n);
+    *found = e ? 1 : 0;
+    if (e) launch_to_ints(e->has_sm100 ? e->sm100 : launch_from_config(e->config, k), launch_out);
+  });
+}
+
 int atmm_table_resolve_launch(const atmm_table* t, int64_t m, int64_t d_in, int64_t rank,
                               int64_t d_out, int32_t launch_out[4]) {
   return guarded([&] {
     if (!launch_out) fail(ATMM_ERR_CONFIG, "null output");
     const LaunchCfg l = t ? t->t.resolve_launch(m, d_in, rank, d_out) : heuristic_launch(m, d_in, rank, d_out);
-    launch_out[0] = l.tile_m;
-    launch_out[1] = l.cluster;
-    launch_out[2] = l.bn;
-    launch_out[3] = l.stages;
+    launch_to_ints(l, launch_out);
   });
 }
 
@@ -703,6 +733,95 @@ int atmm_default_candidates(size_t budget, size_t width, int32_t* out, size_t ca
 // LPT over whole segments: segments sorted by cost
 // descending (ties: ascending adapter id), each placed on the currently
 // least-loaded shard (ties: lowest shard index).
+// The reference TilingConfig recorded beside a B200 launch (the JSON
+// "config" field, read by the reference's TilingTable::load): outer_m = tile
+// rows, outer_n = expand chunk, outer_k = K slice per CTA (powers of two).
+static TilingConfig config_of_launch(const LaunchCfg& l, int64_t d_in) {
+  auto pow2_ceil = [](int64_t v) {
+    int64_t p = 16;
+    while (p < v) p <<= 1;
+    return p;
+  };
+  const int64_t om = pow2_ceil(l.tile_m), on = pow2_ceil(l.bn);
+  int64_t ok = 64;
+  while (ok * 2 * l.cluster <= d_in) ok <<= 1;
+  return TilingConfig{{static_cast<int32_t>(om), static_cast<int32_t>(on), static_cast<int32_t>(ok),
+                       static_cast<int32_t>(std::min<int64_t>(om, 128)), 16, 64}};
+}
+
+// The selection half of tiling_search (atmm.hpp:293-329) over a score grid:
+// per-shape argmin (ties to the lexicographically smallest launch; shapes
+// whose candidates all failed -- INT64_MAX -- are omitted and reported), the
+// most frequent winner as the default.  Two grid shapes can share a table key
+// (m_bucket, d_in, rank) while differing in batch size (segments): the
+// reference keeps the faster measurement of one GEMM shape; here the entry
+// measured on the larger batch (segments x m rows) is kept -- a bigger batch
+// is not comparable by time, and it is the loaded serving case -- with the
+// faster one winning between equal batches.
+int atmm_table_from_scores(const atmm_tune_shape* shapes, int64_t num_shapes, const int32_t* launches,
+                           int64_t num_launches, const int64_t* scores, atmm_table** out, char* failures,
+                           size_t failures_cap) {
+  return guarded([&] {
+    if (!shapes || !launches || !scores || !out || num_shapes < 1 || num_launches < 1) {
+      fail(ATMM_ERR_CONFIG, "table_from_scores needs a nonempty grid, candidates and scores");
+    }
+    std::vector<LaunchCfg> cands;
+    for (int64_t i = 0; i < num_launches; ++i) {
+      cands.push_back(launch_from_ints(launches + 5 * i));
+      validate_launch(cands.back());
+    }
+    auto table = std::make_unique<atmm_table>();
+    std::map<LaunchCfg, int> wins;
+    std::map<LaunchCfg, TilingConfig> cfg_of;
+    std::map<ShapeKey, int64_t> batch_of;  // rows of the batch each entry was measured on
+    std::string fails;
+    constexpr int64_t kFailed = std::numeric_limits<int64_t>::max();
+    for (int64_t si = 0; si < num_shapes; ++si) {
+      const int64_t* sc = scores + si * num_launches;
+      int64_t best = -1;
+      for (int64_t ci = 0; ci < num_launches; ++ci) {
+        if (sc[ci] == kFailed) continue;
+        if (best < 0 || sc[ci] < sc[best] || (sc[ci] == sc[best] && cands[ci] < cands[best])) best = ci;
+      }
+      const atmm_tune_shape& sh = shapes[si];
+      if (best < 0) {
+        fails += "shape " + std::to_string(sh.segments) + "x" + std::to_string(sh.m) + " rows, d " +
+                 std::to_string(sh.d_in) + ", r " + std::to_string(sh.rank) + ": all candidates failed, omitted\n";
+        continue;
+      }
+      const LaunchCfg& lc = cands[static_cast<size_t>(best)];
+      const ShapeKey key{m_bucket_of(sh.m), static_cast<int32_t>(sh.d_in), static_cast<int32_t>(sh.rank)};
+      const TilingConfig tc = config_of_launch(lc, sh.d_in);
+      auto it = table->t.entries().find(key);
+      const int64_t rows = sh.m * sh.segments;
+      auto bt = batch_of.find(key);
+      if (it == table->t.entries().end() || rows > bt->second ||
+          (rows == bt->second && sc[best] < it->second.measured_ns)) {
+        table->t.insert(key, tc, sc[best], &lc);
+        batch_of[key] = rows;
+      }
+      wins[lc] += 1;
+      cfg_of[lc] = tc;
+    }
+    if (!wins.empty()) {
+      const LaunchCfg* top = nullptr;
+      int top_count = -1;
+      for (const auto& [lc, count] : wins) {  // map order: ties go to the lexicographically smallest
+        if (count > top_count) {
+          top = &lc;
+          top_count = count;
+        }
+      }
+      table->t.set_default(cfg_of[*top], top);
+    }
+    if (failures && failures_cap > 0) {
+      std::strncpy(failures, fails.c_str(), failures_cap - 1);
+      failures[failures_cap - 1] = 0;
+    }
+    *out = table.release();
+  });
+}
+
 int atmm_shard_rows(const int32_t* assignment, int64_t n, const int32_t* adapter_ids,
                     const int64_t* adapter_ranks, int64_t num_adapters, int64_t d_in, int64_t d_out,
                     int32_t num_shards, int32_t* shard_of_row) {

@@ -2283,12 +2283,9 @@ template __global__ void atmm_merge_tma_kernel<__nv_bfloat16>(const __grid_const
 // =========================================================================
 namespace atmm {
 
-// Programmatic dependent launch on by default; ATMM_NO_PDL=1 turns it off
-// (A/B measurements).
-static bool pdl_enabled() {
-  static const bool on = std::getenv("ATMM_NO_PDL") == nullptr;
-  return on;
-}
+// Programmatic dependent launch is always on: every kernel waits
+// (griddepcontrol.wait) before touching its predecessor's outputs.
+static constexpr bool pdl_enabled() { return true; }
 
 // Function attributes are raised once per (kernel, device) and only when a
 // launch needs more, so steady-state launches (and CUDA-graph capture) issue
@@ -2421,12 +2418,8 @@ cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t sme
   cfg.dynamicSmemBytes = smem_s;
   cudaError_t e = prepare(atmm_shrink_kernel, smem_s, false);
   if (e != cudaSuccess) return e;
-  static const int only = std::getenv("ATMM_SPLIT_ONLY") ? std::atoi(std::getenv("ATMM_SPLIT_ONLY")) : 0;  // A/B: 1 shrink, 2 expand
-  if (only != 2) {
-    e = cudaLaunchKernelEx(&cfg, atmm_shrink_kernel, p);
-    if (e != cudaSuccess) return e;
-  }
-  if (only == 1) return cudaSuccess;
+  e = cudaLaunchKernelEx(&cfg, atmm_shrink_kernel, p);
+  if (e != cudaSuccess) return e;
   cfg.blockDim = dim3(kExpandThreads, 1, 1);
   cfg.dynamicSmemBytes = smem_e;
   if (y_dtype == 0 && p.expand_g == 1) {

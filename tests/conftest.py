@@ -50,3 +50,23 @@ def gpu(atmm):
 def tol_for(ref) -> float:
     """North-star tolerance (BASELINE.json): 1e-2 * max(1, max|ref|), bf16 in / fp32 acc."""
     return 1e-2 * max(1.0, float(np.max(np.abs(ref))) if np.size(ref) else 0.0)
+
+
+PATH_CODES = {"auto": 0, "a2a": 1, "split": 2, "fused": 3}
+
+
+def path_table(atmm, assignment, ranks, d_in, d_out, path):
+    """A tiling table whose entry for every segment of this batch is the
+    heuristic launch with the kernel path forced (ATMM_PATH_*), i.e. the
+    automatic plan except for the kernel choice.  None for "auto"."""
+    if path == "auto":
+        return None
+    t = atmm.TilingTable()
+    a = np.asarray(assignment)
+    for aid in np.unique(a):
+        m = int(np.count_nonzero(a == aid))
+        r = int(ranks[int(aid)])
+        launch = list(atmm.heuristic_launch(m, d_in, r, d_out))
+        launch[4] = PATH_CODES[path]
+        t.insert(atmm.m_bucket_of(m), d_in, r, (128, 128, 256, 128, 16, 64), 1, sm100=launch)
+    return t

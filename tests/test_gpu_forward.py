@@ -127,7 +127,7 @@ def test_forward_reference_golden(gpu, atmm, oracle):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_forward_random_shapes(gpu, atmm, oracle, monkeypatch, seed):
+def test_forward_random_shapes(gpu, atmm, oracle, seed):
     """Random hidden sizes (multiples of 8, not of 64), ragged segments down
     to one row, ranks 1..128, both GEMM tile widths and shrink K splits."""
     rng = np.random.default_rng(500 + seed)
@@ -142,14 +142,8 @@ def test_forward_random_shapes(gpu, atmm, oracle, monkeypatch, seed):
     want = oracle.forward_f64(x, w, "unmerged", a, facs)
     for bn, ks, pair, kz in [("128", None, "1", "1"), ("256", "1", "1", "1"), ("256", "4", "0", "1"),
                              ("128", "2", "0", "1"), ("128", "2", "0", "4"), ("128", None, "0", "2")]:
-        monkeypatch.setenv("ATMM_FWD_BN", bn)
-        monkeypatch.setenv("ATMM_FWD_PAIR", pair)
-        monkeypatch.setenv("ATMM_FWD_KZ", kz)
-        if ks:
-            monkeypatch.setenv("ATMM_FWD_KS", ks)
-        else:
-            monkeypatch.delenv("ATMM_FWD_KS", raising=False)
-        got = atmm.LayerForward(atmm.BypassPlan(reg, a)).run(_dev(w), _dev(x)).float().cpu().numpy()
+        opts = {"bn": int(bn), "pair": int(pair), "kz": int(kz), "ks": int(ks or 0)}
+        got = atmm.LayerForward(atmm.BypassPlan(reg, a), opts=opts).run(_dev(w), _dev(x)).float().cpu().numpy()
         assert np.max(np.abs(got - want)) <= tol_for(want), (bn, ks, pair, kz, d, L, ranks, lens)
 
 
@@ -191,12 +185,13 @@ def test_forward_errors_and_edges(gpu, atmm, oracle):
     torch.cuda.synchronize()
 
 
-GEMM_CASES = [(1, 64, 8), (7, 104, 136), (130, 256, 512), (300, 1000, 264), (257, 72, 1024), (512, 4096, 4096)]
+GEMM_CASES = [(1, 64, 8), (7, 104, 136), (130, 256, 512), (300, 1000, 264), (257, 72, 1024), (512, 4096, 4096),
+              (257, 192, 512), (384, 576, 264)]  # odd counts of 64-wide K blocks under 128-deep stages
 
 
 @pytest.mark.parametrize("m,k,n", GEMM_CASES)
 @pytest.mark.parametrize("out", ["bf16", "f32"])
-def test_gemm_parity(gpu, atmm, oracle, monkeypatch, m, k, n, out):
+def test_gemm_parity(gpu, atmm, oracle, m, k, n, out):
     """atmm_gemm (the base GEMM of model.hpp:238, atmm_multiply_into with a
     dense operand) against an fp64 product of the same bf16 inputs, over the
     1-SM, split-K and 2-SM tile paths; reruns bit-identical."""
@@ -207,15 +202,14 @@ def test_gemm_parity(gpu, atmm, oracle, monkeypatch, m, k, n, out):
     b = oracle.round_bf16(rng.uniform(-1, 1, (k, n)) / np.sqrt(k))
     want = a @ b
     dt = torch.float32 if out == "f32" else torch.bfloat16
-    for pair, kz in [("1", "1"), ("0", "1"), ("0", "2"), ("0", "4")]:
-        monkeypatch.setenv("ATMM_FWD_PAIR", pair)
-        monkeypatch.setenv("ATMM_FWD_KZ", kz)
+    for opts in [{"pair": 1, "kz": 1}, {"pair": 0, "kz": 1}, {"pair": 0, "kz": 2}, {"pair": 0, "kz": 4},
+                 {"pair": 0, "bn": 256}, {"pair": 1, "bn": 128}, {"pair": 0, "stages": 2}, None]:
         at, bt = _dev(a), _dev(b)
-        got = atmm.gemm(at, bt, out_dtype=dt)
-        again = atmm.gemm(at, bt, out_dtype=dt)
+        got = atmm.gemm(at, bt, out_dtype=dt, opts=opts)
+        again = atmm.gemm(at, bt, out_dtype=dt, opts=opts)
         torch.cuda.synchronize()
         g = got.float().cpu().numpy()
-        assert np.max(np.abs(g - want)) <= tol_for(want), (pair, kz)
+        assert np.max(np.abs(g - want)) <= tol_for(want), opts
         assert torch.equal(got, again)
 
 
@@ -249,20 +243,30 @@ def test_gemm_strides_and_edges(gpu, atmm, oracle):
 
 @pytest.mark.parametrize("mc", ["2", "4"])
 @pytest.mark.parametrize("m,k,n", [(1, 64, 512), (130, 1000, 1024), (300, 4096, 2048)])
-def test_gemm_a_multicast(gpu, atmm, oracle, monkeypatch, mc, m, k, n):
+def test_gemm_a_multicast(gpu, atmm, oracle, mc, m, k, n):
     """The 1-SM GEMM with A multicast over clusters of mc N tiles."""
     import torch
 
-    monkeypatch.setenv("ATMM_FWD_PAIR", "0")
-    monkeypatch.setenv("ATMM_FWD_BN", "128")
-    monkeypatch.setenv("ATMM_GEMM_MC", mc)
+    opts = {"pair": 0, "bn": 128, "mc": int(mc)}
     rng = np.random.default_rng(m + k + n)
     a = oracle.round_bf16(rng.uniform(-1, 1, (m, k)))
     b = oracle.round_bf16(rng.uniform(-1, 1, (k, n)) / np.sqrt(k))
     want = a @ b
     at, bt = _dev(a), _dev(b)
-    got = atmm.gemm(at, bt, out_dtype=torch.float32)
-    again = atmm.gemm(at, bt, out_dtype=torch.float32)
+    got = atmm.gemm(at, bt, out_dtype=torch.float32, opts=opts)
+    again = atmm.gemm(at, bt, out_dtype=torch.float32, opts=opts)
     torch.cuda.synchronize()
     assert np.max(np.abs(got.cpu().numpy() - want)) <= tol_for(want)
     assert torch.equal(got, again)
+
+
+def test_gemm_options_validated(gpu, atmm):
+    import torch
+
+    a = torch.zeros(8, 64, device="cuda", dtype=torch.bfloat16)
+    b = torch.zeros(64, 8, device="cuda", dtype=torch.bfloat16)
+    for bad in ({"bn": 192}, {"kz": 3}, {"pair": 2}, {"stages": 1}, {"mc": 3}):
+        with pytest.raises(atmm.ConfigError):
+            atmm.gemm(a, b, opts=bad)
+    with pytest.raises(atmm.ConfigError):
+        atmm.gemm(a, b, opts={"tile": 1})

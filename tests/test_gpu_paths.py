@@ -2,7 +2,8 @@
 
 The launcher picks, per launch group, the all-to-all fused kernel (small,
 latency-bound tiles), the split shrink + expand pair (large tiles) or the
-general fused kernel.  ATMM_PATH forces one where it applies, so every path
+general fused kernel.  A tiling-table entry's launch path (ATMM_PATH_*)
+forces one where it applies, so every path
 is checked on the same seeded inputs (bf16 and fp32 Y, several ranks, ragged
 segments) against the restated reference, with the north-star tolerance
 1e-2 * max(1, max|ref|) and bit-exact reruns (test_atmm.cpp:72-94).
@@ -10,7 +11,7 @@ segments) against the restated reference, with the north-star tolerance
 import numpy as np
 import pytest
 
-from conftest import tol_for
+from conftest import path_table, tol_for
 
 pytestmark = pytest.mark.gpu
 
@@ -42,16 +43,15 @@ def _inputs(oracle, d_in, d_out, ranks, lens, seed=31):
 @pytest.mark.parametrize("path", ["a2a", "split", "fused"])
 @pytest.mark.parametrize("case", range(len(CASES)))
 @pytest.mark.parametrize("ydt", ["bf16", "f32"])
-def test_path_parity(gpu, atmm, oracle, monkeypatch, path, case, ydt):
+def test_path_parity(gpu, atmm, oracle, path, case, ydt):
     import torch
 
-    monkeypatch.setenv("ATMM_PATH", path)
     d_in, d_out, ranks, lens = CASES[case]
     facs, assignment, x, y0 = _inputs(oracle, d_in, d_out, ranks, lens)
     reg = atmm.AdapterRegistry(1, d_in, d_out)
     for a, (down, up) in facs.items():
         reg.put(a, down, up, scale=0.75)
-    plan = atmm.BypassPlan(reg, assignment)
+    plan = atmm.BypassPlan(reg, assignment, path_table(atmm, assignment, ranks, d_in, d_out, path))
     want = y0.astype(np.float64) + 0.75 * 2.0 * oracle.bypass_rows_f64(x, assignment, facs)
     dt = torch.bfloat16 if ydt == "bf16" else torch.float32
     xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
@@ -65,7 +65,7 @@ def test_path_parity(gpu, atmm, oracle, monkeypatch, path, case, ydt):
     assert np.array_equal(outs[0], outs[1]), "reruns must be bit-identical"
 
 
-def test_paths_agree_closely(gpu, atmm, oracle, monkeypatch):
+def test_paths_agree_closely(gpu, atmm, oracle):
     """All three kernels compute the same rounding of the same sums up to
     one bf16 ulp of Y (they differ only in where mid is rounded)."""
     import torch
@@ -78,8 +78,7 @@ def test_paths_agree_closely(gpu, atmm, oracle, monkeypatch):
     xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
     res = {}
     for path in ("a2a", "split", "fused"):
-        monkeypatch.setenv("ATMM_PATH", path)
-        plan = atmm.BypassPlan(reg, assignment)
+        plan = atmm.BypassPlan(reg, assignment, path_table(atmm, assignment, ranks, d_in, d_out, path))
         yt = torch.from_numpy(y0).to("cuda", torch.float32)
         plan.apply(xt, yt)
         torch.cuda.synchronize()
@@ -90,8 +89,7 @@ def test_paths_agree_closely(gpu, atmm, oracle, monkeypatch):
     assert np.max(np.abs(res["split"] - res["fused"])) <= tol_for(want)
 
 
-def test_split_path_is_chosen_for_large_tiles(gpu, atmm, oracle, monkeypatch):
-    monkeypatch.delenv("ATMM_PATH", raising=False)
+def test_split_path_is_chosen_for_large_tiles(gpu, atmm, oracle):
     d_in, d_out, ranks, lens = CASES[3]
     facs, assignment, _, _ = _inputs(oracle, d_in, d_out, ranks, lens)
     reg = atmm.AdapterRegistry(1, d_in, d_out)
@@ -105,7 +103,7 @@ def test_split_path_is_chosen_for_large_tiles(gpu, atmm, oracle, monkeypatch):
 
 
 @pytest.mark.parametrize("seed", range(8))
-def test_random_shapes_all_paths(gpu, atmm, oracle, monkeypatch, seed):
+def test_random_shapes_all_paths(gpu, atmm, oracle, seed):
     """Random d_in / d_out (incl. not multiples of 8 or 64), ranks 1..128,
     ragged segments down to 1 row, bf16 and fp32 Y: every kernel path the
     launcher can take matches the oracle."""
@@ -128,11 +126,7 @@ def test_random_shapes_all_paths(gpu, atmm, oracle, monkeypatch, seed):
     xpad[:, :d_in] = torch.from_numpy(x).to("cuda", torch.bfloat16)
     xt = xpad[:, :d_in]
     for path in ("auto", "a2a", "split", "fused"):
-        if path == "auto":
-            monkeypatch.delenv("ATMM_PATH", raising=False)
-        else:
-            monkeypatch.setenv("ATMM_PATH", path)
-        plan = atmm.BypassPlan(reg, assignment)
+        plan = atmm.BypassPlan(reg, assignment, path_table(atmm, assignment, ranks, d_in, d_out, path))
         for dt in (torch.bfloat16, torch.float32):
             yt = torch.from_numpy(y0).to("cuda", dt)
             plan.apply(xt, yt)
@@ -180,19 +174,18 @@ def test_large_batch_row_subset(gpu, atmm, oracle):
 
 
 @pytest.mark.parametrize("path", ["a2a", "fused", "split"])
-def test_x_ready_flag_same_results(gpu, atmm, oracle, monkeypatch, path):
+def test_x_ready_flag_same_results(gpu, atmm, oracle, path):
     """ATMM_PLAN_X_READY (X gathered before griddepcontrol.wait): K
     back-to-back applies on one stream over distinct (X, Y) buffers give the
     same bits as without the flag, and match the oracle."""
     import torch
 
-    monkeypatch.setenv("ATMM_PATH", path)
     d_in, d_out, ranks, lens = CASES[2]
     facs, assignment, x, y0 = _inputs(oracle, d_in, d_out, ranks, lens, seed=5)
     reg = atmm.AdapterRegistry(1, d_in, d_out)
     for a, (down, up) in facs.items():
         reg.put(a, down, up)
-    plan = atmm.BypassPlan(reg, assignment)
+    plan = atmm.BypassPlan(reg, assignment, path_table(atmm, assignment, ranks, d_in, d_out, path))
     K = 6
     rng = np.random.default_rng(3)
     xs = [torch.from_numpy(oracle.round_bf16(x * rng.uniform(0.5, 1.5))).to("cuda", torch.bfloat16) for _ in range(K)]

@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol():
 def test_python_binding_covers_the_abi(atmm):
     from paper_2411_00915_b200._lib import EXPORTED, lib
 
-    assert lib.atmm_abi_version() == 1
+    assert lib.atmm_abi_version() == 2
     for s in declared_symbols():
         assert s in EXPORTED, s
 
@@ -152,7 +152,7 @@ def test_table_json_round_trip_and_reference_loadable(atmm, tmp_path, reference)
     assert len(back) == 2
     assert back.lookup(256, 4096, 32) == (64, 32, 32, 32, 32, 32)
     assert back.lookup(8192, 4096, 128) == (64, 64, 64, 32, 64, 64)
-    assert back.resolve_launch(8192, 4096, 128, 4096) == (128, 8, 128, 3)
+    assert back.resolve_launch(8192, 4096, 128, 4096) == (128, 8, 128, 3, 0)
     for (m, k, n) in [(256, 4096, 32), (8192, 4096, 128), (5, 5, 5), (8000, 4096, 128)]:
         out = np.zeros(6, np.int32)
         st = reference.L.ref_table_load_lookup(path.encode(), m, k, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
@@ -178,12 +178,12 @@ def test_table_load_errors(atmm, tmp_path):
 def test_launch_resolution(atmm):
     """B200 reading of the six edges and the heuristic default."""
     t = atmm.TilingTable()
-    tm, c, bn, st = t.resolve_launch(32, 4096, 16, 4096)
+    tm, c, bn, st, path = t.resolve_launch(32, 4096, 16, 4096)
     assert (tm, c) == (128, 8) and bn in (64, 128, 256)
     t2 = atmm.TilingTable((64, 256, 1024, 64, 16, 64))
-    assert t2.resolve_launch(32, 4096, 16, 4096) == (64, 4, 256, 0)
+    assert t2.resolve_launch(32, 4096, 16, 4096) == (64, 4, 256, 0, 0)
     t2.insert(32, 4096, 16, (128, 128, 512, 128, 16, 64), 5)
-    assert t2.resolve_launch(20, 4096, 16, 4096) == (128, 8, 128, 0)
+    assert t2.resolve_launch(20, 4096, 16, 4096) == (128, 8, 128, 0, 0)
     with pytest.raises(atmm.ConfigError):
         t2.insert(32, 4096, 16, (128, 128, 512, 128, 16, 64), 5, sm100=(128, 17, 128, 0))
 
@@ -243,3 +243,27 @@ def test_cpp_shim_host_cases(tmp_path):
     exe = _build_shim(tmp_path)
     out = subprocess.run([str(exe), "host"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+def _build_acceptance(tmp_path):
+    """tests/cpp/acceptance_shim.cpp: the reference's acceptance criteria 1-4
+    against the drop-in header (reference signatures; no CUDA headers)."""
+    exe = tmp_path / "acceptance_shim"
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "acceptance_shim.cpp"),
+           "-L", os.path.dirname(LIB), "-l:libatmm_b200.so", f"-Wl,-rpath,{os.path.dirname(LIB)}", "-o", str(exe)]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    return exe
+
+
+def test_compat_header_builds_and_has_no_cpu_fallback(tmp_path, atmm):
+    """The drop-in compiles against the reference signatures; on a host
+    without a B200 the first operator throws (DeviceError), it never computes
+    on the CPU."""
+    exe = _build_acceptance(tmp_path)
+    if atmm.device_count() > 0:
+        pytest.skip("a device is present: the GPU suite runs the criteria")
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 100, out.stdout + out.stderr
+    assert "no CUDA device" in out.stdout
