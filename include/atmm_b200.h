@@ -106,8 +106,9 @@ void atmm_table_destroy(atmm_table* t);
  * the reference entry (the JSON "sm100" object):
  *   tile_m  rows per tile (1..128)      cluster  CTAs per tile (1..16)
  *   bn      expand N chunk (64..256)    stages   shrink ring depth (0 = auto)
- *   path    ATMM_PATH_* kernel choice (ATMM_PATH_AUTO picks by tile rows). */
-enum { ATMM_PATH_AUTO = 0, ATMM_PATH_A2A = 1, ATMM_PATH_SPLIT = 2, ATMM_PATH_FUSED = 3 };
+ *   path    ATMM_PATH_* kernel choice (ATMM_PATH_AUTO picks by tile rows;
+ *           ATMM_PATH_STREAM runs the whole plan as ONE persistent launch). */
+enum { ATMM_PATH_AUTO = 0, ATMM_PATH_A2A = 1, ATMM_PATH_SPLIT = 2, ATMM_PATH_FUSED = 3, ATMM_PATH_STREAM = 4 };
 int atmm_table_insert(atmm_table* t, int32_t m_bucket, int32_t k, int32_t n,
                       const int32_t cfg[6], int64_t measured_ns, const int32_t* sm100);
 /* TilingTable::set_default (tiling.hpp:169); sm100 (nullable) = the default's

@@ -78,7 +78,7 @@ struct LaunchCfg {
   int32_t cluster = 8;   // CTAs per cluster (K / N split)
   int32_t bn = 128;      // expand N chunk
   int32_t stages = 0;    // 0 = as many as shared memory allows (<= 6)
-  int32_t path = 0;      // kernel: 0 automatic, 1 all-to-all fused, 2 split pair, 3 general fused
+  int32_t path = 0;      // kernel: 0 automatic, 1 all-to-all fused, 2 split pair, 3 general fused, 4 stream
   auto operator<=>(const LaunchCfg&) const = default;
 };
 // A launch as the 5 ints of the C ABI ({tile_m, cluster, bn, stages, path}).

@@ -36,6 +36,7 @@ cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t sme
                          cudaStream_t stream);
 cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassParams& p, int C, int num_tiles,
                               size_t smem, cudaStream_t stream);
+cudaError_t launch_stream(int y_dtype, const StreamParams& p, int grid, size_t smem, cudaStream_t stream);
 cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,
                          cudaStream_t stream);
 cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const MergeParams& p, int grid,
@@ -438,6 +439,22 @@ struct SplitLayout {
   size_t smem_s = 0, smem_e[2] = {0, 0};
 };
 
+// Stream-path (atmm_stream_kernel) geometry of a plan, per Y dtype:
+//   [shrink ring: SS x (X rows8 x 128 B, 128-byte swizzle | down^T r_pad x 128 B)]
+//   [expand ring: ES x (up^T 128 x r_pad bf16 | Y rows x 128 x esz)]
+//   [mid: 2 x rows16 x r_pad bf16]
+// The shrink MMA (M = 128) reads 16 KiB of A from each stage base; the
+// rows past a tile feed TMEM lanes that are never read, so >= 16 KiB of the
+// allocation must follow the last shrink stage.
+struct StreamLayout {
+  bool ok = false;
+  int32_t grid = 0, sstages[2] = {0, 0}, estages[2] = {0, 0};
+  uint32_t s_stage = 0, s_a = 0, e_stage[2] = {0, 0}, off_e[2] = {0, 0}, off_mid[2] = {0, 0};
+  uint32_t mid_bytes = 0, tmem_cols = 0;
+  int32_t rows_max = 0, r_pad_max = 16, nsl = 0;
+  size_t smem[2] = {0, 0};
+};
+
 struct LaunchGroup {
   A2aLayout a2a[2];  // per Y dtype (ATMM_BF16, ATMM_F32)
   SplitLayout split;
@@ -687,6 +704,10 @@ struct atmm_plan {
   int merged_first = -1;
   LaunchGroup merged;
   std::unique_ptr<SplitBufs> merged_bufs;
+  // Stream path (atmm_stream_kernel): every tile of the plan in one launch.
+  StreamLayout stream;
+  int32_t stream_mode = 0;  // 0 never, 1 forced (every segment's launch path is ATMM_PATH_STREAM), 2 automatic
+  std::unique_ptr<SplitBufs> stream_bufs;  // tables: [s_begin | e_begin (P+1 each) | seg_slot0 (P) | nseg | part_off | ncons (T)]
   DevBuf<int32_t> d_rows;
   std::vector<int32_t> rows_host;  // routed entry (plan order) -> X / Y row
   DevBuf<TileDesc> d_tiles;
@@ -750,6 +771,52 @@ static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, 
   return l;
 }
 
+// Stream-path ring depths: each ring gets stages until shared memory runs
+// out, always extending the ring with fewer bytes in flight (both rings
+// stream from HBM at once; ~64 KiB+ in flight per SM covers the latency),
+// capped by the units a CTA actually owns.
+static void resolve_stream(StreamLayout& l, int32_t rows_max, int32_t r_pad, int s_units_cta, int e_units_cta) {
+  l.ok = false;
+  if (r_pad > kMaxRank || rows_max > kTileM || rows_max < 1) return;
+  l.rows_max = rows_max;
+  l.r_pad_max = r_pad;
+  const int64_t rows8 = round_up(rows_max, 8), rows16 = round_up(rows_max, 16);
+  l.s_a = static_cast<uint32_t>(rows8 * 128);
+  l.s_stage = static_cast<uint32_t>(rows8 * 128 + int64_t(r_pad) * 128);
+  l.mid_bytes = static_cast<uint32_t>(round_up(rows16 * r_pad * 2, 1024));
+  uint32_t cols = 32;
+  while (cols < static_cast<uint32_t>(2 * r_pad + 2 * rows16)) cols <<= 1;
+  if (cols > 512) return;
+  l.tmem_cols = cols;
+  const int s_cap = std::clamp(s_units_cta, 1, 16), e_cap = std::clamp(e_units_cta, 1, 16);
+  for (int di = 0; di < 2; ++di) {
+    const int64_t esz = di == 0 ? 2 : 4;
+    const int64_t es = round_up(int64_t(128) * r_pad * 2 + int64_t(rows_max) * 128 * esz, 1024);
+    l.e_stage[di] = static_cast<uint32_t>(es);
+    const int64_t avail = int64_t(kSmemLimit) - 2048 - 2 * int64_t(l.mid_bytes);
+    auto fits = [&](int ss, int e) {
+      const int64_t body = int64_t(ss) * l.s_stage + int64_t(e) * es;
+      return std::max(body, int64_t(ss - 1) * l.s_stage + 16384) <= avail;
+    };
+    int ss = 1, e = 1;
+    if (!fits(ss, e)) return;
+    while (true) {
+      const bool can_s = ss < s_cap && fits(ss + 1, e);
+      const bool can_e = e < e_cap && fits(ss, e + 1);
+      if (!can_s && !can_e) break;
+      if (can_s && (!can_e || int64_t(ss) * l.s_stage <= int64_t(e) * es)) ++ss;
+      else ++e;
+    }
+    l.sstages[di] = ss;
+    l.estages[di] = e;
+    l.off_e[di] = static_cast<uint32_t>(int64_t(ss) * l.s_stage);
+    l.off_mid[di] = static_cast<uint32_t>(l.off_e[di] + int64_t(e) * es);
+    const int64_t body = int64_t(l.off_mid[di]) + 2 * int64_t(l.mid_bytes);
+    l.smem[di] = size_t(1024 + std::max(body, int64_t(ss - 1) * l.s_stage + 16384));
+  }
+  l.ok = true;
+}
+
 // Balanced split of a flattened, weighted work list over `parts` CTAs:
 // begin[b] = first item whose cost prefix reaches b * total / parts.
 static std::vector<int32_t> balance(const std::vector<int64_t>& cost, int parts) {
@@ -769,6 +836,78 @@ static std::vector<int32_t> balance(const std::vector<int64_t>& cost, int parts)
 }  // namespace atmm
 
 namespace atmm {
+
+// Fixed per-unit cost (bytes-equivalent) of the stream kernel's balancing.
+static int64_t stream_fixed_cost() { return 4096; }
+
+// Stream path of a plan: every tile in one launch.  Balanced shrink and
+// expand ranges over the SMs, the per-tile segment slots of the shrink
+// partials (CTA order = fixed reduction order) and consumer counts.
+static void build_stream(atmm_plan& plan, const std::vector<TileDesc>& tiles, const atmm_registry* reg) {
+  StreamLayout& l = plan.stream;
+  l.ok = false;
+  const int T = static_cast<int>(tiles.size());
+  if (T == 0 || reg->d_out % 8 != 0) return;
+  int32_t rows_max = 1, rpm = 16;
+  for (const TileDesc& td : tiles) {
+    rows_max = std::max(rows_max, td.rows);
+    rpm = std::max(rpm, td.r_pad);
+  }
+  const int nkb = static_cast<int>((reg->d_in + kBK - 1) / kBK);
+  const int nsl = static_cast<int>((reg->d_out + 127) / 128);
+  std::vector<int64_t> scost, ecost;
+  scost.reserve(size_t(T) * nkb);
+  ecost.reserve(size_t(T) * nsl);
+  for (const TileDesc& td : tiles) {
+    for (int k = 0; k < nkb; ++k) scost.push_back(int64_t(td.rows) * 128 + int64_t(td.r_pad) * 128 + stream_fixed_cost());
+    for (int k = 0; k < nsl; ++k) ecost.push_back(int64_t(td.rows) * 128 * 2 * 2 + 128 * int64_t(td.r_pad) * 2 + stream_fixed_cost());
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, reg->device);
+  const int P = std::max(1, std::min<int>(sms, static_cast<int>(std::max(scost.size(), ecost.size()))));
+  std::vector<int32_t> sb = balance(scost, P), eb = balance(ecost, P);
+  int s_max = 1, e_max = 1;
+  for (int b = 0; b < P; ++b) {
+    s_max = std::max(s_max, sb[b + 1] - sb[b]);
+    e_max = std::max(e_max, eb[b + 1] - eb[b]);
+  }
+  resolve_stream(l, rows_max, rpm, s_max, e_max);
+  if (!l.ok) return;
+  l.grid = P;
+  l.nsl = nsl;
+  std::vector<int32_t> slot0(static_cast<size_t>(P), 0), nseg(T, 0), off(T), ncons(T, 0);
+  for (int b = 0; b < P; ++b) {
+    if (sb[b] < sb[b + 1]) {
+      const int t0 = sb[b] / nkb, t1 = (sb[b + 1] - 1) / nkb;
+      slot0[static_cast<size_t>(b)] = nseg[t0];
+      for (int t = t0; t <= t1; ++t) ++nseg[t];
+    }
+    if (eb[b] < eb[b + 1]) {
+      const int t0 = eb[b] / nsl, t1 = (eb[b + 1] - 1) / nsl;
+      for (int t = t0; t <= t1; ++t) ++ncons[t];
+    }
+  }
+  int32_t total_seg = 0;
+  for (int t = 0; t < T; ++t) {
+    off[t] = total_seg;
+    total_seg += nseg[t];
+  }
+  std::vector<int32_t> tables;
+  tables.insert(tables.end(), sb.begin(), sb.end());
+  tables.insert(tables.end(), eb.begin(), eb.end());
+  tables.insert(tables.end(), slot0.begin(), slot0.end());
+  tables.insert(tables.end(), nseg.begin(), nseg.end());
+  tables.insert(tables.end(), off.begin(), off.end());
+  tables.insert(tables.end(), ncons.begin(), ncons.end());
+  auto& mb = plan.stream_bufs;
+  mb = std::make_unique<SplitBufs>();
+  mb->grid = P;
+  mb->part_elems = static_cast<size_t>(total_seg) * kTileM * rpm;
+  mb->mid_elems = 0;
+  mb->counter_elems = 2 * static_cast<size_t>(T);
+  mb->tables.alloc(tables.size());
+  CUDA_CHECK(cudaMemcpy(mb->tables.p, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice));
+}
 
 // Builds routing tables and launch groups.  `forced` (tuner) overrides the
 // table for every segment.
@@ -857,6 +996,14 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     }
     plan->groups.push_back(g);
   }
+  {
+    bool all_stream = true, all_auto = true;
+    for (const LaunchGroup& g : plan->groups) {
+      all_stream = all_stream && g.path == ATMM_PATH_STREAM;
+      all_auto = all_auto && g.path == ATMM_PATH_AUTO;
+    }
+    plan->stream_mode = all_stream ? 1 : (all_auto ? 2 : 0);
+  }
   if (plan->merged_first >= 0) {
     plan->merged.split = resolve_split(reg->d_in, reg->d_out, plan->merged.rows_max, plan->merged.r_pad_max);
     if (!plan->merged.split.ok) plan->merged_first = -1;
@@ -938,6 +1085,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     mb->tables.alloc(tables.size());
     CUDA_CHECK(cudaMemcpy(mb->tables.p, tables.data(), tables.size() * 4, cudaMemcpyHostToDevice));
   }
+  build_stream(*plan, all_tiles, reg);
   plan->d_rows.alloc(rows32.size());
   CUDA_CHECK(cudaMemcpy(plan->d_rows.p, rows32.data(), rows32.size() * 4, cudaMemcpyHostToDevice));
   plan->rows_host = std::move(rows32);
@@ -950,6 +1098,64 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
 // Debug-only phase tracing (tools/profile_trace.py): a device buffer of
 // >= ctas * kTraceEvents uint64 filled by the next bypass launches.
 static uint64_t* g_trace = nullptr;
+
+// Whether an apply runs as one stream launch (atmm_stream_kernel).
+static bool stream_auto(const atmm_plan& p) {
+  (void)p;
+  return false;
+}
+static bool use_stream(const atmm_plan& p, bool y_vec) {
+  if (!p.stream.ok || !y_vec || !p.stream_bufs) return false;
+  return p.stream_mode == 1 || (p.stream_mode == 2 && stream_auto(p));
+}
+
+static void launch_stream_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y, int64_t ldy,
+                               int y_dtype, float scale, cudaStream_t stream) {
+  const atmm_registry* reg = p->reg;
+  const StreamLayout& l = p->stream;
+  SplitBufs& sb = *p->stream_bufs;
+  SplitScratch& sc = sb.for_stream(stream);
+  const int P = sb.grid;
+  const int T = static_cast<int>(p->d_tiles.n);
+  const int di = y_dtype == ATMM_BF16 ? 0 : 1;
+  StreamParams sp{};
+  sp.tiles = p->d_tiles.p;
+  sp.row_index = p->d_rows.p;
+  sp.x = static_cast<const uint16_t*>(x);
+  sp.ldx = ldx;
+  sp.y = y;
+  sp.ldy = ldy;
+  sp.d_in = static_cast<int32_t>(reg->d_in);
+  sp.d_out = static_cast<int32_t>(reg->d_out);
+  sp.layer = static_cast<int32_t>(layer);
+  sp.scale = scale;
+  sp.num_tiles = T;
+  sp.nkb = static_cast<int32_t>((reg->d_in + kBK - 1) / kBK);
+  sp.nsl = l.nsl;
+  sp.r_pad_max = l.r_pad_max;
+  sp.rows_max = l.rows_max;
+  sp.sstages = l.sstages[di];
+  sp.estages = l.estages[di];
+  sp.s_stage_bytes = l.s_stage;
+  sp.s_a_bytes = l.s_a;
+  sp.e_stage_bytes = l.e_stage[di];
+  sp.off_e = l.off_e[di];
+  sp.off_mid = l.off_mid[di];
+  sp.mid_bytes = l.mid_bytes;
+  sp.tmem_cols = l.tmem_cols;
+  sp.x_ready = (p->flags & ATMM_PLAN_X_READY) ? 1 : 0;
+  sp.s_begin = sb.tables.p;
+  sp.e_begin = sp.s_begin + (P + 1);
+  sp.seg_slot0 = sp.e_begin + (P + 1);
+  sp.nseg = sp.seg_slot0 + P;
+  sp.part_off = sp.nseg + T;
+  sp.ncons = sp.part_off + T;
+  sp.part = sc.part.p;
+  sp.counter = sc.counter.p;
+  sp.trace = g_trace;
+  const cudaError_t e = launch_stream(di, sp, P, l.smem[di], stream);
+  if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("stream bypass launch failed: ") + cudaGetErrorString(e));
+}
 
 // count > 1: independent calls (xs[c], ys[c], layers[c]) of one plan; the
 // all-to-all kernel runs them as ONE launch, other paths launch per call.
@@ -970,6 +1176,15 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
   if (ldy < reg->d_out) fail(ATMM_ERR_SHAPE, "Y row stride ldy must be >= d_out");
   if (reinterpret_cast<uintptr_t>(y) % ysz != 0) fail(ATMM_ERR_SHAPE, "Y is not element aligned");
   int32_t y_vec = ((ldy * ysz) % 16 == 0 && reinterpret_cast<uintptr_t>(y) % 16 == 0) ? 1 : 0;
+  if (use_stream(*p, y_vec != 0)) {
+    if (count > 1) {
+      if (count > kMaxGroup || !layers || !xs || !ys) fail(ATMM_ERR_CONFIG, "grouped apply: 1..8 calls with layers, xs, ys");
+      for (int c = 0; c < count; ++c) apply_plan(p, layers[c], xs[c], ldx, ys[c], ldy, y_dtype, scale, stream);
+      return;
+    }
+    launch_stream_plan(p, layer, x, ldx, y, ldy, y_dtype, scale, stream);
+    return;
+  }
   if (count > 1) {
     if (count > kMaxGroup || !layers || !xs || !ys) fail(ATMM_ERR_CONFIG, "grouped apply: 1..8 calls with layers, xs, ys");
     bool all_a2a = y_vec != 0;
@@ -1586,7 +1801,7 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
            ", \"nbuf\": " + std::to_string(g.nbuf) + ", \"r_pad\": " + std::to_string(g.r_pad_max) +
            ", \"tmem_cols\": " + std::to_string(g.tmem_cols) + ", \"smem\": " + std::to_string(g.smem) +
            ", \"path_bf16\": \"" +
-           std::string(choose_path(g, ATMM_BF16, true) == BypassPath::kA2a ? "a2a" : (choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? "split" : "fused")) +
+           std::string(use_stream(*p, true) ? "stream" : choose_path(g, ATMM_BF16, true) == BypassPath::kA2a ? "a2a" : (choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? "split" : "fused")) +
            "\", \"split\": " + (g.split.ok ? std::string("{\"stages\": ") + std::to_string(g.split.stages) +
                                                    ", \"estages_bf16\": " + std::to_string(g.split.estages[0]) + "}"
                                              : std::string("null")) +
@@ -1594,6 +1809,13 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
                                                   ", \"tmem_cols\": " + std::to_string(g.a2a[0].tmem_cols) +
                                                   ", \"smem\": " + std::to_string(g.a2a[0].smem) + "}"
                                             : std::string("null")) +
+           ", \"stream\": " +
+           (p->stream.ok ? std::string("{\"grid\": ") + std::to_string(p->stream.grid) +
+                               ", \"sstages_bf16\": " + std::to_string(p->stream.sstages[0]) +
+                               ", \"estages_bf16\": " + std::to_string(p->stream.estages[0]) +
+                               ", \"smem_bf16\": " + std::to_string(p->stream.smem[0]) +
+                               ", \"tmem_cols\": " + std::to_string(p->stream.tmem_cols) + "}"
+                         : std::string("null")) +
            "}";
     }
     s += "]";
@@ -1611,6 +1833,7 @@ int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64
       nl += choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? 0 : 1;  // bf16 Y, aligned
     }
     if (p->merged_first >= 0) nl += 2;  // one shrink + expand pair for all split groups
+    if (use_stream(*p, true)) nl = 1;   // one stream launch for the whole plan
     if (launches) *launches = nl;
     if (tiles) *tiles = t;
     if (ctas) *ctas = p->total_ctas;

@@ -151,6 +151,54 @@ struct SplitParams {
   uint64_t* trace;
 };
 
+// Stream path (atmm_stream_kernel): the shrink AND the expand of every tile
+// in ONE persistent launch, one CTA per SM.  Each CTA owns a host-balanced
+// range of shrink units (tile, 64-wide K block) and, independently, a range
+// of expand units (tile, 128 output columns); two loader groups stream both
+// rings from the start, so the Y rows of the expand (2/3 of the bytes) are in
+// flight while the shrink runs.  A tile's fp32 partial mid rows (one slot per
+// CTA segment, as in SplitParams) are published with a release increment of
+// counter[t]; every CTA that expands tile t waits for counter[t] == nseg[t],
+// sums the partials in FIXED slot order into a bf16 mid in shared memory and
+// runs its units.  The last consumer of a tile (ncons[t]) resets its
+// counters for the next launch on the stream.
+struct StreamParams {
+  const TileDesc* tiles;
+  const int32_t* row_index;
+  const uint16_t* x;   // n x d_in bf16
+  int64_t ldx;
+  void* y;             // n x d_out (bf16 or fp32)
+  int64_t ldy;
+  int32_t d_in;
+  int32_t d_out;
+  int32_t layer;
+  float scale;
+  int32_t num_tiles;
+  int32_t nkb;         // 64-wide K blocks per tile
+  int32_t nsl;         // 128-column expand units per tile
+  int32_t r_pad_max;
+  int32_t rows_max;
+  int32_t sstages;     // shrink ring depth (<= 16)
+  int32_t estages;     // expand ring depth (<= 16)
+  uint32_t s_stage_bytes;  // [X rows8_max x 128 B, 128-byte swizzle | down^T r_pad_max x 128 B]
+  uint32_t s_a_bytes;      // rows8_max x 128
+  uint32_t e_stage_bytes;  // [up^T 128 x r_pad_max | Y rows_max x 128 x esz]
+  uint32_t off_e;          // expand ring
+  uint32_t off_mid;        // 2 mid slots of mid_bytes
+  uint32_t mid_bytes;
+  uint32_t tmem_cols;
+  int32_t x_ready;
+  const int32_t* s_begin;    // [grid + 1]
+  const int32_t* e_begin;    // [grid + 1]
+  const int32_t* seg_slot0;  // [grid]
+  const int32_t* nseg;       // [tile]
+  const int32_t* part_off;   // [tile]
+  const int32_t* ncons;      // [tile] CTAs whose expand range touches the tile
+  float* part;               // [sum nseg][128][r_pad_max]
+  int32_t* counter;          // [2 tiles]: published segments, finished consumers
+  uint64_t* trace;
+};
+
 struct MergeParams {
   const uint16_t* a_t;  // down^T blocked (MN-major A): [kb][g][c][8x8], K = r_pad
   const uint16_t* b_t;  // up^T blocked (K-major B):    [g][c][8x8]

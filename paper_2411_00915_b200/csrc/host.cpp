@@ -81,7 +81,7 @@ void TilingTable::insert(ShapeKey key, const TilingConfig& cfg, int64_t ns,
 
 void validate_launch(const LaunchCfg& l) {
   if (l.tile_m < 1 || l.tile_m > 128 || l.cluster < 1 || l.cluster > 16 || l.bn < 64 || l.bn > 256 ||
-      l.bn % 64 != 0 || l.stages < 0 || l.stages > 8 || l.path < 0 || l.path > 3) {
+      l.bn % 64 != 0 || l.stages < 0 || l.stages > 8 || l.path < 0 || l.path > 4) {
     fail(ATMM_ERR_CONFIG, "invalid sm100 launch parameters");
   }
 }

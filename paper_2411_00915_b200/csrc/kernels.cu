@@ -768,75 +768,95 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
 // Warps: 0..3 up^T staging, partials, reduction; 4 Y staging; 5/6 X
 // gathers (6 also down^T); 7 TMEM owner + MMA issuer; all 8: Y update.
 template <typename YT, int G>
-__device__ __forceinline__ void a2a_update_rows(const uint32_t (&acc)[64], int rb, int nrows, uint32_t ysrc,
-                                                uint32_t pitch, uint8_t* ydst_col, uint32_t rows_s,
-                                                int64_t ldy_b, float s) {
+__device__ __forceinline__ void a2a_row_out(const uint32_t (&acc)[64], int i, const uint32_t* in, uint8_t* gp, float s) {
   constexpr int RB = 64 / G > 32 ? 32 : 64 / G;  // rows per block (acc[j * RB + i])
   constexpr int kBytes = G * static_cast<int>(sizeof(YT));
+  if constexpr (sizeof(YT) == 2) {
+    uint32_t out[(G + 1) / 2];
 #pragma unroll
-  for (int i = 0; i < RB; ++i) {
-    if (i < nrows) {
+    for (int j = 0; j < G; j += 2) {
+      const float lo = fmaf(s, __uint_as_float(acc[j * RB + i]), bf16lo(in[j / 2]));
+      if (G == 1) {
+        out[0] = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+      } else {
+        const float hi = fmaf(s, __uint_as_float(acc[(j + 1) * RB + i]), bf16hi(in[j / 2]));
+        out[j / 2] = pack_bf16x2(lo, hi);
+      }
+    }
+    if constexpr (kBytes == 2) {
+      *reinterpret_cast<uint16_t*>(gp) = static_cast<uint16_t>(out[0]);
+    } else if constexpr (kBytes == 4) {
+      *reinterpret_cast<uint32_t*>(gp) = out[0];
+    } else if constexpr (kBytes == 8) {
+      *reinterpret_cast<uint2*>(gp) = make_uint2(out[0], out[1]);
+    } else {
+      *reinterpret_cast<uint4*>(gp) = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+  } else {
+    float out[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) out[j] = fmaf(s, __uint_as_float(acc[j * RB + i]), __uint_as_float(in[j]));
+    if constexpr (kBytes == 4) {
+      *reinterpret_cast<float*>(gp) = out[0];
+    } else if constexpr (kBytes == 8) {
+      *reinterpret_cast<float2*>(gp) = make_float2(out[0], out[1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < G; q += 4) {
+        *reinterpret_cast<float4*>(gp + q * 4) = make_float4(out[q], out[q + 1], out[q + 2], out[q + 3]);
+      }
+    }
+  }
+}
+
+// Y[row, G columns] += s * acc for the RB rows [rb, rb + nrows) of a block.
+// Called by EVERY lane of the warp (row indices travel by shuffle); lanes
+// with col_ok == false load and store nothing.  All Y loads of the block are
+// issued before the first store (no per-row shared-load round trip), and a
+// full block runs without per-row branches.
+template <typename YT, int G>
+__device__ __forceinline__ void a2a_update_rows(const uint32_t (&acc)[64], int rb, int nrows, uint32_t ysrc,
+                                                uint32_t pitch, uint8_t* ydst_col, uint32_t rows_s,
+                                                int64_t ldy_b, float s, bool col_ok) {
+  constexpr int RB = 64 / G > 32 ? 32 : 64 / G;  // rows per block (acc[j * RB + i])
+  constexpr int kBytes = G * static_cast<int>(sizeof(YT));
+  constexpr int kW = (kBytes + 3) / 4;  // 32-bit words of Y per row and thread
+  const uint32_t lane = threadIdx.x & 31u;
+  const int myrow = static_cast<int32_t>(ld_shared_u32(rows_s + (static_cast<uint32_t>(rb) + lane % RB) * 4u));
+  // sub-batches of SB rows bound the registers holding Y (SB x kW words)
+  constexpr int SB = (16 / kW) < 1 ? 1 : ((16 / kW) > RB ? RB : (16 / kW));
+  const bool full = nrows >= RB;
+#pragma unroll
+  for (int i0 = 0; i0 < RB; i0 += SB) {
+    uint32_t in[SB][kW];
+#pragma unroll
+    for (int ii = 0; ii < SB; ++ii) {
+      const int i = i0 + ii;
       const uint32_t ya = ysrc + static_cast<uint32_t>(rb + i) * pitch;
-      uint8_t* gp = ydst_col + static_cast<int64_t>(static_cast<int32_t>(ld_shared_u32(rows_s + (rb + i) * 4))) * ldy_b;
-      if constexpr (sizeof(YT) == 2) {
-        uint32_t in[(G + 1) / 2];
+      if (col_ok && (full || i < nrows)) {
         if constexpr (kBytes == 2) {
-          in[0] = ld_shared_u16(ya);
+          in[ii][0] = ld_shared_u16(ya);
         } else if constexpr (kBytes == 4) {
-          in[0] = ld_shared_u32(ya);
+          in[ii][0] = ld_shared_u32(ya);
         } else if constexpr (kBytes == 8) {
-          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(in[0]), "=r"(in[1]) : "r"(ya));
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(in[ii][0]), "=r"(in[ii][1]) : "r"(ya));
         } else {
-          const uint4 v = ld_shared_v4(ya);
-          in[0] = v.x; in[1] = v.y; in[2] = v.z; in[3] = v.w;
-        }
-        uint32_t out[(G + 1) / 2];
 #pragma unroll
-        for (int j = 0; j < G; j += 2) {
-          const float lo = fmaf(s, __uint_as_float(acc[j * RB + i]), bf16lo(in[j / 2]));
-          if (G == 1) {
-            out[0] = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
-          } else {
-            const float hi = fmaf(s, __uint_as_float(acc[(j + 1) * RB + i]), bf16hi(in[j / 2]));
-            out[j / 2] = pack_bf16x2(lo, hi);
+          for (int q = 0; q < kW; q += 4) {
+            const uint4 v = ld_shared_v4(ya + q * 4);
+            in[ii][q] = v.x; in[ii][q + 1] = v.y; in[ii][q + 2] = v.z; in[ii][q + 3] = v.w;
           }
-        }
-        if constexpr (kBytes == 2) {
-          *reinterpret_cast<uint16_t*>(gp) = static_cast<uint16_t>(out[0]);
-        } else if constexpr (kBytes == 4) {
-          *reinterpret_cast<uint32_t*>(gp) = out[0];
-        } else if constexpr (kBytes == 8) {
-          *reinterpret_cast<uint2*>(gp) = make_uint2(out[0], out[1]);
-        } else {
-          *reinterpret_cast<uint4*>(gp) = make_uint4(out[0], out[1], out[2], out[3]);
         }
       } else {
-        uint32_t in[G];
-        if constexpr (kBytes == 4) {
-          in[0] = ld_shared_u32(ya);
-        } else if constexpr (kBytes == 8) {
-          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(in[0]), "=r"(in[1]) : "r"(ya));
-        } else {
 #pragma unroll
-          for (int q = 0; q < G; q += 4) {
-            const uint4 v = ld_shared_v4(ya + q * 4);
-            in[q] = v.x; in[q + 1] = v.y; in[q + 2] = v.z; in[q + 3] = v.w;
-          }
-        }
-        float out[G];
-#pragma unroll
-        for (int j = 0; j < G; ++j) out[j] = fmaf(s, __uint_as_float(acc[j * RB + i]), __uint_as_float(in[j]));
-        if constexpr (kBytes == 4) {
-          *reinterpret_cast<float*>(gp) = out[0];
-        } else if constexpr (kBytes == 8) {
-          *reinterpret_cast<float2*>(gp) = make_float2(out[0], out[1]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < G; q += 4) {
-            *reinterpret_cast<float4*>(gp + q * 4) = make_float4(out[q], out[q + 1], out[q + 2], out[q + 3]);
-          }
-        }
+        for (int q = 0; q < kW; ++q) in[ii][q] = 0u;
       }
+    }
+#pragma unroll
+    for (int ii = 0; ii < SB; ++ii) {
+      const int i = i0 + ii;
+      const int r = __shfl_sync(0xffffffffu, myrow, i);
+      if (col_ok && (full || i < nrows)) a2a_row_out<YT, G>(acc, i, in[ii], ydst_col + static_cast<int64_t>(r) * ldy_b, s);
     }
   }
 }
@@ -870,7 +890,7 @@ __device__ __forceinline__ void a2a_epilogue(uint32_t tmem_base, uint32_t lane_a
       tmem_ld_rows<RB>(tmem_base + lane_addr + static_cast<uint32_t>(j * rows16 + rb), &acc[j * RB]);
     }
     tmem_wait_ld();
-    if (col_ok) a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), ysrc, pitch, ydst, rows_s, ldy_b, s);
+    a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), ysrc, pitch, ydst, rows_s, ldy_b, s, col_ok);
   }
 }
 
@@ -1771,10 +1791,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
                            &acc[jj * RB]);
         }
         tmem_wait_ld();
-        if (col_ok) {
-          a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), Yb + static_cast<uint32_t>(c0 * kEsz), ypitch, ydst, rring,
-                                 ldy_b, s);
-        }
+        a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), Yb + static_cast<uint32_t>(c0 * kEsz), ypitch, ydst, rring,
+                               ldy_b, s, col_ok);
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);

@@ -52,7 +52,7 @@ def tol_for(ref) -> float:
     return 1e-2 * max(1.0, float(np.max(np.abs(ref))) if np.size(ref) else 0.0)
 
 
-PATH_CODES = {"auto": 0, "a2a": 1, "split": 2, "fused": 3}
+PATH_CODES = {"auto": 0, "a2a": 1, "split": 2, "fused": 3, "stream": 4}
 
 
 def path_table(atmm, assignment, ranks, d_in, d_out, path):

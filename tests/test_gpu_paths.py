@@ -40,7 +40,7 @@ def _inputs(oracle, d_in, d_out, ranks, lens, seed=31):
     return facs, assignment, x, y0
 
 
-@pytest.mark.parametrize("path", ["a2a", "split", "fused"])
+@pytest.mark.parametrize("path", ["a2a", "split", "fused", "stream"])
 @pytest.mark.parametrize("case", range(len(CASES)))
 @pytest.mark.parametrize("ydt", ["bf16", "f32"])
 def test_path_parity(gpu, atmm, oracle, path, case, ydt):
@@ -125,7 +125,7 @@ def test_random_shapes_all_paths(gpu, atmm, oracle, seed):
     xpad = torch.zeros(x.shape[0], ldx, dtype=torch.bfloat16, device="cuda")
     xpad[:, :d_in] = torch.from_numpy(x).to("cuda", torch.bfloat16)
     xt = xpad[:, :d_in]
-    for path in ("auto", "a2a", "split", "fused"):
+    for path in ("auto", "a2a", "split", "fused", "stream"):
         plan = atmm.BypassPlan(reg, assignment, path_table(atmm, assignment, ranks, d_in, d_out, path))
         for dt in (torch.bfloat16, torch.float32):
             yt = torch.from_numpy(y0).to("cuda", dt)
@@ -173,7 +173,7 @@ def test_large_batch_row_subset(gpu, atmm, oracle):
     assert np.max(np.abs(got - want)) <= tol_for(want)
 
 
-@pytest.mark.parametrize("path", ["a2a", "fused", "split"])
+@pytest.mark.parametrize("path", ["a2a", "fused", "split", "stream"])
 def test_x_ready_flag_same_results(gpu, atmm, oracle, path):
     """ATMM_PLAN_X_READY (X gathered before griddepcontrol.wait): K
     back-to-back applies on one stream over distinct (X, Y) buffers give the
