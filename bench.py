@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--soak-s", type=float, default=1.0, help="load before the timed region while clocks are sampled")
     ap.add_argument("--group", type=int, default=3, help="extra measurement: steps per grouped launch (1 = off)")
     ap.add_argument("--no-forward", action="store_true", help="skip the layer-forward side measurement")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the workload itself over the N ranks (default: weak, one batch per GPU)")
     return ap.parse_args()
 
 
@@ -138,6 +140,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------ distributed -------
+DIST_BACKEND = os.environ.get("ATMM_BENCH_DIST", "nccl")  # "gloo": multi-rank smoke test on one GPU
+
+
 def dist_setup(n_gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -150,8 +155,13 @@ def dist_setup(n_gpus: int):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         import torch
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "gloo":  # every rank on the one visible GPU (code-path test, not a measurement)
+            local = 0
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -168,7 +178,7 @@ def max_over_ranks(v: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if DIST_BACKEND == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -475,19 +485,42 @@ def impl_ours_bypass(args, w):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    step_bytes = w.bytes(2)
+    # Request sharding: the job's global batch is split by
+    # whole segments over the ranks (LPT, every rank derives the same plan);
+    # each rank holds only its shard's adapters and rows.  Weak scaling
+    # (default): the global batch is N independent copies of the workload,
+    # one per GPU.  --strong: the workload itself is split N ways.
+    from paper_2411_00915_b200.sharding import ShardedBypass, replicate_batch, shard_flops
+    from paper_2411_00915_b200.workloads import BypassWorkload
+
+    if args.strong:
+        glob, granks = w.assignment, dict(w.ranks)
+    else:
+        glob, granks = replicate_batch(w.assignment, w.ranks, world)
+    # per-rank shard description (lw): rows, adapters and lengths of this rank
+    from paper_2411_00915_b200.sharding import shard_batch
+
+    shards = shard_batch(glob, granks, w.d_in, w.d_out, world)
+    mine = shards[rank]
+    ids, counts = np.unique(mine.assignment, return_counts=True)
+    lw = BypassWorkload(w.name, w.d_in, w.d_out, int(mine.rows.size), {int(a): granks[int(a)] for a in ids},
+                        {int(a): int(c) for a, c in zip(ids, counts)}, mine.assignment)
+    job_flops = sum(shard_flops(sh, granks, w.d_in, w.d_out) for sh in shards)
+    step_bytes = lw.bytes(2)
     layers = max(2, int(np.ceil(2.5 * L2_BYTES / step_bytes)))
     layers = min(layers, 64)
-    rng = np.random.default_rng(1234 + rank)
-    # Registry: every adapter, every layer (factors differ per layer).
-    reg = atmm.AdapterRegistry(layers, w.d_in, w.d_out, device=local)
-    for a, r in w.ranks.items():
+
+    def factors(a):  # every layer's factors of adapter a (same on every rank)
+        rng = np.random.default_rng(1234 + a)
+        r = granks[a]
         s = 1.0 / np.sqrt(r)
-        down = rng.uniform(-s, s, (layers, w.d_in, r)).astype(np.float32)
-        up = rng.uniform(-s, s, (layers, r, w.d_out)).astype(np.float32)
-        reg.put(a, down, up)
-    assignment = w.assignment if rank == 0 else np.random.default_rng(rank).permutation(w.assignment)
-    plan = atmm.BypassPlan(reg, assignment)
+        return (rng.uniform(-s, s, (layers, w.d_in, r)).astype(np.float32),
+                rng.uniform(-s, s, (layers, r, w.d_out)).astype(np.float32))
+
+    sb = ShardedBypass(glob, granks, w.d_in, w.d_out, world, rank, factors, num_layers=layers, device=local)
+    reg, plan = sb.registry, sb.plan
+    w_job = w
+    w = lw  # per-rank quantities below (tokens, bytes, flops of this rank's shard)
     launches_per_step, tiles, ctas = plan.stats()
     xs = [torch.empty(w.tokens, w.d_in, dtype=torch.bfloat16, device=dev).uniform_(-1, 1) for _ in range(layers)]
     ys = [torch.empty(w.tokens, w.d_out, dtype=torch.bfloat16, device=dev).uniform_(-1, 1) for _ in range(layers)]
@@ -561,7 +594,7 @@ def impl_ours_bypass(args, w):
     torch.cuda.synchronize()
     xms = max_over_ranks(x0.elapsed_time(x1), world)
     x_ready = {"us_per_batch": xms * 1e3 / args.steps,
-               "value": world * w.flops() * args.steps / (xms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "value": job_flops * args.steps / (xms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "roofline_frac": step_bytes / (xms * 1e-3 / args.steps) / 1e9 / measured_peaks()[0],
                "note": "same steps with atmm_plan_set_flags(ATMM_PLAN_X_READY): X gathered under the previous "
                        "launch's tail; not the headline"}
@@ -605,7 +638,7 @@ def impl_ours_bypass(args, w):
         torch.cuda.synchronize()
         gms = max_over_ranks(g0.elapsed_time(g1), world)
         grouped = {"calls_per_launch": G, "us_per_batch": gms * 1e3 / gsteps,
-                   "value": world * w.flops() * gsteps / (gms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "value": job_flops * gsteps / (gms * 1e-3) / 1e12, "unit": "TFLOP/s",
                    "roofline_frac": step_bytes / (gms * 1e-3 / gsteps) / 1e9 / measured_peaks()[0],
                    "note": "same steps, G independent (X, Y, layer) calls per launch; not the headline"}
 
@@ -615,7 +648,7 @@ def impl_ours_bypass(args, w):
                                     cpu_sample_s=0.0 if (args.no_cpu_baseline or world > 1 or rank != 0) else 3.0)
 
     flops_step = w.flops()
-    value = world * flops_step * args.steps / (ms * 1e-3) / 1e12
+    value = job_flops * args.steps / (ms * 1e-3) / 1e12
     ms_per_step = ms / args.steps
     # The step is the hot path: one fused launch (all-to-all or general fused
     # kernel) or the split shrink + expand pair.  Achieved bandwidth = the
@@ -660,14 +693,14 @@ def impl_ours_bypass(args, w):
             return max_over_ranks(time.perf_counter() - t0, world)
 
         e2e_s = timed(lambda a, b, c: atmm.run_bypass_host_bf16_pipelined(plan, a, b, c))
-        e2e = {"value": world * flops_step * e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s",
+        e2e = {"value": job_flops * e2e_steps / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(w.tokens * w.d_in * 2),
                "d2h_bytes_per_step": int(w.tokens * w.d_out * 2),
                "us_per_batch": e2e_s / e2e_steps * 1e6, "steps": e2e_steps,
                "path": "atmm_run_bypass_host_bf16_pipelined = run_bypass (batch.hpp:48) on pinned bf16 host "
                        "buffers: H2D X, fused kernel into a fresh output, D2H; 4 streams"}
         r_s = timed(lambda a, b, c: atmm.residual_host_bf16_pipelined(plan, a, b, c))
-        e2e_res = {"value": world * flops_step * e2e_steps / r_s / 1e12, "unit": "TFLOP/s",
+        e2e_res = {"value": job_flops * e2e_steps / r_s / 1e12, "unit": "TFLOP/s",
                    "h2d_bytes_per_step": int(w.tokens * (w.d_in + w.d_out) * 2),
                    "d2h_bytes_per_step": int(w.tokens * w.d_out * 2), "us_per_batch": r_s / e2e_steps * 1e6,
                    "path": "atmm_bypass_residual_host_bf16_pipelined: H2D X and Y, Y += bypass, D2H Y"}
@@ -691,12 +724,18 @@ def impl_ours_bypass(args, w):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "us_per_batch": ms_per_step * 1e3,
             "single_launch_us": single_launch_us,
             "x_ready": x_ready,
-            "config": bench_config(w, world),
+            "config": bench_config(w_job, world),
+            "sharding": {"mode": "strong" if args.strong else "weak", "global_tokens": int(len(glob)),
+                         "global_adapters": len(granks), "rank0_tokens": int(w.tokens),
+                         "rank0_adapters": len(w.ranks), "collective": None,
+                         "launcher": "paper_2411_00915_b200.sharding.ShardedBypass (LPT over whole segments, "
+                                     "atmm_shard_rows; only the shard's adapters resident)"},
             "timing": {"l2": f"inputs rotate over {layers} layer buffer sets ({layers * step_bytes / 2**20:.0f} MiB "
                              f"> 2x L2); K steps in one CUDA graph, CUDA events on the launch stream"},
             "plan": {"launches_per_step": launches_per_step, "tiles": tiles, "ctas": ctas,

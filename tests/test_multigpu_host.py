@@ -73,3 +73,30 @@ def test_request_sharding_two_ranks(cfg):
         for a in ids:
             assert np.count_nonzero(assignment[owned[r]] == a) == lengths[a]
     assert results[0][3] == results[1][3] == float(world)
+
+
+def test_weak_scaling_batch_shards_evenly():
+    """bench.py --gpus N (weak scaling): N copies of a batch with distinct
+    adapters shard into N shards of exactly one batch each (LPT, host only)."""
+    from paper_2411_00915_b200.sharding import replicate_batch, shard_batch, shard_flops
+    from paper_2411_00915_b200.workloads import bypass_config
+
+    for name in ("cfg2", "cfg5"):
+        w = bypass_config(name)
+        for n in (1, 2, 4, 8):
+            glob, granks = replicate_batch(w.assignment, w.ranks, n)
+            shards = shard_batch(glob, granks, w.d_in, w.d_out, n)
+            assert sorted(s.rows.size for s in shards) == [w.tokens] * n
+            assert all(len(s.adapters) == len(w.ranks) for s in shards)
+            assert sum(shard_flops(s, granks, w.d_in, w.d_out) for s in shards) == n * w.flops()
+
+
+def test_strong_scaling_shards_balance_cfg5():
+    """bench.py --strong: cfg5 (64 equal segments) split 2/4/8 ways is exact."""
+    from paper_2411_00915_b200.sharding import shard_batch
+    from paper_2411_00915_b200.workloads import bypass_config
+
+    w = bypass_config("cfg5")
+    for n in (2, 4, 8):
+        shards = shard_batch(w.assignment, w.ranks, w.d_in, w.d_out, n)
+        assert [s.rows.size for s in shards] == [w.tokens // n] * n
