@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_init(&recv_bar, 1);
     fence_mbar_init();
     tma_prefetch_desc(&xmap);
-    if (ks > 1) mbar_arrive_expect_tx(&recv_bar, static_cast<uint32_t>(ks) * slot_bytes);
+    if (ks > 1) mbar_arrive_expect_tx(&recv_bar, static_cast<uint32_t>(ks - 1) * slot_bytes);  // own slot stays in red
   }
   if (warp == 1) tmem_alloc(&tslot, 128);
   const int ne = item.e_end - item.e_begin;
@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (threadIdx.x == 64) {
         const uint32_t src0 = smem_u32(red), dst0 = smem_u32(recv) + static_cast<uint32_t>(kr) * slot_bytes;
         for (int q2 = 0; q2 < ks; ++q2) {
+          if (q2 == kr) continue;  // my own rows are reduced straight from red
           bulk_s2cluster(map_cta(dst0, static_cast<uint32_t>(q2)), src0 + static_cast<uint32_t>(q2) * slot_bytes, slot_bytes,
                          map_cta(smem_u32(&recv_bar), static_cast<uint32_t>(q2)));
         }
@@ -298,10 +299,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int row = kr * rows_per + lr;
         const int c = (u % groups) * 4;
         const uint32_t off = recv_base + static_cast<uint32_t>(lr * pitch + c) * 4u;
+        const uint32_t own = smem_u32(red) + static_cast<uint32_t>(row * pitch + c) * 4u;  // slot kr = my partial
         uint4 v[16];
 #pragma unroll
         for (int q2 = 0; q2 < 16; ++q2)
-          if (q2 < ks) v[q2] = ld_shared_v4(off + static_cast<uint32_t>(q2) * slot_bytes);
+          if (q2 < ks) v[q2] = ld_shared_v4(q2 == kr ? own : off + static_cast<uint32_t>(q2) * slot_bytes);
         float4 acc = make_float4(__uint_as_float(v[0].x), __uint_as_float(v[0].y), __uint_as_float(v[0].z),
                                  __uint_as_float(v[0].w));
 #pragma unroll
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     fence_mbar_init();
     tma_prefetch_desc(&xmap);
     tma_prefetch_desc(&wmap);
-    if (kz > 1) mbar_arrive_expect_tx(&recv_bar, static_cast<uint32_t>(kz) * slot_bytes);
+    if (kz > 1) mbar_arrive_expect_tx(&recv_bar, static_cast<uint32_t>(kz - 1) * slot_bytes);  // own slot stays in stage
   }
   if (threadIdx.x == 0) FTRACE(4096, 0);
   if (warp == 1) tmem_alloc(&tslot, static_cast<uint32_t>(2 * bn));
@@ -636,6 +638,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (threadIdx.x == 64) {
       const uint32_t src0 = smem_u32(stage), dst0 = smem_u32(recv) + static_cast<uint32_t>(z) * slot_bytes;
       for (int r2 = 0; r2 < kz; ++r2) {
+        if (r2 == z) continue;  // my own rows are reduced straight from stage
         bulk_s2cluster(map_cta(dst0, static_cast<uint32_t>(r2)), src0 + static_cast<uint32_t>(r2) * slot_bytes, slot_bytes,
                        map_cta(smem_u32(&recv_bar), static_cast<uint32_t>(r2)));
       }
@@ -655,7 +658,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = 0.f;
         for (int r2 = 0; r2 < kz; ++r2) {  // rank order: deterministic
-          const uint32_t off = recv_base + static_cast<uint32_t>(r2) * slot_bytes + static_cast<uint32_t>(lr * pitch + c) * 4u;
+          const uint32_t off = r2 == z ? smem_u32(stage) + static_cast<uint32_t>((z * rows_per + lr) * pitch + c) * 4u
+                                       : recv_base + static_cast<uint32_t>(r2) * slot_bytes + static_cast<uint32_t>(lr * pitch + c) * 4u;
           const uint4 v0 = ld_shared_v4(off), v1 = ld_shared_v4(off + 16);
           acc[0] += __uint_as_float(v0.x);
           acc[1] += __uint_as_float(v0.y);

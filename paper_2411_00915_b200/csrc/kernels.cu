@@ -1469,11 +1469,14 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
       const int st = j % S;
       mbar_wait(&empty[st], static_cast<uint32_t>(((j / S) & 1) ^ 1));
       const uint32_t A = smem0 + static_cast<uint32_t>(st) * stage_bytes;
-      const uint16_t* xk = p.x + static_cast<int64_t>(kb) * kBK + ch * 8;
+      // columns past d_in (last K block) are zero-filled, never read
+      const int col = kb * kBK + ch * 8;
+      const uint32_t nb = static_cast<uint32_t>(max(0, min(8, p.d_in - col)) * 2);
+      const uint16_t* xk = p.x + (nb ? col : 0);
 #pragma unroll
       for (int i = 0; i < kRowsPer; ++i) {
         const int r = r0 + kRowStep * i;
-        if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], 16u);
+        if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], nb);
       }
       if (tid == 0) {  // the down^T block is one contiguous run: one TMA bulk copy
         mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(r_pad * kBK * 2));
@@ -1648,13 +1651,17 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       // -> MMA j = nl % G, A row nl / G.
       const uint16_t* us = tile.up_t + static_cast<int64_t>(p.layer) * tile.up_layer_stride;
       const int kc = r_pad / 8;
+      const int n_end = (p.d_out + 127) & ~127;  // the registry pads up^T to d_out_pad = round_up(d_out, 128)
       for (int q = static_cast<int>(tid); q < kCols * kc; q += kSplitLoaders) {
         const int nl = q / kc;
         const int c = q - nl * kc;
         const int n = n0 + nl;
         const int a_row = (nl % G) * kTileM + nl / G;
+        // columns past the padded up^T (last item of a d_out that is not a
+        // multiple of 128 G) are zero-filled, never read from global
+        const bool in = n < n_end;
         cp_async16(U + interleave_off(static_cast<uint32_t>(a_row), static_cast<uint32_t>(c * 8), static_cast<uint32_t>(r_pad)),
-                   us + ((static_cast<int64_t>(n >> 3) * kc + c) * 64 + (n & 7) * 8), 16u);
+                   in ? us + ((static_cast<int64_t>(n >> 3) * kc + c) * 64 + (n & 7) * 8) : us, in ? 16u : 0u);
       }
       // Y rows: the shrink launch (our predecessor) does not write Y and fires
       // its dependents only after its own griddepcontrol.wait, so every earlier

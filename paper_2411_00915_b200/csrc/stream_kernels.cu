@@ -178,11 +178,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) atmm_stream_kernel(const St
       const int st = j % SS;
       mbar_wait(&sempty[st], static_cast<uint32_t>(((j / SS) & 1) ^ 1));
       const uint32_t A = smem0 + static_cast<uint32_t>(st) * p.s_stage_bytes;
-      const uint16_t* xk = p.x + static_cast<int64_t>(kb) * kBK + ch * 8;
+      // columns past d_in (last K block) are zero-filled, never read
+      const int col = kb * kBK + ch * 8;
+      const uint32_t nb = static_cast<uint32_t>(max(0, min(8, p.d_in - col)) * 2);
+      const uint16_t* xk = p.x + (nb ? col : 0);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = r0 + 16 * i;
-        if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], 16u);
+        if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], nb);
       }
       if (tid == 0 && j >= SS) {
         const TileDesc& tile = p.tiles[t];
