@@ -112,7 +112,9 @@ enum { ATMM_PATH_AUTO = 0, ATMM_PATH_A2A = 1, ATMM_PATH_SPLIT = 2, ATMM_PATH_FUS
 int atmm_table_insert(atmm_table* t, int32_t m_bucket, int32_t k, int32_t n,
                       const int32_t cfg[6], int64_t measured_ns, const int32_t* sm100);
 /* TilingTable::set_default (tiling.hpp:169); sm100 (nullable) = the default's
- * B200 launch (JSON "default_sm100"), used for shapes the table misses. */
+ * B200 launch (JSON "default_sm100"), used for shapes the table misses;
+ * sm100 = {0, ...} makes misses resolve through the built-in B200 heuristic
+ * (JSON "default_sm100": "heuristic"). */
 int atmm_table_set_default(atmm_table* t, const int32_t cfg[6], const int32_t* sm100);
 /* TilingTable::lookup (tiling.hpp:181-199): exact -> nearest same-(k,n)
  * bucket within 32 (ties to the smaller bucket) -> default. */
@@ -462,7 +464,12 @@ int atmm_shard_rows(const int32_t* assignment, int64_t n, const int32_t* adapter
  * w_layer_stride elements, the reference's BaseModel layer layout), X and
  * out are n x d bf16 (row strides ldx / ldo, multiples of 8; 16-byte aligned
  * bases; out must not overlap X).  Stream-ordered on `stream`.
- * num_layers = 0 copies X. */
+ * num_layers = 0 copies X.
+ * Concurrency: one forward object is SINGLE-STREAM -- its activation
+ * ping-pong buffers and K-extension images are per object, so two runs of
+ * the same object must be ordered (same stream, or an event between them).
+ * Run concurrent forwards through separate objects (the reference's CPU
+ * forward is reentrant; this is the device equivalent of one call frame). */
 typedef struct atmm_forward atmm_forward;
 int atmm_forward_create(const atmm_plan* plan, int device, int64_t n, int64_t hidden_dim,
                         atmm_forward** out);

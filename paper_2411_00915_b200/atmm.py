@@ -12,6 +12,7 @@ torch is used only for device memory and streams.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Iterable, List, Optional, Sequence, Tuple
 
@@ -429,11 +430,16 @@ class BypassPlan:
 
     def __init__(self, registry: AdapterRegistry, assignment: Sequence[int], table: Optional[TilingTable] = None,
                  rows: Optional[Sequence[int]] = None, n_rows: Optional[int] = None,
-                 launch: Optional[Sequence[int]] = None):
+                 launch: Optional[Sequence[int]] = None, use_default_table: bool = True):
         """rows (optional): routed entry i is row rows[i] of X / Y, which
         have n_rows rows (atmm_plan_create_mapped); default: entry i = row i.
         launch (optional): {tile_m, cluster, bn, stages[, path]} forced for
-        every segment instead of the table's (atmm_plan_create_launch)."""
+        every segment instead of the table's (atmm_plan_create_launch).
+        table None: the packaged B200-profiled table (default_table(); the
+        built-in heuristic for shapes it does not cover), unless
+        use_default_table is False (heuristic only)."""
+        if table is None and launch is None and use_default_table:
+            table = default_table()
         a = _i32(assignment).reshape(-1)
         h = ctypes.c_void_p()
         if launch is not None:
@@ -964,6 +970,19 @@ def _shapes(shapes) -> ctypes.Array:
 
 def _launches(launches) -> np.ndarray:
     return np.ascontiguousarray(np.concatenate([_launch5(l) for l in launches]))
+
+
+_DEFAULT_TABLE = {}
+DEFAULT_TABLE_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tables", "b200_tiling_table.json")
+
+
+def default_table() -> Optional["TilingTable"]:
+    """The packaged B200-profiled tiling table (tools/tune.py: tiling_search
+    over default_shape_grid + the benched batch shapes), loaded once; None
+    when the package ships without one (the built-in heuristic applies)."""
+    if "t" not in _DEFAULT_TABLE:
+        _DEFAULT_TABLE["t"] = TilingTable.load(DEFAULT_TABLE_PATH) if os.path.exists(DEFAULT_TABLE_PATH) else None
+    return _DEFAULT_TABLE["t"]
 
 
 def default_shape_grid(d_in: int, d_out: Optional[int] = None, ranks: Optional[Sequence[int]] = None) -> List[tuple]:

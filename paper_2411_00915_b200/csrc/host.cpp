@@ -88,6 +88,12 @@ void validate_launch(const LaunchCfg& l) {
 
 void TilingTable::set_default(const TilingConfig& cfg, const LaunchCfg* sm100) {
   validate_config(cfg);
+  if (sm100 && sm100->tile_m == 0) {  // {0, ...}: shapes the table misses resolve through the B200 heuristic
+    default_ = cfg;
+    heuristic_default_ = true;
+    has_default_sm100_ = false;
+    return;
+  }
   if (sm100) validate_launch(*sm100);
   default_ = cfg;
   heuristic_default_ = false;
@@ -383,6 +389,7 @@ std::string TilingTable::to_json() const {
   std::ostringstream o;
   o << "{\n  \"default\": " << cfg_json(default_) << ",\n";
   if (has_default_sm100_) o << "  \"default_sm100\": " << launch_json(default_sm100_) << ",\n";
+  else if (heuristic_default_) o << "  \"default_sm100\": \"heuristic\",\n";
   o << "  \"entries\": [";
   bool first = true;
   for (const auto& [k, e] : entries_) {
@@ -404,6 +411,10 @@ TilingTable TilingTable::from_json(const std::string& text) {
   if (auto it = root.obj().find("default_sm100"); it != root.obj().end() && it->second.is_obj()) {
     const LaunchCfg dl = launch_from_json(it->second.obj());
     t.set_default(t.default_config(), &dl);
+  } else if (it != root.obj().end() && std::holds_alternative<std::string>(it->second.v) &&
+             std::get<std::string>(it->second.v) == "heuristic") {
+    const LaunchCfg heur{0, 0, 0, 0, 0};
+    t.set_default(t.default_config(), &heur);
   }
   const json::Value& ents = json::at(root.obj(), "entries");
   if (!ents.is_arr()) fail(ATMM_ERR_IO, "tiling table json: entries must be an array");

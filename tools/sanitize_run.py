@@ -24,6 +24,7 @@ PATHS = {"a2a": 1, "split": 2, "fused": 3, "stream": 4}
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="a2a,split,fused,stream,merge,forward,gemm")
+    ap.add_argument("--small", action="store_true", help="fewer rows (racecheck is slow)")
     args = ap.parse_args()
     only = set(args.only.split(","))
     import torch
@@ -33,7 +34,7 @@ def main():
     rng = np.random.default_rng(0)
     d_in, d_out = 520, 392  # K tail (d_in % 64 != 0) and a partial last expand item
     ranks = {1: 16, 2: 32, 3: 64}
-    lens = {1: 40, 2: 17, 3: 130}
+    lens = {1: 20, 2: 9, 3: 40} if args.small else {1: 40, 2: 17, 3: 130}
     reg = atmm.AdapterRegistry(1, d_in, d_out)
     facs = {}
     for a, r in ranks.items():
