@@ -228,7 +228,22 @@ void atmm_plan_destroy(atmm_plan* p);
  * that launch; Y is still read only after it completes.  Results are
  * unchanged; breaking the promise races on X. */
 #define ATMM_PLAN_X_READY 1u
+/* ATMM_PLAN_NO_OVERLAP: never start an apply's X / Y loads under the
+ * preceding launch.  By default the launcher does so for the all-to-all
+ * kernel when it can prove safety: that kernel releases its successor only
+ * after its own predecessor completed, so at most the immediately preceding
+ * launch on the stream can still run, and the apply proceeds early only when
+ * that launch is an all-to-all bypass whose X / Y bytes are disjoint from
+ * this apply's (consecutive independent batches overlap; Y_i -> X_i+1 chains
+ * keep the full dependency).  Under stream capture the predecessor is also
+ * matched by graph node.  Not visible to the check: a FOREIGN kernel launched
+ * with the programmatic-stream-serialization attribute between two eager
+ * applies on one stream -- set this flag when a caller does that. */
+#define ATMM_PLAN_NO_OVERLAP 2u
 int atmm_plan_set_flags(atmm_plan* p, uint32_t flags);
+/* Process-wide counters: all-to-all bypass launches issued, and how many of
+ * them started their X / Y loads early (ATMM_PLAN_NO_OVERLAP above). */
+int atmm_overlap_stats(int64_t* a2a_launches, int64_t* early_launches);
 /* Routing tables actually uploaded (for bit-exact routing checks):
  * seg_adapter[S], seg_offsets[S+1], row_index[n]. */
 int atmm_plan_routing(const atmm_plan* p, int32_t* seg_adapter, int64_t* seg_offsets,

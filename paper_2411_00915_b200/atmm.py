@@ -425,6 +425,13 @@ def _stream_ptr(stream) -> Optional[int]:
     return stream.cuda_stream
 
 
+def overlap_stats() -> Tuple[int, int]:
+    """(all-to-all bypass launches, launches that started early) so far."""
+    a, e = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib.atmm_overlap_stats(ctypes.byref(a), ctypes.byref(e)))
+    return int(a.value), int(e.value)
+
+
 class BypassPlan:
     """plan_batch + launch grouping for one batch on one registry."""
 
@@ -478,7 +485,16 @@ class BypassPlan:
         before the launch preceding the apply on its stream starts (e.g. the
         bypass follows the base GEMM Y = X W); X is then gathered under that
         launch's tail.  Results are unchanged."""
-        _check(lib.atmm_plan_set_flags(self._h, 1 if ready else 0))
+        self._flags = (getattr(self, "_flags", 0) & ~1) | (1 if ready else 0)
+        _check(lib.atmm_plan_set_flags(self._h, self._flags))
+
+    def set_overlap(self, allowed: bool = True) -> None:
+        """ATMM_PLAN_NO_OVERLAP when not allowed: never start an apply's X / Y
+        loads under the preceding launch (include/atmm_b200.h).  By default the
+        launcher does so only when it proves the preceding launch touches
+        disjoint bytes."""
+        self._flags = (getattr(self, "_flags", 0) & ~2) | (0 if allowed else 2)
+        _check(lib.atmm_plan_set_flags(self._h, self._flags))
 
     def routing(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
         seg = np.zeros(self.n_routed, np.int32)

@@ -709,6 +709,7 @@ struct atmm_plan {
   int32_t stream_mode = 0;  // 0 never, 1 forced (every segment's launch path is ATMM_PATH_STREAM), 2 automatic
   std::unique_ptr<SplitBufs> stream_bufs;  // tables: [s_begin | e_begin (P+1 each) | seg_slot0 (P) | nseg | part_off | ncons (T)]
   DevBuf<int32_t> d_rows;
+  DevBuf<int32_t> d_tile_rows;  // [tile][kTileM] padded row lists (a2a prologue)
   std::vector<int32_t> rows_host;  // routed entry (plan order) -> X / Y row
   DevBuf<TileDesc> d_tiles;
   int64_t total_ctas = 0;
@@ -1089,10 +1090,129 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
   plan->d_rows.alloc(rows32.size());
   CUDA_CHECK(cudaMemcpy(plan->d_rows.p, rows32.data(), rows32.size() * 4, cudaMemcpyHostToDevice));
   plan->rows_host = std::move(rows32);
+  {
+    std::vector<int32_t> tr(all_tiles.size() * kTileM);
+    for (size_t t = 0; t < all_tiles.size(); ++t) {
+      const TileDesc& td = all_tiles[t];
+      for (int i = 0; i < kTileM; ++i) {
+        tr[t * kTileM + i] = plan->rows_host[static_cast<size_t>(td.row_begin + std::min(i, std::max(td.rows, 1) - 1))];
+      }
+    }
+    plan->d_tile_rows.alloc(std::max<size_t>(tr.size(), 1));
+    if (!tr.empty()) CUDA_CHECK(cudaMemcpy(plan->d_tile_rows.p, tr.data(), tr.size() * 4, cudaMemcpyHostToDevice));
+  }
   plan->d_tiles.alloc(all_tiles.size());
   CUDA_CHECK(cudaMemcpy(plan->d_tiles.p, all_tiles.data(), all_tiles.size() * sizeof(TileDesc),
                         cudaMemcpyHostToDevice));
   return plan;
+}
+
+// =========================================================================
+// Programmatic-dependency elision for the all-to-all bypass
+// =========================================================================
+// Every bypass launch carries the programmatic-stream-serialization
+// attribute, and atmm_bypass_a2a_kernel follows a wait-before-trigger
+// protocol (kernels.cu): a thread releases the next launch only after its own
+// griddepcontrol.wait returned, i.e. once the grid BEFORE it is complete.  So
+// when an a2a grid starts, at most one earlier grid can still be running: the
+// launch immediately preceding it on the stream.  If that launch is an a2a
+// bypass whose X / Y bytes are disjoint from this launch's (no RAW on X or Y,
+// no WAW on Y, no WAR on the predecessor's X), nothing this launch reads or
+// writes can be touched by a running grid, and it loads X and Y before its
+// own griddepcontrol.wait (BypassParams::early): consecutive independent
+// batches overlap, dependent ones (Y_i feeds X_i+1) keep the full dependency.
+// The record is per (stream, capture sequence); under stream capture the
+// predecessor is also checked by graph node identity (cudaStreamGetCaptureInfo),
+// so a kernel captured in between can never be mistaken for our launch.
+// Other library launches with the PDL attribute invalidate the record
+// (pdl_note_other); launches without it serialise fully and only make the
+// check conservative.  Limit (documented in include/atmm_b200.h): a foreign
+// kernel launched WITH the PDL attribute between two eager library launches
+// on one stream is not seen; such callers set ATMM_PLAN_NO_OVERLAP.
+namespace {
+struct PdlRange {
+  uintptr_t lo = 0, hi = 0;
+  bool overlaps(const PdlRange& o) const { return lo < o.hi && o.lo < hi; }
+};
+struct PdlRecord {
+  bool valid = false;
+  int n = 0;
+  PdlRange x[kMaxGroup], y[kMaxGroup];
+  cudaGraphNode_t node = nullptr;  // capture: the graph node of the launch
+};
+struct PdlKey {
+  cudaStream_t s;
+  unsigned long long capture;
+  bool operator<(const PdlKey& o) const { return s != o.s ? s < o.s : capture < o.capture; }
+};
+std::mutex g_pdl_mu;
+std::map<PdlKey, PdlRecord> g_pdl;
+std::atomic<int64_t> g_a2a_launches{0}, g_a2a_early{0};
+
+struct PdlCapture {
+  bool capturing = false;
+  unsigned long long id = 0;
+  cudaGraphNode_t single_dep = nullptr;  // the one current dependency, if exactly one
+};
+PdlCapture pdl_capture_info(cudaStream_t s) {
+  PdlCapture c;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, &c.id, nullptr, &deps, &ndeps) != cudaSuccess) {
+    cudaGetLastError();
+    c.capturing = true;  // unknown: treat as a capture with no usable record
+    c.id = ~0ull;
+    return c;
+  }
+  c.capturing = st == cudaStreamCaptureStatusActive;
+  if (!c.capturing) c.id = 0;
+  if (c.capturing && ndeps == 1) c.single_dep = deps[0];
+  return c;
+}
+}  // namespace
+
+void pdl_note_other(cudaStream_t s) {
+  const PdlCapture c = pdl_capture_info(s);
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  auto it = g_pdl.find(PdlKey{s, c.id});
+  if (it != g_pdl.end()) it->second.valid = false;
+}
+
+// Whether an a2a launch touching xs / ys may load them before waiting for
+// the preceding launch on `s` (see above).
+static bool pdl_can_elide(cudaStream_t s, const PdlCapture& c, const PdlRange* xs, const PdlRange* ys, int n) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  auto it = g_pdl.find(PdlKey{s, c.id});
+  if (it == g_pdl.end() || !it->second.valid) return false;
+  const PdlRecord& r = it->second;
+  if (c.capturing && (c.single_dep == nullptr || c.single_dep != r.node)) return false;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < r.n; ++j) {
+      if (xs[i].overlaps(r.y[j]) || ys[i].overlaps(r.y[j]) || ys[i].overlaps(r.x[j])) return false;
+    }
+  }
+  return true;
+}
+
+static void pdl_record_a2a(cudaStream_t s, const PdlRange* xs, const PdlRange* ys, int n) {
+  const PdlCapture c = pdl_capture_info(s);  // after the launch: its node is the dependency
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  if (g_pdl.size() > 4096) g_pdl.clear();  // forgetting records only makes the check conservative
+  PdlRecord& r = g_pdl[PdlKey{s, c.id}];
+  r.valid = !c.capturing || c.single_dep != nullptr;
+  r.node = c.single_dep;
+  r.n = n;
+  for (int i = 0; i < n; ++i) {
+    r.x[i] = xs[i];
+    r.y[i] = ys[i];
+  }
+}
+
+static PdlRange byte_range(const void* base, int64_t rows, int64_t cols, int64_t ld, int64_t esz) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(base);
+  const int64_t bytes = rows > 0 ? ((rows - 1) * ld + cols) * esz : 0;
+  return PdlRange{lo, lo + static_cast<uintptr_t>(bytes)};
 }
 
 // Debug-only phase tracing (tools/profile_trace.py): a device buffer of
@@ -1153,6 +1273,7 @@ static void launch_stream_plan(const atmm_plan* p, int64_t layer, const void* x,
   sp.part = sc.part.p;
   sp.counter = sc.counter.p;
   sp.trace = g_trace;
+  pdl_note_other(stream);
   const cudaError_t e = launch_stream(di, sp, P, l.smem[di], stream);
   if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("stream bypass launch failed: ") + cudaGetErrorString(e));
 }
@@ -1264,6 +1385,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.mid = sc.mid.p;
       sp.counter = sc.counter.p;
       sp.trace = g_trace;
+      pdl_note_other(stream);
       const cudaError_t e = launch_split(sp.y_dtype, sp, P, g.split.smem_s, g.split.smem_e[sp.y_dtype], stream);
       if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
       continue;
@@ -1271,6 +1393,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
     BypassParams bp{};
     bp.tiles = p->d_tiles.p + g.tile_offset;
     bp.row_index = p->d_rows.p;
+    bp.tile_rows = p->d_tile_rows.p + g.tile_offset * kTileM;
     bp.x = static_cast<const uint16_t*>(x);
     bp.ldx = ldx;
     bp.y = y;
@@ -1319,17 +1442,28 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
       GroupArgs ga{};
       ga.num_tiles = static_cast<int32_t>(g.num_tiles);
       ga.count = count > 1 ? count : 1;
+      PdlRange xr[kMaxGroup], yr[kMaxGroup];
       for (int c = 0; c < ga.count; ++c) {
         const void* xc = count > 1 ? xs[c] : x;
         ga.x_map[c] = count > 1 ? cached_map(0, xc, p->n, reg->d_in, ldx) : tmap_x_get();
         ga.x[c] = xc;
         ga.y[c] = count > 1 ? ys[c] : y;
         ga.layer[c] = static_cast<int32_t>(count > 1 ? layers[c] : layer);
+        xr[c] = byte_range(xc, p->n, reg->d_in, ldx, 2);
+        yr[c] = byte_range(ga.y[c], p->n, reg->d_out, ldy, ysz);
       }
+      // X and Y of one call overlapping each other (in-place use) is fine for
+      // the predecessor check but not across calls of one grouped launch;
+      // the latter is the caller's contract (atmm_bypass_apply_group).
+      bp.early = (p->flags & ATMM_PLAN_NO_OVERLAP) ? 0 : (pdl_can_elide(stream, pdl_capture_info(stream), xr, yr, ga.count) ? 1 : 0);
       const cudaError_t e = launch_bypass_a2a(y_dtype, ga, bp, g.cluster, static_cast<int>(g.num_tiles), al.smem, stream);
       if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
+      pdl_record_a2a(stream, xr, yr, ga.count);
+      g_a2a_launches.fetch_add(1, std::memory_order_relaxed);
+      if (bp.early) g_a2a_early.fetch_add(1, std::memory_order_relaxed);
       continue;
     }
+    pdl_note_other(stream);
     const cudaError_t e = launch_bypass(y_dtype, tmap_x_get(), tmap_y_get(), bp, g.cluster, static_cast<int>(g.num_tiles), g.smem, stream);
     if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
   }
@@ -1759,10 +1893,16 @@ int atmm_plan_create_launch(atmm_registry* r, const int32_t* assignment, int64_t
   });
 }
 
+int atmm_overlap_stats(int64_t* a2a_launches, int64_t* early_launches) {
+  if (a2a_launches) *a2a_launches = g_a2a_launches.load();
+  if (early_launches) *early_launches = g_a2a_early.load();
+  return ATMM_OK;
+}
+
 int atmm_plan_set_flags(atmm_plan* p, uint32_t flags) {
   return guarded([&] {
     if (!p) fail(ATMM_ERR_CONFIG, "null plan");
-    if (flags & ~ATMM_PLAN_X_READY) fail(ATMM_ERR_CONFIG, "unknown plan flag");
+    if (flags & ~(ATMM_PLAN_X_READY | ATMM_PLAN_NO_OVERLAP)) fail(ATMM_ERR_CONFIG, "unknown plan flag");
     p->flags = flags;
   });
 }
@@ -2937,6 +3077,7 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
     CUtensorMap xm, xg;  // activations for the shrink / for the GEMM (64-wide K atoms under bk2)
     int cur = -1;  // -1: the caller's X
     if (f->sorted) {
+      pdl_note_other(st);
       CUDA_CHECK(launch_fwd_gather(static_cast<const uint16_t*>(x), ldx, f->buf[0].p, d, f->order.p, n, d, st));
       cur = 0;
       xm = f->bmap[0];
@@ -2982,12 +3123,15 @@ int atmm_forward_run(atmm_forward* f, const void* w, int64_t ldw, int64_t w_laye
       p.out_rows = last && f->sorted ? f->order.p : nullptr;
       if (bypass) {
         p.stages = f->stages_s;
+        pdl_note_other(st);
         CUDA_CHECK(launch_fwd_shrink(xm, p, f->smem_s, st));
       }
       p.stages = f->stages_g;
       if (f->pair) {
+        pdl_note_other(st);
         CUDA_CHECK(launch_fwd_gemm_pair(xg, wmap, f->amap, p, f->grid, f->smem_g, st));
       } else {
+        pdl_note_other(st);
         CUDA_CHECK(launch_fwd_gemm(xg, wmap, p, f->grid, f->smem_g, st));
       }
       cur = nxt;
@@ -3066,8 +3210,10 @@ void gemm_launch(const void* a, int64_t lda, const void* b, int64_t ldb, void* c
     p.out_f32 = c_dtype == ATMM_F32 ? 1 : 0;
     p.trace = g_trace;
     if (pair) {
+      pdl_note_other(st);
       CUDA_CHECK(launch_fwd_gemm_pair(amap, bmap, amap, p, gt.grid, gt.smem, st));
     } else {
+      pdl_note_other(st);
       CUDA_CHECK(launch_fwd_gemm(amap, bmap, p, gt.grid, gt.smem, st));
     }
   }

@@ -87,6 +87,14 @@ struct BypassParams {
   int32_t ypitch;
   int32_t gcols;        // output columns owned per epilogue thread (= expand MMAs per CTA: 1, 2, 4, 8)
   int32_t x_ready;      // 1: X is not written by the preceding launch (gathered before griddepcontrol.wait)
+  // atmm_bypass_a2a_kernel only: 1 = the launcher proved that the preceding
+  // launch on the stream (the only one that can still be running, see the
+  // wait-before-trigger protocol in kernels.cu) touches none of this launch's
+  // X / Y bytes -> X and Y are loaded before griddepcontrol.wait.
+  int32_t early;
+  // atmm_bypass_a2a_kernel only: [tile][kTileM] row indices of each tile
+  // (rows past the tile's end repeat its last row), this launch's tiles.
+  const int32_t* tile_rows;
 };
 
 constexpr int kTraceEvents = 32;

@@ -908,7 +908,15 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
   const uint32_t C = cluster_nctarank();
   const uint32_t crank = cluster_ctarank();
   const int call = static_cast<int>(cluster_id_x()) / ga.num_tiles;  // grouped launch: call, tile
-  const TileDesc tile = p.tiles[static_cast<int>(cluster_id_x()) - call * ga.num_tiles];
+  const int tidx = static_cast<int>(cluster_id_x()) - call * ga.num_tiles;
+  // The tile's padded row list (plan table, independent of the descriptor
+  // load: one memory round trip in the prologue, not two).
+  int32_t my_rows[kTileM / 32];
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < kTileM / 32; ++q) my_rows[q] = p.tile_rows[tidx * kTileM + q * 32 + static_cast<int>(lane)];
+  }
+  const TileDesc tile = p.tiles[tidx];
   const CUtensorMap& tmap_x = ga.x_map[call];
   const int layer = ga.layer[call];
   uint8_t* const ycall = static_cast<uint8_t*>(ga.y[call]);
@@ -950,7 +958,8 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
       const uint32_t cnt = (b == 2 * S || b == 2 * S + 4) ? 128u : (b == 2 * S + 1 ? 32u : 1u);
       mbar_init(bars + b, cnt);
     }
-    for (int i = static_cast<int>(lane); i < kTileM; i += 32) rows_s[i] = p.row_index[tile.row_begin + min(i, rows - 1)];
+#pragma unroll
+    for (int q = 0; q < kTileM / 32; ++q) rows_s[q * 32 + lane] = my_rows[q];
     __syncwarp();
     if (lane == 0) mbar_arrive_expect_tx(red_full, (C - 1) * block_bytes);
     fence_mbar_init();
@@ -962,10 +971,16 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
   const uint32_t tmem_base = *tmem_slot;
   cluster_arrive_relaxed();  // phase 1: barrier inits (fenced above) visible to peers
   if (threadIdx.x == 0) TRACE(1);
-  // Release the next launch now (every thread): its CTAs take the free SM
-  // slots and run their prologue and weight prefetch under this launch; they
-  // read X / Y only after their own griddepcontrol.wait (this grid complete).
-  griddep_launch_dependents();
+  // PDL protocol (wait before trigger): ONE warp per CTA (X producer A)
+  // releases the next launch (griddepcontrol.launch_dependents: one warp
+  // suffices and is released faster than a single lane,
+  // tools/ubench/pdl_trigger.cu) and only after its own
+  // griddepcontrol.wait returned, i.e. once the PRECEDING grid is complete;
+  // no other thread executes the release.  The next launch's
+  // CTAs then take free SM slots and run their prologue, weight prefetch (and,
+  // when the launcher elided the dependency, their X / Y loads) under this
+  // grid, while at most ONE earlier grid -- this one -- can still be running:
+  // the invariant the launcher's hazard check (device.cu pdl_can_elide) rests on.
 
   const uint32_t ybuf_s = smem_u32(ybuf);
   const int ngroups = (rows + 3) / 4;
@@ -977,10 +992,54 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     const int g_hi = xa ? ngroups0 : ngroups;
     const uint32_t b_bytes = static_cast<uint32_t>(r_pad) * kBK * 2u;
     const uint32_t a_bytes = static_cast<uint32_t>(ngroups) * 512u;
-    if (xa && lane == 0) {
-      tma_prefetch_desc(&tmap_x);
+    if (xa && lane == 0) tma_prefetch_desc(&tmap_x);
+    if (!p.x_ready && !p.early) griddep_wait();  // X may be produced by the previous kernel
+    if (xa && lane == 0) TRACE(15);
+    // (group, K block) gather4 requests spread over all 32 lanes, one ring
+    // round at a time, so a round goes out in one parallel burst.  In round
+    // q >= 1 a lane first waits for the MMA to drain its stage (completion q
+    // of empty[stage]: the warp finished round q - 1, which waited for
+    // completion q - 1 of the same stage, so the parity wait cannot alias),
+    // and the lane of the warp's first group re-arms the stage (down^T + tx).
+    const int ng = g_hi - g_lo;
+    const int nkbc = kb_hi - kb_lo;
+    for (int q0 = 0; ng > 0 && q0 < nkbc; q0 += S) {
+      const int nq = min(S, nkbc - q0);
+      const int round = q0 / S;
+      for (int j = static_cast<int>(lane); j < ng * nq; j += 32) {
+        const int kbi = q0 + j / ng;
+        const int g = g_lo + j % ng;
+        const int stage = kbi - q0;
+        uint8_t* st = ring + static_cast<size_t>(stage) * p.stage_bytes;
+        if (round > 0) {
+          mbar_wait(&empty[stage], static_cast<uint32_t>(round - 1) & 1u);
+          if (xa && g == g_lo) {
+            mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+            bulk_g2s(st + p.a_bytes, down_t + static_cast<int64_t>(kb_lo + kbi) * r_pad * kBK, b_bytes, &full[stage]);
+          }
+        }
+        const int r0 = g * 4;
+        tma_gather4(st + g * 512u, &tmap_x, &full[stage], (kb_lo + kbi) * kBK, rows_s[min(r0, rows - 1)],
+                    rows_s[min(r0 + 1, rows - 1)], rows_s[min(r0 + 2, rows - 1)], rows_s[min(r0 + 3, rows - 1)]);
+      }
+      __syncwarp();
+    }
+    if (xa && lane == 0) TRACE(2);
+    if (xa) {  // the CTA's trigger (one warp), after its wait (see the protocol above)
+      griddep_wait();
+      if (lane == 31) TRACE(22);
+      griddep_launch_dependents();
+    }
+    __syncwarp();
+    cluster_wait();
+  } else if (warp == kWarpMMA) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
       // Weights do not depend on the previous kernel: the first ring round of
-      // down^T blocks goes out before griddepcontrol.wait.
+      // down^T blocks goes out at once (this warp is idle until a stage lands)
+      // and arms each stage for its X gathers too.
+      const uint32_t b_bytes = static_cast<uint32_t>(r_pad) * kBK * 2u;
+      const uint32_t a_bytes = static_cast<uint32_t>(ngroups) * 512u;
       for (int kb = kb_lo; kb < min(kb_hi, kb_lo + S); ++kb) {
         const int st = kb - kb_lo;
         mbar_arrive_expect_tx(&full[st], a_bytes + b_bytes);
@@ -988,38 +1047,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
                  down_t + static_cast<int64_t>(kb) * r_pad * kBK, b_bytes, &full[st]);
       }
     }
-    const int g = g_lo + static_cast<int>(lane);
-    int32_t gr[4] = {0, 0, 0, 0};
-    if (g < g_hi) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) gr[q] = rows_s[min(g * 4 + q, rows - 1)];
-    }
-    if (!p.x_ready) griddep_wait();  // X may be produced by the previous kernel
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int kb = kb_lo; kb < kb_hi; ++kb) {
-      uint8_t* st = ring + static_cast<size_t>(stage) * p.stage_bytes;
-      if (kb - kb_lo >= S) {  // ring reuse: wait for the MMA to drain the stage
-        if (lane == 0) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          if (xa) {
-            mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
-            bulk_g2s(st + p.a_bytes, down_t + static_cast<int64_t>(kb) * r_pad * kBK, b_bytes, &full[stage]);
-          }
-        }
-        __syncwarp();
-      }
-      if (g < g_hi) tma_gather4(st + g * 512u, &tmap_x, &full[stage], kb * kBK, gr[0], gr[1], gr[2], gr[3]);
-      if (++stage == S) {
-        stage = 0;
-        phase ^= 1u;
-      }
-    }
-    if (xa && lane == 0) TRACE(2);
     __syncwarp();
-    cluster_wait();
-  } else if (warp == kWarpMMA) {
-    // ===================== MMA issuer =====================
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t idesc_s = idesc_bf16(kTileM, static_cast<uint32_t>(r_pad));
@@ -1075,7 +1103,8 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     // ===================== Y slice -> shared memory (cp.async) =====================
     // Issued by this otherwise idle warp so that the proxy fences of warps
     // 0..3 never wait behind these HBM reads.
-    griddep_wait();
+    if (!p.early) griddep_wait();
+    if (lane == 0) TRACE(16);
     const int cpr = ncols * kEsz / 16;  // 16-byte chunks per row
     const uint8_t* ybase = ycall + static_cast<int64_t>(n_lo) * kEsz;
     const int64_t ldy_b = p.ldy * kEsz;
@@ -1124,6 +1153,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
           tmem_ld16(tmem_base + ((quad * 32u) << 16) + g, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
         }
         tmem_wait_ld();
+        if (tracer && g == 0) TRACE(23);
         if (row < rows) {
           const int nc = min(32, r_pad - g);
           const uint32_t dst = my_block + static_cast<uint32_t>((row * r_pad + g) * 4);
@@ -1134,10 +1164,14 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
         }
       }
     }
+    if (tracer) TRACE(17);
     tc_fence_before();
     fence_proxy_async_smem();  // the block is read by the bulk-copy engine
+    if (tracer) TRACE(18);
     cluster_wait();            // peers' barriers are initialized
+    if (tracer) TRACE(19);
     named_bar_sync(1, 128);
+    if (tracer) TRACE(20);
     if (threadIdx.x == 0) {
       for (uint32_t cc = 1; cc < C; ++cc) {
         const uint32_t peer = (crank + cc) % C;
@@ -1187,7 +1221,6 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     fence_proxy_async_smem();  // mid (generic writes) -> the tensor core (async proxy)
     mbar_arrive(mid_ready);
     if (tracer) TRACE(8);
-    griddep_launch_dependents();
   }
 
   // Every peer has received all its partials once its red_full completed:
@@ -1230,6 +1263,7 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     tmem_dealloc(tmem_base, p.tmem_cols);
   }
   cluster_wait();
+  if (threadIdx.x == 0) TRACE(24);
 }
 
 // =========================================================================

@@ -90,15 +90,17 @@ def test_paths_agree_closely(gpu, atmm, oracle):
 
 
 def test_split_path_is_chosen_for_large_tiles(gpu, atmm, oracle):
+    """The built-in heuristic's path choice (the packaged table may pick
+    otherwise for shapes it profiled: it is checked in test_host.py)."""
     d_in, d_out, ranks, lens = CASES[3]
     facs, assignment, _, _ = _inputs(oracle, d_in, d_out, ranks, lens)
     reg = atmm.AdapterRegistry(1, d_in, d_out)
     for a, (down, up) in facs.items():
         reg.put(a, down, up)
-    groups = atmm.BypassPlan(reg, assignment).describe()
+    groups = atmm.BypassPlan(reg, assignment, use_default_table=False).describe()
     assert all(g["path_bf16"] == "split" for g in groups), groups
     small = np.repeat(np.asarray(sorted(ranks), np.int32), 16)
-    groups = atmm.BypassPlan(reg, small).describe()
+    groups = atmm.BypassPlan(reg, small, use_default_table=False).describe()
     assert all(g["path_bf16"] == "a2a" for g in groups), groups
 
 

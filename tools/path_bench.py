@@ -28,6 +28,11 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--x-ready", action="store_true")
+    ap.add_argument("--launches", default=None,
+                    help="';'-separated tile_m,cluster,bn,stages,path launches to force (instead of --paths)")
+    ap.add_argument("--no-overlap", action="store_true", help="ATMM_PLAN_NO_OVERLAP on every plan")
+    ap.add_argument("--chain", action="store_true",
+                    help="dependent steps: step i+1 reads step i's Y as its X (d_in == d_out)")
     args = ap.parse_args()
     import torch
 
@@ -49,8 +54,12 @@ def main():
         ys = [torch.empty(w.tokens, w.d_out, dtype=torch.bfloat16, device=dev).uniform_(-1, 1) for _ in range(layers)]
         ref = None
         y0 = ys[0].clone()
-        for path in args.paths.split(","):
-            if path == "auto":
+        variants = args.paths.split(",") if not args.launches else [
+            [int(v) for v in l.split(",")] for l in args.launches.split(";")]
+        for path in variants:
+            if isinstance(path, list):
+                plan = atmm.BypassPlan(reg, w.assignment, launch=path)
+            elif path == "auto":
                 plan = atmm.BypassPlan(reg, w.assignment)
             else:
                 ranks = sorted(set(w.ranks.values()))
@@ -59,6 +68,7 @@ def main():
                 launch[4] = PATHS[path]
                 plan = atmm.BypassPlan(reg, w.assignment, launch=launch)
             plan.set_x_ready(args.x_ready)
+            plan.set_overlap(not args.no_overlap)
             desc = plan.describe()
             stream = torch.cuda.Stream(device=dev)
             # correctness spot check vs the first path (same inputs, layer 0)
@@ -77,7 +87,10 @@ def main():
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
                 for i in range(args.steps):
-                    plan.apply(xs[i % layers], ys[i % layers], layer=i % layers, stream=stream)
+                    if args.chain:  # X of step i+1 = Y of step i
+                        plan.apply(ys[i % layers], ys[(i + 1) % layers], layer=i % layers, stream=stream)
+                    else:
+                        plan.apply(xs[i % layers], ys[i % layers], layer=i % layers, stream=stream)
             g.replay()
             torch.cuda.synchronize()
             times = []
@@ -105,7 +118,7 @@ def main():
                 torch.cuda.synchronize()
                 iso.append(e0.elapsed_time(e1) * 1e3)
             del flush
-            print(json.dumps({"config": name, "path": path, "us_per_step": round(us, 3), "all": [round(t, 3) for t in times],
+            print(json.dumps({"config": name, "path": path, "chain": args.chain, "overlap": not args.no_overlap, "us_per_step": round(us, 3), "all": [round(t, 3) for t in times],
                               "frac": round(step_bytes / (us * 1e-6) / 6552.6e9, 3),
                               "isolated_us": round(float(np.median(iso)), 3),
                               "max_abs_diff_vs_first": diff, "launches": plan.stats()[0],
