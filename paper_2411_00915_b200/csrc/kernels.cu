@@ -1172,11 +1172,9 @@ __global__ void __launch_bounds__(kBypassThreads, 2)
     if (tracer) TRACE(19);
     named_bar_sync(1, 128);
     if (tracer) TRACE(20);
-    if (threadIdx.x == 0) {
-      for (uint32_t cc = 1; cc < C; ++cc) {
-        const uint32_t peer = (crank + cc) % C;
-        bulk_s2cluster(map_cta(my_block, peer), my_block, block_bytes, map_cta(smem_u32(red_full), peer));
-      }
+    if (threadIdx.x < C - 1) {  // one bulk DSMEM push per peer, issued by C - 1 lanes in parallel
+      const uint32_t peer = (crank + 1 + threadIdx.x) % C;
+      bulk_s2cluster(map_cta(my_block, peer), my_block, block_bytes, map_cta(smem_u32(red_full), peer));
     }
     if (tracer) TRACE(6);
     // (c) fixed-order sum of the C partials -> bf16 mid (local)
