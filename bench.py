@@ -538,9 +538,15 @@ def impl_ours_bypass(args, w):
 
     # Capture exactly K steps into one graph.
     g = torch.cuda.CUDAGraph()
+    ov0 = atmm.overlap_stats()
     with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
         for i in range(args.steps):
             step(i, stream)
+    ov1 = atmm.overlap_stats()
+    overlap = {"a2a_launches": ov1[0] - ov0[0], "early_launches": ov1[1] - ov0[1],
+               "rule": "an all-to-all launch loads X / Y under its predecessor only when the launcher proved the "
+                       "predecessor (the one grid that can still run) touches disjoint bytes (include/atmm_b200.h "
+                       "ATMM_PLAN_NO_OVERLAP)"}
     # Soak graph for clock steady state.
     soak_steps = min(args.steps, 4 * layers)
     gs = torch.cuda.CUDAGraph()
@@ -598,6 +604,36 @@ def impl_ours_bypass(args, w):
                "roofline_frac": step_bytes / (xms * 1e-3 / args.steps) / 1e9 / measured_peaks()[0],
                "note": "same steps with atmm_plan_set_flags(ATMM_PLAN_X_READY): X gathered under the previous "
                        "launch's tail; not the headline"}
+
+    # ---- dependent chain: step i+1 reads step i's output as its X (a layer
+    # forward's data flow).  The launcher's hazard check then keeps the full
+    # grid dependency (no X / Y loads under the predecessor): the number a
+    # caller with strictly dependent steps sees.  Side measurement ----
+    chain = None
+    if w.d_in == w.d_out:
+        gc = torch.cuda.CUDAGraph()
+        early0 = atmm.overlap_stats()
+        with torch.cuda.graph(gc, stream=stream, capture_error_mode="thread_local"):
+            for i in range(args.steps):
+                plan.apply(ys[i % layers], ys[(i + 1) % layers], layer=i % layers, scale=1.0, stream=stream)
+        early1 = atmm.overlap_stats()
+        gc.replay()
+        torch.cuda.synchronize()
+        c0 = torch.cuda.Event(enable_timing=True)
+        c1 = torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            c0.record(stream)
+            gc.replay()
+            c1.record(stream)
+        torch.cuda.synchronize()
+        cms = max_over_ranks(c0.elapsed_time(c1), world)
+        chain = {"us_per_batch": cms * 1e3 / args.steps,
+                 "value": job_flops * args.steps / (cms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                 "roofline_frac": step_bytes / (cms * 1e-3 / args.steps) / 1e9 / measured_peaks()[0],
+                 "early_launches": early1[1] - early0[1],
+                 "note": "X of step i+1 = Y of step i: every launch keeps the full grid dependency; not the headline"}
 
     # ---- single-launch latency: one eager call bracketed by
     # events on an idle GPU, median of 20 (includes the launch itself) ----
@@ -730,6 +766,8 @@ def impl_ours_bypass(args, w):
             "us_per_batch": ms_per_step * 1e3,
             "single_launch_us": single_launch_us,
             "x_ready": x_ready,
+            "dependent_chain": chain,
+            "overlap": overlap,
             "config": bench_config(w_job, world),
             "sharding": {"mode": "strong" if args.strong else "weak", "global_tokens": int(len(glob)),
                          "global_adapters": len(granks), "rank0_tokens": int(w.tokens),
@@ -747,7 +785,9 @@ def impl_ours_bypass(args, w):
                                             "one launch alone)",
                          "peak_kind": peak_kind, "kernel": " + ".join(kernel_names[p] for p in paths),
                          "scope": f"one step = {launches_per_step} launch(es); bytes and time of the whole step "
-                                  f"(pipelined: consecutive steps overlap their prologues through PDL)",
+                                  f"(pipelined: consecutive independent steps overlap through PDL -- prologues, and "
+                                  f"for the all-to-all kernel the X / Y loads once the launcher proved the preceding "
+                                  f"step disjoint; see dependent_chain for strictly dependent steps)",
                          "step_us": kernel_us, "algorithmic_bytes_per_step": step_bytes},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -164,8 +164,13 @@ int atmm_registry_create(int device, int64_t num_layers, int64_t d_in, int64_t d
 void atmm_registry_destroy(atmm_registry* r);
 /* LoraAdapter(...) (adapter.hpp:26-51) + AdapterSet::emplace: host fp32
  * factors down [L][d_in x r] and up [L][r x d_out]; scale s multiplies the
- * adapter's contribution (the reference's implicit s = 1).  Requires
- * 1 <= r <= 128 (the reference additionally requires r < hidden).
+ * adapter's contribution (the reference's implicit s = 1).  Any rank
+ * 1 <= r < hidden (adapter.hpp:30-31; r <= 128 is also accepted on smaller
+ * layers): r <= 128 is one slot; a larger rank is stored as 128-rank chunk
+ * slots that every bypass applies as extra passes over the same Y rows
+ * (separate launches, one bf16 rounding of Y per pass) and merge / delta_w
+ * sum chunk by chunk.  Rank-chunked adapters are not taken by put_async,
+ * put_combined, precise registries or the fused layer forward (ConfigError).
  * Re-putting an id replaces it. */
 int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const float* down,
                       const float* up, float scale);
@@ -189,7 +194,9 @@ int atmm_registry_remove(atmm_registry* r, int32_t adapter_id);
  *   down = [down_1 | down_2 | ...],  up = [s_1 sign_1 up_1 ; s_2 sign_2 up_2 ; ...],
  * so ONE fused bypass adds sum_i sign_i s_i (x.down_i).up_i with a single
  * rounding into Y (e.g. parts {a, merged} signs {+1, -1}: own adapter minus
- * the cancel branch of the merged adapter).  Sum of padded ranks <= 128.
+ * the cancel branch of the merged adapter).  Sum of padded ranks <= 128
+ * (ConfigError otherwise: the Python MixturePlan then runs those guests in
+ * the two-pass form, own branch then cancel branch).
  * Signs / scales of +-1 (and powers of two) are folded exactly. */
 int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts, const int32_t* part_ids,
                                const float* part_signs);

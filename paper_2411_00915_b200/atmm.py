@@ -588,23 +588,42 @@ class MixturePlan:
             raise ModeError("mixture integrity: subtraction branch missing (merged adapter not in the registry)")
         combos = registry.__dict__.setdefault("_combined", {})
         guest = np.nonzero(a != merged_id)[0].astype(np.int32)
-        virt = np.empty(guest.size, np.int32)
-        for i, row in enumerate(guest):
+        fused_rows, fused_virt, two_rows, two_ids = [], [], [], []
+        for row in guest:
             key = (int(a[row]), int(merged_id))
             if key not in combos:
                 if key[0] not in registry:
                     raise UnknownAdapterError(f"unknown adapter id {key[0]}")
                 vid = -(1 << 20) - len(combos)
-                registry.put_combined(vid, [(key[0], 1.0), (key[1], -1.0)])
-                combos[key] = vid
-            virt[i] = combos[key]
+                try:
+                    registry.put_combined(vid, [(key[0], 1.0), (key[1], -1.0)])
+                    combos[key] = vid
+                except ConfigError:
+                    # combined rank above 128 (or a rank-chunked part): these
+                    # guests take the two-pass form, own branch then cancel
+                    combos[key] = None
+            if combos[key] is None:
+                two_rows.append(row)
+                two_ids.append(key[0])
+            else:
+                fused_rows.append(row)
+                fused_virt.append(combos[key])
         self.n = int(a.size)
         self.guest_rows = guest
-        self.plan = BypassPlan(registry, virt, table, rows=guest, n_rows=self.n) if guest.size else None
+        self.plan = (BypassPlan(registry, fused_virt, table, rows=fused_rows, n_rows=self.n)
+                     if fused_rows else None)
+        self.two_pass_rows = np.asarray(two_rows, np.int32)
+        self.own = self.cancel = None
+        if two_rows:
+            self.own = BypassPlan(registry, two_ids, table, rows=two_rows, n_rows=self.n)
+            self.cancel = BypassPlan(registry, [int(merged_id)] * len(two_rows), table, rows=two_rows, n_rows=self.n)
 
     def apply(self, x, y, layer: int = 0, scale: float = 1.0, stream=None) -> None:
         if self.plan is not None:
             self.plan.apply(x, y, layer, scale, stream)
+        if self.own is not None:
+            self.own.apply(x, y, layer, scale, stream)
+            self.cancel.apply(x, y, layer, -scale, stream)
 
 
 class GemmOpts(ctypes.Structure):
@@ -642,6 +661,9 @@ class LayerForward:
         """opts: explicit GEMM tile options {pair, bn, kz, ks, stages}
         (atmm_gemm_opts), automatic when omitted."""
         if isinstance(plan, MixturePlan):
+            if plan.own is not None:
+                raise ConfigError("the fused layer forward needs every mixture guest in one combined slot "
+                                  "(combined rank <= 128); apply the MixturePlan after the base GEMM instead")
             n = plan.n if n is None else n
             if hidden_dim is None and plan.plan is not None:
                 hidden_dim = plan.plan.registry.d_in

@@ -277,6 +277,7 @@ struct Slot {
   int32_t id = -1;
   int64_t rank = 0, r_pad = 0;
   int64_t alg_rank = 0;  // FLOP accounting rank: the true rank (a combined slot: the sum of its parts')
+  int64_t total_rank = 0;  // the adapter's rank (> rank for chunk 0 of an adapter above kMaxRank)
   float scale = 1.0f;
   uint16_t* down_t = nullptr;
   uint16_t* up_t = nullptr;
@@ -351,6 +352,37 @@ struct atmm_registry {
     auto it = slot_of.find(id);
     if (it == slot_of.end()) fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(id));
     return slots[static_cast<size_t>(it->second)];
+  }
+  // Adapters above kMaxRank: chunk 0 is slot_of[id], chunks 1.. (ranks
+  // [128 c, 128 c + 128)) live in these slots, each applied as its own pass.
+  std::map<int32_t, std::vector<int>> extra;
+  int num_chunks(int32_t id) const {
+    auto it = extra.find(id);
+    return 1 + (it == extra.end() ? 0 : static_cast<int>(it->second.size()));
+  }
+  const Slot& chunk(int32_t id, int c) const { return c == 0 ? at(id) : slots[static_cast<size_t>(extra.at(id)[c - 1])]; }
+  void require_unchunked(int32_t id, const char* what) const {
+    if (num_chunks(id) > 1) {
+      fail(ATMM_ERR_CONFIG, std::string(what) + ": adapter " + std::to_string(id) + " has rank " +
+                                std::to_string(at(id).total_rank) + " > " + std::to_string(kMaxRank) +
+                                " (rank-chunked adapters are served by BypassPlan / merge / delta_w only)");
+    }
+  }
+  int free_index() {
+    for (size_t i = 0; i < slots.size(); ++i) {
+      if (!slots[i].live) return static_cast<int>(i);
+    }
+    slots.emplace_back();
+    return static_cast<int>(slots.size()) - 1;
+  }
+  void drop_extra(int32_t id) {
+    auto it = extra.find(id);
+    if (it == extra.end()) return;
+    for (int idx : it->second) {
+      free_slot(slots[static_cast<size_t>(idx)]);
+      slots[static_cast<size_t>(idx)] = Slot{};
+    }
+    extra.erase(it);
   }
 };
 
@@ -715,6 +747,10 @@ struct atmm_plan {
   int64_t total_ctas = 0;
   uint64_t flops = 0;  // algorithmic FLOPs of one apply (flops.hpp accounting)
   uint32_t flags = 0;  // ATMM_PLAN_*
+  // Adapters above kMaxRank: pass c (>= 1) applies rank chunk c of every
+  // routed row whose adapter has one, as a row-mapped plan over the same X / Y
+  // (separate launches: the passes update the same Y rows).
+  std::vector<std::unique_ptr<atmm_plan>> passes;
 };
 
 namespace atmm {
@@ -915,7 +951,7 @@ static void build_stream(atmm_plan& plan, const std::vector<TileDesc>& tiles, co
 static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* assignment,
                                              int64_t n, const TilingTable* table,
                                              const LaunchCfg* forced, const int32_t* row_map = nullptr,
-                                             int64_t n_rows = -1) {
+                                             int64_t n_rows = -1, int chunk = 0) {
   auto plan = std::make_unique<atmm_plan>();
   plan->reg = reg;
   plan->generation = reg->generation;
@@ -935,7 +971,7 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     const int32_t id = plan->bp.seg_adapter[s];
     auto it = reg->slot_of.find(id);
     if (it == reg->slot_of.end()) fail(ATMM_ERR_UNKNOWN_ADAPTER, "unknown adapter id " + std::to_string(id));
-    const Slot& sl = reg->slots[static_cast<size_t>(it->second)];
+    const Slot& sl = reg->chunk(id, chunk);
     const int64_t b = plan->bp.seg_offsets[s], e = plan->bp.seg_offsets[s + 1];
     const int64_t ns = e - b;
     plan->flops += 2ull * static_cast<uint64_t>(ns) * static_cast<uint64_t>(sl.alg_rank) *
@@ -1104,6 +1140,23 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
   plan->d_tiles.alloc(all_tiles.size());
   CUDA_CHECK(cudaMemcpy(plan->d_tiles.p, all_tiles.data(), all_tiles.size() * sizeof(TileDesc),
                         cudaMemcpyHostToDevice));
+  if (chunk == 0 && !reg->extra.empty()) {
+    int max_ch = 1;
+    for (size_t s = 0; s < S; ++s) max_ch = std::max(max_ch, reg->num_chunks(plan->bp.seg_adapter[s]));
+    for (int c = 1; c < max_ch; ++c) {
+      std::vector<int32_t> asg, map;
+      for (int64_t i = 0; i < n; ++i) {
+        if (reg->num_chunks(assignment[i]) > c) {
+          asg.push_back(assignment[i]);
+          map.push_back(row_map ? row_map[i] : static_cast<int32_t>(i));
+        }
+      }
+      auto ps = build_plan(reg, asg.data(), static_cast<int64_t>(asg.size()), table, forced, map.data(), plan->n, c);
+      plan->flops += ps->flops;
+      plan->total_ctas += ps->total_ctas;
+      plan->passes.push_back(std::move(ps));
+    }
+  }
   return plan;
 }
 
@@ -1280,9 +1333,21 @@ static void launch_stream_plan(const atmm_plan* p, int64_t layer, const void* x,
 
 // count > 1: independent calls (xs[c], ys[c], layers[c]) of one plan; the
 // all-to-all kernel runs them as ONE launch, other paths launch per call.
+static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
+                       int64_t ldy, int y_dtype, float scale, cudaStream_t stream, int count = 1,
+                       const int64_t* layers = nullptr, const void* const* xs = nullptr, void* const* ys = nullptr);
+// One apply: the plan, then its rank-chunk passes (atmm_plan::passes) in
+// stream order over the same X / Y.
 static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
                        int64_t ldy, int y_dtype, float scale, cudaStream_t stream, int count = 1,
                        const int64_t* layers = nullptr, const void* const* xs = nullptr, void* const* ys = nullptr) {
+  apply_pass(p, layer, x, ldx, y, ldy, y_dtype, scale, stream, count, layers, xs, ys);
+  for (const auto& ps : p->passes) apply_pass(ps.get(), layer, x, ldx, y, ldy, y_dtype, scale, stream, count, layers, xs, ys);
+}
+
+static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
+                       int64_t ldy, int y_dtype, float scale, cudaStream_t stream, int count,
+                       const int64_t* layers, const void* const* xs, void* const* ys) {
   const atmm_registry* reg = p->reg;
   if (p->generation != reg->generation) fail(ATMM_ERR_CONFIG, "plan is stale: the registry changed after the plan was built");
   if (layer < 0 || layer >= reg->L) {
@@ -1300,7 +1365,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
   if (use_stream(*p, y_vec != 0)) {
     if (count > 1) {
       if (count > kMaxGroup || !layers || !xs || !ys) fail(ATMM_ERR_CONFIG, "grouped apply: 1..8 calls with layers, xs, ys");
-      for (int c = 0; c < count; ++c) apply_plan(p, layers[c], xs[c], ldx, ys[c], ldy, y_dtype, scale, stream);
+      for (int c = 0; c < count; ++c) apply_pass(p, layers[c], xs[c], ldx, ys[c], ldy, y_dtype, scale, stream);
       return;
     }
     launch_stream_plan(p, layer, x, ldx, y, ldy, y_dtype, scale, stream);
@@ -1317,7 +1382,7 @@ static void apply_plan(const atmm_plan* p, int64_t layer, const void* x, int64_t
     }
     for (const LaunchGroup& g : p->groups) all_a2a = all_a2a && choose_path(g, y_dtype, true) == BypassPath::kA2a;
     if (!all_a2a) {
-      for (int c = 0; c < count; ++c) apply_plan(p, layers[c], xs[c], ldx, ys[c], ldy, y_dtype, scale, stream);
+      for (int c = 0; c < count; ++c) apply_pass(p, layers[c], xs[c], ldx, ys[c], ldy, y_dtype, scale, stream);
       return;
     }
   }
@@ -1597,29 +1662,54 @@ int atmm_registry_put(atmm_registry* r, int32_t adapter_id, int64_t rank, const 
                       const float* up, float scale) {
   return guarded([&] {
     if (!r) fail(ATMM_ERR_CONFIG, "null registry");
-    if (rank < 1 || rank > kMaxRank) fail(ATMM_ERR_CONFIG, "adapter rank must be in [1, 128]");
-    if (!down || !up) fail(ATMM_ERR_SHAPE, "null factors");
-    DeviceGuard g(r->device);
-    const int64_t r_pad = round_up(rank, 16);
-    const size_t dn = static_cast<size_t>(r->d_in_pad * r_pad);
-    const size_t un = static_cast<size_t>(r->d_out_pad * r_pad);
-    std::vector<uint16_t> hd(dn * static_cast<size_t>(r->L)), hu(un * static_cast<size_t>(r->L));
-    for (int64_t l = 0; l < r->L; ++l) {
-      pack_down_t(down + l * r->d_in * rank, r->d_in, rank, rank, r->d_in_pad, r_pad, hd.data() + l * dn);
-      pack_up_t(up + l * rank * r->d_out, rank, r->d_out, r->d_out, r->d_out_pad, r_pad, hu.data() + l * un);
+    // The reference accepts any rank below the hidden size (adapter.hpp:30-31);
+    // ranks above kMaxRank are stored as 128-rank chunk slots.
+    if (rank < 1 || (rank > kMaxRank && rank >= std::min(r->d_in, r->d_out))) {
+      fail(ATMM_ERR_CONFIG, "adapter rank must be >= 1 and < the hidden size");
     }
-    Slot s;
-    s.id = adapter_id;
-    s.rank = rank;
-    s.r_pad = r_pad;
-    s.alg_rank = rank;
-    s.scale = scale;
-    s.live = true;
-    CUDA_CHECK(cudaMalloc(&s.down_t, hd.size() * 2));
-    CUDA_CHECK(cudaMalloc(&s.up_t, hu.size() * 2));
-    CUDA_CHECK(cudaMemcpy(s.down_t, hd.data(), hd.size() * 2, cudaMemcpyHostToDevice));
-    CUDA_CHECK(cudaMemcpy(s.up_t, hu.data(), hu.size() * 2, cudaMemcpyHostToDevice));
+    if (!down || !up) fail(ATMM_ERR_SHAPE, "null factors");
+    const int nch = static_cast<int>((rank + kMaxRank - 1) / kMaxRank);
+    if (nch > 1 && r->precise) fail(ATMM_ERR_CONFIG, "a precise registry takes ranks <= 128");
+    DeviceGuard g(r->device);
+    // One slot per 128-rank chunk (columns [128 c, ..) of down, rows of up).
+    std::vector<Slot> made;
+    for (int c = 0; c < nch; ++c) {
+      const int64_t r0 = int64_t(c) * kMaxRank, rc = std::min<int64_t>(kMaxRank, rank - r0);
+      const int64_t r_pad = round_up(rc, 16);
+      const size_t dn = static_cast<size_t>(r->d_in_pad * r_pad);
+      const size_t un = static_cast<size_t>(r->d_out_pad * r_pad);
+      std::vector<uint16_t> hd(dn * static_cast<size_t>(r->L)), hu(un * static_cast<size_t>(r->L));
+      for (int64_t l = 0; l < r->L; ++l) {
+        pack_down_t(down + l * r->d_in * rank + r0, r->d_in, rc, rank, r->d_in_pad, r_pad, hd.data() + l * dn);
+        pack_up_t(up + l * rank * r->d_out + r0 * r->d_out, rc, r->d_out, r->d_out, r->d_out_pad, r_pad,
+                  hu.data() + l * un);
+      }
+      Slot s;
+      s.id = adapter_id;
+      s.rank = rc;
+      s.r_pad = r_pad;
+      s.alg_rank = rc;
+      s.total_rank = rank;
+      s.scale = scale;
+      s.live = true;
+      CUDA_CHECK(cudaMalloc(&s.down_t, hd.size() * 2));
+      CUDA_CHECK(cudaMalloc(&s.up_t, hu.size() * 2));
+      CUDA_CHECK(cudaMemcpy(s.down_t, hd.data(), hd.size() * 2, cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaMemcpy(s.up_t, hu.data(), hu.size() * 2, cudaMemcpyHostToDevice));
+      made.push_back(s);
+    }
+    Slot s = made[0];
     if (r->precise) build_precise_host(r, s, down, up);
+    r->drop_extra(adapter_id);
+    if (nch > 1) {
+      std::vector<int> idx;
+      for (int c = 1; c < nch; ++c) {
+        const int i = r->free_index();
+        r->slots[static_cast<size_t>(i)] = made[static_cast<size_t>(c)];
+        idx.push_back(i);
+      }
+      r->extra[adapter_id] = idx;
+    }
     auto it = r->slot_of.find(adapter_id);
     if (it != r->slot_of.end()) {
       Slot& old = r->slots[static_cast<size_t>(it->second)];
@@ -1653,17 +1743,20 @@ int atmm_registry_put_combined(atmm_registry* r, int32_t new_id, int64_t n_parts
     std::vector<Slot> parts;
     int64_t r_c = 0, alg = 0;
     for (int64_t i = 0; i < n_parts; ++i) {
+      r->require_unchunked(part_ids[i], "combined slot");
       parts.push_back(r->at(part_ids[i]));
       r_c += parts.back().r_pad;
       alg += parts.back().alg_rank;
     }
     if (r_c > kMaxRank) fail(ATMM_ERR_CONFIG, "combined rank " + std::to_string(r_c) + " exceeds 128");
     DeviceGuard g(r->device);
+    r->drop_extra(new_id);
     Slot s;
     s.id = new_id;
     s.rank = r_c;
     s.r_pad = r_c;
     s.alg_rank = alg;
+    s.total_rank = r_c;
     s.scale = 1.0f;
     s.live = true;
     const size_t dn = static_cast<size_t>(r->d_in_pad * r_c), un = static_cast<size_t>(r->d_out_pad * r_c);
@@ -1720,7 +1813,7 @@ int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, 
                             const float* up, float scale, void* stream) {
   return guarded([&] {
     if (!r) fail(ATMM_ERR_CONFIG, "null registry");
-    if (rank < 1 || rank > kMaxRank) fail(ATMM_ERR_CONFIG, "adapter rank must be in [1, 128]");
+    if (rank < 1 || rank > kMaxRank) fail(ATMM_ERR_CONFIG, "put_async takes ranks in [1, 128] (larger ranks: put)");
     if (!down || !up) fail(ATMM_ERR_SHAPE, "null factors");
     DeviceGuard g(r->device);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1733,6 +1826,7 @@ int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, 
     s.rank = rank;
     s.r_pad = r_pad;
     s.alg_rank = rank;
+    s.total_rank = rank;
     s.scale = scale;
     s.live = true;
     // A swap of the same shape overwrites the slot's buffers in place (stream
@@ -1767,6 +1861,10 @@ int atmm_registry_put_async(atmm_registry* r, int32_t adapter_id, int64_t rank, 
         }
       }
       build_precise_device(r, s, stage, stage + fd, st, true);
+    }
+    if (r->extra.count(adapter_id)) {  // replacing a rank-chunked adapter: its extra chunks go
+      CUDA_CHECK(cudaStreamSynchronize(st));
+      r->drop_extra(adapter_id);
     }
     if (same) {
       *same = s;
@@ -1837,6 +1935,7 @@ int atmm_registry_remove(atmm_registry* r, int32_t adapter_id) {
     free_slot(s);
     s = Slot{};
     r->slot_of.erase(it);
+    r->drop_extra(adapter_id);
     r->sync_slots();
   });
 }
@@ -1848,7 +1947,7 @@ int atmm_registry_contains(const atmm_registry* r, int32_t adapter_id) {
 int atmm_registry_rank(const atmm_registry* r, int32_t adapter_id, int64_t* rank) {
   return guarded([&] {
     if (!r || !rank) fail(ATMM_ERR_CONFIG, "null registry or output");
-    *rank = r->at(adapter_id).rank;
+    *rank = r->at(adapter_id).total_rank;
   });
 }
 
@@ -1932,16 +2031,21 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
   return guarded([&] {
     if (!p || !buf || cap == 0) fail(ATMM_ERR_CONFIG, "null plan or buffer");
     std::string s = "[";
-    for (size_t i = 0; i < p->groups.size(); ++i) {
-      const LaunchGroup& g = p->groups[i];
-      s += (i ? ", " : "") + std::string("{\"cluster\": ") + std::to_string(g.cluster) +
+    std::vector<const atmm_plan*> all{p};
+    for (const auto& ps : p->passes) all.push_back(ps.get());
+    bool firstg = true;
+    for (size_t pi = 0; pi < all.size(); ++pi) {
+    const atmm_plan* pp = all[pi];
+    for (size_t i = 0; i < pp->groups.size(); ++i) {
+      const LaunchGroup& g = pp->groups[i];
+      s += (firstg ? "" : ", ") + std::string("{\"pass\": ") + std::to_string(pi) + ", \"cluster\": " + std::to_string(g.cluster) +
            ", \"tiles\": " + std::to_string(g.num_tiles) + ", \"bn\": " + std::to_string(g.bn) +
            ", \"stages\": " + std::to_string(g.stages) + ", \"ustages\": " + std::to_string(g.ustages) +
            ", \"ny\": " + std::to_string(g.ny) + ", \"rep\": " + std::to_string(g.rep) +
            ", \"nbuf\": " + std::to_string(g.nbuf) + ", \"r_pad\": " + std::to_string(g.r_pad_max) +
            ", \"tmem_cols\": " + std::to_string(g.tmem_cols) + ", \"smem\": " + std::to_string(g.smem) +
            ", \"path_bf16\": \"" +
-           std::string(use_stream(*p, true) ? "stream" : choose_path(g, ATMM_BF16, true) == BypassPath::kA2a ? "a2a" : (choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? "split" : "fused")) +
+           std::string(use_stream(*pp, true) ? "stream" : choose_path(g, ATMM_BF16, true) == BypassPath::kA2a ? "a2a" : (choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? "split" : "fused")) +
            "\", \"split\": " + (g.split.ok ? std::string("{\"stages\": ") + std::to_string(g.split.stages) +
                                                    ", \"estages_bf16\": " + std::to_string(g.split.estages[0]) + "}"
                                              : std::string("null")) +
@@ -1950,13 +2054,15 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
                                                   ", \"smem\": " + std::to_string(g.a2a[0].smem) + "}"
                                             : std::string("null")) +
            ", \"stream\": " +
-           (p->stream.ok ? std::string("{\"grid\": ") + std::to_string(p->stream.grid) +
-                               ", \"sstages_bf16\": " + std::to_string(p->stream.sstages[0]) +
-                               ", \"estages_bf16\": " + std::to_string(p->stream.estages[0]) +
-                               ", \"smem_bf16\": " + std::to_string(p->stream.smem[0]) +
-                               ", \"tmem_cols\": " + std::to_string(p->stream.tmem_cols) + "}"
+           (pp->stream.ok ? std::string("{\"grid\": ") + std::to_string(pp->stream.grid) +
+                               ", \"sstages_bf16\": " + std::to_string(pp->stream.sstages[0]) +
+                               ", \"estages_bf16\": " + std::to_string(pp->stream.estages[0]) +
+                               ", \"smem_bf16\": " + std::to_string(pp->stream.smem[0]) +
+                               ", \"tmem_cols\": " + std::to_string(pp->stream.tmem_cols) + "}"
                          : std::string("null")) +
            "}";
+      firstg = false;
+    }
     }
     s += "]";
     std::strncpy(buf, s.c_str(), cap - 1);
@@ -1968,12 +2074,18 @@ int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64
   return guarded([&] {
     if (!p) fail(ATMM_ERR_CONFIG, "null plan");
     int64_t t = 0, nl = 0;
-    for (const auto& g : p->groups) {
-      t += g.num_tiles;
-      nl += choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? 0 : 1;  // bf16 Y, aligned
+    std::vector<const atmm_plan*> all{p};
+    for (const auto& ps : p->passes) all.push_back(ps.get());
+    for (const atmm_plan* pp : all) {
+      int64_t l = 0;
+      for (const auto& g : pp->groups) {
+        t += g.num_tiles;
+        l += choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? 0 : 1;  // bf16 Y, aligned
+      }
+      if (pp->merged_first >= 0) l += 2;  // one shrink + expand pair for all split groups
+      if (use_stream(*pp, true)) l = 1;   // one stream launch for the whole plan
+      nl += l;
     }
-    if (p->merged_first >= 0) nl += 2;  // one shrink + expand pair for all split groups
-    if (use_stream(*p, true)) nl = 1;   // one stream launch for the whole plan
     if (launches) *launches = nl;
     if (tiles) *tiles = t;
     if (ctas) *ctas = p->total_ctas;
@@ -2153,11 +2265,13 @@ int atmm_merge_apply(atmm_registry* r, int32_t adapter_id, int64_t layer, void* 
     const int64_t wsz = w_dtype == ATMM_BF16 ? 2 : 4;
     if (ldw < r->d_out) fail(ATMM_ERR_SHAPE, "W row stride ldw must be >= d_out");
     if (reinterpret_cast<uintptr_t>(w) % wsz != 0) fail(ATMM_ERR_SHAPE, "W is not element aligned");
-    const Slot& s = r->at(adapter_id);
     DeviceGuard g(r->device);
-    run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
-              r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream));
-    flops_add(2ull * static_cast<uint64_t>(r->d_in * r->d_out * s.alg_rank));  // delta_w_into (model.hpp:124)
+    for (int c = 0; c < r->num_chunks(adapter_id); ++c) {  // rank-chunked adapters: one update per chunk
+      const Slot& s = r->chunk(adapter_id, c);
+      run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
+                r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream));
+      flops_add(2ull * static_cast<uint64_t>(r->d_in * r->d_out * s.alg_rank));  // delta_w_into (model.hpp:124)
+    }
   });
 }
 
@@ -2174,12 +2288,14 @@ int atmm_merge_apply_layers(atmm_registry* r, int32_t adapter_id, int64_t layer0
     if (ldw < r->d_out) fail(ATMM_ERR_SHAPE, "W row stride ldw must be >= d_out");
     if (num_layers > 1 && w_layer_stride < ldw * r->d_in) fail(ATMM_ERR_SHAPE, "W layer stride must be >= ldw * d_in");
     if (reinterpret_cast<uintptr_t>(w) % wsz != 0) fail(ATMM_ERR_SHAPE, "W is not element aligned");
-    const Slot& s = r->at(adapter_id);
     DeviceGuard g(r->device);
-    run_merge(s.down_t + layer0 * r->d_in_pad * s.r_pad, s.up_t + layer0 * r->d_out_pad * s.r_pad, r->d_in,
-              r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream), num_layers,
-              r->d_in_pad * s.r_pad, r->d_out_pad * s.r_pad, w_layer_stride);
-    flops_add(2ull * static_cast<uint64_t>(num_layers * r->d_in * r->d_out * s.alg_rank));
+    for (int c = 0; c < r->num_chunks(adapter_id); ++c) {  // rank-chunked adapters: one update per chunk
+      const Slot& s = r->chunk(adapter_id, c);
+      run_merge(s.down_t + layer0 * r->d_in_pad * s.r_pad, s.up_t + layer0 * r->d_out_pad * s.r_pad, r->d_in,
+                r->d_out, s.r_pad, w, ldw, w_dtype, sign * s.scale, 1.0f, static_cast<cudaStream_t>(stream), num_layers,
+                r->d_in_pad * s.r_pad, r->d_out_pad * s.r_pad, w_layer_stride);
+      flops_add(2ull * static_cast<uint64_t>(num_layers * r->d_in * r->d_out * s.alg_rank));
+    }
   });
 }
 
@@ -2339,10 +2455,14 @@ int atmm_delta_w_host(atmm_registry* r, int32_t adapter_id, int64_t layer, float
     }
     const int64_t ldw = round_up(r->d_out, 8);
     DevBuf<float> w(static_cast<size_t>(r->d_in * ldw));
-    run_merge(s.down_t + layer * r->d_in_pad * s.r_pad, s.up_t + layer * r->d_out_pad * s.r_pad, r->d_in,
-              r->d_out, s.r_pad, w.p, ldw, ATMM_F32, s.scale, 0.0f, nullptr);
+    for (int c = 0; c < r->num_chunks(adapter_id); ++c) {  // sum of the chunks' products (fp32)
+      const Slot& sc = r->chunk(adapter_id, c);
+      run_merge(sc.down_t + layer * r->d_in_pad * sc.r_pad, sc.up_t + layer * r->d_out_pad * sc.r_pad, r->d_in,
+                r->d_out, sc.r_pad, w.p, ldw, ATMM_F32, sc.scale, c == 0 ? 0.0f : 1.0f, nullptr);
+      flops_add(2ull * static_cast<uint64_t>(r->d_in * r->d_out * sc.alg_rank));
+    }
+    (void)s;
     CUDA_CHECK(cudaMemcpy2D(out, r->d_out * 4, w.p, ldw * 4, r->d_out * 4, r->d_in, cudaMemcpyDeviceToHost));
-    flops_add(2ull * static_cast<uint64_t>(r->d_in * r->d_out * s.alg_rank));
   });
 }
 
@@ -2834,6 +2954,10 @@ int atmm_forward_create_opts(const atmm_plan* plan, int device, int64_t n, int64
       if (reg->d_in != reg->d_out) fail(ATMM_ERR_SHAPE, "the layer forward needs square layers (d_in == d_out)");
       if (hidden_dim > 0 && hidden_dim != reg->d_in) fail(ATMM_ERR_SHAPE, "hidden_dim does not match the registry");
       if (n > 0 && n != plan->n) fail(ATMM_ERR_SHAPE, "row count does not match the plan");
+      if (!plan->passes.empty()) {
+        fail(ATMM_ERR_CONFIG, "the fused layer forward takes adapters of rank <= 128 (rank-chunked adapters: "
+                              "BypassPlan.apply after the base GEMM)");
+      }
       f->reg = reg;
       f->generation = reg->generation;
       f->bypass_flops = plan->flops;

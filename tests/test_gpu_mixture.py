@@ -70,11 +70,25 @@ def test_mixture_errors_and_edge_cases(gpu, atmm, oracle):
     atmm.MixturePlan(reg, [2, 2, 2, 2], 2).apply(torch.ones(4, 256, device="cuda", dtype=torch.bfloat16), y)
     torch.cuda.synchronize()
     assert bool((y == 1).all())
-    # combined rank above 128 is refused (the caller then runs two passes)
-    reg.put(3, np.zeros((256, 120), np.float32), np.zeros((120, 256), np.float32))
+    # combined rank above 128: those guests take the two-pass form (own, then
+    # cancel with scale -1), same values within bf16 rounding
+    rng = np.random.default_rng(8)
+    d3 = rng.uniform(-0.1, 0.1, (256, 120)).astype(np.float32)
+    u3 = rng.uniform(-0.1, 0.1, (120, 256)).astype(np.float32)
+    reg.put(3, d3, u3)
+    mp = atmm.MixturePlan(reg, [1, 3, 3], 3)
+    assert mp.own is not None and list(mp.two_pass_rows) == [0]
+    xm = torch.ones(3, 256, device="cuda", dtype=torch.bfloat16)
+    ym = torch.zeros(3, 256, device="cuda")
+    mp.apply(xm, ym)
+    torch.cuda.synchronize()
+    f1, f3 = facs[1], (oracle.round_bf16(d3), oracle.round_bf16(u3))
+    ones = np.ones((1, 256))
+    want = ones @ f1[0].astype(np.float64) @ f1[1] - ones @ f3[0].astype(np.float64) @ f3[1]
+    assert np.max(np.abs(ym[0:1].cpu().numpy() - want)) <= tol_for(want)
+    assert bool((ym[1:] == 0).all())
     with pytest.raises(atmm.ConfigError):
-        atmm.MixturePlan(reg, [1, 3], 3).apply(torch.ones(2, 256, device="cuda", dtype=torch.bfloat16),
-                                               torch.zeros(2, 256, device="cuda"))
+        atmm.LayerForward(mp)
 
 
 def test_mixture_equals_two_pass_composition(gpu, atmm, oracle):
