@@ -264,8 +264,9 @@ int atmm_plan_stats(const atmm_plan* p, int64_t* launches, int64_t* tiles, int64
 /* Y[row, :] += scale * s_a * (X[row, :] . down_a[layer]) . up_a[layer]
  * for every row, a = assignment[row]: ONE pass, shrink+expand fused, the
  * rank-r intermediate kept on chip, the residual add fused in the epilogue.
- * X: n x d_in bf16 (ldx % 8 == 0, 16-byte aligned); Y: n x d_out, y_dtype
- * ATMM_BF16 or ATMM_F32.  scale = -1 gives the deLoRA cancel branch
+ * X: n x d_in bf16, ldx >= d_in (rows that are not 16-byte aligned --
+ * odd d_in, offset views -- are staged into a padded copy first, stream
+ * ordered); Y: n x d_out, y_dtype ATMM_BF16 or ATMM_F32, any ldy >= d_out.  scale = -1 gives the deLoRA cancel branch
  * (model.hpp:315-321).  Device pointers, stream-ordered. */
 int atmm_bypass_apply(const atmm_plan* p, int64_t layer, const void* x, int64_t ldx, void* y,
                       int64_t ldy, int y_dtype, float scale, void* stream);

@@ -2097,7 +2097,22 @@ int atmm_bypass_apply(const atmm_plan* p, int64_t layer, const void* x, int64_t 
   return guarded([&] {
     if (!p) fail(ATMM_ERR_CONFIG, "null plan");
     DeviceGuard g(p->reg->device);
-    apply_plan(p, layer, x, ldx, y, ldy, y_dtype, scale, static_cast<cudaStream_t>(stream));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (x && ldx >= p->reg->d_in && (ldx % 8 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0)) {
+      // Any hidden size / row stride (the reference takes any): X rows that
+      // are not 16-byte aligned are staged once into a padded copy (stream
+      // ordered, capturable); the kernels then read it by TMA / 16-byte loads.
+      const int64_t lds = round_up(p->reg->d_in, 8);
+      void* xs = nullptr;
+      CUDA_CHECK(cudaMallocAsync(&xs, static_cast<size_t>(std::max<int64_t>(p->n, 1) * lds * 2), st));
+      CUDA_CHECK(cudaMemsetAsync(xs, 0, static_cast<size_t>(std::max<int64_t>(p->n, 1) * lds * 2), st));
+      CUDA_CHECK(cudaMemcpy2DAsync(xs, lds * 2, x, ldx * 2, p->reg->d_in * 2, p->n, cudaMemcpyDeviceToDevice, st));
+      pdl_note_other(st);
+      apply_plan(p, layer, xs, lds, y, ldy, y_dtype, scale, st);
+      CUDA_CHECK(cudaFreeAsync(xs, st));
+    } else {
+      apply_plan(p, layer, x, ldx, y, ldy, y_dtype, scale, st);
+    }
     flops_add(p->flops);
   });
 }
