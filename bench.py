@@ -706,6 +706,7 @@ def impl_ours_bypass(args, w):
     # form (Y in, Y += bypass, Y out) is reported beside it.
     e2e = None
     e2e_res = None
+    e2e_rb = None
     if not args.no_e2e:
         # enough batches that pipeline fill / drain (3 slots) is amortised;
         # independent of --steps (the e2e leg is a few ms of PCIe traffic)
@@ -740,6 +741,23 @@ def impl_ours_bypass(args, w):
                    "h2d_bytes_per_step": int(w.tokens * (w.d_in + w.d_out) * 2),
                    "d2h_bytes_per_step": int(w.tokens * w.d_out * 2), "us_per_batch": r_s / e2e_steps * 1e6,
                    "path": "atmm_bypass_residual_host_bf16_pipelined: H2D X and Y, Y += bypass, D2H Y"}
+        # the reference's own signature, one synchronous call per batch:
+        # run_bypass(x, plan, adapters, layer, table) (batch.hpp:48) with fp32
+        # host buffers, as include/loraserve_compat.hpp calls it
+        xf32 = np.random.default_rng(9).uniform(-1, 1, (w.tokens, w.d_in)).astype(np.float32)
+        for _ in range(3):
+            atmm.run_bypass(reg, xf32, w.assignment, layer=0)
+        torch.cuda.synchronize()
+        calls = 30
+        t0 = time.perf_counter()
+        for i in range(calls):
+            atmm.run_bypass(reg, xf32, w.assignment, layer=i % layers)
+        rb_s = max_over_ranks(time.perf_counter() - t0, world)
+        e2e_rb = {"value": job_flops * calls / rb_s / 1e12, "unit": "TFLOP/s",
+                  "h2d_bytes_per_step": int(w.tokens * w.d_in * 4), "d2h_bytes_per_step": int(w.tokens * w.d_out * 4),
+                  "us_per_batch": rb_s / calls * 1e6,
+                  "path": "atmm_run_bypass_host = run_bypass (batch.hpp:48) signature: fp32 host x in, fresh fp32 "
+                          "bypass out, one synchronous call per batch (plan cached, buffers reused)"}
 
     # ---- CPU baseline: the reference itself, bounded sample, rank 0, N=1 ----
     cpu = None
@@ -792,6 +810,7 @@ def impl_ours_bypass(args, w):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_residual": e2e_res,
+            "e2e_run_bypass": e2e_rb,
             "grouped": grouped,
             "layer_forward": layer_fwd,
             "clocks": clocks,
