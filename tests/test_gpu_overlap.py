@@ -161,3 +161,25 @@ def test_foreign_kernel_between_applies(gpu, atmm, oracle):
         res.append(work)
     for u, v in zip(*res):
         assert torch.equal(u, v)
+
+
+def test_two_streams_interleaved(gpu, atmm, oracle):
+    """Records are per stream: interleaved applies on two streams (each its
+    own chain of disjoint and dependent steps) equal the full-dependency bits."""
+    import torch
+
+    _, _, _, plan, ref_plan, bufs = _setup(atmm, oracle)
+    res = []
+    for p in (plan, ref_plan):
+        work = [b.clone() for b in bufs]
+        sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+        for i in range(4):
+            with torch.cuda.stream(sa):
+                p.apply(work[0], work[1 + (i % 2)], stream=sa)      # A: X0 -> Y1 / Y2
+            with torch.cuda.stream(sb):
+                p.apply(work[4 + (i % 2)], work[6], stream=sb)      # B: X4 / X5 -> Y6
+                p.apply(work[6], work[7], stream=sb)                # B: dependent on the previous
+        torch.cuda.synchronize()
+        res.append(work)
+    for u, v in zip(*res):
+        assert torch.equal(u, v)
