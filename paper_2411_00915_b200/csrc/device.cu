@@ -1451,6 +1451,7 @@ static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.part_off = sp.nseg + T;
       sp.red_off = sp.part_off + T;
       sp.red_tile0 = sp.red_off + T + 1;
+      sp.tile_rows = p->d_tile_rows.p + g.tile_offset * kTileM;
       sp.part = sc.part.p;
       sp.mid = sc.mid.p;
       sp.counter = sc.counter.p;

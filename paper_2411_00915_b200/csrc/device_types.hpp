@@ -157,6 +157,7 @@ struct SplitParams {
   const int32_t* red_off;    // [tile + 1] prefix of rows x r_pad / 4 reduction items
   const int32_t* red_tile0;  // [grid] tile holding the CTA's first reduction item
   uint64_t* trace;
+  const int32_t* tile_rows;  // [tile][kTileM] padded row lists of this launch's tiles
 };
 
 // Stream path (atmm_stream_kernel): the shrink AND the expand of every tile

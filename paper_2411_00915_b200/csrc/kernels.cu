@@ -1492,10 +1492,11 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
         rows = tile.rows;
         r_pad = tile.r_pad;
         down_t = tile.down_t + static_cast<int64_t>(p.layer) * tile.down_layer_stride;
+        // padded per-tile row table: independent of the descriptor load
 #pragma unroll
         for (int i = 0; i < kRowsPer; ++i) {
           const int r = r0 + kRowStep * i;
-          xoff[i] = r < rows ? static_cast<int64_t>(p.row_index[tile.row_begin + r]) * p.ldx : 0;
+          xoff[i] = r < kTileM ? static_cast<int64_t>(p.tile_rows[t * kTileM + r]) * p.ldx : 0;
         }
       }
       const int st = j % S;
@@ -1642,6 +1643,13 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   const int i_beg = p.e_begin[blockIdx.x];
   const int i_end = p.e_begin[blockIdx.x + 1];
   if (tid == 0) STRACE(8);
+  if (p.trace && tid == 0) {  // debug: the CTA's expand items and their Y bytes
+    const int nsl_ = (p.d_out + kCols - 1) / kCols;
+    long long yb = 0;
+    for (int it = i_beg; it < i_end; ++it) yb += static_cast<long long>(p.tiles[it / nsl_].rows) * kCols * kEsz;
+    p.trace[static_cast<size_t>(blockIdx.x) * kTraceEvents + 20] = static_cast<uint64_t>(i_end - i_beg);
+    p.trace[static_cast<size_t>(blockIdx.x) * kTraceEvents + 21] = static_cast<uint64_t>(yb);
+  }
   // The next launch may start as SMs free up: it waits for this grid itself.
   griddep_launch_dependents();
   const int64_t ldy_b = p.ldy * kEsz;
@@ -1677,7 +1685,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       const uint32_t M = U + up_bytes;
       const uint32_t Yb = M + mid_bytes;
       const uint32_t Rb = Yb + y_bytes;  // rows of this stage
-      if (tid < static_cast<uint32_t>(kTileM)) st_shared_u32(Rb + tid * 4, static_cast<uint32_t>(p.row_index[tile.row_begin + min(static_cast<int>(tid), rows - 1)]));
+      if (tid < static_cast<uint32_t>(kTileM)) st_shared_u32(Rb + tid * 4, static_cast<uint32_t>(p.tile_rows[t * kTileM + static_cast<int>(tid)]));
       named_bar_sync(2, kSplitLoaders);  // the stage's row indices are written
       // up^T rows n0 .. n0 + kCols - 1, 16-byte units permuted: column n0 + nl
       // -> MMA j = nl % G, A row nl / G.

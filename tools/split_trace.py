@@ -64,6 +64,17 @@ def main():
             rel = (col - t0) / 1e3
             print(f"  {name:<26} n={col.size:4d} min {rel.min():7.2f} p10 {np.percentile(rel, 10):7.2f} "
                   f"med {np.median(rel):7.2f} p90 {np.percentile(rel, 90):7.2f} max {rel.max():7.2f} us")
+        # per-CTA expand: items, Y bytes vs the time its loaders finish
+        sel = raw[:, 9] > 0
+        if sel.any():
+            items, yb = raw[sel, 20], raw[sel, 21]
+            start, done = (raw[sel, 8] - t0) / 1e3, (raw[sel, 9] - t0) / 1e3
+            order = np.argsort(done)
+            print("  expand per CTA (slowest 8 / fastest 4): [cta, items, Y KB, start us, loaders done us]")
+            idx = np.nonzero(sel)[0]
+            for k in list(order[-8:]) + list(order[:4]):
+                print(f"    {idx[k]:4d} {int(items[k]):3d} {yb[k] / 1024:7.1f} {start[k]:7.2f} {done[k]:7.2f}")
+            print(f"  corr(Y bytes, done) = {np.corrcoef(yb, done)[0, 1]:.2f}  corr(start, done) = {np.corrcoef(start, done)[0, 1]:.2f}")
 
 
 if __name__ == "__main__":
