@@ -23,7 +23,7 @@ PATHS = {"a2a": 1, "split": 2, "fused": 3, "stream": 4}
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="a2a,split,fused,stream,merge,forward,gemm")
+    ap.add_argument("--only", default="a2a,split,fused,stream,overlap,chunks,merge,forward,gemm")
     ap.add_argument("--small", action="store_true", help="fewer rows (racecheck is slow)")
     args = ap.parse_args()
     only = set(args.only.split(","))
@@ -74,6 +74,40 @@ def main():
             err = float(np.max(np.abs(yy.float().cpu().numpy() - want_bypass(y0))))
             print(f"{name:7s} {str(ydt):15s} paths={sorted({g['path_bf16'] for g in plan.describe()})} max|err|={err:.3e}",
                   flush=True)
+    if "overlap" in only:
+        # consecutive independent applies on one stream: the later ones load
+        # X / Y under their predecessor (dependency elision), then a dependent
+        # one (X = the previous Y) that must wait
+        t = atmm.TilingTable()
+        for a, r in ranks.items():
+            launch = list(atmm.heuristic_launch(lens[a], d_in, r, d_out))
+            launch[4] = PATHS["a2a"]
+            t.insert(atmm.m_bucket_of(lens[a]), d_in, r, (128, 128, 256, 128, 16, 64), 1, sm100=launch)
+        plan = atmm.BypassPlan(reg, asg, t)
+        ys = [torch.empty(asg.size, d_out, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1) for _ in range(3)]
+        y0 = [y.float().cpu().numpy() for y in ys]
+        before = atmm.overlap_stats()
+        s_ = torch.cuda.Stream()
+        with torch.cuda.stream(s_):
+            for y in ys:
+                plan.apply(x, y, stream=s_)
+        s_.synchronize()
+        after = atmm.overlap_stats()
+        err = max(float(np.max(np.abs(y.float().cpu().numpy() - want_bypass(v)))) for y, v in zip(ys, y0))
+        print(f"overlap early={after[1] - before[1]} of {after[0] - before[0]} max|err|={err:.3e}", flush=True)
+    if "chunks" in only:
+        rc = atmm.AdapterRegistry(1, d_in, d_out)
+        s = 1.0 / np.sqrt(200)
+        dn, up = rng.uniform(-s, s, (d_in, 200)).astype(np.float32), rng.uniform(-s, s, (200, d_out)).astype(np.float32)
+        rc.put(7, dn, up)
+        pl = atmm.BypassPlan(rc, np.full(48, 7, np.int32))
+        xc = x[:48].contiguous()
+        y = torch.zeros(48, d_out, dtype=torch.float32, device="cuda")
+        pl.apply(xc, y)
+        torch.cuda.synchronize()
+        ref = (xc.double().cpu().numpy() @ dn.astype(np.float64)) @ up.astype(np.float64)
+        print(f"chunks  passes={len({g['pass'] for g in pl.describe()})} max|err|={float(np.max(np.abs(y.cpu().numpy() - ref))):.3e}",
+              flush=True)
     if "merge" in only:
         for wdt in (torch.bfloat16, torch.float32):
             W = torch.empty(d_in, d_out, dtype=wdt, device="cuda").uniform_(-0.05, 0.05)
