@@ -219,7 +219,7 @@ class TilingTable:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals are None at interpreter exit)
             lib.atmm_table_destroy(h)
             self._h = None
 
@@ -309,7 +309,7 @@ class AdapterRegistry:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals are None at interpreter exit)
             lib.atmm_registry_destroy(h)
             self._h = None
 
@@ -472,7 +472,7 @@ class BypassPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals are None at interpreter exit)
             lib.atmm_plan_destroy(h)
             self._h = None
 
@@ -678,7 +678,7 @@ class LayerForward:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals are None at interpreter exit)
             lib.atmm_forward_destroy(h)
             self._h = None
 
@@ -904,7 +904,7 @@ class ModelState:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals are None at interpreter exit)
             lib.atmm_state_destroy(h)
             self._h = None
 
