@@ -183,3 +183,29 @@ def test_two_streams_interleaved(gpu, atmm, oracle):
         res.append(work)
     for u, v in zip(*res):
         assert torch.equal(u, v)
+
+
+def test_grouped_launches_overlap_same_bits(gpu, atmm, oracle):
+    """Grouped applies (one launch, several (X, Y) calls sharing X, like the
+    q / k / v projections) overlap the next group only when disjoint."""
+    import torch
+
+    _, _, _, plan, ref_plan, bufs = _setup(atmm, oracle)
+    groups = [((0, 1), (0, 2), (0, 3)), ((4, 5), (4, 6), (4, 7)),  # disjoint from the first
+              ((1, 5), (2, 6), (3, 7))]                            # reads the first group's outputs
+    res, early = [], []
+    for p in (plan, ref_plan):
+        work = [b.clone() for b in bufs]
+        s = torch.cuda.Stream()
+        before = atmm.overlap_stats()
+        with torch.cuda.stream(s):
+            for grp in groups:
+                p.apply_group([work[x] for x, _ in grp], [work[y] for _, y in grp], [0] * len(grp), stream=s)
+        s.synchronize()
+        after = atmm.overlap_stats()
+        early.append(after[1] - before[1])
+        res.append(work)
+    for u, v in zip(*res):
+        assert torch.equal(u, v)
+    # the second group is disjoint from the first; the third reads Y5 / Y6 / Y7 the second wrote (RAW)
+    assert early[1] == 0 and early[0] <= 2
