@@ -474,6 +474,8 @@ struct SplitLayout {
   bool ok_dt[2] = {false, false};  // usable for bf16 / fp32 Y
   int32_t g_bf16 = 2;              // bf16 expand item width: 128 g_bf16 columns
   size_t smem_s = 0, smem_e[2] = {0, 0};
+  uint32_t tmem_e[2] = {0, 0};     // expand TMEM columns (two accumulators of G x rows16)
+  int32_t rows16 = 0;
 };
 
 // Stream-path (atmm_stream_kernel) geometry of a plan, per Y dtype:
@@ -673,8 +675,8 @@ static A2aLayout resolve_a2a(int64_t d_in, int64_t d_out, int32_t cluster, int32
 // Split path scratch written by the shrink and read by the expand: mid
 // partials (fp32, per tile x K slice), bf16 mid per tile and per-tile mid
 // readiness counters.  One set per CUDA stream that applies the plan, so
-// applies of one plan on different streams never share scratch (the shrink
-// resets the counters its own stream's previous expand polled).
+// applies of one plan on different streams never share scratch (the last
+// CTA of each expand resets the counters for the next expand on its stream).
 struct SplitScratch {
   DevBuf<float> part;
   DevBuf<uint16_t> mid;
@@ -795,6 +797,7 @@ static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, 
   l.stages = static_cast<int32_t>(std::min<int64_t>(8, avail / stage));
   l.smem_s = size_t(1024 + l.stages * stage);
   const int64_t rows16 = round_up(rows_max, 16);
+  l.rows16 = static_cast<int32_t>(rows16);
   for (int di = 0; di < 2; ++di) {
     const int64_t esz = di == 0 ? 2 : 4;
     // bf16 items are 256 columns wide unless two of them do not fit (large
@@ -806,6 +809,17 @@ static SplitLayout resolve_split(int64_t d_in, int64_t d_out, int32_t rows_max, 
       l.smem_e[di] = size_t(128 + l.estages[di] * est);
       if (di == 0) l.g_bf16 = g;
       if (l.estages[di] >= 2) break;
+    }
+    // TMEM: the expand holds two accumulators of G x rows16 columns from its
+    // start (before its reduction share, which other CTAs' items wait for):
+    // pad shared memory so co-resident expand CTAs always fit in 512 columns.
+    {
+      const int64_t g = di == 0 ? l.g_bf16 : 1;
+      int64_t cols = 32;
+      while (cols < 2 * g * rows16) cols <<= 1;
+      const int64_t max_co = std::max<int64_t>(1, 512 / cols);
+      while (int64_t(kSmemPerSM) / int64_t(l.smem_e[di] + 1024) > max_co) l.smem_e[di] += 4096;
+      l.tmem_e[di] = static_cast<uint32_t>(cols);
     }
     l.ok_dt[di] = l.stages >= 2 && l.estages[di] >= 2;
   }
@@ -1443,6 +1457,7 @@ static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.y_dtype = y_dtype == ATMM_BF16 ? 0 : 1;
       sp.estages = g.split.estages[sp.y_dtype];
       sp.expand_g = sp.y_dtype == 0 ? g.split.g_bf16 : 1;
+      sp.e_tmem_cols = g.split.tmem_e[sp.y_dtype];
       sp.rows_max = g.rows_max;
       sp.s_begin = sb.tables.p;
       sp.e_begin = sb.tables.p + (P + 1) * (sp.y_dtype == 0 ? 1 : 2);
@@ -2053,7 +2068,12 @@ int atmm_plan_describe(const atmm_plan* p, char* buf, size_t cap) {
            ", \"path_bf16\": \"" +
            std::string(use_stream(*pp, true) ? "stream" : choose_path(g, ATMM_BF16, true) == BypassPath::kA2a ? "a2a" : (choose_path(g, ATMM_BF16, true) == BypassPath::kSplit ? "split" : "fused")) +
            "\", \"split\": " + (g.split.ok ? std::string("{\"stages\": ") + std::to_string(g.split.stages) +
-                                                   ", \"estages_bf16\": " + std::to_string(g.split.estages[0]) + "}"
+                                                   ", \"estages_bf16\": " + std::to_string(g.split.estages[0]) +
+                                                   ", \"g_bf16\": " + std::to_string(g.split.g_bf16) +
+                                                   ", \"rows16\": " + std::to_string(g.split.rows16) +
+                                                   ", \"etmem\": [" + std::to_string(g.split.tmem_e[0]) + ", " +
+                                                   std::to_string(g.split.tmem_e[1]) + "], \"smem_e\": [" +
+                                                   std::to_string(g.split.smem_e[0]) + ", " + std::to_string(g.split.smem_e[1]) + "]}"
                                              : std::string("null")) +
            ", \"a2a_bf16\": " + (g.a2a[0].ok ? std::string("{\"stages\": ") + std::to_string(g.a2a[0].stages) +
                                                   ", \"tmem_cols\": " + std::to_string(g.a2a[0].tmem_cols) +

@@ -141,6 +141,7 @@ struct SplitParams {
   int32_t num_tiles;
   int32_t nkb;           // 64-wide K blocks per tile
   int32_t expand_g;      // output columns per expand epilogue thread (items of 128 G columns)
+  uint32_t e_tmem_cols;  // expand TMEM allocation: >= 2 x G x rows16 (two accumulators)
   int32_t r_pad_max;
   int32_t stages;        // shrink ring depth
   int32_t estages;       // expand ring depth
@@ -153,7 +154,7 @@ struct SplitParams {
   const int32_t* part_off;   // [tile]
   float* part;               // [sum nseg][128][r_pad_max]
   uint16_t* mid;             // [tile][128 x r_pad_max] bf16, interleave layout
-  int32_t* counter;          // [2] reserved, then [tile] reduced mid items (reset by the shrink launch)
+  int32_t* counter;          // [0] exited expand CTAs, [1] reserved, then [tile] reduced mid items (reset by the expand's last CTA)
   const int32_t* red_off;    // [tile + 1] prefix of rows x r_pad / 4 reduction items
   const int32_t* red_tile0;  // [grid] tile holding the CTA's first reduction item
   uint64_t* trace;

@@ -1452,12 +1452,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
   // the partials only after their own griddepcontrol.wait).
   griddep_wait();
   griddep_launch_dependents();
-  // The expand launch that follows counts reduced mid items per tile: reset
-  // (after the wait: the previous expand, which polled them, is complete; the
-  // next expand reads them after its own wait, i.e. after this grid).
-  if (blockIdx.x == 0) {
-    for (int t = static_cast<int>(tid); t < p.num_tiles; t += static_cast<int>(blockDim.x)) p.counter[2 + t] = 0;
-  }
+  // (The expand launch's per-tile readiness counters are zero here: the
+  // previous expand on this stream reset them as its last CTA left.)
 
   if (warp == 0) {
     // full: the 8 loader warps + the down^T bulk copy's expect_tx arrival
@@ -1639,7 +1635,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   // + the global row index of each Y row (kTileM int32) at the end of the stage
   const uint32_t stage_bytes = (up_bytes + mid_bytes + y_bytes + kTileM * 4 + 127) & ~127u;
   const uint32_t acc_cols = static_cast<uint32_t>(G * rows16_max);
-  const uint32_t tcols = acc_cols <= 16 ? 32u : (acc_cols <= 32 ? 64u : (acc_cols <= 64 ? 128u : 256u));  // 2 accumulators
+  // 2 accumulators of acc_cols (<= 2 x 128) columns each, buffer 1 at
+  // tcols / 2 >= acc_cols; the host pads shared memory so co-resident expand
+  // CTAs fit in 512 columns (resolve_split).
+  const uint32_t tcols = p.e_tmem_cols;
+  if (tcols < 2u * acc_cols || tcols > 512u) __trap();
   const int i_beg = p.e_begin[blockIdx.x];
   const int i_end = p.e_begin[blockIdx.x + 1];
   if (tid == 0) STRACE(8);
@@ -1692,7 +1692,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       const uint16_t* us = tile.up_t + static_cast<int64_t>(p.layer) * tile.up_layer_stride;
       const int kc = r_pad / 8;
       const int n_end = (p.d_out + 127) & ~127;  // the registry pads up^T to d_out_pad = round_up(d_out, 128)
-      for (int q = static_cast<int>(tid); q < kCols * kc; q += kSplitLoaders) {
+      // G = 1: the 128 columns' blocked up^T is one contiguous run of the
+      // registry layout (interleave_off(n, c, r_pad) == its global offset):
+      // one TMA bulk copy below instead of 16-byte LSU copies.
+      for (int q = static_cast<int>(tid); G > 1 && q < kCols * kc; q += kSplitLoaders) {
         const int nl = q / kc;
         const int c = q - nl * kc;
         const int n = n0 + nl;
@@ -1733,7 +1736,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
           waited = true;
           STRACE(12);
         }
-        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows16 * r_pad * 2));
+        const uint32_t ub = G == 1 ? static_cast<uint32_t>(kCols * r_pad * 2) : 0u;
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows16 * r_pad * 2) + ub);
+        if (G == 1) bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes, us + static_cast<int64_t>(n0 >> 3) * kc * 64, ub, &full[st]);
         bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes + up_bytes, ms, static_cast<uint32_t>(rows16 * r_pad * 2),
                  &full[st]);
       }
@@ -1848,7 +1853,19 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
   }
   if (tid == kSplitWarpEpi * 32) STRACE(10);
   __syncthreads();
-  if (tid == 0) STRACE(11);
+  if (tid == 0) {
+    STRACE(11);
+    // The last CTA out resets the per-tile readiness counters for the next
+    // expand on this stream: every CTA has finished polling them by now.
+    // (Not the next shrink: its dependents -- the next expand -- may start
+    // polling before a reset that follows the shrink's release.)
+    __threadfence();
+    if (atomicAdd(p.counter, 1) == static_cast<int>(gridDim.x) - 1) {
+      for (int t = 0; t < p.num_tiles; ++t) p.counter[2 + t] = 0;
+      p.counter[0] = 0;
+      __threadfence();
+    }
+  }
   griddep_launch_dependents();
   if (warp == kSplitWarpMMA) {
     tc_fence_after();

@@ -77,6 +77,10 @@ def bypass_config(name: str, seed: int = 3) -> BypassWorkload:
     elif name == "cfg5":
         ids = list(range(64))
         w = BypassWorkload(name, 5120, 5120, 8192, {a: 64 for a in ids}, equal_lengths(8192, ids))
+    elif name == "paper_in1":  # the paper's ATMM Input 1: 256 x 4096 . 4096 x 32
+        w = BypassWorkload(name, 4096, 4096, 256, {0: 32}, {0: 256})
+    elif name == "paper_in2":  # the paper's ATMM Input 2: 8192 x 4096 . 4096 x 128
+        w = BypassWorkload(name, 4096, 4096, 8192, {0: 128}, {0: 8192})
     elif name == "cfg5_r16":
         ids = list(range(64))
         w = BypassWorkload(name, 5120, 5120, 8192, {a: 16 for a in ids}, equal_lengths(8192, ids))
