@@ -152,3 +152,50 @@ def test_cfg4_bf16_round_trip_drift_report(gpu, atmm, oracle, capsys):
     with capsys.disabled():
         for label, (dr, rel) in results.items():
             print(f"\n  bf16 W 100-cycle merge/unmerge drift, {label}: max|dW_drift| = {dr:.3e} ({rel:.2%} of max|W|)")
+
+
+@pytest.mark.parametrize("name,per_segment", [("cfg2", None), ("cfg3", None), ("cfg5", 4)])
+def test_bench_mode_graph_of_independent_steps(gpu, atmm, oracle, name, per_segment):
+    """The bench's timed mode: consecutive applies on distinct (X, Y) buffers
+    and alternating layers, captured in one CUDA graph (programmatic launches
+    overlapping where the launcher proved them disjoint), every step against
+    the oracle."""
+    import torch
+
+    from paper_2411_00915_b200.workloads import bypass_config
+
+    w = bypass_config(name)
+    L = 2
+    reg = atmm.AdapterRegistry(L, w.d_in, w.d_out)
+    facs = {0: {}, 1: {}}
+    for a, r in w.ranks.items():
+        rng = oracle.rng(2000 + a)
+        s = 1.0 / np.sqrt(np.float32(r))
+        down = oracle.round_bf16(oracle.random_matrix(rng, L * w.d_in, r, -s, s).reshape(L, w.d_in, r))
+        up = oracle.round_bf16(oracle.random_matrix(rng, L * r, w.d_out, -s, s).reshape(L, r, w.d_out))
+        reg.put(a, down, up)
+        for l in range(L):
+            facs[l][a] = (down[l], up[l])
+    plan = atmm.BypassPlan(reg, w.assignment)
+    steps = 4
+    xs = [oracle.round_bf16(oracle.random_matrix(oracle.rng(30 + i), w.tokens, w.d_in)) for i in range(steps)]
+    ys = [oracle.round_bf16(oracle.random_matrix(oracle.rng(40 + i), w.tokens, w.d_out)) for i in range(steps)]
+    xt = [torch.from_numpy(x).to("cuda", torch.bfloat16) for x in xs]
+    yt = [torch.from_numpy(y).to("cuda", torch.bfloat16) for y in ys]
+    s = torch.cuda.Stream()
+    warm = torch.empty_like(yt[0])
+    with torch.cuda.stream(s):
+        plan.apply(xt[0], warm, layer=0, stream=s)  # tensor maps, scratch, attributes outside the capture
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        for i in range(steps):
+            plan.apply(xt[i], yt[i], layer=i % L, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    rows = np.arange(w.tokens) if per_segment is None else _stratified_rows(w.assignment, per_segment)
+    for i in range(steps):
+        got = yt[i].float().cpu().numpy()[rows]
+        want = ys[i][rows].astype(np.float64) + oracle.bypass_rows_f64(xs[i][rows], w.assignment[rows], facs[i % L])
+        err = float(np.max(np.abs(got - want)))
+        assert err <= tol_for(want), f"{name} step {i}: max|err| {err} > {tol_for(want)}"
