@@ -1423,6 +1423,53 @@ __device__ __forceinline__ void split_reduce_mid(const SplitParams& p, const Red
   }
 }
 
+// Split expand, staged output: Y[row, c0 .. c0 + G) += s * acc, in place in
+// the stage's Y rows (shared memory); the rows then leave by 16-byte stores
+// (split_rows_out).  Same fp32 math and one rounding as a2a_row_out.
+template <typename YT, int G>
+__device__ __forceinline__ void split_update_smem(const uint32_t (&acc)[64], int rb, int nrows, uint32_t ysrc,
+                                                  uint32_t pitch, float s) {
+  constexpr int RB = 64 / G > 32 ? 32 : 64 / G;
+  const bool full = nrows >= RB;
+  uint32_t in[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    const uint32_t ya = ysrc + static_cast<uint32_t>(rb + i) * pitch;
+    in[i] = (full || i < nrows) ? (sizeof(YT) == 2 && G == 1 ? ld_shared_u16(ya) : ld_shared_u32(ya)) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    if (!(full || i < nrows)) continue;
+    const uint32_t ya = ysrc + static_cast<uint32_t>(rb + i) * pitch;
+    if constexpr (sizeof(YT) == 2) {
+      const float lo = fmaf(s, __uint_as_float(acc[i]), bf16lo(in[i]));
+      if constexpr (G == 1) {
+        st_shared_u16(ya, __bfloat16_as_ushort(__float2bfloat16_rn(lo)));
+      } else {
+        const float hi = fmaf(s, __uint_as_float(acc[RB + i]), bf16hi(in[i]));
+        st_shared_u32(ya, pack_bf16x2(lo, hi));
+      }
+    } else {
+      st_shared_u32(ya, __float_as_uint(fmaf(s, __uint_as_float(acc[i]), __uint_as_float(in[i]))));
+    }
+  }
+}
+
+// Copy an item's updated Y rows (shared memory, pitch bytes apart) to their
+// global rows: warp w of nw takes rows w, w + nw, ...; lanes move 16-byte
+// chunks (a 512-byte row is one warp instruction).
+__device__ __forceinline__ void split_rows_out(uint32_t ysrc, uint32_t pitch, uint32_t rows_s, int rows, int row_bytes,
+                                               uint8_t* ycol, int64_t ldy_b, int w, int nw, uint32_t lane) {
+  const int cpr = row_bytes / 16;
+  for (int r = w; r < rows; r += nw) {
+    const int64_t grow = static_cast<int32_t>(ld_shared_u32(rows_s + static_cast<uint32_t>(r) * 4u));
+    for (int c = static_cast<int>(lane); c < cpr; c += 32) {
+      const uint4 v = ld_shared_v4(ysrc + static_cast<uint32_t>(r) * pitch + static_cast<uint32_t>(c) * 16u);
+      *reinterpret_cast<uint4*>(ycol + grow * ldy_b + c * 16) = v;
+    }
+  }
+}
+
 // ---- shrink: partial mid rows per (tile, CTA) segment, stream-K over K ----
 //   stage = [A: 128 rows x 128 B, 128-byte swizzle | B: r_pad_max x 64 down^T]
 __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const SplitParams p) {
@@ -1607,7 +1654,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
 //   m G + j), so epilogue thread (quadrant q, lane l) owns the G adjacent
 //   output columns (32 q + l) G .. + G - 1 (one 2 G-byte access per row).
 //   stage = [up^T 128 G x r_pad_max | mid rows16_max x r_pad_max | Y rows_max x 128 G | rows]
-template <typename YT, int G>
+template <typename YT, int G, bool kStaged>
 __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const SplitParams p) {
   extern __shared__ uint8_t smem_raw[];
   // interleave (no-swizzle) operands only need 16-byte alignment: align to 128
@@ -1843,11 +1890,20 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
                            &acc[jj * RB]);
         }
         tmem_wait_ld();
-        a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), Yb + static_cast<uint32_t>(c0 * kEsz), ypitch, ydst, rring,
-                               ldy_b, s, col_ok);
+        if constexpr (kStaged) {
+          if (col_ok) split_update_smem<YT, G>(acc, rb, min(RB, rows - rb), Yb + static_cast<uint32_t>(c0 * kEsz), ypitch, s);
+        } else {
+          a2a_update_rows<YT, G>(acc, rb, min(RB, rows - rb), Yb + static_cast<uint32_t>(c0 * kEsz), ypitch, ydst, rring,
+                                 ldy_b, s, col_ok);
+        }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
+      if constexpr (kStaged) {
+        named_bar_sync(5, 256);  // every epilogue warp's updates of this item are in shared memory
+        split_rows_out(Yb, ypitch, rring, rows, ncols * kEsz, reinterpret_cast<uint8_t*>(p.y) + static_cast<int64_t>(n0) * kEsz,
+                       ldy_b, static_cast<int>(warp - kSplitWarpEpi), 8, lane);
+      }
       mbar_arrive(&empty[st]);
     }
   }
@@ -2349,9 +2405,12 @@ template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant
 template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap,
                                                    const BypassParams);
-template __global__ void atmm_expand_kernel<__nv_bfloat16, 2>(const SplitParams);
-template __global__ void atmm_expand_kernel<__nv_bfloat16, 1>(const SplitParams);
-template __global__ void atmm_expand_kernel<float, 1>(const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 2, false>(const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 2, true>(const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 1, false>(const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 1, true>(const SplitParams);
+template __global__ void atmm_expand_kernel<float, 1, false>(const SplitParams);
+template __global__ void atmm_expand_kernel<float, 1, true>(const SplitParams);
 template __global__ void atmm_merge_kernel<float>(const MergeParams);
 template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
 template __global__ void atmm_merge_tma_kernel<float>(const __grid_constant__ CUtensorMap, const MergeParams);
@@ -2504,19 +2563,14 @@ cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t sme
   if (e != cudaSuccess) return e;
   cfg.blockDim = dim3(kExpandThreads, 1, 1);
   cfg.dynamicSmemBytes = smem_e;
+  void (*k)(const SplitParams);
   if (y_dtype == 0 && p.expand_g == 1) {
-    auto k = atmm_expand_kernel<__nv_bfloat16, 1>;
-    e = prepare(k, smem_e, false);
-    if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, k, p);
+    k = p.out_staged ? atmm_expand_kernel<__nv_bfloat16, 1, true> : atmm_expand_kernel<__nv_bfloat16, 1, false>;
+  } else if (y_dtype == 0) {
+    k = p.out_staged ? atmm_expand_kernel<__nv_bfloat16, 2, true> : atmm_expand_kernel<__nv_bfloat16, 2, false>;
+  } else {
+    k = p.out_staged ? atmm_expand_kernel<float, 1, true> : atmm_expand_kernel<float, 1, false>;
   }
-  if (y_dtype == 0) {
-    auto k = atmm_expand_kernel<__nv_bfloat16, 2>;
-    e = prepare(k, smem_e, false);
-    if (e != cudaSuccess) return e;
-    return cudaLaunchKernelEx(&cfg, k, p);
-  }
-  auto k = atmm_expand_kernel<float, 1>;
   e = prepare(k, smem_e, false);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, k, p);

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--x-ready", action="store_true")
+    ap.add_argument("--y-dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--launches", default=None,
                     help="';'-separated tile_m,cluster,bn,stages,path launches to force (instead of --paths)")
     ap.add_argument("--no-overlap", action="store_true", help="ATMM_PLAN_NO_OVERLAP on every plan")
@@ -42,7 +43,7 @@ def main():
     dev = torch.device("cuda", 0)
     for name in args.configs.split(","):
         w = workloads.bypass_config(name)
-        step_bytes = w.bytes(2)
+        step_bytes = w.bytes(2 if args.y_dtype == "bf16" else 4)
         layers = min(64, max(2, int(np.ceil(2.5 * L2_BYTES / step_bytes))))
         reg = atmm.AdapterRegistry(layers, w.d_in, w.d_out, device=0)
         rng = np.random.default_rng(5)
@@ -51,7 +52,8 @@ def main():
             reg.put(a, rng.uniform(-s, s, (layers, w.d_in, r)).astype(np.float32),
                     rng.uniform(-s, s, (layers, r, w.d_out)).astype(np.float32))
         xs = [torch.empty(w.tokens, w.d_in, dtype=torch.bfloat16, device=dev).uniform_(-1, 1) for _ in range(layers)]
-        ys = [torch.empty(w.tokens, w.d_out, dtype=torch.bfloat16, device=dev).uniform_(-1, 1) for _ in range(layers)]
+        ydt = torch.bfloat16 if args.y_dtype == "bf16" else torch.float32
+        ys = [torch.empty(w.tokens, w.d_out, dtype=ydt, device=dev).uniform_(-1, 1) for _ in range(layers)]
         ref = None
         y0 = ys[0].clone()
         variants = args.paths.split(",") if not args.launches else [
