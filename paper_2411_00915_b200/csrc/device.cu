@@ -3107,7 +3107,8 @@ int atmm_forward_create_opts(const atmm_plan* plan, int device, int64_t n, int64
     f->nkb = static_cast<int32_t>((d + kBK - 1) / kBK);
     f->row_tiles = static_cast<int32_t>((n_ + kTileM - 1) / kTileM);
     // 2-SM CTA pairs (cta_group::2, M = 256) whenever there are two row tiles:
-    // each SM then stages half of every W block (ATMM_FWD_PAIR=0: 1-SM tiles).
+    // each SM then stages half of every W block (without a bypass,
+    // atmm_gemm_opts::pair forces either).
     // With a bypass, pairs pay for the union of two row tiles' extension
     // chunks; they are taken when the GEMM is large enough to amortise it
     // (measured: cfg5-sized batches win, cfg2/cfg3-sized ones lose).

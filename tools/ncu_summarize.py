@@ -42,8 +42,7 @@ def raw(rep):
                 key = METRICS[h]
                 try:
                     fv = float(v.replace(",", ""))
-                except ValueError:
-                    d.setdefault(key, (v, u))
+                except ValueError:  # "n/a" and the like: not a number, skip
                     continue
                 if key in ("duration", "dram_read", "dram_write", "l2_bytes") and key in d:
                     d[key] = (d[key][0] + fv, u)
