@@ -785,23 +785,13 @@ static int expand_g_bf16() { return 2; }
 
 // Split expand output: staged in shared memory and stored by 16-byte
 // accesses, or stored straight from the epilogue registers (G x element
-// bytes per thread and row).  Measured per kernel variant; the environment
-// variable ATMM_SPLIT_STORE=staged|direct overrides (A/B measurement).
-static int split_out_staged(int y_dtype, int g) {
-  static const int force = [] {
-    const char* e = std::getenv("ATMM_SPLIT_STORE");
-    if (!e) return -1;
-    return std::strcmp(e, "staged") == 0 ? 1 : (std::strcmp(e, "direct") == 0 ? 0 : -1);
-  }();
-  if (force >= 0) return force;
-  // measured (tools/path_bench.py, B200): staged wins for G = 1 items (bf16:
-  // 2-byte direct stores, rank-128 Input2 94.8 -> 81.3 us; fp32 cfg3 46.4 ->
-  // 43.8, cfg5 118.3 -> 113.5 us) and loses for bf16 G = 2, whose direct
-  // 4-byte stores already fill a line per warp row (cfg3 37.7 vs 40.6, cfg5
-  // 89.4 vs 96.7 us: the per-item barrier and the extra shared-memory pass)
-  (void)y_dtype;
-  return g == 1 ? 1 : 0;
-}
+// bytes per thread and row).  Measured (tools/path_bench.py, B200): staged
+// wins for G = 1 items (bf16: 2-byte direct stores, rank-128 Input2 94.8 ->
+// 81.3 us; fp32 cfg3 46.4 -> 43.8, cfg5 118.3 -> 113.5 us) and loses for
+// bf16 G = 2, whose direct 4-byte stores already fill a line per warp row
+// (cfg3 37.7 vs 40.6, cfg5 89.4 vs 96.7 us: the per-item barrier and the
+// extra shared-memory pass).
+static int split_out_staged(int g) { return g == 1 ? 1 : 0; }
 
 // Fixed per-item costs (bytes-equivalent: barriers, 4 MMAs) of the split
 // kernels' work balancing.
@@ -1478,7 +1468,7 @@ static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.estages = g.split.estages[sp.y_dtype];
       sp.expand_g = sp.y_dtype == 0 ? g.split.g_bf16 : 1;
       sp.e_tmem_cols = g.split.tmem_e[sp.y_dtype];
-      sp.out_staged = split_out_staged(sp.y_dtype, sp.expand_g);
+      sp.out_staged = split_out_staged(sp.expand_g);
       sp.rows_max = g.rows_max;
       sp.s_begin = sb.tables.p;
       sp.e_begin = sb.tables.p + (P + 1) * (sp.y_dtype == 0 ? 1 : 2);
