@@ -242,7 +242,10 @@ void atmm_plan_destroy(atmm_plan* p);
  * launch on the stream can still run, and the apply proceeds early only when
  * that launch is an all-to-all bypass whose X / Y bytes are disjoint from
  * this apply's (consecutive independent batches overlap; Y_i -> X_i+1 chains
- * keep the full dependency).  Under stream capture the predecessor is also
+ * keep the full dependency).  The split path's shrink likewise computes under
+ * the preceding bypass launch when that launch's Y writes miss this apply's X
+ * (it reads only X, the factors and a scratch set private to this apply; it
+ * waits and releases the expand at its end).  Under stream capture the predecessor is also
  * matched by graph node.  Not visible to the check: a FOREIGN kernel launched
  * with the programmatic-stream-serialization attribute between two eager
  * applies on one stream -- set this flag when a caller does that. */
@@ -251,6 +254,9 @@ int atmm_plan_set_flags(atmm_plan* p, uint32_t flags);
 /* Process-wide counters: all-to-all bypass launches issued, and how many of
  * them started their X / Y loads early (ATMM_PLAN_NO_OVERLAP above). */
 int atmm_overlap_stats(int64_t* a2a_launches, int64_t* early_launches);
+/* The same for split-path applies: shrink + expand pairs issued, and how many
+ * shrinks computed under the preceding launch. */
+int atmm_split_overlap_stats(int64_t* split_launches, int64_t* early_launches);
 /* Routing tables actually uploaded (for bit-exact routing checks):
  * seg_adapter[S], seg_offsets[S+1], row_index[n]. */
 int atmm_plan_routing(const atmm_plan* p, int32_t* seg_adapter, int64_t* seg_offsets,

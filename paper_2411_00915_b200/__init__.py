@@ -22,7 +22,7 @@ _ATMM_NAMES = (
     "save_matrix", "shard_rows", "flops_read", "flops_reset", "FlopScope", "bypass_flops",
     "TuneShape", "default_shape_grid", "default_launch_candidates", "benchmark_launch", "grid_bench_ns",
     "tiling_search", "table_from_scores", "gemm_f32", "forward_f32", "UNMERGED", "MERGED", "MIXTURE",
-    "default_table", "DEFAULT_TABLE_PATH", "overlap_stats",
+    "default_table", "DEFAULT_TABLE_PATH", "overlap_stats", "split_overlap_stats",
 )
 
 __all__ = list(_ATMM_NAMES)

@@ -31,6 +31,7 @@ _SIGS = {
     "atmm_abi_version": (c_int, []),
     "atmm_device_count": (c_int, []),
     "atmm_overlap_stats": (c_int, [i64p, i64p]),
+    "atmm_split_overlap_stats": (c_int, [i64p, i64p]),
     "atmm_flops_read": (ctypes.c_uint64, []),
     "atmm_flops_reset": (None, []),
     "atmm_bypass_flops": (c_int, [i32p, c_int64, i32p, i64p, c_int64, c_int64, c_int64, POINTER(ctypes.c_uint64)]),

@@ -432,6 +432,13 @@ def overlap_stats() -> Tuple[int, int]:
     return int(a.value), int(e.value)
 
 
+def split_overlap_stats() -> Tuple[int, int]:
+    """(split-path shrink + expand pairs launched, shrinks that started early) so far."""
+    a, e = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib.atmm_split_overlap_stats(ctypes.byref(a), ctypes.byref(e)))
+    return int(a.value), int(e.value)
+
+
 class BypassPlan:
     """plan_batch + launch grouping for one batch on one registry."""
 

@@ -690,21 +690,48 @@ struct SplitBufs {
   int32_t grid = 0;
   size_t part_elems = 0, mid_elems = 0, counter_elems = 0;
   std::mutex mu;
-  std::vector<std::pair<cudaStream_t, std::unique_ptr<SplitScratch>>> scratch;
+  // per stream: two scratch sets (the split path alternates them so that a
+  // shrink may run under the previous apply's expand, SplitParams::early);
+  // the stream path uses set 0 only
+  struct StreamSets {
+    cudaStream_t stream = nullptr;
+    std::unique_ptr<SplitScratch> set[2];
+    int next = 0;
+  };
+  std::vector<std::unique_ptr<StreamSets>> scratch;
   static constexpr size_t kMaxStreams = 32;
 
-  // The scratch set of `stream`.  A new stream's set is allocated and zeroed
-  // outside the caller's stream (relaxed capture mode for this thread, a
-  // private non-blocking stream for the zero fill), so the first apply on a
-  // stream may happen inside a CUDA graph capture.
+  // Scratch set `k` of `stream`.  A new set is allocated and zeroed outside
+  // the caller's stream (relaxed capture mode for this thread, a private
+  // non-blocking stream for the zero fill), so the first apply on a stream
+  // may happen inside a CUDA graph capture.
   SplitScratch& for_stream(cudaStream_t stream) {
     std::lock_guard<std::mutex> lk(mu);
-    for (auto& [s, sc] : scratch) {
-      if (s == stream) return *sc;
+    return set_of(sets_of(stream), 0);
+  }
+  // The split path: the set after the one this stream used last.
+  SplitScratch& alternate(cudaStream_t stream) {
+    std::lock_guard<std::mutex> lk(mu);
+    StreamSets& ss = sets_of(stream);
+    const int k = ss.next;
+    ss.next ^= 1;
+    return set_of(ss, k);
+  }
+
+ private:
+  StreamSets& sets_of(cudaStream_t stream) {
+    for (auto& ss : scratch) {
+      if (ss->stream == stream) return *ss;
     }
     if (scratch.size() >= kMaxStreams) {
       fail(ATMM_ERR_CONFIG, "split-path plan applied on more than 32 distinct streams");
     }
+    scratch.push_back(std::make_unique<StreamSets>());
+    scratch.back()->stream = stream;
+    return *scratch.back();
+  }
+  SplitScratch& set_of(StreamSets& ss, int k) {
+    if (ss.set[k]) return *ss.set[k];
     cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
     cudaThreadExchangeStreamCaptureMode(&mode);
     auto sc = std::make_unique<SplitScratch>();
@@ -726,8 +753,8 @@ struct SplitBufs {
     if (init) cudaStreamDestroy(init);
     cudaThreadExchangeStreamCaptureMode(&mode);
     if (err != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("split scratch init failed: ") + cudaGetErrorString(err));
-    scratch.emplace_back(stream, std::move(sc));
-    return *scratch.back().second;
+    ss.set[k] = std::move(sc);
+    return *ss.set[k];
   }
 };
 
@@ -1229,7 +1256,7 @@ struct PdlKey {
 };
 std::mutex g_pdl_mu;
 std::map<PdlKey, PdlRecord> g_pdl;
-std::atomic<int64_t> g_a2a_launches{0}, g_a2a_early{0};
+std::atomic<int64_t> g_a2a_launches{0}, g_a2a_early{0}, g_split_launches{0}, g_split_early{0};
 
 struct PdlCapture {
   bool capturing = false;
@@ -1272,6 +1299,24 @@ static bool pdl_can_elide(cudaStream_t s, const PdlCapture& c, const PdlRange* x
   for (int i = 0; i < n; ++i) {
     for (int j = 0; j < r.n; ++j) {
       if (xs[i].overlaps(r.y[j]) || ys[i].overlaps(r.y[j]) || ys[i].overlaps(r.x[j])) return false;
+    }
+  }
+  return true;
+}
+
+// Whether a launch that only READS xs before its own griddepcontrol.wait
+// (the split shrink; it writes nothing but private scratch) may start under
+// the preceding launch on `s`: that launch is a recorded bypass whose Y
+// writes miss xs.
+static bool pdl_can_elide_reads(cudaStream_t s, const PdlCapture& c, const PdlRange* xs, int n) {
+  std::lock_guard<std::mutex> lk(g_pdl_mu);
+  auto it = g_pdl.find(PdlKey{s, c.id});
+  if (it == g_pdl.end() || !it->second.valid) return false;
+  const PdlRecord& r = it->second;
+  if (c.capturing && (c.single_dep == nullptr || c.single_dep != r.node)) return false;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < r.n; ++j) {
+      if (xs[i].overlaps(r.y[j])) return false;
     }
   }
   return true;
@@ -1446,7 +1491,7 @@ static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t
     if (path == BypassPath::kSplit && !as_merged) path = BypassPath::kFused;  // split runs only as the merged range
     if (path == BypassPath::kSplit) {
       SplitBufs& sb = *p->merged_bufs;
-      SplitScratch& sc = sb.for_stream(stream);
+      SplitScratch& sc = sb.alternate(stream);
       const int P = sb.grid;
       const int T = static_cast<int>(g.num_tiles);
       SplitParams sp{};
@@ -1469,6 +1514,12 @@ static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.expand_g = sp.y_dtype == 0 ? g.split.g_bf16 : 1;
       sp.e_tmem_cols = g.split.tmem_e[sp.y_dtype];
       sp.out_staged = split_out_staged(sp.expand_g);
+      // The shrink may run under the preceding launch (until its own end)
+      // when that launch is a recorded bypass whose writes miss X: it reads
+      // only X, the factors and its own scratch set (the other set than the
+      // preceding apply of this plan on this stream).
+      PdlRange xr = byte_range(x, p->n, reg->d_in, ldx, 2), yr = byte_range(y, p->n, reg->d_out, ldy, ysz);
+      sp.early = (p->flags & ATMM_PLAN_NO_OVERLAP) ? 0 : (pdl_can_elide_reads(stream, pdl_capture_info(stream), &xr, 1) ? 1 : 0);
       sp.rows_max = g.rows_max;
       sp.s_begin = sb.tables.p;
       sp.e_begin = sb.tables.p + (P + 1) * (sp.y_dtype == 0 ? 1 : 2);
@@ -1485,6 +1536,9 @@ static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t
       pdl_note_other(stream);
       const cudaError_t e = launch_split(sp.y_dtype, sp, P, g.split.smem_s, g.split.smem_e[sp.y_dtype], stream);
       if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
+      pdl_record_a2a(stream, &xr, &yr, 1);  // the expand: reads / writes Y, the shrink read X
+      g_split_launches.fetch_add(1, std::memory_order_relaxed);
+      if (sp.early) g_split_early.fetch_add(1, std::memory_order_relaxed);
       continue;
     }
     BypassParams bp{};
@@ -2027,6 +2081,12 @@ int atmm_plan_create_launch(atmm_registry* r, const int32_t* assignment, int64_t
 int atmm_overlap_stats(int64_t* a2a_launches, int64_t* early_launches) {
   if (a2a_launches) *a2a_launches = g_a2a_launches.load();
   if (early_launches) *early_launches = g_a2a_early.load();
+  return ATMM_OK;
+}
+
+int atmm_split_overlap_stats(int64_t* split_launches, int64_t* early_launches) {
+  if (split_launches) *split_launches = g_split_launches.load();
+  if (early_launches) *early_launches = g_split_early.load();
   return ATMM_OK;
 }
 

@@ -143,6 +143,8 @@ struct SplitParams {
   int32_t expand_g;      // output columns per expand epilogue thread (items of 128 G columns)
   uint32_t e_tmem_cols;  // expand TMEM allocation: >= 2 x G x rows16 (two accumulators)
   int32_t out_staged;    // expand: update Y rows in shared memory, store them with 16-byte accesses
+  int32_t early;         // shrink: compute before waiting for the preceding launch (the host proved
+                         // it writes nothing the shrink reads); wait + release at the shrink's end
   int32_t r_pad_max;
   int32_t stages;        // shrink ring depth
   int32_t estages;       // expand ring depth

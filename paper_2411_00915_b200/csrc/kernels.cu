@@ -1497,8 +1497,14 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
   // launch at once: its CTAs take the SMs of finished shrink CTAs and stage
   // their prologue and first up^T / Y loads under this grid's tail (they read
   // the partials only after their own griddepcontrol.wait).
-  griddep_wait();
-  griddep_launch_dependents();
+  // Early (p.early): the preceding launch writes nothing this grid reads, and
+  // this apply's scratch set is not the one it uses: compute first, then wait
+  // and release at the end (wait-before-release: when the expand starts, every
+  // earlier grid is complete, so it may still read Y before its own wait).
+  if (!p.early) {
+    griddep_wait();
+    griddep_launch_dependents();
+  }
   // (The expand launch's per-tile readiness counters are zero here: the
   // previous expand on this stream reset them as its last CTA left.)
 
@@ -1524,7 +1530,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
     int64_t xoff[kRowsPer];
     int cur_t = -1, rows = 0, r_pad = 0;
     const uint16_t* down_t = nullptr;
-    griddep_wait();  // X may be produced by the previous kernel
+    if (!p.early) griddep_wait();  // X may be produced by the previous kernel
     int j = 0;
     for (int item = i_beg; item < i_end; ++item, ++j) {
       const int t = item / p.nkb;
@@ -1641,6 +1647,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
   __threadfence();
   __syncthreads();
   if (tid == 0) STRACE(3);
+  if (p.early) griddep_wait();
   griddep_launch_dependents();
   if (warp == kSplitWarpMMA) {
     tc_fence_after();

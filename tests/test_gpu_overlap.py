@@ -209,3 +209,102 @@ def test_grouped_launches_overlap_same_bits(gpu, atmm, oracle):
         assert torch.equal(u, v)
     # the second group is disjoint from the first; the third reads Y5 / Y6 / Y7 the second wrote (RAW)
     assert early[1] == 0 and early[0] <= 2
+
+
+def _split_setup(atmm, oracle, seed=9):
+    import torch
+
+    reg = atmm.AdapterRegistry(2, D, D)
+    rng = oracle.rng(seed)
+    ranks = {0: 16, 1: 64, 2: 32}
+    facs = {0: {}, 1: {}}
+    for a, r in ranks.items():
+        s = 1.0 / np.sqrt(np.float32(r))
+        down = oracle.round_bf16(oracle.random_matrix(rng, 2 * D, r, -s, s).reshape(2, D, r))
+        up = oracle.round_bf16(oracle.random_matrix(rng, 2 * r, D, -s, s).reshape(2, r, D))
+        reg.put(a, down, up)
+        for l in range(2):
+            facs[l][a] = (down[l], up[l])
+    assignment = np.repeat(np.asarray(sorted(ranks), np.int32), 128)
+    assignment = assignment[np.random.default_rng(seed).permutation(assignment.size)]
+    from conftest import path_table
+
+    plan = atmm.BypassPlan(reg, assignment, path_table(atmm, assignment, ranks, D, D, "split"))
+    ref_plan = atmm.BypassPlan(reg, assignment, path_table(atmm, assignment, ranks, D, D, "split"))
+    ref_plan.set_overlap(False)
+    assert {g["path_bf16"] for g in plan.describe()} == {"split"}
+    n = assignment.size
+    bufs = [torch.empty(n, D, dtype=torch.bfloat16, device="cuda").uniform_(-1, 1) for _ in range(8)]
+    return plan, ref_plan, bufs, assignment, facs
+
+
+@pytest.mark.parametrize("steps,min_early,max_early", [
+    ([(0, 1), (2, 3), (4, 5), (6, 7), (0, 3)], 4, 5),   # independent: every shrink after the first runs early
+    ([(0, 1), (1, 2), (2, 3), (3, 4)], 0, 0),           # Y_i is X_i+1: the shrink must wait
+    ([(0, 1), (2, 0), (0, 5)], 1, 1),                   # WAR on X0 is harmless for the shrink; (0, 5) reads Y of (2, 0)
+])
+def test_split_shrink_early_same_bits(gpu, atmm, oracle, steps, min_early, max_early):
+    """Split-path applies: the shrink computes under the preceding expand only
+    when that expand's Y writes miss its X, with alternating scratch sets;
+    results equal the full-dependency plan bit for bit, eager and captured."""
+    import torch
+
+    plan, ref_plan, bufs, _, _ = _split_setup(atmm, oracle)
+    res = []
+    for p in (plan, ref_plan):
+        work = [b.clone() for b in bufs]
+        s = torch.cuda.Stream()
+        before = atmm.split_overlap_stats()
+        with torch.cuda.stream(s):
+            for i, (xi, yi) in enumerate(steps):
+                p.apply(work[xi], work[yi], layer=i % 2, stream=s)
+        s.synchronize()
+        after = atmm.split_overlap_stats()
+        if p is plan:
+            assert after[0] - before[0] == len(steps)
+            assert min_early <= after[1] - before[1] <= max_early, (before, after)
+        else:
+            assert after[1] == before[1]
+        res.append(work)
+    for u, v in zip(*res):
+        assert torch.equal(u, v)
+
+
+def test_split_shrink_early_graph_fresh_inputs_oracle(gpu, atmm, oracle):
+    """A captured graph of independent split applies (early shrinks, scratch
+    sets alternating, odd step count so replays start on the other set)
+    replayed twice, every output against the oracle."""
+    import torch
+
+    from conftest import tol_for
+
+    plan, _, _, assignment, facs = _split_setup(atmm, oracle, seed=13)
+    n = assignment.size
+    steps = 5
+    rng = oracle.rng(3)
+    xs = [oracle.round_bf16(oracle.random_matrix(rng, n, D)) for _ in range(steps)]
+    ys = [oracle.round_bf16(oracle.random_matrix(rng, n, D)) for _ in range(steps)]
+    xt = [torch.from_numpy(x).to("cuda", torch.bfloat16) for x in xs]
+    yt = [torch.from_numpy(y).to("cuda", torch.bfloat16) for y in ys]
+    s = torch.cuda.Stream()
+    warm = torch.empty_like(yt[0])
+    with torch.cuda.stream(s):
+        plan.apply(xt[0], warm, layer=0, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    before = atmm.split_overlap_stats()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        for i in range(steps):
+            plan.apply(xt[i], yt[i], layer=i % 2, stream=s)
+    after = atmm.split_overlap_stats()
+    assert after[1] - before[1] == steps - 1
+    for rep in range(2):
+        for i in range(steps):
+            yt[i].copy_(torch.from_numpy(ys[i]).to("cuda", torch.bfloat16))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        for i in range(steps):
+            want = ys[i].astype(np.float64) + oracle.bypass_rows_f64(xs[i], assignment, facs[i % 2])
+            got = yt[i].float().cpu().numpy()
+            assert float(np.max(np.abs(got - want))) <= tol_for(want), (rep, i)
