@@ -380,8 +380,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   auto tile_of = [&](int g) { return mc == 1 ? g : (g / gpr) * p.ntn + (g % gpr) * mc + mr; };
   const int kb0 = p.nkb * z / kz, kb1 = p.nkb * (z + 1) / kz;
   const int nk2 = (p.nkb + 1) / 2, j0 = nk2 * z / kz, j1 = nk2 * (z + 1) / kz;  // bk2: 128-deep K blocks
-  const bool do_ext = p.exts != nullptr && z == kz - 1;
-  const int rows_per = kTileM / kz;
+  // K-extension (bypass) blocks of a split-K tile are dealt round-robin over
+  // the cluster's ranks (ext e to rank (e - first) % kz): no rank's K loop is
+  // longer than the others' by all of them
+  const bool do_ext = p.exts != nullptr;
+  // split-K: one tile per cluster; only its valid rows (a batch of n < 128
+  // rows pads the tile) are staged, exchanged and reduced, rows_per per rank
+  const int64_t left = p.n - int64_t(cl / (p.ntn > 0 ? p.ntn : 1)) * kTileM;
+  const int valid = kz > 1 ? static_cast<int>(left < 0 ? 0 : (left > kTileM ? kTileM : left)) : kTileM;
+  const int rows_per = kz > 1 ? ((valid + kz - 1) / kz + 7) & ~7 : kTileM;
   const int pitch = bn + 4;  // fp32 words per staged row (16-byte skew)
   const uint32_t slot_bytes = static_cast<uint32_t>(rows_per * pitch) * 4u;
 
@@ -461,7 +468,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
         if (!do_ext) continue;
-        for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
+        for (int e = p.ext_begin[t] + z; e < p.ext_begin[t + 1]; e += kz, ++i) {
           if (!waited) {
             griddep_wait();  // the A images are the shrink launch's output
             FTRACE(4096, 3);
@@ -537,7 +544,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
         }
         if (do_ext) {
-          for (int e = p.ext_begin[t]; e < p.ext_begin[t + 1]; ++e, ++i) {
+          for (int e = p.ext_begin[t] + z; e < p.ext_begin[t + 1]; e += kz, ++i) {
             const int kk = p.exts[e].kk;
             const int s = i % S;
             mbar_wait(&full[s], static_cast<uint32_t>(i / S) & 1u);
@@ -611,7 +618,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (threadIdx.x == 64) FTRACE(4096, 4);
       tc_fence_after();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
-      for (int c = 0; c < bn; c += 32) {
+      // quadrants wholly past the exchanged rows stage nothing
+      for (int c = 0; q * 32 < rows_per * kz && c < bn; c += 32) {
         uint32_t v[32];
         tmem_ld32(tbase + static_cast<uint32_t>(c), v);
         tmem_wait_ld();
