@@ -3215,7 +3215,17 @@ int atmm_forward_create_opts(const atmm_plan* plan, int device, int64_t n, int64
     const int64_t pair_tiles = int64_t((f->row_tiles + 1) / 2) * ((d + 255) / 256);
     f->pair = bypass_plan ? f->row_tiles >= 2 && pair_tiles >= 2 * sms : pair_without_bypass(n_, d, d, sms, o);
     if (o.pair >= 0) f->pair = f->row_tiles >= 2 && o.pair != 0;
-    const GemmTiling gt = gemm_tiling(n_, d, d, sms, f->pair, o);
+    GemmTiling gt = gemm_tiling(n_, d, d, sms, f->pair, o);
+    // With a bypass, the shrink launch (a cluster of up to 16 K slices per
+    // item) runs beside the GEMM: a split-K grid that leaves less than two
+    // such clusters of SMs free has clusters that only start once the shrink
+    // is done and then set the layer's end (tools/fwd_trace.py --graph, cfg1:
+    // kz 4 -> 2 measured 20.2 -> 19.2 us per layer).
+    if (bypass_plan && !f->pair && o.kz == 0 && gt.kz > 1 && gt.grid + 32 > sms) {
+      atmm_gemm_opts o2 = o;
+      o2.kz = gt.kz / 2;
+      gt = gemm_tiling(n_, d, d, sms, f->pair, o2);
+    }
     f->bk2 = gt.bk2;
     f->bn = gt.bn;
     f->ntn = gt.ntn;
