@@ -37,7 +37,8 @@ cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t sme
 cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassParams& p, int C, int num_tiles,
                               size_t smem, cudaStream_t stream);
 cudaError_t launch_stream(int y_dtype, const StreamParams& p, int grid, size_t smem, cudaStream_t stream);
-cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,
+cudaError_t launch_split(int y_dtype, const CUtensorMap& xtile, const CUtensorMap& ytile, const SplitParams& p, int grid,
+                         size_t smem_s, size_t smem_e,
                          cudaStream_t stream);
 cudaError_t launch_merge_tma(int w_dtype, const CUtensorMap& tmap_w, const MergeParams& p, int grid,
                              size_t smem, cudaStream_t stream);
@@ -152,6 +153,22 @@ CUtensorMap make_x_map(const void* x, int64_t n, int64_t d_in, int64_t ldx) {
   return m;
 }
 
+// X as 128-row tiles (split shrink, tiles of consecutive rows): box = 128
+// rows x one 64-wide K block, 128-byte swizzle = the K-major MMA operand.
+CUtensorMap make_x_tile_map(const void* x, int64_t n, int64_t d_in, int64_t ldx) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d_in), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldx) * 2};
+  const cuuint32_t box[2] = {kBK, kTileM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(X tiles) failed: " + std::to_string(r));
+  return m;
+}
+
 // Y (n x d_out, bf16 or fp32): box = one 128-byte row slice, 128-byte
 // swizzle, gathered 4 rows at a time into the kernel's Y ring.
 CUtensorMap make_y_map(const void* y, int64_t n, int64_t d_out, int64_t ldy, int y_dtype) {
@@ -169,7 +186,47 @@ CUtensorMap make_y_map(const void* y, int64_t n, int64_t d_out, int64_t ldy, int
   return m;
 }
 
-// Small per-thread cache of encoded X / Y maps (kind 0: X, 1 + y_dtype: Y).
+// Y as blocks of box_rows consecutive rows x box_cols columns (split expand,
+// tiles of consecutive rows), no swizzle: the stage's dense Y rows.  Cached
+// per thread like cached_map.
+CUtensorMap y_tile_map(const void* y, int64_t n, int64_t d_out, int64_t ldy, int y_dtype, int box_cols, int box_rows) {
+  struct Entry {
+    const void* base = nullptr;
+    int64_t n = 0, d = 0, ld = 0;
+    int dt = 0, bc = 0, br = 0;
+    CUtensorMap map;
+  };
+  thread_local Entry cache[4];
+  thread_local int next = 0;
+  for (const auto& e : cache) {
+    if (e.base == y && e.n == n && e.d == d_out && e.ld == ldy && e.dt == y_dtype && e.bc == box_cols && e.br == box_rows) {
+      return e.map;
+    }
+  }
+  Entry& e = cache[next];
+  next = (next + 1) % 4;
+  const int64_t esz = y_dtype == ATMM_BF16 ? 2 : 4;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(d_out), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldy * esz)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&e.map, y_dtype == ATMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 2, const_cast<void*>(y), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ATMM_ERR_CUDA, "cuTensorMapEncodeTiled(Y tiles) failed: " + std::to_string(r));
+  e.base = y;
+  e.n = n;
+  e.d = d_out;
+  e.ld = ldy;
+  e.dt = y_dtype;
+  e.bc = box_cols;
+  e.br = box_rows;
+  return e.map;
+}
+
+// Small per-thread cache of encoded X / Y maps (kind 0: X rows, 1 + y_dtype:
+// Y, 3: X tiles).
 CUtensorMap cached_map(int kind, const void* base, int64_t rows, int64_t cols, int64_t ld) {
   struct Entry {
     const void* base;
@@ -189,7 +246,9 @@ CUtensorMap cached_map(int kind, const void* base, int64_t rows, int64_t cols, i
   }
   Entry& e = cache[next];
   next = (next + 1) % 8;
-  e.map = kind == 0 ? make_x_map(base, rows, cols, ld) : make_y_map(base, rows, cols, ld, kind - 1);
+  e.map = kind == 0   ? make_x_map(base, rows, cols, ld)
+          : kind == 3 ? make_x_tile_map(base, rows, cols, ld)
+                      : make_y_map(base, rows, cols, ld, kind - 1);
   e.base = base;
   e.rows = rows;
   e.cols = cols;
@@ -777,6 +836,7 @@ struct atmm_plan {
   DevBuf<int32_t> d_rows;
   DevBuf<int32_t> d_tile_rows;  // [tile][kTileM] padded row lists (a2a prologue)
   std::vector<int32_t> rows_host;  // routed entry (plan order) -> X / Y row
+  bool any_contig = false;         // some tile's rows are consecutive (TileDesc::x_row0)
   DevBuf<TileDesc> d_tiles;
   int64_t total_ctas = 0;
   uint64_t flops = 0;  // algorithmic FLOPs of one apply (flops.hpp accounting)
@@ -1185,10 +1245,16 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
   {
     std::vector<int32_t> tr(all_tiles.size() * kTileM);
     for (size_t t = 0; t < all_tiles.size(); ++t) {
-      const TileDesc& td = all_tiles[t];
+      TileDesc& td = all_tiles[t];
       for (int i = 0; i < kTileM; ++i) {
         tr[t * kTileM + i] = plan->rows_host[static_cast<size_t>(td.row_begin + std::min(i, std::max(td.rows, 1) - 1))];
       }
+      // consecutive rows (a prefill request, a sorted batch): the split
+      // kernels move the tile's X / Y by TMA boxes instead of row gathers
+      bool contig = td.rows > 0;
+      for (int i = 1; contig && i < td.rows; ++i) contig = tr[t * kTileM + i] == tr[t * kTileM] + i;
+      td.x_row0 = contig ? tr[t * kTileM] : -1;
+      if (contig) plan->any_contig = true;
     }
     plan->d_tile_rows.alloc(std::max<size_t>(tr.size(), 1));
     if (!tr.empty()) CUDA_CHECK(cudaMemcpy(plan->d_tile_rows.p, tr.data(), tr.size() * 4, cudaMemcpyHostToDevice));
@@ -1534,7 +1600,14 @@ static void apply_pass(const atmm_plan* p, int64_t layer, const void* x, int64_t
       sp.counter = sc.counter.p;
       sp.trace = g_trace;
       pdl_note_other(stream);
-      const cudaError_t e = launch_split(sp.y_dtype, sp, P, g.split.smem_s, g.split.smem_e[sp.y_dtype], stream);
+      // tiles of consecutive rows load X by 128-row TMA boxes (TileDesc::x_row0)
+      CUtensorMap xtile{}, ytile{};
+      sp.contig = p->any_contig ? 1 : 0;
+      if (p->any_contig) {
+        xtile = cached_map(3, x, p->n, reg->d_in, ldx);
+        ytile = y_tile_map(y, p->n, reg->d_out, ldy, y_dtype, 128 * sp.expand_g, sp.rows_max);
+      }
+      const cudaError_t e = launch_split(sp.y_dtype, xtile, ytile, sp, P, g.split.smem_s, g.split.smem_e[sp.y_dtype], stream);
       if (e != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("bypass launch failed: ") + cudaGetErrorString(e));
       pdl_record_a2a(stream, &xr, &yr, 1);  // the expand: reads / writes Y, the shrink read X
       g_split_launches.fetch_add(1, std::memory_order_relaxed);

@@ -28,6 +28,8 @@ struct TileDesc {
   int32_t rows;
   int32_t r_pad;
   float scale;
+  int32_t x_row0 = -1;        // the tile's rows are X / Y rows x_row0 .. x_row0 + rows - 1 (one
+                              // TMA box, split path), else -1 (gathered row by row)
 };
 
 // One registry slot (adapter), device resident.  Factors are bf16 in the
@@ -143,6 +145,7 @@ struct SplitParams {
   int32_t expand_g;      // output columns per expand epilogue thread (items of 128 G columns)
   uint32_t e_tmem_cols;  // expand TMEM allocation: >= 2 x G x rows16 (two accumulators)
   int32_t out_staged;    // expand: update Y rows in shared memory, store them with 16-byte accesses
+  int32_t contig;        // some tile has consecutive rows (TileDesc::x_row0): X / Y by TMA boxes
   int32_t early;         // shrink: compute before waiting for the preceding launch (the host proved
                          // it writes nothing the shrink reads); wait + release at the shrink's end
   int32_t r_pad_max;

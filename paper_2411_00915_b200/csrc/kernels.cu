@@ -1472,7 +1472,9 @@ __device__ __forceinline__ void split_rows_out(uint32_t ysrc, uint32_t pitch, ui
 
 // ---- shrink: partial mid rows per (tile, CTA) segment, stream-K over K ----
 //   stage = [A: 128 rows x 128 B, 128-byte swizzle | B: r_pad_max x 64 down^T]
-__global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const SplitParams p) {
+template <bool kContig>  // some tile of the launch has consecutive rows (TileDesc::x_row0)
+__global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const __grid_constant__ CUtensorMap xtile,
+                                                                          const SplitParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -1528,7 +1530,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
     const int ch = static_cast<int>(tid & 7);
     const int r0 = static_cast<int>(tid >> 3);
     int64_t xoff[kRowsPer];
-    int cur_t = -1, rows = 0, r_pad = 0;
+    int cur_t = -1, rows = 0, r_pad = 0, x_row0 = -1;
     const uint16_t* down_t = nullptr;
     if (!p.early) griddep_wait();  // X may be produced by the previous kernel
     int j = 0;
@@ -1540,6 +1542,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
         cur_t = t;
         rows = tile.rows;
         r_pad = tile.r_pad;
+        x_row0 = kContig ? tile.x_row0 : -1;
         down_t = tile.down_t + static_cast<int64_t>(p.layer) * tile.down_layer_stride;
         // padded per-tile row table: independent of the descriptor load
 #pragma unroll
@@ -1551,17 +1554,26 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
       const int st = j % S;
       mbar_wait(&empty[st], static_cast<uint32_t>(((j / S) & 1) ^ 1));
       const uint32_t A = smem0 + static_cast<uint32_t>(st) * stage_bytes;
-      // columns past d_in (last K block) are zero-filled, never read
-      const int col = kb * kBK + ch * 8;
-      const uint32_t nb = static_cast<uint32_t>(max(0, min(8, p.d_in - col)) * 2);
-      const uint16_t* xk = p.x + (nb ? col : 0);
+      if (!kContig || x_row0 < 0) {
+        // columns past d_in (last K block) are zero-filled, never read
+        const int col = kb * kBK + ch * 8;
+        const uint32_t nb = static_cast<uint32_t>(max(0, min(8, p.d_in - col)) * 2);
+        const uint16_t* xk = p.x + (nb ? col : 0);
 #pragma unroll
-      for (int i = 0; i < kRowsPer; ++i) {
-        const int r = r0 + kRowStep * i;
-        if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], nb);
+        for (int i = 0; i < kRowsPer; ++i) {
+          const int r = r0 + kRowStep * i;
+          if (r < rows) cp_async16(A + static_cast<uint32_t>(r * 128 + ((ch ^ (r & 7)) << 4)), xk + xoff[i], nb);
+        }
       }
       if (tid == 0) {  // the down^T block is one contiguous run: one TMA bulk copy
-        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(r_pad * kBK * 2));
+        // consecutive rows: the X block is one 128-row TMA box (rows past the
+        // tile belong to other tiles or are zero-filled past n; their partial
+        // rows are never stored)
+        const uint32_t xb = kContig && x_row0 >= 0 ? a_bytes : 0u;
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(r_pad * kBK * 2) + xb);
+        if (kContig && x_row0 >= 0) {
+          tma_load_2d(smem + static_cast<size_t>(st) * stage_bytes, &xtile, &full[st], kb * kBK, x_row0);
+        }
         bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes + a_bytes, down_t + static_cast<int64_t>(kb) * r_pad * kBK,
                  static_cast<uint32_t>(r_pad * kBK * 2), &full[st]);
       }
@@ -1662,7 +1674,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) atmm_shrink_kernel(const Sp
 //   output columns (32 q + l) G .. + G - 1 (one 2 G-byte access per row).
 //   stage = [up^T 128 G x r_pad_max | mid rows16_max x r_pad_max | Y rows_max x 128 G | rows]
 template <typename YT, int G, bool kStaged>
-__global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const SplitParams p) {
+__global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const __grid_constant__ CUtensorMap ytile,
+                                                                        const SplitParams p) {
   extern __shared__ uint8_t smem_raw[];
   // interleave (no-swizzle) operands only need 16-byte alignment: align to 128
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
@@ -1765,10 +1778,19 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       // writer of Y has completed: Y may be read before our own wait.
       const int cpr = ncols * kEsz / 16;
       const uint8_t* yb = reinterpret_cast<const uint8_t*>(p.y) + static_cast<int64_t>(n0) * kEsz;
-      for (int q = static_cast<int>(tid); q < rows * cpr; q += kSplitLoaders) {
-        const int r = q / cpr;
-        const int c = q - r * cpr;
-        cp_async16(Yb + static_cast<uint32_t>(r) * ypitch + c * 16, yb + static_cast<int64_t>(static_cast<int32_t>(ld_shared_u32(Rb + r * 4))) * ldy_b + c * 16, 16u);
+      // consecutive rows: the Y block is one TMA box of rows_max rows x 128 G
+      // columns (rows past the tile are loaded, never stored; columns past
+      // d_out are zero-filled)
+      if (tile.x_row0 >= 0 && tid == 0) {
+        mbar_expect_tx(&full[st], y_bytes);
+        tma_load_2d(smem + static_cast<size_t>(st) * stage_bytes + up_bytes + mid_bytes, &ytile, &full[st], n0, tile.x_row0);
+      }
+      if (tile.x_row0 < 0) {
+        for (int q = static_cast<int>(tid); q < rows * cpr; q += kSplitLoaders) {
+          const int r = q / cpr;
+          const int c = q - r * cpr;
+          cp_async16(Yb + static_cast<uint32_t>(r) * ypitch + c * 16, yb + static_cast<int64_t>(static_cast<int32_t>(ld_shared_u32(Rb + r * 4))) * ldy_b + c * 16, 16u);
+        }
       }
       const uint16_t* ms = p.mid + static_cast<int64_t>(t) * kTileM * p.r_pad_max;
       const int rows16 = (rows + 15) & ~15;
@@ -1907,9 +1929,23 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const Sp
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
       if constexpr (kStaged) {
-        named_bar_sync(5, 256);  // every epilogue warp's updates of this item are in shared memory
-        split_rows_out(Yb, ypitch, rring, rows, ncols * kEsz, reinterpret_cast<uint8_t*>(p.y) + static_cast<int64_t>(n0) * kEsz,
-                       ldy_b, static_cast<int>(warp - kSplitWarpEpi), 8, lane);
+        fence_proxy_async_smem();  // (a TMA store below reads these shared-memory rows)
+        named_bar_sync(5, 256);    // every epilogue warp's updates of this item are in shared memory
+        if (tile.x_row0 >= 0 && rows == p.rows_max) {
+          // consecutive rows filling the box: one TMA store of the block
+          // (columns past d_out are clipped); the stage is released once the
+          // store has read it
+          if (warp == kSplitWarpEpi && lane == 0) {
+            fence_proxy_async_smem();
+            tma_store_2d(&ytile, smem + static_cast<size_t>(st) * stage_bytes + up_bytes + mid_bytes, n0, tile.x_row0);
+            bulk_commit();
+            bulk_wait_read0();
+          }
+          __syncwarp();
+        } else {
+          split_rows_out(Yb, ypitch, rring, rows, ncols * kEsz, reinterpret_cast<uint8_t*>(p.y) + static_cast<int64_t>(n0) * kEsz,
+                         ldy_b, static_cast<int>(warp - kSplitWarpEpi), 8, lane);
+        }
       }
       mbar_arrive(&empty[st]);
     }
@@ -2412,12 +2448,14 @@ template __global__ void atmm_bypass_kernel<__nv_bfloat16>(const __grid_constant
 template __global__ void atmm_bypass_kernel<float>(const __grid_constant__ CUtensorMap,
                                                    const __grid_constant__ CUtensorMap,
                                                    const BypassParams);
-template __global__ void atmm_expand_kernel<__nv_bfloat16, 2, false>(const SplitParams);
-template __global__ void atmm_expand_kernel<__nv_bfloat16, 2, true>(const SplitParams);
-template __global__ void atmm_expand_kernel<__nv_bfloat16, 1, false>(const SplitParams);
-template __global__ void atmm_expand_kernel<__nv_bfloat16, 1, true>(const SplitParams);
-template __global__ void atmm_expand_kernel<float, 1, false>(const SplitParams);
-template __global__ void atmm_expand_kernel<float, 1, true>(const SplitParams);
+template __global__ void atmm_shrink_kernel<false>(const __grid_constant__ CUtensorMap, const SplitParams);
+template __global__ void atmm_shrink_kernel<true>(const __grid_constant__ CUtensorMap, const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 2, false>(const __grid_constant__ CUtensorMap, const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 2, true>(const __grid_constant__ CUtensorMap, const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 1, false>(const __grid_constant__ CUtensorMap, const SplitParams);
+template __global__ void atmm_expand_kernel<__nv_bfloat16, 1, true>(const __grid_constant__ CUtensorMap, const SplitParams);
+template __global__ void atmm_expand_kernel<float, 1, false>(const __grid_constant__ CUtensorMap, const SplitParams);
+template __global__ void atmm_expand_kernel<float, 1, true>(const __grid_constant__ CUtensorMap, const SplitParams);
 template __global__ void atmm_merge_kernel<float>(const MergeParams);
 template __global__ void atmm_merge_kernel<__nv_bfloat16>(const MergeParams);
 template __global__ void atmm_merge_tma_kernel<float>(const __grid_constant__ CUtensorMap, const MergeParams);
@@ -2552,8 +2590,8 @@ cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassPara
   }
 }
 
-cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t smem_s, size_t smem_e,
-                         cudaStream_t stream) {
+cudaError_t launch_split(int y_dtype, const CUtensorMap& xtile, const CUtensorMap& ytile, const SplitParams& p, int grid,
+                         size_t smem_s, size_t smem_e, cudaStream_t stream) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -2564,13 +2602,14 @@ cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t sme
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cfg.dynamicSmemBytes = smem_s;
-  cudaError_t e = prepare(atmm_shrink_kernel, smem_s, false);
+  auto shrink = p.contig ? atmm_shrink_kernel<true> : atmm_shrink_kernel<false>;
+  cudaError_t e = prepare(shrink, smem_s, false);
   if (e != cudaSuccess) return e;
-  e = cudaLaunchKernelEx(&cfg, atmm_shrink_kernel, p);
+  e = cudaLaunchKernelEx(&cfg, shrink, xtile, p);
   if (e != cudaSuccess) return e;
   cfg.blockDim = dim3(kExpandThreads, 1, 1);
   cfg.dynamicSmemBytes = smem_e;
-  void (*k)(const SplitParams);
+  void (*k)(const CUtensorMap, const SplitParams);
   if (y_dtype == 0 && p.expand_g == 1) {
     k = p.out_staged ? atmm_expand_kernel<__nv_bfloat16, 1, true> : atmm_expand_kernel<__nv_bfloat16, 1, false>;
   } else if (y_dtype == 0) {
@@ -2580,7 +2619,7 @@ cudaError_t launch_split(int y_dtype, const SplitParams& p, int grid, size_t sme
   }
   e = prepare(k, smem_e, false);
   if (e != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, k, p);
+  return cudaLaunchKernelEx(&cfg, k, ytile, p);
 }
 
 int bypass_max_active_clusters(int C, size_t smem) {

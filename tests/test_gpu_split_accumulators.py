@@ -36,13 +36,22 @@ def _registry(atmm, oracle, d, ranks, seed):
     ({0: 300, 1: 64}, 200),                   # rank chunks: passes of r_pad 128 (G = 1) and 48 (G = 2)
 ])
 @pytest.mark.parametrize("ydt", ["bf16", "f32"])
-def test_split_fresh_inputs_every_apply(gpu, atmm, oracle, ranks, rows, ydt):
+@pytest.mark.parametrize("order", ["shuffled", "sorted", "runs"])
+def test_split_fresh_inputs_every_apply(gpu, atmm, oracle, ranks, rows, ydt, order):
+    """order: shuffled rows (every tile gathered row by row), sorted (every
+    tile's rows consecutive: X / Y by TMA boxes, TileDesc::x_row0), runs
+    (requests of 40 consecutive rows interleaved: some tiles of each kind)."""
     import torch
 
     d = 1024
     reg, facs = _registry(atmm, oracle, d, ranks, 11)
     asg = np.repeat(np.asarray(sorted(ranks), np.int32), rows)
-    asg = asg[np.random.default_rng(3).permutation(asg.size)]
+    if order == "shuffled":
+        asg = asg[np.random.default_rng(3).permutation(asg.size)]
+    elif order == "runs":
+        runs = [asg[i:i + 40] for i in range(0, asg.size, 40)]
+        perm = np.random.default_rng(3).permutation(len(runs))
+        asg = np.concatenate([runs[i] for i in perm])
     n = asg.size
     plan = atmm.BypassPlan(reg, asg, path_table(atmm, asg, ranks, d, d, "split"))
     assert {g["path_bf16"] for g in plan.describe()} == {"split"}

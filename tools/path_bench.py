@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--x-ready", action="store_true")
     ap.add_argument("--y-dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--sorted", action="store_true",
+                    help="rows grouped by adapter (consecutive runs: the split kernels' TMA-box path)")
     ap.add_argument("--launches", default=None,
                     help="';'-separated tile_m,cluster,bn,stages,path launches to force (instead of --paths)")
     ap.add_argument("--no-overlap", action="store_true", help="ATMM_PLAN_NO_OVERLAP on every plan")
@@ -43,6 +45,8 @@ def main():
     dev = torch.device("cuda", 0)
     for name in args.configs.split(","):
         w = workloads.bypass_config(name)
+        if args.sorted:
+            w.assignment = workloads.make_assignment(w.lengths, shuffle=False)
         step_bytes = w.bytes(2 if args.y_dtype == "bf16" else 4)
         layers = min(64, max(2, int(np.ceil(2.5 * L2_BYTES / step_bytes))))
         reg = atmm.AdapterRegistry(layers, w.d_in, w.d_out, device=0)
