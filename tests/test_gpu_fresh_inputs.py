@@ -26,7 +26,8 @@ CASES = [
 
 @pytest.mark.parametrize("path,ranks,rows,d_in,d_out", CASES)
 @pytest.mark.parametrize("ydt", ["bf16", "f32"])
-def test_back_to_back_fresh_inputs(gpu, atmm, oracle, path, ranks, rows, d_in, d_out, ydt):
+@pytest.mark.parametrize("order", ["shuffled", "sorted"])  # sorted: tiles of consecutive rows (TMA boxes)
+def test_back_to_back_fresh_inputs(gpu, atmm, oracle, path, ranks, rows, d_in, d_out, ydt, order):
     import torch
 
     reg = atmm.AdapterRegistry(2, d_in, d_out)
@@ -40,7 +41,8 @@ def test_back_to_back_fresh_inputs(gpu, atmm, oracle, path, ranks, rows, d_in, d
         for l in range(2):
             facs[l][a] = (down[l], up[l])
     asg = np.repeat(np.asarray(sorted(ranks), np.int32), rows)
-    asg = asg[np.random.default_rng(4).permutation(asg.size)]
+    if order == "shuffled":
+        asg = asg[np.random.default_rng(4).permutation(asg.size)]
     n = asg.size
     table = path_table(atmm, asg, ranks, d_in, d_out, path) if path != "auto" and max(ranks.values()) <= 128 else None
     plan = atmm.BypassPlan(reg, asg, table)
