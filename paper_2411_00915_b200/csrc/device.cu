@@ -37,6 +37,8 @@ cudaError_t launch_merge(int w_dtype, const MergeParams& p, int grid, size_t sme
 cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassParams& p, int C, int num_tiles,
                               size_t smem, cudaStream_t stream);
 cudaError_t launch_stream(int y_dtype, const StreamParams& p, int grid, size_t smem, cudaStream_t stream);
+cudaError_t launch_permute_up_g2(const uint16_t* src, int64_t src_ls, uint16_t* dst, int64_t dst_ls, int64_t L,
+                                 int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad, cudaStream_t stream);
 cudaError_t launch_split(int y_dtype, const CUtensorMap& xtile, const CUtensorMap& ytile, const SplitParams& p, int grid,
                          size_t smem_s, size_t smem_e,
                          cudaStream_t stream);
@@ -340,6 +342,10 @@ struct Slot {
   float scale = 1.0f;
   uint16_t* down_t = nullptr;
   uint16_t* up_t = nullptr;
+  // up^T in the split expand's 256-column MMA order (TileDesc::up_t2), made on
+  // a plan's first use of the slot on that path (stream-ordered allocation,
+  // so free_slot may release it either way)
+  uint16_t* up_t2 = nullptr;
   bool live = false;
   bool async_owned = false;  // buffers from cudaMallocAsync (put_async): freed stream-ordered
   // fp32-faithful images (precise registries only), bf16 hi / lo splits per layer:
@@ -352,7 +358,7 @@ struct Slot {
 // Frees a slot's device buffers (stream-ordered when `async`: buffers from
 // stream-ordered allocation, released after every earlier use on `st`).
 static void free_slot(Slot& s, cudaStream_t st = nullptr, bool async = false) {
-  for (uint16_t* p : {s.down_t, s.up_t, s.p_down_b, s.p_up_b, s.p_down_a}) {
+  for (uint16_t* p : {s.down_t, s.up_t, s.p_down_b, s.p_up_b, s.p_down_a, s.up_t2}) {
     if (!p) continue;
     if (async) {
       cudaFreeAsync(p, st);
@@ -360,7 +366,7 @@ static void free_slot(Slot& s, cudaStream_t st = nullptr, bool async = false) {
       cudaFree(p);
     }
   }
-  s.down_t = s.up_t = s.p_down_b = s.p_up_b = s.p_down_a = nullptr;
+  s.down_t = s.up_t = s.p_down_b = s.p_up_b = s.p_down_a = s.up_t2 = nullptr;
 }
 
 }  // namespace atmm
@@ -368,6 +374,7 @@ static void free_slot(Slot& s, cudaStream_t st = nullptr, bool async = false) {
 using namespace atmm;
 
 struct atmm_registry {
+  std::mutex up2_mu;  // lazily made Slot::up_t2 (plans may be built on several threads)
   int device = 0;
   int64_t L = 0, d_in = 0, d_out = 0, d_in_pad = 0, d_out_pad = 0;
   std::map<int32_t, int> slot_of;
@@ -1064,6 +1071,46 @@ static void build_stream(atmm_plan& plan, const std::vector<TileDesc>& tiles, co
 
 // Builds routing tables and launch groups.  `forced` (tuner) overrides the
 // table for every segment.
+// The MMA-ordered up^T copy (Slot::up_t2) of the live slot whose up^T is
+// `up_t`, made on first use: a permute kernel on a private stream, allocated
+// stream-ordered, outside any capture on this thread (relaxed mode), waited
+// for before the plan that needs it exists.  Null when no slot matches.
+static const uint16_t* slot_up_t2(atmm_registry* reg, const uint16_t* up_t, int32_t r_pad) {
+  std::lock_guard<std::mutex> lk(reg->up2_mu);
+  Slot* sl = nullptr;
+  for (Slot& s : reg->slots) {
+    if (s.live && s.up_t == up_t && s.r_pad == r_pad) sl = &s;
+  }
+  // put_async slots: their factors are written stream-ordered on the
+  // caller's stream (not necessarily done when a plan is built): no copy,
+  // the expand stages their up^T by 16-byte copies
+  if (!sl || sl->async_owned) return nullptr;
+  if (sl->up_t2) return sl->up_t2;
+  const int64_t d_out_pad2 = round_up(reg->d_out_pad, 256);
+  const size_t elems = static_cast<size_t>(reg->L) * static_cast<size_t>(d_out_pad2) * static_cast<size_t>(r_pad);
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  cudaStream_t st = nullptr;
+  uint16_t* dst = nullptr;
+  cudaError_t err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaMallocAsync(&dst, elems * 2, st);
+  if (err == cudaSuccess) {
+    err = launch_permute_up_g2(sl->up_t, reg->d_out_pad * r_pad, dst, d_out_pad2 * r_pad, reg->L, reg->d_out_pad,
+                               d_out_pad2, r_pad, st);
+  }
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  if (err != cudaSuccess && dst) {
+    cudaFreeAsync(dst, st);
+    cudaStreamSynchronize(st);
+    dst = nullptr;
+  }
+  if (st) cudaStreamDestroy(st);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (err != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("up^T permute failed: ") + cudaGetErrorString(err));
+  sl->up_t2 = dst;
+  return dst;
+}
+
 static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* assignment,
                                              int64_t n, const TilingTable* table,
                                              const LaunchCfg* forced, const int32_t* row_map = nullptr,
@@ -1159,6 +1206,14 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
   }
   if (plan->merged_first >= 0) {
     plan->merged.split = resolve_split(reg->d_in, reg->d_out, plan->merged.rows_max, plan->merged.r_pad_max);
+    // 256-column expand items (bf16 Y, G = 2) load up^T by one bulk copy
+    // from the slot's MMA-ordered copy
+    if (plan->merged.split.ok_dt[0] && plan->merged.split.g_bf16 == 2) {
+      for (int64_t t = plan->merged.tile_offset; t < plan->merged.tile_offset + plan->merged.num_tiles; ++t) {
+        TileDesc& td = all_tiles[static_cast<size_t>(t)];
+        td.up_t2 = slot_up_t2(reg, td.up_t, td.r_pad);
+      }
+    }
     if (!plan->merged.split.ok) plan->merged_first = -1;
   }
   std::vector<int32_t> rows32(plan->bp.row_index.begin(), plan->bp.row_index.end());

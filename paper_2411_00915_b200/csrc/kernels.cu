@@ -1754,15 +1754,14 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const __
       const uint32_t Rb = Yb + y_bytes;  // rows of this stage
       if (tid < static_cast<uint32_t>(kTileM)) st_shared_u32(Rb + tid * 4, static_cast<uint32_t>(p.tile_rows[t * kTileM + static_cast<int>(tid)]));
       named_bar_sync(2, kSplitLoaders);  // the stage's row indices are written
-      // up^T rows n0 .. n0 + kCols - 1, 16-byte units permuted: column n0 + nl
-      // -> MMA j = nl % G, A row nl / G.
+      // up^T rows n0 .. n0 + kCols - 1 in MMA order: column n0 + nl -> MMA
+      // j = nl % G, A row nl / G (16-byte units, unless one bulk copy below).
       const uint16_t* us = tile.up_t + static_cast<int64_t>(p.layer) * tile.up_layer_stride;
       const int kc = r_pad / 8;
       const int n_end = (p.d_out + 127) & ~127;  // the registry pads up^T to d_out_pad = round_up(d_out, 128)
-      // G = 1: the 128 columns' blocked up^T is one contiguous run of the
-      // registry layout (interleave_off(n, c, r_pad) == its global offset):
-      // one TMA bulk copy below instead of 16-byte LSU copies.
-      for (int q = static_cast<int>(tid); G > 1 && q < kCols * kc; q += kSplitLoaders) {
+      // G = 2: the slice's up^T in MMA order (TileDesc::up_t2) is one bulk copy too
+      const bool up_bulk = G == 1 || tile.up_t2 != nullptr;
+      for (int q = static_cast<int>(tid); !up_bulk && q < kCols * kc; q += kSplitLoaders) {
         const int nl = q / kc;
         const int c = q - nl * kc;
         const int n = n0 + nl;
@@ -1773,6 +1772,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const __
         cp_async16(U + interleave_off(static_cast<uint32_t>(a_row), static_cast<uint32_t>(c * 8), static_cast<uint32_t>(r_pad)),
                    in ? us + ((static_cast<int64_t>(n >> 3) * kc + c) * 64 + (n & 7) * 8) : us, in ? 16u : 0u);
       }
+      // (G = 1: the 128 columns' blocked up^T is one contiguous run of the
+      // registry layout, interleave_off(n, c, r_pad) == its global offset.)
       // Y rows: the shrink launch (our predecessor) does not write Y and fires
       // its dependents only after its own griddepcontrol.wait, so every earlier
       // writer of Y has completed: Y may be read before our own wait.
@@ -1812,9 +1813,17 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const __
           waited = true;
           STRACE(12);
         }
-        const uint32_t ub = G == 1 ? static_cast<uint32_t>(kCols * r_pad * 2) : 0u;
+        // G = 1: the run of the registry layout; G = 2: the slice of up_t2
+        // (zero past d_out_pad)
+        const uint32_t ub = up_bulk ? static_cast<uint32_t>(kCols * r_pad * 2) : 0u;
         mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>(rows16 * r_pad * 2) + ub);
-        if (G == 1) bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes, us + static_cast<int64_t>(n0 >> 3) * kc * 64, ub, &full[st]);
+        if (G == 1) {
+          bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes, us + static_cast<int64_t>(n0 >> 3) * kc * 64, ub, &full[st]);
+        } else if (up_bulk) {
+          const int64_t ls2 = static_cast<int64_t>((p.d_out + 255) & ~255) * r_pad;
+          bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes,
+                   tile.up_t2 + static_cast<int64_t>(p.layer) * ls2 + static_cast<int64_t>(n0) * r_pad, ub, &full[st]);
+        }
         bulk_g2s(smem + static_cast<size_t>(st) * stage_bytes + up_bytes, ms, static_cast<uint32_t>(rows16 * r_pad * 2),
                  &full[st]);
       }
@@ -2386,6 +2395,28 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
 }
 
 // ---------------------------------------------------------------- utils --
+// up^T (registry layout: per layer [g = d_out_pad / 8][c = r_pad / 8][8 x 8])
+// -> the split expand's 256-column-slice operand order: slice s, A row
+// a = 128 j + m holds column 256 s + 2 m + j, rows in the interleave layout
+// of interleave_off(a, c, r_pad).  Columns past d_out_pad are zero.
+__global__ void permute_up_g2_kernel(const uint16_t* __restrict__ src, int64_t src_ls, uint16_t* __restrict__ dst,
+                                     int64_t dst_ls, int64_t L, int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad) {
+  const int64_t kc = r_pad / 8;
+  const int64_t per_layer = d_out_pad2 * kc;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < L * per_layer; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t l = q / per_layer;
+    const int64_t rem = q - l * per_layer;
+    const int64_t n2 = rem / kc;  // permuted position
+    const int64_t c = rem - n2 * kc;
+    const int64_t sl = n2 / 256, a = n2 % 256;
+    const int64_t n = sl * 256 + 2 * (a % 128) + a / 128;  // source column
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (n < d_out_pad) v = *reinterpret_cast<const uint4*>(src + l * src_ls + ((n >> 3) * kc + c) * 64 + (n & 7) * 8);
+    const int64_t off = (a >> 3) * (r_pad * 8) + c * 64 + (a & 7) * 8;  // interleave_off(a, 8 c, r_pad) / 2
+    *reinterpret_cast<uint4*>(dst + l * dst_ls + sl * 256 * r_pad + off) = v;
+  }
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, uint16_t* __restrict__ dst,
                                    int64_t rows, int64_t cols, int64_t lds, int64_t ldd) {
   const int64_t total = rows * cols;
@@ -2688,6 +2719,14 @@ cudaError_t launch_scale_bf16_2d(uint16_t* base, int64_t rows, int64_t cols, int
   const int64_t total = rows * cols;
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
   scale_bf16_2d_kernel<<<blocks > 0 ? blocks : 1, 256, 0, stream>>>(base, rows, cols, ld, f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_permute_up_g2(const uint16_t* src, int64_t src_ls, uint16_t* dst, int64_t dst_ls, int64_t L,
+                                 int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad, cudaStream_t stream) {
+  const int64_t total = L * d_out_pad2 * (r_pad / 8);
+  const int grid = static_cast<int>(std::min<int64_t>(4096, (total + 255) / 256));
+  permute_up_g2_kernel<<<std::max(grid, 1), 256, 0, stream>>>(src, src_ls, dst, dst_ls, L, d_out_pad, d_out_pad2, r_pad);
   return cudaGetLastError();
 }
 

@@ -93,3 +93,48 @@ def test_expand_tmem_holds_two_accumulators(gpu, atmm, oracle, rows, rank):
             assert cols >= 2 * gg * sp["rows16"] and cols <= 512, (sp, di)
             co = smem_per_sm // (sp["smem_e"][di] + 1024)
             assert co * cols <= 512, (sp, di, co)
+
+
+@pytest.mark.parametrize("swap", ["put", "put_async"])
+def test_split_up_copy_follows_adapter_replacement(gpu, atmm, oracle, swap):
+    """256-column expand items read an MMA-ordered copy of up^T made when a
+    split plan first uses the slot (Slot::up_t2): replacing the adapter (put,
+    or put_async on a stream) must never leave a plan reading the old copy."""
+    import torch
+
+    d = 1024
+    ranks = {0: 32, 1: 64}
+    reg, facs = _registry(atmm, oracle, d, ranks, 21)
+    asg = np.repeat(np.asarray([0, 1], np.int32), 128)
+    asg = asg[np.random.default_rng(2).permutation(asg.size)]
+    n = asg.size
+    tbl = path_table(atmm, asg, ranks, d, d, "split")
+    rng = oracle.rng(5)
+    x = oracle.round_bf16(oracle.random_matrix(rng, n, d))
+    xt = torch.from_numpy(x).to("cuda", torch.bfloat16)
+
+    def check(plan, facs):
+        y0 = oracle.round_bf16(oracle.random_matrix(rng, n, d))
+        yt = torch.from_numpy(y0).to("cuda", torch.bfloat16)
+        plan.apply(xt, yt, layer=0)
+        torch.cuda.synchronize()
+        want = y0.astype(np.float64) + oracle.bypass_rows_f64(x, asg, facs)
+        assert float(np.max(np.abs(yt.float().cpu().numpy() - want))) <= tol_for(want)
+
+    plan = atmm.BypassPlan(reg, asg, tbl)
+    check(plan, facs)
+    # replace adapter 1 (same rank) with new factors
+    r = ranks[1]
+    s = 1.0 / np.sqrt(np.float32(r))
+    down = oracle.round_bf16(oracle.random_matrix(rng, d, r, -s, s))
+    up = oracle.round_bf16(oracle.random_matrix(rng, r, d, -s, s))
+    if swap == "put":
+        reg.put(1, down[None], up[None])
+    else:
+        st = torch.cuda.Stream()
+        reg.put_async(1, down[None], up[None], stream=st)
+        st.synchronize()
+    facs = dict(facs)
+    facs[1] = (down, up)
+    plan2 = atmm.BypassPlan(reg, asg, tbl)
+    check(plan2, facs)
