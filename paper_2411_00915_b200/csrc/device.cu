@@ -38,7 +38,7 @@ cudaError_t launch_bypass_a2a(int y_dtype, const GroupArgs& ga, const BypassPara
                               size_t smem, cudaStream_t stream);
 cudaError_t launch_stream(int y_dtype, const StreamParams& p, int grid, size_t smem, cudaStream_t stream);
 cudaError_t launch_permute_up_g2(const uint16_t* src, int64_t src_ls, uint16_t* dst, int64_t dst_ls, int64_t L,
-                                 int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad, cudaStream_t stream);
+                                 int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad, int64_t G, cudaStream_t stream);
 cudaError_t launch_split(int y_dtype, const CUtensorMap& xtile, const CUtensorMap& ytile, const SplitParams& p, int grid,
                          size_t smem_s, size_t smem_e,
                          cudaStream_t stream);
@@ -342,10 +342,10 @@ struct Slot {
   float scale = 1.0f;
   uint16_t* down_t = nullptr;
   uint16_t* up_t = nullptr;
-  // up^T in the split expand's 256-column MMA order (TileDesc::up_t2), made on
-  // a plan's first use of the slot on that path (stream-ordered allocation,
-  // so free_slot may release it either way)
-  uint16_t* up_t2 = nullptr;
+  // up^T in the (128 G)-column MMA order for G = 2, 4, 8 (TileDesc::up_t2),
+  // each made on a plan's first use of the slot with that G (stream-ordered
+  // allocation, so free_slot may release it either way)
+  uint16_t* up_tg[3] = {nullptr, nullptr, nullptr};
   bool live = false;
   bool async_owned = false;  // buffers from cudaMallocAsync (put_async): freed stream-ordered
   // fp32-faithful images (precise registries only), bf16 hi / lo splits per layer:
@@ -358,7 +358,7 @@ struct Slot {
 // Frees a slot's device buffers (stream-ordered when `async`: buffers from
 // stream-ordered allocation, released after every earlier use on `st`).
 static void free_slot(Slot& s, cudaStream_t st = nullptr, bool async = false) {
-  for (uint16_t* p : {s.down_t, s.up_t, s.p_down_b, s.p_up_b, s.p_down_a, s.up_t2}) {
+  for (uint16_t* p : {s.down_t, s.up_t, s.p_down_b, s.p_up_b, s.p_down_a, s.up_tg[0], s.up_tg[1], s.up_tg[2]}) {
     if (!p) continue;
     if (async) {
       cudaFreeAsync(p, st);
@@ -366,7 +366,8 @@ static void free_slot(Slot& s, cudaStream_t st = nullptr, bool async = false) {
       cudaFree(p);
     }
   }
-  s.down_t = s.up_t = s.p_down_b = s.p_up_b = s.p_down_a = s.up_t2 = nullptr;
+  s.down_t = s.up_t = s.p_down_b = s.p_up_b = s.p_down_a = nullptr;
+  s.up_tg[0] = s.up_tg[1] = s.up_tg[2] = nullptr;
 }
 
 }  // namespace atmm
@@ -374,7 +375,7 @@ static void free_slot(Slot& s, cudaStream_t st = nullptr, bool async = false) {
 using namespace atmm;
 
 struct atmm_registry {
-  std::mutex up2_mu;  // lazily made Slot::up_t2 (plans may be built on several threads)
+  std::mutex up2_mu;  // lazily made Slot::up_tg (plans may be built on several threads)
   int device = 0;
   int64_t L = 0, d_in = 0, d_out = 0, d_in_pad = 0, d_out_pad = 0;
   std::map<int32_t, int> slot_of;
@@ -1071,11 +1072,15 @@ static void build_stream(atmm_plan& plan, const std::vector<TileDesc>& tiles, co
 
 // Builds routing tables and launch groups.  `forced` (tuner) overrides the
 // table for every segment.
-// The MMA-ordered up^T copy (Slot::up_t2) of the live slot whose up^T is
-// `up_t`, made on first use: a permute kernel on a private stream, allocated
-// stream-ordered, outside any capture on this thread (relaxed mode), waited
-// for before the plan that needs it exists.  Null when no slot matches.
-static const uint16_t* slot_up_t2(atmm_registry* reg, const uint16_t* up_t, int32_t r_pad) {
+// The MMA-ordered up^T copy for G (Slot::up_tg) of the live slot whose up^T
+// is `up_t`, made on first use: a permute kernel on a private stream,
+// allocated stream-ordered, outside any capture on this thread (relaxed
+// mode), waited for before the plan that needs it exists.  G = 1 is the
+// registry layout itself.  Null when no slot matches.
+static const uint16_t* slot_up_tg(atmm_registry* reg, const uint16_t* up_t, int32_t r_pad, int G) {
+  if (G == 1) return up_t;
+  const int gi = G == 2 ? 0 : (G == 4 ? 1 : (G == 8 ? 2 : -1));
+  if (gi < 0) return nullptr;
   std::lock_guard<std::mutex> lk(reg->up2_mu);
   Slot* sl = nullptr;
   for (Slot& s : reg->slots) {
@@ -1083,10 +1088,10 @@ static const uint16_t* slot_up_t2(atmm_registry* reg, const uint16_t* up_t, int3
   }
   // put_async slots: their factors are written stream-ordered on the
   // caller's stream (not necessarily done when a plan is built): no copy,
-  // the expand stages their up^T by 16-byte copies
+  // the kernels stage their up^T by 16-byte copies
   if (!sl || sl->async_owned) return nullptr;
-  if (sl->up_t2) return sl->up_t2;
-  const int64_t d_out_pad2 = round_up(reg->d_out_pad, 256);
+  if (sl->up_tg[gi]) return sl->up_tg[gi];
+  const int64_t d_out_pad2 = round_up(reg->d_out_pad, 128 * G);
   const size_t elems = static_cast<size_t>(reg->L) * static_cast<size_t>(d_out_pad2) * static_cast<size_t>(r_pad);
   cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
   cudaThreadExchangeStreamCaptureMode(&mode);
@@ -1096,7 +1101,7 @@ static const uint16_t* slot_up_t2(atmm_registry* reg, const uint16_t* up_t, int3
   if (err == cudaSuccess) err = cudaMallocAsync(&dst, elems * 2, st);
   if (err == cudaSuccess) {
     err = launch_permute_up_g2(sl->up_t, reg->d_out_pad * r_pad, dst, d_out_pad2 * r_pad, reg->L, reg->d_out_pad,
-                               d_out_pad2, r_pad, st);
+                               d_out_pad2, r_pad, G, st);
   }
   if (err == cudaSuccess) err = cudaStreamSynchronize(st);
   if (err != cudaSuccess && dst) {
@@ -1107,7 +1112,7 @@ static const uint16_t* slot_up_t2(atmm_registry* reg, const uint16_t* up_t, int3
   if (st) cudaStreamDestroy(st);
   cudaThreadExchangeStreamCaptureMode(&mode);
   if (err != cudaSuccess) fail(ATMM_ERR_CUDA, std::string("up^T permute failed: ") + cudaGetErrorString(err));
-  sl->up_t2 = dst;
+  sl->up_tg[gi] = dst;
   return dst;
 }
 
@@ -1211,7 +1216,8 @@ static std::unique_ptr<atmm_plan> build_plan(atmm_registry* reg, const int32_t* 
     if (plan->merged.split.ok_dt[0] && plan->merged.split.g_bf16 == 2) {
       for (int64_t t = plan->merged.tile_offset; t < plan->merged.tile_offset + plan->merged.num_tiles; ++t) {
         TileDesc& td = all_tiles[static_cast<size_t>(t)];
-        td.up_t2 = slot_up_t2(reg, td.up_t, td.r_pad);
+        td.up_t2 = slot_up_tg(reg, td.up_t, td.r_pad, 2);
+        td.up_g = td.up_t2 ? 2 : 0;
       }
     }
     if (!plan->merged.split.ok) plan->merged_first = -1;

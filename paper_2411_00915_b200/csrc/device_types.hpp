@@ -28,11 +28,13 @@ struct TileDesc {
   int32_t rows;
   int32_t r_pad;
   float scale;
-  const uint16_t* up_t2 = nullptr;  // split expand, 256-column items: up^T with the columns of every
-                                    // 256-column slice in MMA order (col 2m + j -> A row 128 j + m),
-                                    // one bulk copy per item; layer stride round_up(d_out, 256) r_pad
+  const uint16_t* up_t2 = nullptr;  // up^T with the columns of every (128 up_g)-column slice in MMA
+                                    // order (column up_g m + j -> A row 128 j + m): one bulk copy per
+                                    // slice in the split expand (up_g 2); layer stride
+                                    // round_up(d_out, 128 up_g) r_pad
   int32_t x_row0 = -1;        // the tile's rows are X / Y rows x_row0 .. x_row0 + rows - 1 (one
                               // TMA box, split path), else -1 (gathered row by row)
+  int32_t up_g = 0;           // the G of up_t2 (0: none)
 };
 
 // One registry slot (adapter), device resident.  Factors are bf16 in the

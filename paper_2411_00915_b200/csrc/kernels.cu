@@ -1760,7 +1760,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) atmm_expand_kernel(const __
       const int kc = r_pad / 8;
       const int n_end = (p.d_out + 127) & ~127;  // the registry pads up^T to d_out_pad = round_up(d_out, 128)
       // G = 2: the slice's up^T in MMA order (TileDesc::up_t2) is one bulk copy too
-      const bool up_bulk = G == 1 || tile.up_t2 != nullptr;
+      const bool up_bulk = G == 1 || (tile.up_t2 != nullptr && tile.up_g == G);
       for (int q = static_cast<int>(tid); !up_bulk && q < kCols * kc; q += kSplitLoaders) {
         const int nl = q / kc;
         const int c = q - nl * kc;
@@ -2396,11 +2396,13 @@ __global__ void __launch_bounds__(kMergeThreads, 1)
 
 // ---------------------------------------------------------------- utils --
 // up^T (registry layout: per layer [g = d_out_pad / 8][c = r_pad / 8][8 x 8])
-// -> the split expand's 256-column-slice operand order: slice s, A row
-// a = 128 j + m holds column 256 s + 2 m + j, rows in the interleave layout
-// of interleave_off(a, c, r_pad).  Columns past d_out_pad are zero.
+// -> the (128 G)-column-slice operand order of the split expand (G = 2):
+// slice s, A row a = 128 j + m holds column
+// 128 G s + G m + j, rows in the interleave layout of interleave_off(a, c,
+// r_pad).  Columns past d_out_pad are zero.
 __global__ void permute_up_g2_kernel(const uint16_t* __restrict__ src, int64_t src_ls, uint16_t* __restrict__ dst,
-                                     int64_t dst_ls, int64_t L, int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad) {
+                                     int64_t dst_ls, int64_t L, int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad,
+                                     int64_t G) {
   const int64_t kc = r_pad / 8;
   const int64_t per_layer = d_out_pad2 * kc;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < L * per_layer; q += int64_t(gridDim.x) * blockDim.x) {
@@ -2408,12 +2410,13 @@ __global__ void permute_up_g2_kernel(const uint16_t* __restrict__ src, int64_t s
     const int64_t rem = q - l * per_layer;
     const int64_t n2 = rem / kc;  // permuted position
     const int64_t c = rem - n2 * kc;
-    const int64_t sl = n2 / 256, a = n2 % 256;
-    const int64_t n = sl * 256 + 2 * (a % 128) + a / 128;  // source column
+    const int64_t W = 128 * G;
+    const int64_t sl = n2 / W, a = n2 % W;
+    const int64_t n = sl * W + G * (a % 128) + a / 128;  // source column
     uint4 v = make_uint4(0u, 0u, 0u, 0u);
     if (n < d_out_pad) v = *reinterpret_cast<const uint4*>(src + l * src_ls + ((n >> 3) * kc + c) * 64 + (n & 7) * 8);
     const int64_t off = (a >> 3) * (r_pad * 8) + c * 64 + (a & 7) * 8;  // interleave_off(a, 8 c, r_pad) / 2
-    *reinterpret_cast<uint4*>(dst + l * dst_ls + sl * 256 * r_pad + off) = v;
+    *reinterpret_cast<uint4*>(dst + l * dst_ls + sl * W * r_pad + off) = v;
   }
 }
 
@@ -2723,10 +2726,10 @@ cudaError_t launch_scale_bf16_2d(uint16_t* base, int64_t rows, int64_t cols, int
 }
 
 cudaError_t launch_permute_up_g2(const uint16_t* src, int64_t src_ls, uint16_t* dst, int64_t dst_ls, int64_t L,
-                                 int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad, cudaStream_t stream) {
+                                 int64_t d_out_pad, int64_t d_out_pad2, int64_t r_pad, int64_t G, cudaStream_t stream) {
   const int64_t total = L * d_out_pad2 * (r_pad / 8);
   const int grid = static_cast<int>(std::min<int64_t>(4096, (total + 255) / 256));
-  permute_up_g2_kernel<<<std::max(grid, 1), 256, 0, stream>>>(src, src_ls, dst, dst_ls, L, d_out_pad, d_out_pad2, r_pad);
+  permute_up_g2_kernel<<<std::max(grid, 1), 256, 0, stream>>>(src, src_ls, dst, dst_ls, L, d_out_pad, d_out_pad2, r_pad, G);
   return cudaGetLastError();
 }
 
