@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
 """bench.py -- ATMM batched-LoRA benchmark (BASELINE.json metric).
 
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config cfg2|cfg1|cfg3|cfg5|cfg4|paper_in1|paper_in2]
-                    [--config cfg2|cfg1|cfg3|cfg5|cfg4]
 
 A step is ONE fused bypass pass  Y[rows] += (X[rows] . down_a) . up_a  over
 one batch (default cfg2 = BASELINE.json configs[1]: hidden 4096, rank 16,
